@@ -1,0 +1,409 @@
+"""Benchmark: all-to-all algBW of the lowered decomposed-MCF schedule on B200.
+
+Contract:
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config gk8_2] [--m 16777216]
+N=1 runs in-process; N>1 is launched by torchrun (one rank per GPU, NCCL only
+for bootstrap / barriers / the NCCL baseline, never on the executor path).
+
+Workload: BASELINE.json configs[1], GenKautz N=8 d=2, 16 MiB per pair, the
+frozen decomposed-MCF schedule (artifacts/gk8_2), hop i of every route at step
+i; the 8 virtual nodes are placed v*G//8 on G GPUs (one per GPU at G=8).
+A "step" = one complete all-to-all.  value = whole-job algBW
+N(N-1)m / T (GB/s); per_gpu = value / G.
+Timing: W warm-up steps, then K steps each bracketed by CUDA events on the
+launching stream, L2 flushed (512 MiB memset) between steps outside the
+events; barrier + synchronize around the timed region; per-step max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "all2all algBW GB/s/GPU vs topology lower bound at 1/2/4/8 B200; vs NCCL a2a"
+HBM_FALLBACK = 6650.0
+NVLINK_NOMINAL = 900.0     # GB/s per direction per GPU (BASELINE.json north_star)
+NVLINK_MEASURED = 770.0    # peer copy per direction (B200_PROFILING.md)
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(
+                        ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                         "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                        timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.1)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 8
+                          for i in range(4) if r[4 + i].lower() == "active"})
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return world, rank, local
+
+
+def _cpu_oracle_run(art, m, budget_s, nthreads, max_iters=None):
+    """Time the C oracle (byte-moving restatement of the reference executor)."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from c_oracle import ops_array, replay_bytes_c
+    n = art.g.n
+    rng = np.random.default_rng(0)
+    send = rng.integers(0, 256, size=(n, n, m), dtype=np.uint8)
+    recv = np.zeros_like(send)
+    ops = ops_array(art.sched)
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        replay_bytes_c(art.g, art.sched, send, m, nthreads=nthreads, recv=recv, ops=ops)
+        times.append(time.perf_counter() - t0)
+        if max_iters:
+            if len(times) >= max_iters:
+                break
+        elif time.perf_counter() - t_start > budget_s:
+            break
+    ok = bool(np.array_equal(recv, np.swapaxes(send, 0, 1)))
+    return times, ok
+
+
+def _host_fits(n, m, frac=0.4):
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 16 << 30
+    return 3 * n * n * m < frac * avail
+
+
+def run_reference(args, art, m):
+    """--impl reference: the reference's CPU executor path, restated to move
+    bytes (oracle/replay_bytes.c), on all host threads; rank 0 only."""
+    world, rank, _ = _dist()
+    if rank != 0:
+        return
+    n = art.g.n
+    nthreads = os.cpu_count() or 1
+    m_cpu, note = m, "full workload"
+    while not _host_fits(n, m_cpu) and m_cpu > 4096:
+        m_cpu //= 2
+        note = f"bounded sample: m reduced to {m_cpu} B to fit host memory"
+    times, ok = _cpu_oracle_run(art, m_cpu, budget_s=0, nthreads=nthreads,
+                                max_iters=args.warmup + args.steps)
+    timed = times[args.warmup:] or times
+    T = sum(timed) / len(timed)
+    val = n * (n - 1) * m_cpu / T / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(val, 4), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": len(timed), "warmup": args.warmup,
+        "ms_per_step": round(T * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": f"{args.config} (frozen decomposed-MCF schedule, hop-indexed)",
+                   "m_bytes": m_cpu, "nodes": n, "hop_ops": len(art.sched.instructions),
+                   "nsteps": art.sched.nsteps},
+        "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": nthreads,
+                         "kind": "port",
+                         "sample": f"{note}; oracle/replay_bytes.c, OpenMP {nthreads} threads, "
+                                   f"{len(timed)} full all-to-alls", "recv_ok": ok},
+        "e2e": {"value": round(val, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="gk8_2")
+    ap.add_argument("--m", type=int, default=16 << 20)
+    ap.add_argument("--num-ctas", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    args = ap.parse_args(argv)
+    args.warmup = max(args.warmup, 3)
+
+    from paper_2309_13541_b200.artifacts import load_artifact
+    art = load_artifact(args.config)
+    m = args.m
+    if args.impl == "reference":
+        return run_reference(args, art, m)
+
+    import numpy as np
+    import torch
+
+    from paper_2309_13541_b200.executor import Plan, contiguous_placement
+    from paper_2309_13541_b200.graphs import distance_sum
+
+    world, rank, local = _dist()
+    G = world
+    if G != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if G > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+
+    def barrier():
+        if pg:
+            pg.barrier()
+
+    def allmax(x):
+        if not pg:
+            return x
+        t = torch.tensor(x, dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        return t.tolist()
+
+    n = art.g.n
+    plan = Plan(art.g, art.sched, m=m, n_gpus=G)
+    plan.bind(rank, device=local, num_ctas=args.num_ctas)
+    if G > 1:
+        hs = [None] * G
+        pg.all_gather_object(hs, plan.export_handle())
+        plan.import_handles(hs)
+    info = plan.gpu_info(rank)
+    infos = [plan.gpu_info(g) for g in range(G)]
+    V, first = info["n_local_nodes"], info["first_node"]
+    nodes = [v for v in range(n) if contiguous_placement(n, G)[v] == rank]
+
+    def node_send(s):  # deterministic synthetic shards of node s: [n, m]
+        gen = torch.Generator(device=dev).manual_seed(1000003 * (s + 1))
+        return torch.randint(0, 256, (n, m), dtype=torch.uint8, device=dev, generator=gen)
+
+    send = torch.empty((V, n, m), dtype=torch.uint8, device=dev)
+    for i, s in enumerate(nodes):
+        send[i] = node_send(s)
+    recv = plan.recv_buffer() if G > 1 else torch.empty_like(send)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    # ---- warm-up + correctness of the exact buffers we time
+    for _ in range(args.warmup):
+        plan.execute(send, recv, stream=stream)
+    plan.sync()
+    barrier()
+    ok = True
+    for s in range(n):
+        row = node_send(s)
+        for i, v in enumerate(nodes):
+            ok &= bool(torch.equal(recv[i, s], row[v]))
+    ok = bool(allmax([0.0 if ok else 1.0])[0] == 0.0) if pg else ok
+
+    # ---- timed region: K all-to-alls, L2 flushed between them
+    clk = Clocks(local)
+    e0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    e1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize(dev)
+    clk.start()
+    for k in range(args.steps):
+        flush.zero_()
+        e0[k].record(stream)
+        plan.execute(send, recv, stream=stream)
+        e1[k].record(stream)
+    plan.sync()
+    torch.cuda.synchronize(dev)
+    clocks = clk.stop()
+    barrier()
+    per = [a.elapsed_time(b) for a, b in zip(e0, e1)]
+    per = allmax(per)
+    T = sum(per) / len(per) / 1e3                      # s per all-to-all (max over ranks)
+    payload = n * (n - 1) * m
+    value = payload / T / 1e9
+
+    # ---- roofline of the (only) kernel, a2a_exec_kernel
+    hbm, hbm_kind = _peaks()
+    if G == 1:
+        algo = 2 * (info["hop_bytes"] + n * m)        # read + write per hop, + self shards
+        achieved = algo / T / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
+                "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,
+                "peak_kind": f"{hbm_kind} copy bandwidth (MEASURED_PEAKS.json)",
+                "algorithmic_bytes_per_launch": algo}
+        t_lb = 2 * m * distance_sum(art.g) / (hbm * 1e9)
+    else:
+        xfer = max(max(i["egress_bytes"], i["ingress_bytes"]) for i in infos)
+        achieved = xfer / T / 1e9
+        roof = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_MEASURED,
+                "unit": "GB/s", "frac": round(achieved / NVLINK_MEASURED, 4), "traffic": None,
+                "peak_kind": "measured peer-copy GB/s per direction (B200_PROFILING.md)",
+                "algorithmic_bytes_per_launch": xfer}
+        t_lb = xfer / (NVLINK_NOMINAL * 1e9)
+    traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(traffic_file):
+        with open(traffic_file) as fh:
+            tr = json.load(fh).get(f"{args.config}:{m}:G{G}")
+        if tr:
+            roof["traffic"] = tr
+
+    # ---- NCCL all_to_all_single on the same bytes (baseline, not the target)
+    nccl = None
+    if G > 1 and not args.no_nccl:
+        inp = send.reshape(-1)
+        out = torch.empty_like(inp)
+        for _ in range(3):
+            pg.all_to_all_single(out, inp)
+        torch.cuda.synchronize(dev)
+        ts = []
+        for _ in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            pg.all_to_all_single(out, inp)
+            b.record(stream)
+            ts.append((a, b))
+        torch.cuda.synchronize(dev)
+        tn = allmax([a.elapsed_time(b) for a, b in ts])
+        Tn = sum(tn) / len(tn) / 1e3
+        nccl = {"value": round(payload / Tn / 1e9, 2), "unit": "GB/s",
+                "ms_per_step": round(Tn * 1e3, 4),
+                "note": "torch.distributed.all_to_all_single, same send bytes, direct routes"}
+
+    # ---- e2e through the public API with host buffers (H2D + a2a + D2H per step)
+    e2e = None
+    if not args.no_e2e:
+        hs = torch.empty((V, n, m), dtype=torch.uint8, pin_memory=True)
+        hs.copy_(send.cpu())
+        hr = torch.empty((V, n, m), dtype=torch.uint8, pin_memory=True)
+        ke = max(3, min(args.steps, 10))
+        ev = []
+        barrier()
+        torch.cuda.synchronize(dev)
+        for k in range(ke + 2):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            send.copy_(hs, non_blocking=True)
+            plan.execute(send, recv, stream=stream)
+            hr.copy_(recv, non_blocking=True)
+            b.record(stream)
+            if k >= 2:
+                ev.append((a, b))
+        plan.sync()
+        torch.cuda.synchronize(dev)
+        te = allmax([a.elapsed_time(b) for a, b in ev])
+        Te = sum(te) / len(te) / 1e3
+        e2e = {"value": round(payload / Te / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": int(V * n * m * G), "d2h_bytes_per_step": int(V * n * m * G),
+               "ms_per_step": round(Te * 1e3, 3),
+               "path": "pinned host send -> H2D -> Plan.execute -> D2H recv (every step)"}
+
+    # ---- CPU baseline: rank 0, N=1 only, bounded sample
+    cpu = None
+    if rank == 0 and G == 1 and not args.no_cpu_baseline:
+        nthreads = os.cpu_count() or 1
+        m_cpu = m
+        while not _host_fits(n, m_cpu) and m_cpu > 4096:
+            m_cpu //= 2
+        times, cok = _cpu_oracle_run(art, m_cpu, args.cpu_budget_s, nthreads)
+        tc = sorted(times)[len(times) // 2]
+        cpu = {"value": round(n * (n - 1) * m_cpu / tc / 1e9, 4), "unit": "GB/s",
+               "cores": nthreads, "kind": "port",
+               "sample": f"{len(times)} full all-to-alls of {args.config} at m={m_cpu} B "
+                         f"(median) with oracle/replay_bytes.c on {nthreads} threads",
+               "recv_ok": cok}
+
+    plan.sync()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": G,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(T * 1e3, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u8", "data": "synthetic",
+            "config": {"workload": f"{args.config}: frozen decomposed-MCF schedule "
+                                   f"(hop i of every route at step i), N={n} virtual nodes, "
+                                   f"m={m} B per pair, placement v*G//N",
+                       "m_bytes": m, "nodes": n, "hop_ops": len(art.sched.instructions),
+                       "nsteps": art.sched.nsteps, "Q": art.sched.Q,
+                       "l2": "flushed between timed steps (512 MiB memset, outside events)",
+                       "num_ctas": plan_ctas(plan, args.num_ctas)},
+            "per_gpu": round(value / G, 3),
+            "bound": {"t_lb_ms": round(t_lb * 1e3, 4), "frac": round(t_lb / T, 4),
+                      "def": "G=1: 2*m*sum(dist)/HBM; G>1: max_g max(egress,ingress)/900 GB/s"},
+            "recv_ok": ok,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "nccl": nccl,
+            "gpu_launches": args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
+
+
+def plan_ctas(plan, requested):
+    if requested:
+        return requested
+    try:
+        import torch
+        return torch.cuda.get_device_properties(plan.device).multi_processor_count
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,133 @@
+/*
+ * a2a_exec.h — C ABI of the B200 executor for lowered all-to-all schedules.
+ *
+ * This library takes the slot of the reference's CPU executor
+ *   a2aflow.evaluate.replay_timestep_schedule(g, sched, m, b, sync_latency)
+ *   (reference pkg/src/a2aflow/evaluate.py:56-127)
+ * and actually moves the bytes: every instruction (t, src, dst, s, d, c0, c1)
+ * of a mode="ts" ChunkedSchedule (reference pkg/src/a2aflow/schedule.py:49-72)
+ * copies bytes [floor(c0*m/Q), floor(c1*m/Q)) of shard (s,d) from node src's
+ * buffer to node dst's buffer, hop by hop, on sm_100a kernels; virtual nodes
+ * placed on other GPUs are reached with direct NVLink peer stores, steps are
+ * ordered with system-scope release/acquire flags, and no NCCL call is made.
+ *
+ * The reference has no FFI for this path (it is pure Python); the entry points
+ * below are what its evaluate.replay_timestep_schedule call site would bind
+ * (see INTEGRATION.md for the ctypes stub).  Conventions:
+ *   - plain C types only; no C++ exceptions cross the boundary;
+ *   - every call returns an a2a_status (0 = OK); on failure the message is in
+ *     a2a_last_error() (thread-local).  A rejected schedule returns
+ *     A2A_ERR_EVAL with exactly the reference's EvalError text
+ *     (evaluate.py:70-73, :91-100, :114-126);
+ *   - a plan is not thread-safe; one execute in flight per plan.
+ */
+#ifndef A2A_EXEC_H
+#define A2A_EXEC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  A2A_OK = 0,
+  A2A_ERR_INVALID = 1, /* bad argument / descriptor                       */
+  A2A_ERR_EVAL = 2,    /* schedule rejected; text == reference EvalError  */
+  A2A_ERR_CUDA = 3,    /* CUDA runtime error                              */
+  A2A_ERR_TIMEOUT = 4, /* a device-side flag wait timed out (peer missing)*/
+  A2A_ERR_STATE = 5,   /* call order violated (e.g. execute before bind)  */
+  A2A_ERR_NOMEM = 6    /* device or host allocation failed                */
+} a2a_status;
+
+/* == schedule.Instruction (reference pkg/src/a2aflow/schedule.py:49-62), mode "ts" */
+typedef struct {
+  int32_t t, src, dst, s, d, c0, c1;
+} a2a_op;
+
+/* descriptor flags */
+#define A2A_COPY_SELF 1 /* also copy the self shard send[v][v] -> recv[v][v] */
+
+typedef struct {
+  int32_t n_nodes;         /* Digraph.n (must equal ChunkedSchedule.n)      */
+  int32_t n_steps;         /* ChunkedSchedule.nsteps                         */
+  int32_t q;               /* ChunkedSchedule.Q                              */
+  int32_t n_edges;         /* Digraph.num_edges                              */
+  int64_t m_bytes;         /* shard size m (bytes, integer)                  */
+  const int32_t* edge_uv;  /* [n_edges][2] Digraph.edges (u, v), edge id = index */
+  const double* edge_cap;  /* [n_edges] capacities (only for the modelled T) */
+  const a2a_op* ops;       /* instructions in list order                    */
+  int64_t n_ops;
+  const int32_t* node_gpu; /* [n_nodes] virtual node -> GPU rank; NULL = all on 0 */
+  int32_t n_gpus;          /* >= 1                                           */
+  int32_t flags;           /* A2A_COPY_SELF ...                              */
+} a2a_schedule_desc;
+
+typedef struct a2a_plan a2a_plan;
+
+/* per-GPU shape of a plan (host-side, no device needed) */
+typedef struct {
+  int32_t n_local_nodes;   /* V_g: virtual nodes placed on this GPU          */
+  int32_t first_node;      /* smallest node id on this GPU (-1 if none)      */
+  int64_t send_bytes;      /* V_g * N * m: send buffer, [V_g][N][m] u8        */
+  int64_t recv_bytes;      /* V_g * N * m: recv buffer, recv[v][s] = shard (s,v) */
+  int64_t scratch_bytes;   /* forwarding scratch resident on this GPU        */
+  int64_t n_items;         /* copy items this GPU executes (all steps)       */
+  int64_t hop_bytes;       /* bytes this GPU copies over schedule links      */
+  int64_t egress_bytes;    /* of which to other GPUs (NVLink)                */
+  int64_t ingress_bytes;   /* bytes other GPUs write into this GPU           */
+  int64_t local_bytes;     /* hop bytes that stay on this GPU (+ self copies)*/
+} a2a_gpu_info;
+
+/* ---- plan construction: validation exactly like the reference replay ---- */
+int a2a_plan_create(const a2a_schedule_desc* desc, a2a_plan** out);
+int a2a_plan_destroy(a2a_plan* plan);
+const char* a2a_last_error(void);
+const char* a2a_version(void);
+
+/* modelled store-and-forward time, bit-identical to replay_timestep_schedule's T
+ * (evaluate.py:101-107) for the same (m, b, sync_latency) */
+int a2a_plan_model_time(const a2a_plan* plan, double m, double b, double sync_latency,
+                        double* out_T);
+/* schedule bytes per (step, edge): out[t * n_edges + e] (int64, this plan's m) */
+int a2a_plan_link_bytes(const a2a_plan* plan, int64_t* out);
+int a2a_plan_gpu_info(const a2a_plan* plan, int32_t gpu, a2a_gpu_info* out);
+
+/* ---- device side ---- */
+/* Bind the plan to one GPU: rank `gpu` of the placement on CUDA device
+ * `device_ordinal`, with `num_ctas` persistent CTAs (0 = one per SM).  Allocates
+ * the device arena (flags | recv | scratch) and uploads this rank's tables.
+ * num_ctas must be equal on all ranks of a multi-GPU plan. */
+int a2a_plan_bind(a2a_plan* plan, int32_t gpu, int32_t device_ordinal, int32_t num_ctas);
+/* 64-byte cudaIpcMemHandle of this rank's arena (multi-process, n_gpus > 1) */
+int a2a_plan_export_handle(const a2a_plan* plan, void* out_handle64);
+/* import all ranks' handles ([n_gpus][64] bytes, own entry ignored) */
+int a2a_plan_import_handles(a2a_plan* plan, const void* handles);
+/* single-process multi-GPU alternative to handles: every rank's arena pointer
+ * (a2a_plan_arena), peer access is enabled on this rank's device */
+int a2a_plan_arena(const a2a_plan* plan, void** out_ptr);
+int a2a_plan_import_pointers(a2a_plan* plan, void* const* arenas);
+/* pointer to this rank's arena recv buffer ([V_g][N][m]); with n_gpus > 1
+ * peers store into it directly, so execute must be given this buffer */
+int a2a_plan_recv_buffer(const a2a_plan* plan, void** out_ptr);
+
+/* execute options */
+#define A2A_EXEC_COUNT_LINKS 1 /* accumulate device per-(step,edge) byte counters */
+
+/* Launch one all-to-all on `stream` (cudaStream_t; NULL = legacy default).
+ * send: this rank's [V_g][N][m] buffer; recv: [V_g][N][m] (NULL = arena recv).
+ * Asynchronous; call a2a_plan_sync to wait and collect device errors. */
+int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
+                     int32_t options);
+/* wait for the plan's last execute; returns A2A_ERR_TIMEOUT if a device wait timed out */
+int a2a_plan_sync(a2a_plan* plan);
+/* device byte counters of this rank, out[t * n_edges + e]; then zeroes them */
+int a2a_plan_read_link_counters(a2a_plan* plan, int64_t* out);
+/* device-side flag-wait timeout (ns, default 10 s) */
+int a2a_plan_set_timeout(a2a_plan* plan, int64_t timeout_ns);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* A2A_EXEC_H */

@@ -1,0 +1,564 @@
+// Device side of the executor: one persistent, cooperatively launched kernel
+// per GPU and all-to-all.
+//
+// Per step t the kernel runs this GPU's copy items (hop-ops whose source
+// virtual node lives here).  Each item is a contiguous byte range; hop 0 reads
+// the caller's send buffer directly (pack fused), the last hop writes the
+// destination's recv buffer directly (unpack fused), intermediate hops go
+// through forwarding scratch.  Destinations on other GPUs are written with
+// plain 128-bit stores through CUDA-IPC-mapped peer pointers (NVLink5 via
+// NVSwitch).  The step's bytes are split into one contiguous range per CTA.
+//
+// Ordering (store-and-forward, reference evaluate.py:93-113: a chunk received
+// at step t is forwarded at t+1 at the earliest):
+//   producer GPU g, step t: every CTA with work does bar.sync; fence.sc.sys;
+//       atomicAdd on g's step-t arrival counter.  The CTA that arrives last
+//       fences again and publishes st.release.sys flag[h][t][g] = epoch on
+//       every GPU h that g wrote to in step t (one flag per producer GPU,
+//       not per CTA: consumers poll <= G flags per step).
+//   consumer CTA on GPU h, before its first work of step t+1:
+//       warp 0 polls (ld.acquire.sys, one flag per lane) the producer flags
+//       of the steps it has not acquired yet (host-precomputed lists),
+//       __all_sync, fence, bar.sync
+//   entry barrier (multi-GPU): every GPU announces the epoch to all peers and
+//       waits for theirs before storing into peer memory, so a peer's buffers
+//       are never overwritten while its previous all-to-all is still live.
+//   exit: CTA 0 waits for every step's incoming flags, so kernel completion
+//       implies this GPU's recv buffer is final.
+// Every spin is bounded by a %globaltimer timeout and reports A2A_ERR_TIMEOUT.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "a2a_internal.h"
+
+namespace a2a {
+
+struct KParams {
+  char* base[1 + 2 * A2A_MAX_GPUS];        // send | recv[G] | scratch[G]
+  uint32_t* step_flags[A2A_MAX_GPUS];      // per GPU: [T'][G] u32, slot (t, producer gpu)
+  uint32_t* entry_flags[A2A_MAX_GPUS];     // per GPU: [G] u32
+  unsigned long long* arrive;              // own: [T'] per-step CTA arrival counters
+  const DevItem* items;
+  const int64_t* step_begin;               // [T'+1]
+  const int64_t* step_bytes;               // [T']
+  const uint32_t* step_mask;               // [T'] bit h: this GPU writes to GPU h at step t
+  const uint32_t* step_nwork;              // [T'] CTAs of this GPU with work at step t
+  const int32_t* wait_off;                 // [T'+1] ranges into wait_idx
+  const int32_t* wait_idx;                 // flag indices (t*G + g) in own step_flags
+  unsigned long long* counters;            // [T'][E]
+  int32_t* err;
+  int64_t timeout_ns;
+  uint32_t epoch;
+  int32_t G, rank, nC, T, E, count_links;
+};
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int4 ld_stream(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(int4* p, const int4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// Whole-CTA byte copy.  Fast path when src == dst (mod 16): byte head,
+// 128-bit body with kUnroll loads in flight per thread, byte tail.
+template <int kUnroll>
+__device__ __forceinline__ void cta_copy(char* __restrict__ dst, const char* __restrict__ src,
+                                         int64_t n) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if ((((uintptr_t)src ^ (uintptr_t)dst) & 15) != 0) {
+    for (int64_t i = tid; i < n; i += nt) dst[i] = src[i];
+    return;
+  }
+  int64_t head = (16 - ((uintptr_t)dst & 15)) & 15;
+  if (head > n) head = n;
+  if (tid < head) dst[tid] = src[tid];
+  dst += head;
+  src += head;
+  n -= head;
+  const int64_t nv = n >> 4;
+  const int4* s4 = reinterpret_cast<const int4*>(src);
+  int4* d4 = reinterpret_cast<int4*>(dst);
+  int64_t i = tid;
+  const int64_t stride = (int64_t)nt * kUnroll;
+  for (; i + (int64_t)(kUnroll - 1) * nt < nv; i += stride) {
+    int4 r[kUnroll];
+#pragma unroll
+    for (int j = 0; j < kUnroll; ++j) r[j] = ld_stream(s4 + i + (int64_t)j * nt);
+#pragma unroll
+    for (int j = 0; j < kUnroll; ++j) st_stream(d4 + i + (int64_t)j * nt, r[j]);
+  }
+  for (; i < nv; i += nt) st_stream(d4 + i, ld_stream(s4 + i));
+  const int64_t tail = n & 15;
+  if (tid < tail) dst[nv * 16 + tid] = src[nv * 16 + tid];
+}
+
+// Warp 0 waits until every listed flag reached `epoch`.  Returns false on timeout.
+__device__ bool warp_wait_flags(const uint32_t* flags, const int32_t* idx, int32_t lo, int32_t hi,
+                                uint32_t epoch, int64_t timeout_ns, int32_t* err) {
+  const int lane = threadIdx.x & 31;
+  bool ok = true;
+  uint64_t t0 = 0;
+  for (int32_t i = lo + lane; i < hi; i += 32) {
+    const uint32_t* f = flags + idx[i];
+    uint32_t spins = 0;
+    while ((int32_t)(ld_acquire_sys(f) - epoch) < 0) {
+      if ((++spins & 255) == 0) {
+        uint64_t now = globaltimer();
+        if (t0 == 0) t0 = now;
+        if ((int64_t)(now - t0) > timeout_ns || *(volatile int32_t*)err != 0) {
+          ok = false;
+          break;
+        }
+      }
+    }
+    if (!ok) break;
+  }
+  ok = __all_sync(0xffffffffu, ok);
+  if (!ok && lane == 0) atomicCAS(err, 0, (int32_t)A2A_ERR_TIMEOUT);
+  return ok;
+}
+
+template <int kUnroll>
+__global__ void __launch_bounds__(1024, 1) a2a_exec_kernel(const KParams p) {
+  __shared__ int s_abort;
+  const int c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5;
+  if (tid == 0) s_abort = 0;
+  __syncthreads();
+  const uint32_t* my_flags = p.step_flags[p.rank];
+
+  // ---- entry barrier: announce epoch to every peer, then wait for theirs
+  if (p.G > 1) {
+    if (c == 0 && tid < p.G && tid != p.rank) st_release_sys(p.entry_flags[tid] + p.rank, p.epoch);
+    if (warp == 0) {
+      const int lane = tid & 31;
+      bool ok = true;
+      if (lane < p.G && lane != p.rank) {
+        const uint32_t* f = p.entry_flags[p.rank] + lane;
+        uint64_t t0 = globaltimer();
+        uint32_t spins = 0;
+        while ((int32_t)(ld_acquire_sys(f) - p.epoch) < 0) {
+          if ((++spins & 255) == 0 && ((int64_t)(globaltimer() - t0) > p.timeout_ns ||
+                                       *(volatile int32_t*)p.err != 0)) {
+            ok = false;
+            break;
+          }
+        }
+      }
+      ok = __all_sync(0xffffffffu, ok);
+      if (!ok) {
+        if (lane == 0) { atomicCAS(p.err, 0, (int32_t)A2A_ERR_TIMEOUT); s_abort = 1; }
+      }
+    }
+    __syncthreads();
+    if (s_abort) return;
+  }
+
+  int waited = 0;  // incoming flags of steps [0, waited) already acquired
+  for (int t = 0; t < p.T; ++t) {
+    const int64_t B = p.step_bytes[t];
+    const int64_t lo = cta_lo(B, c, p.nC), hi = cta_lo(B, c + 1, p.nC);
+    if (hi <= lo) continue;
+    if (waited < t) {
+      if (warp == 0) {
+        bool ok = warp_wait_flags(my_flags, p.wait_idx, p.wait_off[waited], p.wait_off[t], p.epoch,
+                                  p.timeout_ns, p.err);
+        if (!ok && tid == 0) s_abort = 1;
+        if (tid == 0) __threadfence_system();
+      }
+      waited = t;
+      __syncthreads();
+      if (s_abort) return;
+    }
+    // items overlapping [lo, hi): binary search the first
+    int64_t a = p.step_begin[t], b = p.step_begin[t + 1] - 1;
+    while (a < b) {
+      int64_t mid = (a + b + 1) >> 1;
+      if (p.items[mid].prefix <= lo) a = mid; else b = mid - 1;
+    }
+    for (int64_t k = a; k < p.step_begin[t + 1]; ++k) {
+      const DevItem it = p.items[k];
+      if (it.prefix >= hi) break;
+      const int64_t x0 = max(lo, it.prefix) - it.prefix;
+      const int64_t x1 = min(hi, it.prefix + it.nbytes) - it.prefix;
+      if (x1 <= x0) continue;
+      cta_copy<kUnroll>(p.base[it.dst_loc] + it.dst_off + x0, p.base[it.src_loc] + it.src_off + x0,
+                        x1 - x0);
+      if (p.count_links && tid == 0 && it.edge >= 0)
+        atomicAdd(p.counters + (int64_t)t * p.E + it.edge, (unsigned long long)(x1 - x0));
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence_system();
+      const unsigned long long nw = p.step_nwork[t];
+      const unsigned long long old = atomicAdd(p.arrive + t, 1ull);
+      if ((old + 1) % nw == 0) {  // last CTA of this GPU to finish step t
+        __threadfence_system();
+        uint32_t mask = p.step_mask[t];
+        while (mask) {
+          const int h = __ffs(mask) - 1;
+          mask &= mask - 1;
+          st_release_sys(p.step_flags[h] + (int64_t)t * p.G + p.rank, p.epoch);
+        }
+      }
+    }
+  }
+  // ---- exit: all incoming stores of every step have landed
+  if (c == 0 && p.G > 1 && waited < p.T) {
+    if (warp == 0)
+      warp_wait_flags(my_flags, p.wait_idx, p.wait_off[waited], p.wait_off[p.T], p.epoch,
+                      p.timeout_ns, p.err);
+  }
+}
+
+static int cuda_fail(cudaError_t e, const char* what) {
+  char buf[256];
+  snprintf(buf, sizeof buf, "%s: %s", what, cudaGetErrorString(e));
+  return fail(A2A_ERR_CUDA, buf);
+}
+
+#define CK(call)                                   \
+  do {                                             \
+    cudaError_t e_ = (call);                       \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+static const int kUnrollDefault = 4;
+
+// arena flag region: entry[G] u32 | step flags [T'][G] u32 | arrive [T'] u64
+static inline int64_t entry_flags_off() { return 0; }
+static inline int64_t step_flags_off() { return 256; }
+static inline int64_t arrive_off(int G, int TE) {
+  return (step_flags_off() + (int64_t)TE * G * 4 + 255) & ~255LL;
+}
+static inline int64_t flag_region_bytes(int G, int TE) {
+  return (arrive_off(G, TE) + (int64_t)TE * 8 + 65535) & ~65535LL;
+}
+
+static void free_device(Plan& P) {
+  if (P.device < 0) return;
+  DeviceGuard dg(P.device);
+  for (int g = 0; g < A2A_MAX_GPUS; ++g) {
+    if (P.peer_opened[g] && P.peer_arena[g]) cudaIpcCloseMemHandle(P.peer_arena[g]);
+    P.peer_opened[g] = false;
+    P.peer_arena[g] = nullptr;
+  }
+  void** bufs[] = {&P.arena, &P.d_items, &P.d_step_begin, &P.d_step_bytes, &P.d_step_mask, &P.d_step_nwork,
+                   &P.d_wait_off, &P.d_wait_idx, &P.d_counters};
+  for (void** b : bufs) {
+    if (*b) cudaFree(*b);
+    *b = nullptr;
+  }
+  if (P.h_err) cudaFreeHost(P.h_err);
+  P.h_err = nullptr;
+  P.d_err = nullptr;
+  P.bound = P.imported = false;
+}
+
+template <typename T>
+static int upload(void** dst, const std::vector<T>& v) {
+  size_t bytes = std::max<size_t>(v.size() * sizeof(T), 16);
+  CK(cudaMalloc(dst, bytes));
+  if (!v.empty()) CK(cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return A2A_OK;
+}
+
+static int bind_plan(Plan& P, int gpu, int dev, int nC) {
+  if (gpu < 0 || gpu >= P.G) return fail(A2A_ERR_INVALID, "gpu rank out of range");
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (dev < 0 || dev >= ndev) return fail(A2A_ERR_INVALID, "device ordinal out of range");
+  DeviceGuard dg(dev);
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major < 10) return fail(A2A_ERR_CUDA, "this library is built for sm_100a (B200) only");
+  int coop = 0;
+  CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+  if (!coop) return fail(A2A_ERR_CUDA, "device does not support cooperative launch");
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, a2a_exec_kernel<kUnrollDefault>,
+                                                   P.nT, 0));
+  const int max_ctas = per_sm * prop.multiProcessorCount;
+  if (nC <= 0) nC = prop.multiProcessorCount;
+  if (nC > max_ctas) return fail(A2A_ERR_INVALID, "num_ctas exceeds co-resident capacity");
+  P.rank = gpu;
+  P.device = dev;
+  P.nC = nC;
+  const int G = P.G, TE = P.T_exec;
+
+  // ---- per-step destination masks / working-CTA counts of every GPU, and
+  //      the flags this rank waits for: (t, g) for every g that writes here at t
+  std::vector<std::vector<uint32_t>> smask(G, std::vector<uint32_t>(TE, 0));
+  std::vector<std::vector<uint32_t>> nwork(G, std::vector<uint32_t>(TE, 0));
+  for (int g = 0; g < G; ++g) {
+    const GpuTables& tb = P.tables[g];
+    for (int t = 0; t < TE; ++t) {
+      for (int64_t j = tb.step_begin[t]; j < tb.step_begin[t + 1]; ++j)
+        smask[g][t] |= 1u << tb.items[j].dst_gpu;
+      for (int c = 0; c < nC; ++c)
+        if (cta_lo(tb.step_bytes[t], c + 1, nC) > cta_lo(tb.step_bytes[t], c, nC)) ++nwork[g][t];
+    }
+  }
+  std::vector<int32_t> wait_off(TE + 1, 0), wait_idx;
+  for (int t = 0; t < TE; ++t) {
+    wait_off[t] = (int32_t)wait_idx.size();
+    for (int g = 0; g < G; ++g)
+      if (smask[g][t] & (1u << gpu)) wait_idx.push_back(t * G + g);
+  }
+  wait_off[TE] = (int32_t)wait_idx.size();
+
+  // ---- arena layout, identical on every rank: flags | recv | scratch
+  P.flags_bytes = flag_region_bytes(G, TE);
+  P.recv_off.assign(G, 0);
+  P.scratch_off.assign(G, 0);
+  P.arena_bytes.assign(G, 0);
+  for (int g = 0; g < G; ++g) {
+    P.recv_off[g] = P.flags_bytes;
+    P.scratch_off[g] = P.recv_off[g] + ((P.info[g].recv_bytes + 4095) & ~4095LL);
+    P.arena_bytes[g] = P.scratch_off[g] + P.info[g].scratch_bytes;
+  }
+  cudaError_t e = cudaMalloc(&P.arena, (size_t)P.arena_bytes[gpu]);
+  if (e != cudaSuccess) {
+    P.arena = nullptr;
+    char buf[200];
+    snprintf(buf, sizeof buf, "cannot allocate %.3f GiB device arena: %s",
+             P.arena_bytes[gpu] / 1073741824.0, cudaGetErrorString(e));
+    return fail(A2A_ERR_NOMEM, buf);
+  }
+  CK(cudaMemset(P.arena, 0, (size_t)P.flags_bytes));
+  int rc;
+  if ((rc = upload(&P.d_items, P.tables[gpu].items)) != A2A_OK) return rc;
+  if ((rc = upload(&P.d_step_begin, P.tables[gpu].step_begin)) != A2A_OK) return rc;
+  if ((rc = upload(&P.d_step_bytes, P.tables[gpu].step_bytes)) != A2A_OK) return rc;
+  if ((rc = upload(&P.d_step_mask, smask[gpu])) != A2A_OK) return rc;
+  if ((rc = upload(&P.d_step_nwork, nwork[gpu])) != A2A_OK) return rc;
+  if ((rc = upload(&P.d_wait_off, wait_off)) != A2A_OK) return rc;
+  if ((rc = upload(&P.d_wait_idx, wait_idx)) != A2A_OK) return rc;
+  size_t cbytes = std::max<size_t>((size_t)TE * std::max(P.E, 1) * 8, 16);
+  CK(cudaMalloc(&P.d_counters, cbytes));
+  CK(cudaMemset(P.d_counters, 0, cbytes));
+  CK(cudaHostAlloc((void**)&P.h_err, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+  *P.h_err = 0;
+  CK(cudaHostGetDevicePointer((void**)&P.d_err, P.h_err, 0));
+  P.peer_arena[gpu] = P.arena;
+  P.bound = true;
+  P.imported = (G == 1);
+  return A2A_OK;
+}
+
+}  // namespace a2a
+
+using namespace a2a;
+
+extern "C" {
+
+int a2a_plan_destroy(a2a_plan* plan) {
+  if (!plan) return A2A_OK;
+  if (plan->p.launched && plan->p.device >= 0) {
+    DeviceGuard dg(plan->p.device);
+    cudaDeviceSynchronize();
+  }
+  free_device(plan->p);
+  delete plan;
+  return A2A_OK;
+}
+
+int a2a_plan_bind(a2a_plan* plan, int32_t gpu, int32_t device_ordinal, int32_t num_ctas) {
+  if (!plan) return fail(A2A_ERR_INVALID, "null plan");
+  if (plan->p.bound) return fail(A2A_ERR_STATE, "plan already bound");
+  int rc = bind_plan(plan->p, gpu, device_ordinal, num_ctas);
+  if (rc != A2A_OK) {
+    std::string msg = a2a_last_error();
+    free_device(plan->p);
+    set_error(msg);
+  }
+  return rc;
+}
+
+int a2a_plan_export_handle(const a2a_plan* plan, void* out_handle64) {
+  if (!plan || !out_handle64) return fail(A2A_ERR_INVALID, "null argument");
+  if (!plan->p.bound) return fail(A2A_ERR_STATE, "plan not bound");
+  DeviceGuard dg(plan->p.device);
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, plan->p.arena));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
+  std::memcpy(out_handle64, &h, 64);
+  return A2A_OK;
+}
+
+int a2a_plan_import_handles(a2a_plan* plan, const void* handles) {
+  if (!plan || !handles) return fail(A2A_ERR_INVALID, "null argument");
+  Plan& P = plan->p;
+  if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound");
+  if (P.imported && P.G > 1) return fail(A2A_ERR_STATE, "peer handles already imported");
+  DeviceGuard dg(P.device);
+  for (int g = 0; g < P.G; ++g) {
+    if (g == P.rank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, (const char*)handles + 64 * g, 64);
+    void* ptr = nullptr;
+    CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    P.peer_arena[g] = ptr;
+    P.peer_opened[g] = true;
+  }
+  P.imported = true;
+  return A2A_OK;
+}
+
+// single-process multi-GPU: peers' arenas given directly (peer access is enabled here)
+int a2a_plan_import_pointers(a2a_plan* plan, void* const* arenas) {
+  if (!plan || !arenas) return fail(A2A_ERR_INVALID, "null argument");
+  Plan& P = plan->p;
+  if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound");
+  DeviceGuard dg(P.device);
+  for (int g = 0; g < P.G; ++g) {
+    if (g == P.rank) continue;
+    cudaPointerAttributes attr;
+    CK(cudaPointerGetAttributes(&attr, arenas[g]));
+    if (attr.device != P.device) {
+      cudaError_t e = cudaDeviceEnablePeerAccess(attr.device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+    }
+    P.peer_arena[g] = arenas[g];
+    P.peer_opened[g] = false;
+  }
+  P.imported = true;
+  return A2A_OK;
+}
+
+int a2a_plan_arena(const a2a_plan* plan, void** out_ptr) {
+  if (!plan || !out_ptr) return fail(A2A_ERR_INVALID, "null argument");
+  if (!plan->p.bound) return fail(A2A_ERR_STATE, "plan not bound");
+  *out_ptr = plan->p.arena;
+  return A2A_OK;
+}
+
+int a2a_plan_recv_buffer(const a2a_plan* plan, void** out_ptr) {
+  if (!plan || !out_ptr) return fail(A2A_ERR_INVALID, "null argument");
+  if (!plan->p.bound) return fail(A2A_ERR_STATE, "plan not bound");
+  *out_ptr = (char*)plan->p.arena + plan->p.recv_off[plan->p.rank];
+  return A2A_OK;
+}
+
+int a2a_plan_set_timeout(a2a_plan* plan, int64_t timeout_ns) {
+  if (!plan || timeout_ns <= 0) return fail(A2A_ERR_INVALID, "bad argument");
+  plan->p.timeout_ns = timeout_ns;
+  return A2A_OK;
+}
+
+int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream, int32_t options) {
+  if (!plan) return fail(A2A_ERR_INVALID, "null plan");
+  Plan& P = plan->p;
+  if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound to a device");
+  if (!P.imported) return fail(A2A_ERR_STATE, "peer arenas not imported");
+  if (*P.h_err != 0) return fail(*P.h_err, "a previous execute failed on the device (timeout)");
+  char* own_recv = (char*)P.arena + P.recv_off[P.rank];
+  if (!recv) recv = own_recv;
+  if (P.G > 1 && recv != own_recv)
+    return fail(A2A_ERR_INVALID, "multi-GPU plans must receive into the arena recv buffer");
+  if (!send && P.info[P.rank].send_bytes > 0) return fail(A2A_ERR_INVALID, "null send buffer");
+  DeviceGuard dg(P.device);
+  KParams kp;
+  std::memset(&kp, 0, sizeof kp);
+  kp.base[loc_send()] = (char*)send;
+  for (int g = 0; g < P.G; ++g) {
+    char* ar = (char*)P.peer_arena[g];
+    kp.base[loc_recv(g)] = (g == P.rank) ? (char*)recv : ar + P.recv_off[g];
+    kp.base[loc_scratch(g, P.G)] = ar + P.scratch_off[g];
+    kp.entry_flags[g] = (uint32_t*)(ar + entry_flags_off());
+    kp.step_flags[g] = (uint32_t*)(ar + step_flags_off());
+  }
+  kp.arrive = (unsigned long long*)((char*)P.arena + arrive_off(P.G, P.T_exec));
+  kp.items = (const DevItem*)P.d_items;
+  kp.step_begin = (const int64_t*)P.d_step_begin;
+  kp.step_bytes = (const int64_t*)P.d_step_bytes;
+  kp.step_mask = (const uint32_t*)P.d_step_mask;
+  kp.step_nwork = (const uint32_t*)P.d_step_nwork;
+  kp.wait_off = (const int32_t*)P.d_wait_off;
+  kp.wait_idx = (const int32_t*)P.d_wait_idx;
+  kp.counters = (unsigned long long*)P.d_counters;
+  kp.err = P.d_err;
+  kp.timeout_ns = P.timeout_ns;
+  kp.epoch = ++P.epoch;
+  if (kp.epoch == 0) kp.epoch = ++P.epoch;  // 0 is the "never written" value
+  kp.G = P.G;
+  kp.rank = P.rank;
+  kp.nC = P.nC;
+  kp.T = P.T_exec;
+  kp.E = P.E;
+  kp.count_links = (options & A2A_EXEC_COUNT_LINKS) ? 1 : 0;
+  void* args[] = {&kp};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)a2a_exec_kernel<kUnrollDefault>,
+                                              dim3(P.nC), dim3(P.nT), args, 0,
+                                              (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchCooperativeKernel");
+  P.last_stream = stream;
+  P.launched = true;
+  return A2A_OK;
+}
+
+int a2a_plan_sync(a2a_plan* plan) {
+  if (!plan) return fail(A2A_ERR_INVALID, "null plan");
+  Plan& P = plan->p;
+  if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound");
+  DeviceGuard dg(P.device);
+  CK(cudaStreamSynchronize((cudaStream_t)P.last_stream));
+  if (*P.h_err != 0) {
+    return fail(*P.h_err, "device-side flag wait timed out (a peer did not arrive)");
+  }
+  return A2A_OK;
+}
+
+int a2a_plan_read_link_counters(a2a_plan* plan, int64_t* out) {
+  if (!plan || !out) return fail(A2A_ERR_INVALID, "null argument");
+  Plan& P = plan->p;
+  if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound");
+  DeviceGuard dg(P.device);
+  CK(cudaDeviceSynchronize());
+  size_t cnt = (size_t)P.T * P.E;
+  if (cnt) {
+    CK(cudaMemcpy(out, P.d_counters, cnt * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemset(P.d_counters, 0, cnt * 8));
+  }
+  return A2A_OK;
+}
+
+}  // extern "C"

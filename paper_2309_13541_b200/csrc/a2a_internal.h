@@ -1,0 +1,112 @@
+// Internal plan representation shared by the host plan builder (a2a_plan.cpp)
+// and the device side (a2a_exec.cu).  Not part of the C ABI.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "a2a_exec.h"
+
+#define A2A_MAX_GPUS 8
+
+#ifdef __CUDACC__
+#define A2A_HD __host__ __device__ __forceinline__
+#else
+#define A2A_HD inline
+#endif
+
+namespace a2a {
+
+// Buffer classes a copy item reads from / writes to.  The pointer table of a
+// launch is [send(local) | recv(gpu 0..G-1) | scratch(gpu 0..G-1)].
+inline int loc_send() { return 0; }
+inline int loc_recv(int gpu) { return 1 + gpu; }
+inline int loc_scratch(int gpu, int G) { return 1 + G + gpu; }
+
+// One contiguous byte copy of one hop-op (or self-shard copy), 48 bytes.
+struct DevItem {
+  int64_t src_off;   // byte offset inside base[src_loc]
+  int64_t dst_off;   // byte offset inside base[dst_loc]
+  int64_t nbytes;
+  int64_t prefix;    // start of this item in the step's concatenated byte space
+  int32_t src_loc;
+  int32_t dst_loc;
+  int32_t edge;      // schedule edge id (-1: self-shard copy, not a link)
+  int32_t dst_gpu;
+};
+static_assert(sizeof(DevItem) == 48, "DevItem layout");
+
+// Per-GPU execution tables: items of every step, steps concatenated.
+struct GpuTables {
+  std::vector<DevItem> items;
+  std::vector<int64_t> step_begin;  // [T'+1] item index ranges
+  std::vector<int64_t> step_bytes;  // [T']
+};
+
+struct Interval {
+  int32_t a, b;       // chunk range [a, b)
+  int64_t base;       // scratch byte offset of chunk a's first byte
+};
+
+struct Plan {
+  // ---- descriptor copy
+  int32_t n = 0, T = 0, Q = 1, E = 0, G = 1, flags = 0;
+  int64_t m = 0;
+  std::vector<int32_t> edge_uv;
+  std::vector<double> cap;
+  std::vector<a2a_op> ops;
+  std::vector<std::vector<int64_t>> step_ops;   // op indices per step, list order
+  std::vector<int32_t> node_gpu, local_idx;
+  int32_t T_exec = 1;                           // max(T, 1): self copies need a step
+
+  // ---- layout / tables (host)
+  std::vector<a2a_gpu_info> info;               // per gpu
+  std::vector<GpuTables> tables;                // per gpu
+  std::vector<int64_t> link_bytes;              // [T * E]
+
+  // ---- device binding (a2a_exec.cu)
+  bool bound = false, imported = false;
+  int32_t rank = -1, device = -1, nC = 0, nT = 1024;
+  int64_t flags_bytes = 0;                      // arena flag region size
+  std::vector<int64_t> recv_off, scratch_off;   // per gpu, inside that gpu's arena
+  std::vector<int64_t> arena_bytes;             // per gpu
+  void* arena = nullptr;                        // own arena (cudaMalloc)
+  void* peer_arena[A2A_MAX_GPUS] = {nullptr};   // mapped arenas (own included)
+  bool peer_opened[A2A_MAX_GPUS] = {false};     // opened via IPC (must close)
+  void* d_items = nullptr;
+  void* d_step_begin = nullptr;
+  void* d_step_bytes = nullptr;
+  void* d_step_mask = nullptr;
+  void* d_step_nwork = nullptr;
+  void* d_wait_off = nullptr;
+  void* d_wait_idx = nullptr;
+  void* d_counters = nullptr;
+  int32_t* h_err = nullptr;                     // mapped pinned error word
+  int32_t* d_err = nullptr;
+  uint32_t epoch = 0;
+  int64_t timeout_ns = 10000000000LL;
+  void* last_stream = nullptr;
+  bool launched = false;
+};
+
+// chunk c of an m-byte shard split in Q chunks starts at floor(c*m/Q)
+inline int64_t chunk_off(int64_t c, int64_t m, int64_t Q) {
+  return (int64_t)(((__int128)c * m) / Q);
+}
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+
+// CTA work split shared by host (flag lists) and device (copy ranges)
+A2A_HD int64_t cta_lo(int64_t B, int c, int nC) {
+  if (c >= nC) return B;
+  int64_t x = (int64_t)(((__int128)B * c) / nC);
+  return x & ~(int64_t)63;
+}
+
+}  // namespace a2a
+
+struct a2a_plan {
+  a2a::Plan p;
+};

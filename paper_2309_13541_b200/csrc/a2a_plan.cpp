@@ -1,0 +1,410 @@
+// Host plan builder: validation, scratch layout and per-GPU copy tables.
+//
+// Validation restates the reference executor
+//   a2aflow.evaluate.replay_timestep_schedule  (pkg/src/a2aflow/evaluate.py:56-127)
+// with holdings kept as interval sets instead of Python sets of chunk ids:
+//   * ops grouped by t in list order; t outside [0, nsteps) ignored (:82-90)
+//   * per op, against holdings as of the start of the step (:91-100):
+//       non-edge   -> "step {t}: no link {src}->{dst}"
+//       un-held    -> "step {t}: node {src} sends chunk {c} of shard ({s},{d}) it does not hold"
+//   * arrivals applied after the step's checks; holdings only grow (:108-113)
+//   * final scan s, d, c ascending (:114-126):
+//       "shard ({s},{d}) chunk {c} never delivered" / "... delivered {k} times"
+// The same holdings, mapped to byte locations (send at s, recv at d, scratch
+// elsewhere), resolve every op's source and destination address.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <new>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "a2a_internal.h"
+
+namespace a2a {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+namespace {
+
+// Sorted, disjoint, non-adjacent chunk intervals.
+struct IntervalSet {
+  std::vector<std::pair<int32_t, int32_t>> iv;
+
+  // first chunk of [c0, c1) not covered, or INT32_MIN if all covered
+  int64_t first_missing(int64_t c0, int64_t c1) const {
+    if (c0 >= c1) return INT64_MIN;
+    auto it = std::upper_bound(iv.begin(), iv.end(), std::make_pair((int32_t)c0, INT32_MAX));
+    if (it == iv.begin()) return c0;
+    --it;
+    if (it->second <= c0) return c0;
+    if (it->second >= c1) return INT64_MIN;
+    return it->second;
+  }
+
+  void add(int32_t a, int32_t b) {
+    if (a >= b) return;
+    std::vector<std::pair<int32_t, int32_t>> out;
+    out.reserve(iv.size() + 1);
+    bool placed = false;
+    for (auto& x : iv) {
+      if (x.second < a) {
+        out.push_back(x);
+      } else if (b < x.first) {
+        if (!placed) { out.emplace_back(a, b); placed = true; }
+        out.push_back(x);
+      } else {  // overlap or adjacency: merge
+        a = std::min(a, x.first);
+        b = std::max(b, x.second);
+      }
+    }
+    if (!placed) out.emplace_back(a, b);
+    iv.swap(out);
+  }
+};
+
+inline uint64_t key3(int64_t v, int64_t s, int64_t d, int64_t n) {
+  return (uint64_t)((v * n + s) * n + d);
+}
+
+std::string fmt_missing(int t, int src, int64_t c, int s, int d) {
+  char buf[256];
+  snprintf(buf, sizeof buf, "step %d: node %d sends chunk %lld of shard (%d,%d) it does not hold",
+           t, src, (long long)c, s, d);
+  return buf;
+}
+
+}  // namespace
+
+static int build_plan(Plan& P, const a2a_schedule_desc* D) {
+  if (!D) return fail(A2A_ERR_INVALID, "null descriptor");
+  if (D->n_nodes < 1) return fail(A2A_ERR_INVALID, "n_nodes must be >= 1");
+  if (D->n_steps < 0) return fail(A2A_ERR_INVALID, "n_steps must be >= 0");
+  if (D->q < 1) return fail(A2A_ERR_INVALID, "q must be >= 1");
+  if (D->m_bytes < 0) return fail(A2A_ERR_INVALID, "m_bytes must be >= 0");
+  if (D->n_edges < 0 || (D->n_edges > 0 && !D->edge_uv))
+    return fail(A2A_ERR_INVALID, "bad edge list");
+  if (D->n_ops < 0 || (D->n_ops > 0 && !D->ops)) return fail(A2A_ERR_INVALID, "bad op list");
+  if (D->n_gpus < 1 || D->n_gpus > A2A_MAX_GPUS)
+    return fail(A2A_ERR_INVALID, "n_gpus must be in [1, 8]");
+  const int n = D->n_nodes, T = D->n_steps, E = D->n_edges, G = D->n_gpus;
+  const int64_t Q = D->q, m = D->m_bytes;
+  P.n = n; P.T = T; P.Q = (int32_t)Q; P.E = E; P.G = G; P.m = m; P.flags = D->flags;
+  P.T_exec = std::max(T, 1);
+  P.edge_uv.assign(D->edge_uv, D->edge_uv + 2 * (size_t)E);
+  P.cap.resize(E, 1.0);
+  if (D->edge_cap) P.cap.assign(D->edge_cap, D->edge_cap + E);
+  P.ops.assign(D->ops, D->ops + D->n_ops);
+  P.node_gpu.assign(n, 0);
+  if (D->node_gpu) {
+    for (int v = 0; v < n; ++v) {
+      if (D->node_gpu[v] < 0 || D->node_gpu[v] >= G)
+        return fail(A2A_ERR_INVALID, "node_gpu entry out of range");
+      P.node_gpu[v] = D->node_gpu[v];
+    }
+  }
+  // edge index (Digraph.edge_index, reference src/graphs.py:84-86)
+  std::unordered_map<uint64_t, int32_t> eidx;
+  eidx.reserve(E * 2 + 1);
+  for (int e = 0; e < E; ++e) {
+    int u = P.edge_uv[2 * e], v = P.edge_uv[2 * e + 1];
+    if (u < 0 || u >= n || v < 0 || v >= n) return fail(A2A_ERR_INVALID, "edge endpoint out of range");
+    eidx[((uint64_t)(uint32_t)u << 32) | (uint32_t)v] = e;
+  }
+  auto edge_of = [&](int32_t u, int32_t v) -> int32_t {
+    auto it = eidx.find(((uint64_t)(uint32_t)u << 32) | (uint32_t)v);
+    return it == eidx.end() ? -1 : it->second;
+  };
+  // group by step in list order (evaluate.py:82-84); out-of-range t ignored
+  P.step_ops.assign(T, {});
+  for (int64_t i = 0; i < (int64_t)P.ops.size(); ++i) {
+    int t = P.ops[i].t;
+    if (t >= 0 && t < T) P.step_ops[t].push_back(i);
+  }
+
+  // ---- replay: holdings as interval sets
+  std::unordered_map<uint64_t, IntervalSet> held;     // (v,s,d), v != s (s holds all implicitly)
+  std::unordered_map<uint64_t, IntervalSet> written;  // (v,s,d), v != d: scratch contents
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> delivered((size_t)n * n);
+  auto in_range = [&](int x) { return x >= 0 && x < n; };
+  auto first_missing = [&](const a2a_op& o) -> int64_t {
+    if (o.c0 >= o.c1) return INT64_MIN;
+    if (!in_range(o.s) || !in_range(o.d)) return o.c0;
+    if (o.src == o.s && o.s != o.d) {  // initial holdings {0..Q-1} (evaluate.py:76-80)
+      if (o.c0 < 0) return o.c0;
+      if (o.c1 > Q) return std::max<int64_t>(o.c0, Q);
+      return INT64_MIN;
+    }
+    auto it = held.find(key3(o.src, o.s, o.d, n));
+    if (it == held.end()) return o.c0;
+    return it->second.first_missing(o.c0, o.c1);
+  };
+  for (int t = 0; t < T; ++t) {
+    for (int64_t i : P.step_ops[t]) {
+      const a2a_op& o = P.ops[i];
+      if (edge_of(o.src, o.dst) < 0) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "step %d: no link %d->%d", t, o.src, o.dst);
+        return fail(A2A_ERR_EVAL, buf);
+      }
+      int64_t c = first_missing(o);
+      if (c != INT64_MIN) return fail(A2A_ERR_EVAL, fmt_missing(t, o.src, c, o.s, o.d));
+    }
+    for (int64_t i : P.step_ops[t]) {
+      const a2a_op& o = P.ops[i];
+      if (o.c0 >= o.c1) continue;
+      if (o.dst != o.s) held[key3(o.dst, o.s, o.d, n)].add(o.c0, o.c1);
+      if (o.dst != o.d) written[key3(o.dst, o.s, o.d, n)].add(o.c0, o.c1);
+      if (o.dst == o.d) delivered[(size_t)o.s * n + o.d].emplace_back(o.c0, o.c1);
+    }
+  }
+  // transpose check (evaluate.py:114-126)
+  for (int s = 0; s < n; ++s) {
+    for (int d = 0; d < n; ++d) {
+      if (s == d) continue;
+      auto& dl = delivered[(size_t)s * n + d];
+      // sweep: coverage count per chunk, first chunk with count != 1
+      std::vector<std::pair<int64_t, int>> ev;
+      ev.reserve(dl.size() * 2);
+      for (auto& x : dl) { ev.emplace_back(x.first, +1); ev.emplace_back(x.second, -1); }
+      std::sort(ev.begin(), ev.end());
+      int64_t pos = 0;
+      int cover = 0;
+      size_t k = 0;
+      while (pos < Q) {
+        while (k < ev.size() && ev[k].first <= pos) { cover += ev[k].second; ++k; }
+        if (cover != 1) {
+          char buf[160];
+          if (cover == 0)
+            snprintf(buf, sizeof buf, "shard (%d,%d) chunk %lld never delivered", s, d, (long long)pos);
+          else
+            snprintf(buf, sizeof buf, "shard (%d,%d) chunk %lld delivered %d times", s, d,
+                     (long long)pos, cover);
+          return fail(A2A_ERR_EVAL, buf);
+        }
+        pos = (k < ev.size()) ? std::min<int64_t>(ev[k].first, Q) : Q;
+      }
+    }
+  }
+
+  // ---- placement: local node index per GPU
+  P.local_idx.assign(n, 0);
+  P.info.assign(G, a2a_gpu_info{});
+  for (int g = 0; g < G; ++g) P.info[g].first_node = -1;
+  for (int v = 0; v < n; ++v) {
+    auto& I = P.info[P.node_gpu[v]];
+    if (I.first_node < 0) I.first_node = v;
+    P.local_idx[v] = I.n_local_nodes++;
+  }
+  for (int g = 0; g < G; ++g) {
+    P.info[g].send_bytes = (int64_t)P.info[g].n_local_nodes * n * m;
+    P.info[g].recv_bytes = P.info[g].send_bytes;
+  }
+
+  // ---- scratch layout: per (v,s,d) the merged intervals ever written there.
+  // A slot starts at the same residue mod 64 as the shard offset of its first
+  // chunk, so every copy has src == dst (mod 64) whenever m % 64 == 0.
+  std::vector<uint64_t> keys;
+  keys.reserve(written.size());
+  for (auto& kv : written) keys.push_back(kv.first);
+  std::sort(keys.begin(), keys.end());  // deterministic across ranks
+  std::unordered_map<uint64_t, std::vector<Interval>> slots;
+  slots.reserve(keys.size() * 2 + 1);
+  std::vector<int64_t> cursor(G, 0);
+  for (uint64_t k : keys) {
+    int v = (int)(k / ((uint64_t)n * n));
+    int g = P.node_gpu[v];
+    auto& out = slots[k];
+    for (auto& x : written[k].iv) {
+      int64_t lo = chunk_off(x.first, m, Q), hi = chunk_off(x.second, m, Q);
+      int64_t base = ((cursor[g] + 63) & ~(int64_t)63) + (lo & 63);
+      out.push_back(Interval{x.first, x.second, base});
+      cursor[g] = base + (hi - lo);
+    }
+  }
+  for (int g = 0; g < G; ++g) P.info[g].scratch_bytes = (cursor[g] + 4095) & ~(int64_t)4095;
+  auto slot_addr = [&](int v, int s, int d, int32_t c0, int64_t byte_lo, int64_t* out) -> bool {
+    auto it = slots.find(key3(v, s, d, n));
+    if (it == slots.end()) return false;
+    for (auto& x : it->second)
+      if (x.a <= c0 && c0 < x.b) {
+        *out = x.base + (byte_lo - chunk_off(x.a, m, Q));
+        return true;
+      }
+    return false;
+  };
+
+  // ---- copy items per GPU per step
+  const int TE = P.T_exec;
+  P.tables.assign(G, GpuTables{});
+  P.link_bytes.assign((size_t)T * E, 0);
+  std::vector<std::vector<std::vector<DevItem>>> per(G, std::vector<std::vector<DevItem>>(TE));
+  for (int t = 0; t < T; ++t) {
+    for (int64_t i : P.step_ops[t]) {
+      const a2a_op& o = P.ops[i];
+      if (o.c0 >= o.c1) continue;
+      int64_t lo = chunk_off(o.c0, m, Q), hi = chunk_off(o.c1, m, Q);
+      int e = edge_of(o.src, o.dst);
+      P.link_bytes[(size_t)t * E + e] += hi - lo;
+      if (hi == lo) continue;
+      int g = P.node_gpu[o.src], h = P.node_gpu[o.dst];
+      DevItem it{};
+      it.nbytes = hi - lo;
+      it.edge = e;
+      it.dst_gpu = h;
+      if (o.src == o.s) {
+        it.src_loc = loc_send();
+        it.src_off = ((int64_t)P.local_idx[o.src] * n + o.d) * m + lo;
+      } else if (o.src == o.d) {
+        it.src_loc = loc_recv(g);
+        it.src_off = ((int64_t)P.local_idx[o.src] * n + o.s) * m + lo;
+      } else {
+        it.src_loc = loc_scratch(g, G);
+        if (!slot_addr(o.src, o.s, o.d, o.c0, lo, &it.src_off))
+          return fail(A2A_ERR_INVALID, "internal: source chunk has no scratch slot");
+      }
+      if (o.dst == o.d) {
+        it.dst_loc = loc_recv(h);
+        it.dst_off = ((int64_t)P.local_idx[o.dst] * n + o.s) * m + lo;
+      } else {
+        it.dst_loc = loc_scratch(h, G);
+        if (!slot_addr(o.dst, o.s, o.d, o.c0, lo, &it.dst_off))
+          return fail(A2A_ERR_INVALID, "internal: destination chunk has no scratch slot");
+      }
+      per[g][t].push_back(it);
+      auto& Ig = P.info[g];
+      Ig.hop_bytes += it.nbytes;
+      if (h != g) {
+        Ig.egress_bytes += it.nbytes;
+        P.info[h].ingress_bytes += it.nbytes;
+      } else {
+        Ig.local_bytes += it.nbytes;
+      }
+    }
+  }
+  if ((P.flags & A2A_COPY_SELF) && m > 0) {
+    for (int v = 0; v < n; ++v) {
+      int g = P.node_gpu[v];
+      DevItem it{};
+      it.src_loc = loc_send();
+      it.dst_loc = loc_recv(g);
+      it.src_off = it.dst_off = ((int64_t)P.local_idx[v] * n + v) * m;
+      it.nbytes = m;
+      it.edge = -1;
+      it.dst_gpu = g;
+      per[g][0].push_back(it);
+      P.info[g].local_bytes += m;
+    }
+  }
+  // order each (gpu, step) list by destination GPU (stable): CTAs then cover
+  // few destinations each (fewer flags) while all destinations stay busy.
+  for (int g = 0; g < G; ++g) {
+    auto& tb = P.tables[g];
+    tb.step_begin.assign(TE + 1, 0);
+    tb.step_bytes.assign(TE, 0);
+    for (int t = 0; t < TE; ++t) {
+      auto& L = per[g][t];
+      std::stable_sort(L.begin(), L.end(), [&](const DevItem& a, const DevItem& b) {
+        int ka = (a.dst_gpu - g + G) % G, kb = (b.dst_gpu - g + G) % G;
+        return ka < kb;
+      });
+      tb.step_begin[t] = (int64_t)tb.items.size();
+      int64_t pre = 0;
+      for (auto& it : L) {
+        it.prefix = pre;
+        pre += it.nbytes;
+        tb.items.push_back(it);
+      }
+      tb.step_bytes[t] = pre;
+    }
+    tb.step_begin[TE] = (int64_t)tb.items.size();
+    P.info[g].n_items = (int64_t)tb.items.size();
+  }
+  return A2A_OK;
+}
+
+}  // namespace a2a
+
+using namespace a2a;
+
+extern "C" {
+
+const char* a2a_last_error(void) { return g_last_error.c_str(); }
+const char* a2a_version(void) { return "b200-a2a 0.1.0 (sm_100a)"; }
+
+int a2a_plan_create(const a2a_schedule_desc* desc, a2a_plan** out) {
+  if (!out) return fail(A2A_ERR_INVALID, "null output pointer");
+  *out = nullptr;
+  a2a_plan* plan = new (std::nothrow) a2a_plan();
+  if (!plan) return fail(A2A_ERR_NOMEM, "out of host memory");
+  int rc;
+  try {
+    rc = build_plan(plan->p, desc);
+  } catch (const std::bad_alloc&) {
+    rc = fail(A2A_ERR_NOMEM, "out of host memory building the plan");
+  } catch (...) {
+    rc = fail(A2A_ERR_INVALID, "internal error building the plan");
+  }
+  if (rc != A2A_OK) {
+    delete plan;
+    return rc;
+  }
+  g_last_error.clear();
+  *out = plan;
+  return A2A_OK;
+}
+
+int a2a_plan_model_time(const a2a_plan* plan, double m, double b, double sync_latency,
+                        double* out_T) {
+  if (!plan || !out_T) return fail(A2A_ERR_INVALID, "null argument");
+  const Plan& P = plan->p;
+  // evaluate.py:74, :88-107 — same float operations in the same order
+  const double chunk_bytes = m / (double)P.Q;
+  std::vector<double> lb(P.E, 0.0);
+  std::vector<char> used(P.E, 0);
+  std::unordered_map<uint64_t, int32_t> eidx;
+  for (int e = 0; e < P.E; ++e)
+    eidx[((uint64_t)(uint32_t)P.edge_uv[2 * e] << 32) | (uint32_t)P.edge_uv[2 * e + 1]] = e;
+  double T = 0.0;
+  for (int t = 0; t < P.T; ++t) {
+    std::vector<int32_t> touched;
+    for (int64_t i : P.step_ops[t]) {
+      const a2a_op& o = P.ops[i];
+      int e = eidx[((uint64_t)(uint32_t)o.src << 32) | (uint32_t)o.dst];
+      if (!used[e]) { used[e] = 1; lb[e] = 0.0; touched.push_back(e); }
+      lb[e] += (double)(o.c1 - o.c0) * chunk_bytes;
+    }
+    double step = 0.0;
+    for (int e : touched) {
+      double x = lb[e] / (P.cap[e] * b);
+      if (x > step) step = x;
+      used[e] = 0;
+    }
+    T += step + sync_latency;
+  }
+  *out_T = T;
+  return A2A_OK;
+}
+
+int a2a_plan_link_bytes(const a2a_plan* plan, int64_t* out) {
+  if (!plan || !out) return fail(A2A_ERR_INVALID, "null argument");
+  std::memcpy(out, plan->p.link_bytes.data(), plan->p.link_bytes.size() * sizeof(int64_t));
+  return A2A_OK;
+}
+
+int a2a_plan_gpu_info(const a2a_plan* plan, int32_t gpu, a2a_gpu_info* out) {
+  if (!plan || !out) return fail(A2A_ERR_INVALID, "null argument");
+  if (gpu < 0 || gpu >= plan->p.G) return fail(A2A_ERR_INVALID, "gpu out of range");
+  *out = plan->p.info[gpu];
+  return A2A_OK;
+}
+
+}  // extern "C"

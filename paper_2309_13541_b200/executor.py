@@ -1,0 +1,282 @@
+"""Host-side mirror of the reference executor interface.
+
+Reference slot: ``a2aflow.evaluate.replay_timestep_schedule(g, sched, m=1.0,
+b=1.0, sync_latency=0.0) -> (T, True)`` raising ``EvalError``
+(pkg/src/a2aflow/evaluate.py:30-31, :56-127).  This module keeps that shape:
+
+* ``replay_timestep_schedule(g, sched, m, b, sync_latency)`` — same signature,
+  same result, same error texts; validation and the modelled T are computed by
+  the native plan builder (csrc/a2a_plan.cpp) instead of Python sets.
+* ``execute_timestep_schedule(g, sched, send, recv, ...) -> (T_measured, True)``
+  — the byte-moving B200 execution of the same schedule on one GPU.
+* ``Plan`` — the reusable handle (validate once, bind to a GPU, execute many
+  times; multi-GPU via CUDA IPC handles, see ``dist.py``).
+
+Everything accepts the reference's own ``Digraph`` / ``ChunkedSchedule``
+objects as well as this package's mirrors (duck typing on ``n``, ``edges``,
+``nsteps``, ``Q``, ``mode``, ``instructions``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+
+__all__ = ["EvalError", "ExecutorError", "Plan", "replay_timestep_schedule",
+           "execute_timestep_schedule", "contiguous_placement"]
+
+
+class EvalError(RuntimeError):
+    """A schedule the reference replay would reject; same messages
+    (reference pkg/src/a2aflow/evaluate.py:30-31)."""
+
+
+class ExecutorError(RuntimeError):
+    """Device-side failure: CUDA error, flag-wait timeout, bad call order."""
+
+
+def _raise(rc: int, what: str):
+    msg = N.lib.a2a_last_error().decode()
+    if rc == 2:
+        raise EvalError(msg)
+    if rc == 1:
+        raise ValueError(f"{what}: {msg}")
+    raise ExecutorError(f"{what}: [{N.STATUS.get(rc, rc)}] {msg}")
+
+
+def contiguous_placement(n: int, n_gpus: int) -> list:
+    """Virtual node v -> GPU v*G//n: contiguous blocks (u // (N/G) when G | N),
+    i.e. subcubes for the hypercube and 1x2x4 slabs for the 4x4x4 torus."""
+    return [v * n_gpus // n for v in range(n)]
+
+
+def _ops_array(instructions) -> np.ndarray:
+    if isinstance(instructions, np.ndarray):
+        return np.ascontiguousarray(instructions, dtype=np.int32).reshape(-1, 7)
+    arr = np.fromiter((x for i in instructions
+                       for x in (i.t, i.src, i.dst, i.s, i.d, i.c0, i.c1)),
+                      dtype=np.int64, count=7 * len(instructions))
+    if arr.size and (arr.min() < -2**31 or arr.max() >= 2**31):
+        raise ValueError("instruction field does not fit int32")
+    return arr.astype(np.int32).reshape(-1, 7)
+
+
+def _check_mode(g, sched):
+    # evaluate.py:70-73
+    if sched.mode != "ts":
+        raise EvalError("replay_timestep_schedule expects a ts-mode schedule")
+    if g.n != sched.n:
+        raise EvalError(f"graph has {g.n} nodes, schedule says {sched.n}")
+
+
+class Plan:
+    """Validated, laid-out execution plan of one ts schedule at shard size m."""
+
+    def __init__(self, g, sched, m: int, placement=None, n_gpus: int = 1,
+                 copy_self: bool = True, ops: np.ndarray | None = None):
+        _check_mode(g, sched)
+        if int(m) != m or m < 0:
+            raise ValueError(f"shard size m must be a non-negative integer, got {m}")
+        self.n, self.nsteps, self.Q, self.m = g.n, sched.nsteps, sched.Q, int(m)
+        self.n_gpus = int(n_gpus)
+        self.E = len(g.edges)
+        self._edge_uv = np.ascontiguousarray(
+            [(u, v) for u, v, _ in g.edges], dtype=np.int32).reshape(-1, 2)
+        self._cap = np.ascontiguousarray([c for _, _, c in g.edges], dtype=np.float64)
+        self._ops = _ops_array(sched.instructions if ops is None else ops)
+        if placement is None:
+            placement = contiguous_placement(self.n, self.n_gpus)
+        self.placement = np.ascontiguousarray(placement, dtype=np.int32)
+        if self.placement.shape != (self.n,):
+            raise ValueError("placement must list one GPU per node")
+        d = N.ScheduleDesc()
+        d.n_nodes, d.n_steps, d.q, d.n_edges = self.n, self.nsteps, self.Q, self.E
+        d.m_bytes = self.m
+        d.edge_uv = self._edge_uv.ctypes.data_as(C.POINTER(C.c_int32))
+        d.edge_cap = self._cap.ctypes.data_as(C.POINTER(C.c_double))
+        d.ops = self._ops.ctypes.data_as(C.POINTER(N.A2AOp))
+        d.n_ops = self._ops.shape[0]
+        d.node_gpu = self.placement.ctypes.data_as(C.POINTER(C.c_int32))
+        d.n_gpus = self.n_gpus
+        d.flags = N.A2A_COPY_SELF if copy_self else 0
+        h = C.c_void_p()
+        rc = N.lib.a2a_plan_create(C.byref(d), C.byref(h))
+        if rc:
+            _raise(rc, "a2a_plan_create")
+        self._h = h
+        self.rank = None
+        self.device = None
+
+    # ---- lifetime
+    def close(self):
+        if getattr(self, "_h", None):
+            N.lib.a2a_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def _ck(self, rc, what):
+        if rc:
+            _raise(rc, what)
+
+    # ---- host-side queries
+    def model_time(self, m: float | None = None, b: float = 1.0,
+                   sync_latency: float = 0.0) -> float:
+        """replay_timestep_schedule's T for (m, b, sync) — bit-identical."""
+        out = C.c_double()
+        self._ck(N.lib.a2a_plan_model_time(self._h, float(self.m if m is None else m),
+                                           float(b), float(sync_latency), C.byref(out)),
+                 "a2a_plan_model_time")
+        return out.value
+
+    def link_bytes(self) -> np.ndarray:
+        """Schedule bytes per (step, edge id), int64 [nsteps, E]."""
+        out = np.zeros((self.nsteps, self.E), dtype=np.int64)
+        self._ck(N.lib.a2a_plan_link_bytes(self._h, out.ctypes.data_as(C.POINTER(C.c_int64))),
+                 "a2a_plan_link_bytes")
+        return out
+
+    def gpu_info(self, gpu: int) -> dict:
+        info = N.GpuInfo()
+        self._ck(N.lib.a2a_plan_gpu_info(self._h, int(gpu), C.byref(info)), "a2a_plan_gpu_info")
+        return {f: getattr(info, f) for f, _ in N.GpuInfo._fields_}
+
+    # ---- device side
+    def bind(self, gpu: int = 0, device: int | None = None, num_ctas: int = 0):
+        device = gpu if device is None else device
+        self._ck(N.lib.a2a_plan_bind(self._h, int(gpu), int(device), int(num_ctas)),
+                 "a2a_plan_bind")
+        self.rank, self.device = int(gpu), int(device)
+        return self
+
+    def export_handle(self) -> bytes:
+        buf = C.create_string_buffer(64)
+        self._ck(N.lib.a2a_plan_export_handle(self._h, buf), "a2a_plan_export_handle")
+        return buf.raw
+
+    def import_handles(self, handles):
+        blob = b"".join(bytes(h) for h in handles)
+        if len(blob) != 64 * self.n_gpus:
+            raise ValueError("need one 64-byte handle per GPU")
+        buf = C.create_string_buffer(blob, len(blob))
+        self._ck(N.lib.a2a_plan_import_handles(self._h, buf), "a2a_plan_import_handles")
+
+    def arena_ptr(self) -> int:
+        p = C.c_void_p()
+        self._ck(N.lib.a2a_plan_arena(self._h, C.byref(p)), "a2a_plan_arena")
+        return p.value
+
+    def import_pointers(self, ptrs):
+        arr = (C.c_void_p * self.n_gpus)(*ptrs)
+        self._ck(N.lib.a2a_plan_import_pointers(self._h, arr), "a2a_plan_import_pointers")
+
+    def recv_buffer(self):
+        """torch uint8 view [V_g, N, m] of this rank's arena recv buffer."""
+        import torch
+        p = C.c_void_p()
+        self._ck(N.lib.a2a_plan_recv_buffer(self._h, C.byref(p)), "a2a_plan_recv_buffer")
+        V = self.gpu_info(self.rank)["n_local_nodes"]
+        return _device_tensor(p.value, (V, self.n, self.m), self.device, torch)
+
+    def set_timeout(self, seconds: float):
+        self._ck(N.lib.a2a_plan_set_timeout(self._h, int(seconds * 1e9)), "a2a_plan_set_timeout")
+
+    def execute(self, send, recv=None, stream=None, count_links: bool = False):
+        """Launch one all-to-all (asynchronous on ``stream``)."""
+        import torch
+        info = self.gpu_info(self.rank)
+        _check_buf(send, info["send_bytes"], self.device, "send", torch)
+        rp = None
+        if recv is not None:
+            _check_buf(recv, info["recv_bytes"], self.device, "recv", torch)
+            rp = recv.data_ptr()
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        self._ck(N.lib.a2a_plan_execute(
+            self._h, C.c_void_p(send.data_ptr()), C.c_void_p(rp), C.c_void_p(sp),
+            N.A2A_EXEC_COUNT_LINKS if count_links else 0), "a2a_plan_execute")
+
+    def sync(self):
+        self._ck(N.lib.a2a_plan_sync(self._h), "a2a_plan_sync")
+
+    def read_link_counters(self) -> np.ndarray:
+        """Device-counted bytes per (step, edge) this rank moved since the last read."""
+        out = np.zeros((self.nsteps, self.E), dtype=np.int64)
+        self._ck(N.lib.a2a_plan_read_link_counters(
+            self._h, out.ctypes.data_as(C.POINTER(C.c_int64))), "a2a_plan_read_link_counters")
+        return out
+
+
+class _CAI:
+    def __init__(self, ptr, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "|u1",
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None}
+
+
+def _device_tensor(ptr, shape, device, torch):
+    with torch.cuda.device(device):
+        return torch.as_tensor(_CAI(ptr, shape), device=f"cuda:{device}")
+
+
+def _check_buf(t, nbytes, device, name, torch):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.device.index != device:
+        raise ValueError(f"{name} is on {t.device}, plan is bound to cuda:{device}")
+    if t.dtype != torch.uint8 or not t.is_contiguous():
+        raise TypeError(f"{name} must be a contiguous uint8 tensor")
+    if t.numel() != nbytes:
+        raise ValueError(f"{name} has {t.numel()} bytes, plan needs {nbytes}")
+
+
+def replay_timestep_schedule(g, sched, m: float = 1.0, b: float = 1.0,
+                             sync_latency: float = 0.0):
+    """Drop-in for the reference's symbolic replay: (T, True) or EvalError.
+
+    Same validation order and messages and a bit-identical T
+    (evaluate.py:56-127), computed natively; no GPU needed.
+    """
+    with Plan(g, sched, m=0, copy_self=False) as p:
+        return p.model_time(m=m, b=b, sync_latency=sync_latency), True
+
+
+def execute_timestep_schedule(g, sched, send, recv=None, num_ctas: int = 0,
+                              copy_self: bool = True):
+    """Execute the schedule on real bytes on one GPU: (T_seconds, True).
+
+    send: CUDA uint8 tensor [N, N, m] (send[s, d] = shard (s, d));
+    recv: same shape (allocated if None), recv[d, s] = shard (s, d) after the
+    call.  T is the measured device time of the all-to-all (CUDA events).
+    """
+    import torch
+    n = g.n
+    if send.numel() % (n * n):
+        raise ValueError("send must hold N*N shards")
+    m = send.numel() // (n * n)
+    if recv is None:
+        recv = torch.empty_like(send)
+    with Plan(g, sched, m=m, copy_self=copy_self) as p:
+        p.bind(0, device=send.device.index, num_ctas=num_ctas)
+        stream = torch.cuda.current_stream(send.device)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        p.execute(send, recv, stream=stream)
+        e1.record(stream)
+        p.sync()
+        e1.synchronize()
+        return e0.elapsed_time(e1) / 1e3, True

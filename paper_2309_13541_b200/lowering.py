@@ -1,0 +1,115 @@
+"""Drop-in-side lowering helpers the reference does not have.
+
+``compile_path_schedule`` (reference src/schedule.py:244-312) emits a
+``mode="path"`` schedule: one instruction per route, ``dst`` = route id,
+``nsteps = 1``.  The reference replay only accepts ``mode="ts"``
+(src/evaluate.py:70-71).  The executor runs the paper's hop-by-hop semantics
+("copy it from the source buffer of v1 to the scratch buffer of
+v2, then ... v3 and so on"): hop i of every route at step i.  The result is a
+legal ts schedule that the reference replay accepts unchanged.
+
+For the host-augmented ("without extra NIC-forwarding bandwidth") lowering
+(src/graphs.py:447-475), routes live on augmented ids host=3v, nic_in=3v+1,
+nic_out=3v+2 and must be collapsed to physical node sequences first.
+"""
+from __future__ import annotations
+
+from .schedule import ChunkedSchedule, Instruction, ScheduleError
+
+__all__ = ["lower_path_to_steps", "collapse_aug_routes", "collapse_aug_schedule",
+           "schedule_link_chunks", "hop_histogram"]
+
+
+def _ts_key(i):
+    # the ts sort key of reference src/schedule.py:237
+    return (i.t, i.src, i.dst, i.s, i.d, i.c0)
+
+
+def lower_path_to_steps(routes, sched, n: int | None = None) -> ChunkedSchedule:
+    """Expand each route instruction into one hop-op per link, hop i at step i.
+
+    ``routes`` is the route list returned by compile_path_schedule (or its
+    ``.routes.json`` sidecar); ``sched`` the ``mode="path"`` schedule.
+    """
+    if sched.mode != "path":
+        raise ScheduleError(f"expected a path-mode schedule, got {sched.mode!r}")
+    ops = []
+    nsteps = 0
+    for ins in sched.instructions:
+        if not 0 <= ins.dst < len(routes):
+            raise ScheduleError(f"route id {ins.dst} out of range")
+        r = routes[ins.dst]
+        nodes = list(r["nodes"])
+        if (r["s"], r["d"]) != (ins.s, ins.d) or nodes[0] != ins.s or nodes[-1] != ins.d:
+            raise ScheduleError(
+                f"route {ins.dst} {nodes} does not join shard ({ins.s},{ins.d})")
+        if len(nodes) < 2:
+            raise ScheduleError(f"route {ins.dst} has no hops")
+        for i in range(len(nodes) - 1):
+            ops.append(Instruction(t=i, src=nodes[i], dst=nodes[i + 1],
+                                   s=ins.s, d=ins.d, c0=ins.c0, c1=ins.c1))
+        nsteps = max(nsteps, len(nodes) - 1)
+    ops.sort(key=_ts_key)
+    return ChunkedSchedule(n=sched.n if n is None else n, nsteps=nsteps,
+                           chunk_bytes=sched.chunk_bytes, Q=sched.Q, mode="ts",
+                           instructions=ops)
+
+
+def _phys_of(mapping):
+    phys = {}
+    for v, (h, a, b) in enumerate(zip(mapping.host, mapping.nic_in, mapping.nic_out)):
+        phys[h] = phys[a] = phys[b] = v
+    return phys
+
+
+def collapse_aug_routes(routes, mapping) -> list:
+    """Map augmented node ids to physical nodes and drop repeats.
+
+    host_u -> nic_out_u -> nic_in_v -> host_v collapses to the physical hop
+    u -> v.  A simple augmented path visits each host at most once, so the
+    collapsed sequence is simple.
+    """
+    phys = _phys_of(mapping)
+    out = []
+    for r in routes:
+        seq = []
+        for x in r["nodes"]:
+            v = phys[x]
+            if not seq or seq[-1] != v:
+                seq.append(v)
+        if len(set(seq)) != len(seq):
+            raise ScheduleError(f"collapsed route {seq} is not simple")
+        out.append({"s": phys[r["s"]], "d": phys[r["d"]], "nodes": seq})
+    return out
+
+
+def collapse_aug_schedule(routes, sched, mapping):
+    """(physical routes, physical path schedule) for an augmented lowering."""
+    phys = _phys_of(mapping)
+    routes_p = collapse_aug_routes(routes, mapping)
+    ins = [Instruction(t=i.t, src=phys[i.src], dst=i.dst, s=phys[i.s], d=phys[i.d],
+                       c0=i.c0, c1=i.c1) for i in sched.instructions]
+    sp = ChunkedSchedule(n=len(mapping.host), nsteps=sched.nsteps,
+                         chunk_bytes=sched.chunk_bytes, Q=sched.Q, mode="path",
+                         instructions=ins)
+    return routes_p, sp
+
+
+def schedule_link_chunks(sched, g) -> dict:
+    """{(t, edge id): chunks} of a ts schedule (what the executor must move)."""
+    eidx = g.edge_index
+    out: dict = {}
+    for i in sched.instructions:
+        if 0 <= i.t < sched.nsteps and i.c1 > i.c0:
+            k = (i.t, eidx[(i.src, i.dst)])
+            out[k] = out.get(k, 0) + (i.c1 - i.c0)
+    return out
+
+
+def hop_histogram(sched) -> list:
+    """Hop-ops per step of a ts schedule."""
+    h = [0] * sched.nsteps
+    for i in sched.instructions:
+        if 0 <= i.t < sched.nsteps:
+            h[i.t] += 1
+    return h

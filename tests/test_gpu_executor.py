@@ -1,0 +1,134 @@
+"""GPU parity: the sm_100a executor vs the CPU oracle and the schedule.
+
+Bit-exact receive buffers against oracle/replay_bytes.py (itself pinned to the
+reference replay by tests/test_oracle.py) on every small artifact at several
+shard sizes, including sizes that break 16-byte alignment; device-counted
+per-(step, link) bytes equal to the plan's schedule bytes; at full sizes the
+size-independent transpose property recv[d][s] == send[s][d].
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+SMALL = ["torus2x4", "hypercube3", "gk8_2", "torus2x4_h1", "torus2x4_h2", "gk8_2_h1",
+         "ts_ring3", "ts_torus2x4", "ts_hypercube3", "ts_gk8_2", "ts_torus3x3"]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    yield
+    torch.cuda.synchronize()
+
+
+def _send(n, m, seed=0):
+    from replay_bytes import make_send
+    return make_send(n, m, seed=seed)
+
+
+@pytest.mark.parametrize("name", SMALL)
+@pytest.mark.parametrize("m", [1, 7, 1000, 4096, 65536 + 3])
+def test_recv_bit_exact_vs_oracle(name, m, artifacts):
+    from paper_2309_13541_b200.executor import execute_timestep_schedule
+    from replay_bytes import replay_bytes
+    a = artifacts(name)
+    send = _send(a.g.n, m, seed=m)
+    _, want, _ = replay_bytes(a.g, a.sched, send, m)
+    s = torch.from_numpy(send).cuda()
+    r = torch.zeros_like(s)
+    T, ok = execute_timestep_schedule(a.g, a.sched, s, r)
+    assert ok and T > 0
+    assert np.array_equal(r.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_device_link_counters_equal_schedule(name, artifacts):
+    from paper_2309_13541_b200.executor import Plan
+    from replay_bytes import replay_bytes
+    a = artifacts(name)
+    m = 3 * a.sched.Q + 5
+    send = _send(a.g.n, m)
+    _, _, ob = replay_bytes(a.g, a.sched, send, m)
+    with Plan(a.g, a.sched, m=m) as p:
+        p.bind(0)
+        s = torch.from_numpy(send).cuda()
+        r = torch.empty_like(s)
+        p.execute(s, r, count_links=True)
+        p.sync()
+        dev = p.read_link_counters()
+        want = p.link_bytes()
+    ref = np.zeros_like(want)
+    for (t, e), x in ob.items():
+        ref[t, e] = x
+    assert np.array_equal(want, ref)
+    assert np.array_equal(dev, want)
+
+
+@pytest.mark.parametrize("num_ctas", [1, 3, 64, 0])
+def test_cta_counts_and_repeats(num_ctas, artifacts):
+    """Any grid size gives the same bytes; repeated executes (epochs) stay exact."""
+    from paper_2309_13541_b200.executor import Plan
+    a = artifacts("gk8_2")
+    m = 12345
+    with Plan(a.g, a.sched, m=m) as p:
+        p.bind(0, num_ctas=num_ctas)
+        for seed in range(4):
+            s = torch.from_numpy(_send(a.g.n, m, seed)).cuda()
+            r = torch.zeros_like(s)
+            p.execute(s, r)
+            p.sync()
+            assert torch.equal(r, s.transpose(0, 1).contiguous())
+
+
+@pytest.mark.parametrize("name,m", [("torus4x4x4", 65536), ("gk64_4", 65536 + 48),
+                                    ("gk64_4_h2", 4096), ("torus4x4x4", 1000)])
+def test_n64_transpose_and_counters(name, m, artifacts):
+    from paper_2309_13541_b200.artifacts import list_artifacts
+    from paper_2309_13541_b200.executor import Plan
+    if name not in list_artifacts():
+        pytest.skip(f"artifact {name} not generated")
+    a = artifacts(name)
+    n = a.g.n
+    g = torch.Generator(device="cuda").manual_seed(7)
+    s = torch.randint(0, 256, (n, n, m), dtype=torch.uint8, device="cuda", generator=g)
+    r = torch.zeros_like(s)
+    with Plan(a.g, a.sched, m=m) as p:
+        p.bind(0)
+        p.execute(s, r, count_links=True)
+        p.sync()
+        dev = p.read_link_counters()
+        assert np.array_equal(dev, p.link_bytes())
+    assert torch.equal(r, s.transpose(0, 1).contiguous())
+
+
+def test_full_size_gk8_16mib(artifacts):
+    """configs[1] workload on one GPU: GenKautz(8,2), 16 MiB per pair."""
+    from paper_2309_13541_b200.executor import execute_timestep_schedule
+    a = artifacts("gk8_2")
+    m = 16 << 20
+    g = torch.Generator(device="cuda").manual_seed(1)
+    s = torch.randint(0, 256, (8, 8, m), dtype=torch.uint8, device="cuda", generator=g)
+    r = torch.zeros_like(s)
+    T, ok = execute_timestep_schedule(a.g, a.sched, s, r)
+    assert ok
+    assert torch.equal(r, s.transpose(0, 1).contiguous())
+
+
+def test_execute_rejects_wrong_buffers(artifacts):
+    from paper_2309_13541_b200.executor import Plan
+    a = artifacts("torus2x4")
+    with Plan(a.g, a.sched, m=64) as p:
+        p.bind(0)
+        s = torch.zeros((8, 8, 64), dtype=torch.uint8, device="cuda")
+        with pytest.raises(ValueError):
+            p.execute(s[:, :, :32].contiguous())
+        with pytest.raises(TypeError):
+            p.execute(s.float())
+        with pytest.raises(TypeError):
+            p.execute(s.cpu())
