@@ -295,7 +295,8 @@ def main(argv=None):
         with open(traffic_file) as fh:
             tr = json.load(fh).get(f"{args.config}:{m}:G{G}")
         if tr:
-            roof["traffic"] = tr
+            roof["traffic"] = tr["per_launch_bytes"]
+            roof["traffic_source"] = tr["source"]
 
     # ---- NCCL all_to_all_single on the same bytes (baseline, not the target)
     nccl = None

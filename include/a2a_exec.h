@@ -94,6 +94,18 @@ int a2a_plan_model_time(const a2a_plan* plan, double m, double b, double sync_la
 int a2a_plan_link_bytes(const a2a_plan* plan, int64_t* out);
 int a2a_plan_gpu_info(const a2a_plan* plan, int32_t gpu, a2a_gpu_info* out);
 
+/* CTA work split + exact producer dependency lists for `num_ctas` CTAs per GPU
+ * (host only; a2a_plan_bind calls it).  Stats: flags each GPU acquires in total
+ * and at exit. */
+int a2a_plan_prepare(a2a_plan* plan, int32_t num_ctas);
+int a2a_plan_sync_stats(const a2a_plan* plan, int32_t gpu, int64_t* n_wait, int64_t* n_exit);
+/* Host emulation of the device protocol on host buffers (send[g], recv[g] per GPU
+ * rank, same layout as on the device): CTAs of all GPUs run in a random
+ * interleaving (xorshift `seed`) constrained only by the dependency lists.
+ * Used by the CPU tests to prove the lists are sufficient. */
+int a2a_plan_emulate(a2a_plan* plan, int32_t num_ctas, void* const* send, void* const* recv,
+                     uint64_t seed);
+
 /* ---- device side ---- */
 /* Bind the plan to one GPU: rank `gpu` of the placement on CUDA device
  * `device_ordinal`, with `num_ctas` persistent CTAs (0 = one per SM).  Allocates

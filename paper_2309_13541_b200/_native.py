@@ -59,6 +59,9 @@ def _load():
                                  C.POINTER(C.c_double)], C.c_int),
         "a2a_plan_link_bytes": ([P, C.POINTER(C.c_int64)], C.c_int),
         "a2a_plan_gpu_info": ([P, C.c_int32, C.POINTER(GpuInfo)], C.c_int),
+        "a2a_plan_prepare": ([P, C.c_int32], C.c_int),
+        "a2a_plan_sync_stats": ([P, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], C.c_int),
+        "a2a_plan_emulate": ([P, C.c_int32, C.POINTER(P), C.POINTER(P), C.c_uint64], C.c_int),
         "a2a_plan_bind": ([P, C.c_int32, C.c_int32, C.c_int32], C.c_int),
         "a2a_plan_export_handle": ([P, C.c_void_p], C.c_int),
         "a2a_plan_import_handles": ([P, C.c_void_p], C.c_int),

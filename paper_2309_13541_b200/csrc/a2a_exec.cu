@@ -10,21 +10,22 @@
 // NVSwitch).  The step's bytes are split into one contiguous range per CTA.
 //
 // Ordering (store-and-forward, reference evaluate.py:93-113: a chunk received
-// at step t is forwarded at t+1 at the earliest):
-//   producer GPU g, step t: every CTA with work does bar.sync; fence.sc.sys;
-//       atomicAdd on g's step-t arrival counter.  The CTA that arrives last
-//       fences again and publishes st.release.sys flag[h][t][g] = epoch on
-//       every GPU h that g wrote to in step t (one flag per producer GPU,
-//       not per CTA: consumers poll <= G flags per step).
-//   consumer CTA on GPU h, before its first work of step t+1:
-//       warp 0 polls (ld.acquire.sys, one flag per lane) the producer flags
-//       of the steps it has not acquired yet (host-precomputed lists),
-//       __all_sync, fence, bar.sync
+// at step t is forwarded at t+1 at the earliest) — exact producer dependencies,
+// no step barrier (chunk-pipelined execution):
+//   producer CTA c of GPU g, after its step-t byte range:
+//       bar.sync; fence.sc.sys; st.release.sys flag_h[t][g][c] = epoch on every
+//       GPU h it wrote to in step t
+//   consumer CTA c' of GPU h, before its step-t' range: warp 0 polls
+//       (ld.acquire.sys, one flag per lane, __all_sync) exactly the producer
+//       CTAs that wrote the bytes its pieces read (host-computed from the static
+//       work split: interval overlap of source ranges with earlier writes),
+//       then fence + bar.sync.  Steps therefore overlap: a CTA starts step t+1
+//       as soon as its own inputs exist, not when the whole GPU finished step t.
 //   entry barrier (multi-GPU): every GPU announces the epoch to all peers and
 //       waits for theirs before storing into peer memory, so a peer's buffers
 //       are never overwritten while its previous all-to-all is still live.
-//   exit: CTA 0 waits for every step's incoming flags, so kernel completion
-//       implies this GPU's recv buffer is final.
+//   exit (multi-GPU): CTA 0 polls every producer flag of this GPU, so kernel
+//       completion implies this GPU's recv buffer is final.
 // Every spin is bounded by a %globaltimer timeout and reports A2A_ERR_TIMEOUT.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -41,16 +42,16 @@ namespace a2a {
 
 struct KParams {
   char* base[1 + 2 * A2A_MAX_GPUS];        // send | recv[G] | scratch[G]
-  uint32_t* step_flags[A2A_MAX_GPUS];      // per GPU: [T'][G] u32, slot (t, producer gpu)
+  uint32_t* step_flags[A2A_MAX_GPUS];      // per GPU: [T'][G][nC] u32, slot (t, producer gpu, cta)
   uint32_t* entry_flags[A2A_MAX_GPUS];     // per GPU: [G] u32
-  unsigned long long* arrive;              // own: [T'] per-step CTA arrival counters
   const DevItem* items;
   const int64_t* step_begin;               // [T'+1]
   const int64_t* step_bytes;               // [T']
-  const uint32_t* step_mask;               // [T'] bit h: this GPU writes to GPU h at step t
-  const uint32_t* step_nwork;              // [T'] CTAs of this GPU with work at step t
-  const int32_t* wait_off;                 // [T'+1] ranges into wait_idx
-  const int32_t* wait_idx;                 // flag indices (t*G + g) in own step_flags
+  const uint32_t* dst_mask;                // [T'][nC] bit h: CTA wrote to GPU h in step t
+  const int32_t* wait_off;                 // [T'*nC + 1] ranges into wait_idx
+  const int32_t* wait_idx;                 // producer flag indices in own step_flags
+  const int32_t* exit_idx;                 // every producer flag of this GPU (exit wait)
+  int32_t n_exit;
   unsigned long long* counters;            // [T'][E]
   int32_t* err;
   int64_t timeout_ns;
@@ -178,19 +179,17 @@ __global__ void __launch_bounds__(1024, 1) a2a_exec_kernel(const KParams p) {
     if (s_abort) return;
   }
 
-  int waited = 0;  // incoming flags of steps [0, waited) already acquired
   for (int t = 0; t < p.T; ++t) {
     const int64_t B = p.step_bytes[t];
     const int64_t lo = cta_lo(B, c, p.nC), hi = cta_lo(B, c + 1, p.nC);
     if (hi <= lo) continue;
-    if (waited < t) {
+    const int32_t w0 = p.wait_off[t * p.nC + c], w1 = p.wait_off[t * p.nC + c + 1];
+    if (w1 > w0) {
       if (warp == 0) {
-        bool ok = warp_wait_flags(my_flags, p.wait_idx, p.wait_off[waited], p.wait_off[t], p.epoch,
-                                  p.timeout_ns, p.err);
+        bool ok = warp_wait_flags(my_flags, p.wait_idx, w0, w1, p.epoch, p.timeout_ns, p.err);
         if (!ok && tid == 0) s_abort = 1;
         if (tid == 0) __threadfence_system();
       }
-      waited = t;
       __syncthreads();
       if (s_abort) return;
     }
@@ -213,25 +212,32 @@ __global__ void __launch_bounds__(1024, 1) a2a_exec_kernel(const KParams p) {
     }
     __syncthreads();
     if (tid == 0) {
+      uint32_t mask = p.dst_mask[(int64_t)t * p.nC + c];
       __threadfence_system();
-      const unsigned long long nw = p.step_nwork[t];
-      const unsigned long long old = atomicAdd(p.arrive + t, 1ull);
-      if ((old + 1) % nw == 0) {  // last CTA of this GPU to finish step t
-        __threadfence_system();
-        uint32_t mask = p.step_mask[t];
-        while (mask) {
-          const int h = __ffs(mask) - 1;
-          mask &= mask - 1;
-          st_release_sys(p.step_flags[h] + (int64_t)t * p.G + p.rank, p.epoch);
-        }
+      const int64_t slot = ((int64_t)t * p.G + p.rank) * p.nC + c;
+      while (mask) {
+        const int h = __ffs(mask) - 1;
+        mask &= mask - 1;
+        st_release_sys(p.step_flags[h] + slot, p.epoch);
       }
     }
   }
-  // ---- exit: all incoming stores of every step have landed
-  if (c == 0 && p.G > 1 && waited < p.T) {
-    if (warp == 0)
-      warp_wait_flags(my_flags, p.wait_idx, p.wait_off[waited], p.wait_off[p.T], p.epoch,
-                      p.timeout_ns, p.err);
+  // ---- exit: all incoming stores of every step have landed (multi-GPU)
+  if (c == 0 && p.G > 1) {
+    bool ok = true;
+    for (int32_t i = tid; i < p.n_exit && ok; i += blockDim.x) {
+      const uint32_t* f = my_flags + p.exit_idx[i];
+      uint64_t t0 = globaltimer();
+      uint32_t spins = 0;
+      while ((int32_t)(ld_acquire_sys(f) - p.epoch) < 0) {
+        if ((++spins & 255) == 0 && ((int64_t)(globaltimer() - t0) > p.timeout_ns ||
+                                     *(volatile int32_t*)p.err != 0)) {
+          ok = false;
+          break;
+        }
+      }
+    }
+    if (!ok) atomicCAS(p.err, 0, (int32_t)A2A_ERR_TIMEOUT);
   }
 }
 
@@ -262,14 +268,11 @@ struct DeviceGuard {
 
 static const int kUnrollDefault = 4;
 
-// arena flag region: entry[G] u32 | step flags [T'][G] u32 | arrive [T'] u64
+// arena flag region: entry[G] u32 | step flags [T'][G][nC] u32
 static inline int64_t entry_flags_off() { return 0; }
 static inline int64_t step_flags_off() { return 256; }
-static inline int64_t arrive_off(int G, int TE) {
-  return (step_flags_off() + (int64_t)TE * G * 4 + 255) & ~255LL;
-}
-static inline int64_t flag_region_bytes(int G, int TE) {
-  return (arrive_off(G, TE) + (int64_t)TE * 8 + 65535) & ~65535LL;
+static inline int64_t flag_region_bytes(int G, int TE, int nC) {
+  return (step_flags_off() + (int64_t)TE * G * nC * 4 + 65535) & ~65535LL;
 }
 
 static void free_device(Plan& P) {
@@ -280,7 +283,7 @@ static void free_device(Plan& P) {
     P.peer_opened[g] = false;
     P.peer_arena[g] = nullptr;
   }
-  void** bufs[] = {&P.arena, &P.d_items, &P.d_step_begin, &P.d_step_bytes, &P.d_step_mask, &P.d_step_nwork,
+  void** bufs[] = {&P.arena, &P.d_items, &P.d_step_begin, &P.d_step_bytes, &P.d_dst_mask, &P.d_exit_idx,
                    &P.d_wait_off, &P.d_wait_idx, &P.d_counters};
   for (void** b : bufs) {
     if (*b) cudaFree(*b);
@@ -323,29 +326,13 @@ static int bind_plan(Plan& P, int gpu, int dev, int nC) {
   P.nC = nC;
   const int G = P.G, TE = P.T_exec;
 
-  // ---- per-step destination masks / working-CTA counts of every GPU, and
-  //      the flags this rank waits for: (t, g) for every g that writes here at t
-  std::vector<std::vector<uint32_t>> smask(G, std::vector<uint32_t>(TE, 0));
-  std::vector<std::vector<uint32_t>> nwork(G, std::vector<uint32_t>(TE, 0));
-  for (int g = 0; g < G; ++g) {
-    const GpuTables& tb = P.tables[g];
-    for (int t = 0; t < TE; ++t) {
-      for (int64_t j = tb.step_begin[t]; j < tb.step_begin[t + 1]; ++j)
-        smask[g][t] |= 1u << tb.items[j].dst_gpu;
-      for (int c = 0; c < nC; ++c)
-        if (cta_lo(tb.step_bytes[t], c + 1, nC) > cta_lo(tb.step_bytes[t], c, nC)) ++nwork[g][t];
-    }
-  }
-  std::vector<int32_t> wait_off(TE + 1, 0), wait_idx;
-  for (int t = 0; t < TE; ++t) {
-    wait_off[t] = (int32_t)wait_idx.size();
-    for (int g = 0; g < G; ++g)
-      if (smask[g][t] & (1u << gpu)) wait_idx.push_back(t * G + g);
-  }
-  wait_off[TE] = (int32_t)wait_idx.size();
+  // ---- CTA split + producer dependency lists (host, identical on all ranks)
+  int rc = build_sync(P, nC);
+  if (rc != A2A_OK) return rc;
+  const SyncTables& S = P.sync;
 
   // ---- arena layout, identical on every rank: flags | recv | scratch
-  P.flags_bytes = flag_region_bytes(G, TE);
+  P.flags_bytes = flag_region_bytes(G, TE, nC);
   P.recv_off.assign(G, 0);
   P.scratch_off.assign(G, 0);
   P.arena_bytes.assign(G, 0);
@@ -363,14 +350,13 @@ static int bind_plan(Plan& P, int gpu, int dev, int nC) {
     return fail(A2A_ERR_NOMEM, buf);
   }
   CK(cudaMemset(P.arena, 0, (size_t)P.flags_bytes));
-  int rc;
   if ((rc = upload(&P.d_items, P.tables[gpu].items)) != A2A_OK) return rc;
   if ((rc = upload(&P.d_step_begin, P.tables[gpu].step_begin)) != A2A_OK) return rc;
   if ((rc = upload(&P.d_step_bytes, P.tables[gpu].step_bytes)) != A2A_OK) return rc;
-  if ((rc = upload(&P.d_step_mask, smask[gpu])) != A2A_OK) return rc;
-  if ((rc = upload(&P.d_step_nwork, nwork[gpu])) != A2A_OK) return rc;
-  if ((rc = upload(&P.d_wait_off, wait_off)) != A2A_OK) return rc;
-  if ((rc = upload(&P.d_wait_idx, wait_idx)) != A2A_OK) return rc;
+  if ((rc = upload(&P.d_dst_mask, S.dst_mask[gpu])) != A2A_OK) return rc;
+  if ((rc = upload(&P.d_wait_off, S.wait_off[gpu])) != A2A_OK) return rc;
+  if ((rc = upload(&P.d_wait_idx, S.wait_idx[gpu])) != A2A_OK) return rc;
+  if ((rc = upload(&P.d_exit_idx, S.exit_idx[gpu])) != A2A_OK) return rc;
   size_t cbytes = std::max<size_t>((size_t)TE * std::max(P.E, 1) * 8, 16);
   CK(cudaMalloc(&P.d_counters, cbytes));
   CK(cudaMemset(P.d_counters, 0, cbytes));
@@ -506,12 +492,12 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
     kp.entry_flags[g] = (uint32_t*)(ar + entry_flags_off());
     kp.step_flags[g] = (uint32_t*)(ar + step_flags_off());
   }
-  kp.arrive = (unsigned long long*)((char*)P.arena + arrive_off(P.G, P.T_exec));
   kp.items = (const DevItem*)P.d_items;
   kp.step_begin = (const int64_t*)P.d_step_begin;
   kp.step_bytes = (const int64_t*)P.d_step_bytes;
-  kp.step_mask = (const uint32_t*)P.d_step_mask;
-  kp.step_nwork = (const uint32_t*)P.d_step_nwork;
+  kp.dst_mask = (const uint32_t*)P.d_dst_mask;
+  kp.exit_idx = (const int32_t*)P.d_exit_idx;
+  kp.n_exit = (int32_t)P.sync.exit_idx[P.rank].size();
   kp.wait_off = (const int32_t*)P.d_wait_off;
   kp.wait_idx = (const int32_t*)P.d_wait_idx;
   kp.counters = (unsigned long long*)P.d_counters;

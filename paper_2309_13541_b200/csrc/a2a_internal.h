@@ -44,6 +44,17 @@ struct GpuTables {
   std::vector<int64_t> step_bytes;  // [T']
 };
 
+// CTA split + exact producer dependencies for a given CTA count (host-built,
+// identical on every rank).  Flag slot of producer (t, g, c) = (t*G + g)*nC + c
+// in every GPU's step-flag array.
+struct SyncTables {
+  int32_t nC = 0;
+  std::vector<std::vector<uint32_t>> dst_mask;  // [g][t*nC + c] bit h: (g,c) wrote to h at t
+  std::vector<std::vector<int32_t>> wait_off;   // [g][t*nC + c .. +1] into wait_idx[g]
+  std::vector<std::vector<int32_t>> wait_idx;   // [g] producer slots to acquire
+  std::vector<std::vector<int32_t>> exit_idx;   // [g] every producer slot that writes into g
+};
+
 struct Interval {
   int32_t a, b;       // chunk range [a, b)
   int64_t base;       // scratch byte offset of chunk a's first byte
@@ -65,6 +76,8 @@ struct Plan {
   std::vector<GpuTables> tables;                // per gpu
   std::vector<int64_t> link_bytes;              // [T * E]
 
+  SyncTables sync;
+
   // ---- device binding (a2a_exec.cu)
   bool bound = false, imported = false;
   int32_t rank = -1, device = -1, nC = 0, nT = 1024;
@@ -77,8 +90,8 @@ struct Plan {
   void* d_items = nullptr;
   void* d_step_begin = nullptr;
   void* d_step_bytes = nullptr;
-  void* d_step_mask = nullptr;
-  void* d_step_nwork = nullptr;
+  void* d_dst_mask = nullptr;
+  void* d_exit_idx = nullptr;
   void* d_wait_off = nullptr;
   void* d_wait_idx = nullptr;
   void* d_counters = nullptr;
@@ -96,6 +109,7 @@ inline int64_t chunk_off(int64_t c, int64_t m, int64_t Q) {
 }
 
 void set_error(const std::string& msg);
+int build_sync(Plan& P, int nC);
 int fail(int code, const std::string& msg);
 
 // CTA work split shared by host (flag lists) and device (copy ranges)

@@ -13,6 +13,7 @@
 // The same holdings, mapped to byte locations (send at s, recv at d, scratch
 // elsewhere), resolve every op's source and destination address.
 #include <algorithm>
+#include <array>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -331,6 +332,169 @@ static int build_plan(Plan& P, const a2a_schedule_desc* D) {
   return A2A_OK;
 }
 
+// ---- CTA split and exact producer dependencies ---------------------------
+//
+// Every GPU splits each step's concatenated item bytes into nC contiguous
+// ranges (cta_lo).  A piece of an item written by CTA (t, g, c) lands in a
+// destination byte segment of some GPU's recv or scratch; a consumer piece
+// (t', h, c') that reads bytes of its own recv/scratch must acquire every
+// producer whose segment overlaps its source range and whose step t < t'.
+namespace {
+struct Seg {
+  int64_t a, b;
+  int32_t t, slot;
+};
+template <typename F>
+void for_each_piece(const GpuTables& tb, int t, int nC, F&& f) {
+  const int64_t B = tb.step_bytes[t];
+  int64_t k = tb.step_begin[t];
+  for (int c = 0; c < nC; ++c) {
+    const int64_t lo = cta_lo(B, c, nC), hi = cta_lo(B, c + 1, nC);
+    if (hi <= lo) continue;
+    while (k < tb.step_begin[t + 1] && tb.items[k].prefix + tb.items[k].nbytes <= lo) ++k;
+    for (int64_t j = k; j < tb.step_begin[t + 1] && tb.items[j].prefix < hi; ++j) {
+      const DevItem& it = tb.items[j];
+      const int64_t x0 = std::max(lo, it.prefix) - it.prefix;
+      const int64_t x1 = std::min(hi, it.prefix + it.nbytes) - it.prefix;
+      if (x1 > x0) f(c, it, x0, x1);
+    }
+  }
+}
+}  // namespace
+
+int build_sync(Plan& P, int nC) {
+  if (P.sync.nC == nC) return A2A_OK;
+  if (nC < 1) return fail(A2A_ERR_INVALID, "num_ctas must be >= 1");
+  const int G = P.G, TE = P.T_exec;
+  SyncTables S;
+  S.nC = nC;
+  S.dst_mask.assign(G, std::vector<uint32_t>((size_t)TE * nC, 0));
+  // segs[h][0] = writes into h's recv, segs[h][1] = into h's scratch
+  std::vector<std::array<std::vector<Seg>, 2>> segs(G);
+  for (int g = 0; g < G; ++g) {
+    for (int t = 0; t < TE; ++t) {
+      for_each_piece(P.tables[g], t, nC, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
+        S.dst_mask[g][(size_t)t * nC + c] |= 1u << it.dst_gpu;
+        const int cls = (it.dst_loc == loc_recv(it.dst_gpu)) ? 0 : 1;
+        segs[it.dst_gpu][cls].push_back(
+            Seg{it.dst_off + x0, it.dst_off + x1, t, (int32_t)(((int64_t)t * G + g) * nC + c)});
+      });
+    }
+  }
+  // sorted by start, with running max of ends for the backward overlap walk
+  std::vector<std::array<std::vector<int64_t>, 2>> maxend(G);
+  for (int h = 0; h < G; ++h)
+    for (int cls = 0; cls < 2; ++cls) {
+      auto& v = segs[h][cls];
+      std::sort(v.begin(), v.end(), [](const Seg& x, const Seg& y) { return x.a < y.a; });
+      auto& me = maxend[h][cls];
+      me.resize(v.size());
+      int64_t m = INT64_MIN;
+      for (size_t i = 0; i < v.size(); ++i) me[i] = m = std::max(m, v[i].b);
+    }
+  S.wait_off.assign(G, {});
+  S.wait_idx.assign(G, {});
+  S.exit_idx.assign(G, {});
+  std::vector<int32_t> deps;
+  for (int h = 0; h < G; ++h) {
+    auto& off = S.wait_off[h];
+    auto& idx = S.wait_idx[h];
+    off.assign((size_t)TE * nC + 1, 0);
+    std::vector<std::vector<int32_t>> per((size_t)TE * nC);
+    for (int t = 0; t < TE; ++t) {
+      for_each_piece(P.tables[h], t, nC, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
+        if (it.src_loc == loc_send()) return;
+        const int cls = (it.src_loc == loc_recv(h)) ? 0 : 1;
+        const int64_t a = it.src_off + x0, b = it.src_off + x1;
+        const auto& v = segs[h][cls];
+        const auto& me = maxend[h][cls];
+        // segments with start < b, walking back while some end can exceed a
+        size_t j = std::lower_bound(v.begin(), v.end(), b,
+                                    [](const Seg& s, int64_t x) { return s.a < x; }) - v.begin();
+        auto& out = per[(size_t)t * nC + c];
+        while (j > 0) {
+          --j;
+          if (me[j] <= a) break;
+          if (v[j].b > a && v[j].t < t) out.push_back(v[j].slot);
+        }
+      });
+    }
+    for (size_t k = 0; k < per.size(); ++k) {
+      auto& d = per[k];
+      std::sort(d.begin(), d.end());
+      d.erase(std::unique(d.begin(), d.end()), d.end());
+      off[k] = (int32_t)idx.size();
+      idx.insert(idx.end(), d.begin(), d.end());
+    }
+    off[per.size()] = (int32_t)idx.size();
+    for (int t = 0; t < TE; ++t)
+      for (int g = 0; g < G; ++g)
+        for (int c = 0; c < nC; ++c)
+          if (S.dst_mask[g][(size_t)t * nC + c] & (1u << h))
+            S.exit_idx[h].push_back((int32_t)(((int64_t)t * G + g) * nC + c));
+  }
+  P.sync = std::move(S);
+  return A2A_OK;
+}
+
+// Host emulation of the device protocol: CTAs of all GPUs run their step
+// ranges in a random interleaving constrained ONLY by the dependency lists;
+// memory is host memory.  Insufficient dependencies show up as wrong bytes.
+static int emulate(Plan& P, int nC, uint8_t* const* send, uint8_t* const* recv, uint64_t seed) {
+  int rc = build_sync(P, nC);
+  if (rc) return rc;
+  const int G = P.G, TE = P.T_exec;
+  std::vector<std::vector<uint8_t>> scratch(G);
+  for (int g = 0; g < G; ++g) scratch[g].assign((size_t)P.info[g].scratch_bytes + 64, 0);
+  std::vector<char> flag((size_t)TE * G * nC, 0);
+  // per (g, c): list of (t, pieces) in step order
+  struct Piece { int32_t src_loc, dst_loc; int64_t src, dst, n; };
+  std::vector<std::vector<std::vector<std::vector<Piece>>>> work(
+      G, std::vector<std::vector<std::vector<Piece>>>(nC, std::vector<std::vector<Piece>>(TE)));
+  std::vector<std::vector<std::vector<char>>> has(G, std::vector<std::vector<char>>(nC, std::vector<char>(TE, 0)));
+  for (int g = 0; g < G; ++g)
+    for (int t = 0; t < TE; ++t) {
+      const int64_t B = P.tables[g].step_bytes[t];
+      for (int c = 0; c < nC; ++c) has[g][c][t] = cta_lo(B, c + 1, nC) > cta_lo(B, c, nC);
+      for_each_piece(P.tables[g], t, nC, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
+        work[g][c][t].push_back(Piece{it.src_loc, it.dst_loc, it.src_off + x0, it.dst_off + x0, x1 - x0});
+      });
+    }
+  auto base = [&](int g, int loc) -> uint8_t* {
+    if (loc == loc_send()) return send[g];
+    if (loc >= 1 && loc < 1 + G) return recv[loc - 1];
+    return scratch[loc - 1 - G].data();
+  };
+  std::vector<std::vector<int>> next(G, std::vector<int>(nC, 0));
+  uint64_t x = seed * 0x9E3779B97F4A7C15ULL + 1;
+  auto rnd = [&]() { x ^= x << 13; x ^= x >> 7; x ^= x << 17; return x; };
+  for (;;) {
+    std::vector<std::pair<int, int>> ready;
+    bool left = false;
+    for (int g = 0; g < G; ++g)
+      for (int c = 0; c < nC; ++c) {
+        int& t = next[g][c];
+        while (t < TE && !has[g][c][t]) ++t;
+        if (t >= TE) continue;
+        left = true;
+        const auto& off = P.sync.wait_off[g];
+        bool ok = true;
+        for (int32_t i = off[(size_t)t * nC + c]; i < off[(size_t)t * nC + c + 1] && ok; ++i)
+          ok = flag[P.sync.wait_idx[g][i]];
+        if (ok) ready.emplace_back(g, c);
+      }
+    if (!left) break;
+    if (ready.empty()) return fail(A2A_ERR_INVALID, "emulation deadlock: unsatisfiable dependencies");
+    auto [g, c] = ready[rnd() % ready.size()];
+    int t = next[g][c];
+    for (const Piece& pc : work[g][c][t])
+      std::memmove(base(g, pc.dst_loc) + pc.dst, base(g, pc.src_loc) + pc.src, (size_t)pc.n);
+    flag[((size_t)t * G + g) * nC + c] = 1;
+    ++next[g][c];
+  }
+  return A2A_OK;
+}
+
 }  // namespace a2a
 
 using namespace a2a;
@@ -398,6 +562,37 @@ int a2a_plan_link_bytes(const a2a_plan* plan, int64_t* out) {
   if (!plan || !out) return fail(A2A_ERR_INVALID, "null argument");
   std::memcpy(out, plan->p.link_bytes.data(), plan->p.link_bytes.size() * sizeof(int64_t));
   return A2A_OK;
+}
+
+int a2a_plan_prepare(a2a_plan* plan, int32_t num_ctas) {
+  if (!plan) return fail(A2A_ERR_INVALID, "null plan");
+  if (plan->p.bound && plan->p.sync.nC != num_ctas)
+    return fail(A2A_ERR_STATE, "plan already bound with another CTA count");
+  try {
+    return build_sync(plan->p, num_ctas);
+  } catch (const std::bad_alloc&) {
+    return fail(A2A_ERR_NOMEM, "out of host memory building the CTA tables");
+  }
+}
+
+int a2a_plan_sync_stats(const a2a_plan* plan, int32_t gpu, int64_t* n_wait, int64_t* n_exit) {
+  if (!plan || !n_wait || !n_exit) return fail(A2A_ERR_INVALID, "null argument");
+  const SyncTables& S = plan->p.sync;
+  if (S.nC == 0) return fail(A2A_ERR_STATE, "call a2a_plan_prepare first");
+  if (gpu < 0 || gpu >= plan->p.G) return fail(A2A_ERR_INVALID, "gpu out of range");
+  *n_wait = (int64_t)S.wait_idx[gpu].size();
+  *n_exit = (int64_t)S.exit_idx[gpu].size();
+  return A2A_OK;
+}
+
+int a2a_plan_emulate(a2a_plan* plan, int32_t num_ctas, void* const* send, void* const* recv,
+                     uint64_t seed) {
+  if (!plan || !send || !recv) return fail(A2A_ERR_INVALID, "null argument");
+  try {
+    return emulate(plan->p, num_ctas, (uint8_t* const*)send, (uint8_t* const*)recv, seed);
+  } catch (const std::bad_alloc&) {
+    return fail(A2A_ERR_NOMEM, "out of host memory in emulation");
+  }
 }
 
 int a2a_plan_gpu_info(const a2a_plan* plan, int32_t gpu, a2a_gpu_info* out) {

@@ -153,6 +153,34 @@ class Plan:
         self._ck(N.lib.a2a_plan_gpu_info(self._h, int(gpu), C.byref(info)), "a2a_plan_gpu_info")
         return {f: getattr(info, f) for f, _ in N.GpuInfo._fields_}
 
+    def prepare(self, num_ctas: int):
+        """Build the CTA split and exact producer-dependency lists (host only)."""
+        self._ck(N.lib.a2a_plan_prepare(self._h, int(num_ctas)), "a2a_plan_prepare")
+        return self
+
+    def sync_stats(self, gpu: int) -> dict:
+        w, e = C.c_int64(), C.c_int64()
+        self._ck(N.lib.a2a_plan_sync_stats(self._h, int(gpu), C.byref(w), C.byref(e)),
+                 "a2a_plan_sync_stats")
+        return {"wait_flags": w.value, "exit_flags": e.value}
+
+    def emulate(self, sends, num_ctas: int, seed: int = 0) -> list:
+        """Host emulation of the device protocol (CPU): every GPU's CTAs run in a
+        random interleaving constrained only by the dependency lists.
+        sends: per GPU uint8 arrays [V_g, N, m]; returns per GPU recv arrays."""
+        if len(sends) != self.n_gpus:
+            raise ValueError("one send array per GPU")
+        sends = [np.ascontiguousarray(x, dtype=np.uint8) for x in sends]
+        recvs = [np.zeros_like(x) for x in sends]
+        for g, x in enumerate(sends):
+            if x.nbytes != self.gpu_info(g)["send_bytes"]:
+                raise ValueError(f"send[{g}] has the wrong size")
+        sp = (C.c_void_p * self.n_gpus)(*[x.ctypes.data for x in sends])
+        rp = (C.c_void_p * self.n_gpus)(*[x.ctypes.data for x in recvs])
+        self._ck(N.lib.a2a_plan_emulate(self._h, int(num_ctas), sp, rp, int(seed)),
+                 "a2a_plan_emulate")
+        return recvs
+
     # ---- device side
     def bind(self, gpu: int = 0, device: int | None = None, num_ctas: int = 0):
         device = gpu if device is None else device
