@@ -163,111 +163,103 @@ def run_reference(args, art, m):
     print(json.dumps(line), flush=True)
 
 
-def main(argv=None):
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="gk8_2")
-    ap.add_argument("--m", type=int, default=16 << 20)
-    ap.add_argument("--num-ctas", type=int, default=0)
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-nccl", action="store_true")
-    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
-    args = ap.parse_args(argv)
-    args.warmup = max(args.warmup, 3)
+class Ctx:
+    """Process/GPU context: rank, device, optional torch.distributed group."""
 
-    from paper_2309_13541_b200.artifacts import load_artifact
-    art = load_artifact(args.config)
-    m = args.m
-    if args.impl == "reference":
-        return run_reference(args, art, m)
+    def __init__(self):
+        import torch
+        self.world, self.rank, self.local = _dist()
+        torch.cuda.set_device(self.local)
+        self.dev = torch.device("cuda", self.local)
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group("nccl", device_id=self.dev)
+            self.pg = dist
 
-    import numpy as np
-    import torch
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
 
-    from paper_2309_13541_b200.executor import Plan, contiguous_placement
-    from paper_2309_13541_b200.graphs import distance_sum
-
-    world, rank, local = _dist()
-    G = world
-    if G != args.gpus:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    pg = None
-    if G > 1:
-        import torch.distributed as dist
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=dev)
-        pg = dist
-
-    def barrier():
-        if pg:
-            pg.barrier()
-
-    def allmax(x):
-        if not pg:
-            return x
-        t = torch.tensor(x, dtype=torch.float64, device=dev)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    def allmax(self, x):
+        if not self.pg:
+            return list(x)
+        import torch
+        t = torch.tensor(list(x), dtype=torch.float64, device=self.dev)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return t.tolist()
 
+    def close(self):
+        if self.pg:
+            self.pg.barrier()
+            self.pg.destroy_process_group()
+
+
+def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=True,
+            flush_bytes=512 << 20):
+    """Time K all-to-alls of `art` at shard size m on ctx.world GPUs.
+
+    Returns a dict (identical on every rank) with T, algBW, bound, roofline,
+    NCCL baseline and e2e numbers."""
+    import torch
+
+    from paper_2309_13541_b200.dist import connect, local_nodes
+    from paper_2309_13541_b200.executor import Plan
+    from paper_2309_13541_b200.graphs import distance_sum
+
+    G, rank, dev = ctx.world, ctx.rank, ctx.dev
     n = art.g.n
     plan = Plan(art.g, art.sched, m=m, n_gpus=G)
-    plan.bind(rank, device=local, num_ctas=args.num_ctas)
+    plan.bind(rank, device=ctx.local, num_ctas=num_ctas)
     if G > 1:
-        hs = [None] * G
-        pg.all_gather_object(hs, plan.export_handle())
-        plan.import_handles(hs)
+        connect(plan)
     info = plan.gpu_info(rank)
     infos = [plan.gpu_info(g) for g in range(G)]
-    V, first = info["n_local_nodes"], info["first_node"]
-    nodes = [v for v in range(n) if contiguous_placement(n, G)[v] == rank]
+    V = info["n_local_nodes"]
+    nodes = local_nodes(plan, rank)
 
     def node_send(s):  # deterministic synthetic shards of node s: [n, m]
-        gen = torch.Generator(device=dev).manual_seed(1000003 * (s + 1))
+        gen = torch.Generator(device=dev).manual_seed(1000003 * (s + 1) + m)
         return torch.randint(0, 256, (n, m), dtype=torch.uint8, device=dev, generator=gen)
 
     send = torch.empty((V, n, m), dtype=torch.uint8, device=dev)
     for i, s in enumerate(nodes):
         send[i] = node_send(s)
     recv = plan.recv_buffer() if G > 1 else torch.empty_like(send)
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    flush = torch.empty(flush_bytes, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    clk = Clocks(ctx.local) if clocks else None
+    if clk:
+        clk.start()
     # ---- warm-up + correctness of the exact buffers we time
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         plan.execute(send, recv, stream=stream)
     plan.sync()
-    barrier()
+    ctx.barrier()
     ok = True
     for s in range(n):
         row = node_send(s)
         for i, v in enumerate(nodes):
             ok &= bool(torch.equal(recv[i, s], row[v]))
-    ok = bool(allmax([0.0 if ok else 1.0])[0] == 0.0) if pg else ok
+    ok = ctx.allmax([0.0 if ok else 1.0])[0] == 0.0
 
-    # ---- timed region: K all-to-alls, L2 flushed between them
-    clk = Clocks(local)
-    e0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    e1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    barrier()
+    # ---- timed region: K all-to-alls, L2 flushed between them (outside the events)
+    e0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    e1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ctx.barrier()
     torch.cuda.synchronize(dev)
-    clk.start()
-    for k in range(args.steps):
+    for k in range(steps):
         flush.zero_()
         e0[k].record(stream)
         plan.execute(send, recv, stream=stream)
         e1[k].record(stream)
     plan.sync()
     torch.cuda.synchronize(dev)
-    clocks = clk.stop()
-    barrier()
-    per = [a.elapsed_time(b) for a, b in zip(e0, e1)]
-    per = allmax(per)
+    clock_rec = clk.stop() if clk else None
+    ctx.barrier()
+    per = ctx.allmax([a.elapsed_time(b) for a, b in zip(e0, e1)])
     T = sum(per) / len(per) / 1e3                      # s per all-to-all (max over ranks)
     payload = n * (n - 1) * m
     value = payload / T / 1e9
@@ -293,43 +285,45 @@ def main(argv=None):
     traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(traffic_file):
         with open(traffic_file) as fh:
-            tr = json.load(fh).get(f"{args.config}:{m}:G{G}")
+            tr = json.load(fh).get(f"{art.name}:{m}:G{G}")
         if tr:
             roof["traffic"] = tr["per_launch_bytes"]
             roof["traffic_source"] = tr["source"]
 
     # ---- NCCL all_to_all_single on the same bytes (baseline, not the target)
-    nccl = None
-    if G > 1 and not args.no_nccl:
+    nres = None
+    if G > 1 and nccl and (V * n * m) % G == 0:
         inp = send.reshape(-1)
         out = torch.empty_like(inp)
         for _ in range(3):
-            pg.all_to_all_single(out, inp)
+            ctx.pg.all_to_all_single(out, inp)
         torch.cuda.synchronize(dev)
         ts = []
-        for _ in range(args.steps):
+        for _ in range(steps):
             flush.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            pg.all_to_all_single(out, inp)
+            ctx.pg.all_to_all_single(out, inp)
             b.record(stream)
             ts.append((a, b))
         torch.cuda.synchronize(dev)
-        tn = allmax([a.elapsed_time(b) for a, b in ts])
+        tn = ctx.allmax([a.elapsed_time(b) for a, b in ts])
         Tn = sum(tn) / len(tn) / 1e3
-        nccl = {"value": round(payload / Tn / 1e9, 2), "unit": "GB/s",
+        nres = {"value": round(payload / Tn / 1e9, 2), "unit": "GB/s",
+                "per_gpu": round(payload / Tn / 1e9 / G, 2),
                 "ms_per_step": round(Tn * 1e3, 4),
                 "note": "torch.distributed.all_to_all_single, same send bytes, direct routes"}
+        del inp, out
 
     # ---- e2e through the public API with host buffers (H2D + a2a + D2H per step)
-    e2e = None
-    if not args.no_e2e:
+    eres = None
+    if e2e:
         hs = torch.empty((V, n, m), dtype=torch.uint8, pin_memory=True)
         hs.copy_(send.cpu())
         hr = torch.empty((V, n, m), dtype=torch.uint8, pin_memory=True)
-        ke = max(3, min(args.steps, 10))
+        ke = max(3, min(steps, 10))
         ev = []
-        barrier()
+        ctx.barrier()
         torch.cuda.synchronize(dev)
         for k in range(ke + 2):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -342,16 +336,58 @@ def main(argv=None):
                 ev.append((a, b))
         plan.sync()
         torch.cuda.synchronize(dev)
-        te = allmax([a.elapsed_time(b) for a, b in ev])
+        te = ctx.allmax([a.elapsed_time(b) for a, b in ev])
         Te = sum(te) / len(te) / 1e3
-        e2e = {"value": round(payload / Te / 1e9, 3), "unit": "GB/s",
-               "h2d_bytes_per_step": int(V * n * m * G), "d2h_bytes_per_step": int(V * n * m * G),
-               "ms_per_step": round(Te * 1e3, 3),
-               "path": "pinned host send -> H2D -> Plan.execute -> D2H recv (every step)"}
+        ok &= bool(torch.equal(hr.to(dev), recv))
+        eres = {"value": round(payload / Te / 1e9, 3), "unit": "GB/s",
+                "h2d_bytes_per_step": int(V * n * m * G), "d2h_bytes_per_step": int(V * n * m * G),
+                "ms_per_step": round(Te * 1e3, 3),
+                "path": "pinned host send -> H2D -> Plan.execute -> D2H recv (every step)"}
+        del hs, hr
+    plan.sync()
+    res = {"T": T, "per_step_ms": per, "value": value, "per_gpu": value / G,
+           "t_lb": t_lb, "bound_frac": t_lb / T, "roofline": roof, "nccl": nres, "e2e": eres,
+           "recv_ok": bool(ok), "clocks": clock_rec, "sync": plan.sync_stats(rank),
+           "num_ctas": plan_ctas(plan, num_ctas), "egress_max": max(i["egress_bytes"] for i in infos),
+           "scratch_bytes": info["scratch_bytes"]}
+    plan.close()
+    del send, recv, flush
+    torch.cuda.empty_cache()
+    return res
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="gk8_2")
+    ap.add_argument("--m", type=int, default=16 << 20)
+    ap.add_argument("--num-ctas", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    args = ap.parse_args(argv)
+    args.warmup = max(args.warmup, 3)
+
+    from paper_2309_13541_b200.artifacts import load_artifact
+    art = load_artifact(args.config)
+    m = args.m
+    if args.impl == "reference":
+        return run_reference(args, art, m)
+
+    ctx = Ctx()
+    if ctx.world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ctx.world}")
+    r = measure(ctx, art, m, args.steps, args.warmup, num_ctas=args.num_ctas,
+                nccl=not args.no_nccl, e2e=not args.no_e2e)
+    G, n = ctx.world, art.g.n
 
     # ---- CPU baseline: rank 0, N=1 only, bounded sample
     cpu = None
-    if rank == 0 and G == 1 and not args.no_cpu_baseline:
+    if ctx.rank == 0 and G == 1 and not args.no_cpu_baseline:
         nthreads = os.cpu_count() or 1
         m_cpu = m
         while not _host_fits(n, m_cpu) and m_cpu > 4096:
@@ -364,11 +400,10 @@ def main(argv=None):
                          f"(median) with oracle/replay_bytes.c on {nthreads} threads",
                "recv_ok": cok}
 
-    plan.sync()
-    if rank == 0:
+    if ctx.rank == 0:
         line = {
-            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": G,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(T * 1e3, 4),
+            "metric": METRIC, "value": round(r["value"], 3), "unit": "GB/s", "n_gpus": G,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["T"] * 1e3, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u8", "data": "synthetic",
             "config": {"workload": f"{args.config}: frozen decomposed-MCF schedule "
@@ -377,23 +412,20 @@ def main(argv=None):
                        "m_bytes": m, "nodes": n, "hop_ops": len(art.sched.instructions),
                        "nsteps": art.sched.nsteps, "Q": art.sched.Q,
                        "l2": "flushed between timed steps (512 MiB memset, outside events)",
-                       "num_ctas": plan_ctas(plan, args.num_ctas)},
-            "per_gpu": round(value / G, 3),
-            "bound": {"t_lb_ms": round(t_lb * 1e3, 4), "frac": round(t_lb / T, 4),
+                       "num_ctas": r["num_ctas"]},
+            "per_gpu": round(r["per_gpu"], 3),
+            "bound": {"t_lb_ms": round(r["t_lb"] * 1e3, 4), "frac": round(r["bound_frac"], 4),
                       "def": "G=1: 2*m*sum(dist)/HBM; G>1: max_g max(egress,ingress)/900 GB/s"},
-            "recv_ok": ok,
-            "roofline": roof,
+            "recv_ok": r["recv_ok"],
+            "roofline": r["roofline"],
             "cpu_baseline": cpu,
-            "e2e": e2e,
-            "nccl": nccl,
+            "e2e": r["e2e"],
+            "nccl": r["nccl"],
             "gpu_launches": args.steps,
-            "clocks": clocks,
+            "clocks": r["clocks"],
         }
         print(json.dumps(line), flush=True)
-    plan.close()
-    if pg:
-        pg.barrier()
-        pg.destroy_process_group()
+    ctx.close()
 
 
 def plan_ctas(plan, requested):

@@ -1,0 +1,91 @@
+"""Scaling / message-size sweeps on B200 (BASELINE.json configs 2-5).
+
+Runs bench.measure for a list of (artifact, m) cases on the GPUs of this job
+(single process for G=1, torchrun for G>1) and appends one JSON line per case
+to --out (rank 0).  Every line carries our algBW (whole job and per GPU), the
+topology-bound fraction, the roofline and NCCL all_to_all_single on the same
+bytes.
+
+Presets:
+  scaling         gk8_2 16 MiB, hypercube3 4 MiB, torus4x4x4 4 MiB, gk64_4 1 MiB
+  hypercube       hypercube3, m = 4 KiB * 4^k, k = 0..7 (4 KiB .. 64 MiB)
+  gk256           gk256_4 and gk256_4_h2 at 1 MiB (cases whose memory does not fit skip)
+
+  torchrun --nproc-per-node 8 tools/sweep.py --preset scaling --out profiles/x.jsonl
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+PRESETS = {
+    "scaling": [("gk8_2", 16 << 20), ("hypercube3", 4 << 20), ("torus4x4x4", 4 << 20),
+                ("gk64_4", 1 << 20)],
+    "hypercube": [("hypercube3", 4096 * 4 ** k) for k in range(8)],
+    "gk256": [("gk256_4", 1 << 20), ("gk256_4_h2", 1 << 20)],
+}
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--preset", default=None)
+    ap.add_argument("--cases", default="", help="config:m,config:m,...")
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--mem-limit-gib", type=float, default=150.0)
+    ap.add_argument("--no-nccl", action="store_true")
+    a = ap.parse_args(argv)
+    cases = list(PRESETS.get(a.preset, [])) if a.preset else []
+    for c in filter(None, a.cases.split(",")):
+        name, m = c.split(":")
+        cases.append((name, int(m)))
+
+    import bench
+    from paper_2309_13541_b200.artifacts import list_artifacts, load_artifact
+    from paper_2309_13541_b200.executor import Plan
+
+    ctx = bench.Ctx()
+    have = set(list_artifacts())
+    for name, m in cases:
+        rec = {"config": name, "m_bytes": m, "n_gpus": ctx.world}
+        if name not in have:
+            rec["skipped"] = "artifact not generated"
+        else:
+            art = load_artifact(name)
+            with Plan(art.g, art.sched, m=m, n_gpus=ctx.world) as p:
+                mem = max(p.gpu_info(g)["send_bytes"] * 2 + p.gpu_info(g)["scratch_bytes"]
+                          for g in range(ctx.world))
+            if mem > a.mem_limit_gib * 2 ** 30:
+                rec["skipped"] = f"needs {mem / 2**30:.1f} GiB per GPU"
+            else:
+                t0 = time.time()
+                r = bench.measure(ctx, art, m, a.steps, a.warmup, nccl=not a.no_nccl,
+                                  e2e=False, clocks=True)
+                rec.update({
+                    "nodes": art.g.n, "hop_ops": len(art.sched.instructions),
+                    "nsteps": art.sched.nsteps, "Q": art.sched.Q,
+                    "ms": round(r["T"] * 1e3, 4), "algbw_gbs": round(r["value"], 2),
+                    "algbw_per_gpu_gbs": round(r["per_gpu"], 2),
+                    "t_lb_ms": round(r["t_lb"] * 1e3, 4), "bound_frac": round(r["bound_frac"], 4),
+                    "roofline": r["roofline"], "nccl": r["nccl"], "recv_ok": r["recv_ok"],
+                    "clocks": r["clocks"], "sync_flags": r["sync"],
+                    "egress_max_bytes": r["egress_max"], "scratch_bytes": r["scratch_bytes"],
+                    "wall_s": round(time.time() - t0, 1)})
+        if ctx.rank == 0:
+            line = json.dumps(rec)
+            print(line, flush=True)
+            if a.out:
+                with open(a.out, "a") as fh:
+                    fh.write(line + "\n")
+    ctx.close()
+
+
+if __name__ == "__main__":
+    main()
