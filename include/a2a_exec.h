@@ -136,6 +136,10 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
 int a2a_plan_sync(a2a_plan* plan);
 /* device byte counters of this rank, out[t * n_edges + e]; then zeroes them */
 int a2a_plan_read_link_counters(a2a_plan* plan, int64_t* out);
+/* copy engine, before bind: 0 = SM 128-bit load/store loop (default),
+ * 1 = TMA bulk copies (cp.async.bulk global->smem->global, mbarrier ring of
+ * `tma_stages` x `tma_chunk` bytes per CTA; 0 = defaults 6 x 32 KiB) */
+int a2a_plan_set_engine(a2a_plan* plan, int32_t engine, int32_t tma_chunk, int32_t tma_stages);
 /* device-side flag-wait timeout (ns, default 10 s) */
 int a2a_plan_set_timeout(a2a_plan* plan, int64_t timeout_ns);
 

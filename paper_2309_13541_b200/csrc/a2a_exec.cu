@@ -57,6 +57,7 @@ struct KParams {
   int64_t timeout_ns;
   uint32_t epoch;
   int32_t G, rank, nC, T, E, count_links;
+  int32_t tma_chunk, tma_stages;           // TMA engine: bytes per bulk copy, ring depth
 };
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -118,6 +119,50 @@ __device__ __forceinline__ void cta_copy(char* __restrict__ dst, const char* __r
   if (tid < tail) dst[nv * 16 + tid] = src[nv * 16 + tid];
 }
 
+// ---- TMA bulk-copy engine helpers (cp.async.bulk + mbarrier, SASS UBLKCP) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(smem_src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // Warp 0 waits until every listed flag reached `epoch`.  Returns false on timeout.
 __device__ bool warp_wait_flags(const uint32_t* flags, const int32_t* idx, int32_t lo, int32_t hi,
                                 uint32_t epoch, int64_t timeout_ns, int32_t* err) {
@@ -144,11 +189,54 @@ __device__ bool warp_wait_flags(const uint32_t* flags, const int32_t* idx, int32
   return ok;
 }
 
-template <int kUnroll>
-__global__ void __launch_bounds__(1024, 1) a2a_exec_kernel(const KParams p) {
+// Chunk cursor over the 16-byte-aligned bodies of one CTA's pieces in a step
+// (TMA engine).  Heads/tails and misaligned pieces are copied by threads.
+struct BodyCursor {
+  int64_t k, kend, off, lo, hi;
+  __device__ bool next(const KParams& p, uint32_t ch, const char** src, char** dst, uint32_t* n) {
+    while (k < kend) {
+      const DevItem& it = p.items[k];
+      if (it.prefix >= hi) { k = kend; break; }
+      const int64_t x0 = max(lo, it.prefix) - it.prefix;
+      const int64_t x1 = min(hi, it.prefix + it.nbytes) - it.prefix;
+      const char* s0 = p.base[it.src_loc] + it.src_off + x0;
+      char* d0 = p.base[it.dst_loc] + it.dst_off + x0;
+      const int64_t len = x1 - x0;
+      if (len <= 0 || (((uintptr_t)s0 ^ (uintptr_t)d0) & 15) != 0) { ++k; off = 0; continue; }
+      int64_t head = (16 - ((uintptr_t)d0 & 15)) & 15;
+      if (head > len) head = len;
+      const int64_t body = (len - head) & ~(int64_t)15;
+      if (off >= body) { ++k; off = 0; continue; }
+      const int64_t c = min((int64_t)ch, body - off);
+      *src = s0 + head + off;
+      *dst = d0 + head + off;
+      *n = (uint32_t)c;
+      off += c;
+      return true;
+    }
+    return false;
+  }
+};
+
+template <int kEngine, int kThreads>
+__global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) {
   __shared__ int s_abort;
+  extern __shared__ __align__(128) unsigned char dsmem[];
   const int c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5;
-  if (tid == 0) s_abort = 0;
+  // TMA ring: [S mbarriers | S dst ptrs | S sizes | pad | S stages of tma_chunk bytes]
+  const int S = p.tma_stages;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dsmem);
+  char** ring_dst = reinterpret_cast<char**>(dsmem + 8 * S);
+  uint32_t* ring_n = reinterpret_cast<uint32_t*>(dsmem + 16 * S);
+  char* stages = reinterpret_cast<char*>(dsmem + ((20 * S + 127) & ~127));
+  uint32_t gi = 0;  // TMA chunks consumed so far (thread 0): stage/phase bookkeeping
+  if (tid == 0) {
+    s_abort = 0;
+    if (kEngine == 1) {
+      for (int i = 0; i < S; ++i) mbar_init(&bars[i], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
   __syncthreads();
   const uint32_t* my_flags = p.step_flags[p.rank];
 
@@ -199,16 +287,72 @@ __global__ void __launch_bounds__(1024, 1) a2a_exec_kernel(const KParams p) {
       int64_t mid = (a + b + 1) >> 1;
       if (p.items[mid].prefix <= lo) a = mid; else b = mid - 1;
     }
-    for (int64_t k = a; k < p.step_begin[t + 1]; ++k) {
+    const int64_t kend = p.step_begin[t + 1];
+    for (int64_t k = a; k < kend; ++k) {
       const DevItem it = p.items[k];
       if (it.prefix >= hi) break;
       const int64_t x0 = max(lo, it.prefix) - it.prefix;
       const int64_t x1 = min(hi, it.prefix + it.nbytes) - it.prefix;
       if (x1 <= x0) continue;
-      cta_copy<kUnroll>(p.base[it.dst_loc] + it.dst_off + x0, p.base[it.src_loc] + it.src_off + x0,
-                        x1 - x0);
+      char* d0 = p.base[it.dst_loc] + it.dst_off + x0;
+      const char* s0 = p.base[it.src_loc] + it.src_off + x0;
+      if (kEngine == 0) {
+        cta_copy<4>(d0, s0, x1 - x0);
+      } else {  // threads: heads, tails, misaligned pieces; bodies go to the TMA ring
+        const int64_t len = x1 - x0;
+        if ((((uintptr_t)s0 ^ (uintptr_t)d0) & 15) != 0) {
+          for (int64_t i = tid; i < len; i += kThreads) d0[i] = s0[i];
+        } else {
+          int64_t head = (16 - ((uintptr_t)d0 & 15)) & 15;
+          if (head > len) head = len;
+          const int64_t body = (len - head) & ~(int64_t)15, tail = len - head - body;
+          if (tid < head) d0[tid] = s0[tid];
+          if (tid < tail) d0[head + body + tid] = s0[head + body + tid];
+        }
+      }
       if (p.count_links && tid == 0 && it.edge >= 0)
         atomicAdd(p.counters + (int64_t)t * p.E + it.edge, (unsigned long long)(x1 - x0));
+    }
+    if (kEngine == 1 && tid == 0) {
+      // single-thread TMA pipeline: S loads in flight, stores drained one behind
+      fence_proxy_async();
+      const uint32_t CH = (uint32_t)p.tma_chunk;
+      BodyCursor cur{a, kend, 0, lo, hi};
+      const uint32_t g0 = gi;
+      uint32_t nl = 0, ns = 0;
+      bool more = true;
+      auto issue = [&]() -> bool {
+        const char* src;
+        char* dst;
+        uint32_t n;
+        if (!cur.next(p, CH, &src, &dst, &n)) return false;
+        const uint32_t st = (g0 + nl) % S;
+        ring_dst[st] = dst;
+        ring_n[st] = n;
+        mbar_expect_tx(&bars[st], n);
+        bulk_load(stages + (size_t)st * CH, src, n, &bars[st]);
+        ++nl;
+        return true;
+      };
+      while (more && nl < (uint32_t)S) more = issue();
+      while (ns < nl) {
+        const uint32_t st = (g0 + ns) % S;
+        mbar_wait(&bars[st], ((g0 + ns) / S) & 1);
+        bulk_store(ring_dst[st], stages + (size_t)st * CH, ring_n[st]);
+        ++ns;
+        if (more) {
+          if (S == 1) {
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            more = issue();
+          } else if (ns >= 2 && nl - (uint32_t)S == ns - 2) {
+            bulk_wait_read1();
+            more = issue();
+          }
+        }
+      }
+      bulk_wait_all();
+      fence_proxy_async();
+      gi = g0 + nl;
     }
     __syncthreads();
     if (tid == 0) {
@@ -225,7 +369,7 @@ __global__ void __launch_bounds__(1024, 1) a2a_exec_kernel(const KParams p) {
   // ---- exit: all incoming stores of every step have landed (multi-GPU)
   if (c == 0 && p.G > 1) {
     bool ok = true;
-    for (int32_t i = tid; i < p.n_exit && ok; i += blockDim.x) {
+    for (int32_t i = tid; i < p.n_exit && ok; i += kThreads) {
       const uint32_t* f = my_flags + p.exit_idx[i];
       uint64_t t0 = globaltimer();
       uint32_t spins = 0;
@@ -266,7 +410,20 @@ struct DeviceGuard {
   }
 };
 
-static const int kUnrollDefault = 4;
+// copy engines: 0 = SM load/store (LDG.128/STG.128), 1 = TMA bulk copies (UBLKCP)
+struct EngineCfg {
+  const void* fn;
+  int threads;
+  size_t smem;
+};
+static EngineCfg engine_cfg(const Plan& P) {
+  if (P.engine == 1) {
+    size_t smem = ((20 * (size_t)P.tma_stages + 127) & ~(size_t)127) +
+                  (size_t)P.tma_stages * P.tma_chunk;
+    return {(const void*)a2a_exec_kernel<1, 256>, 256, smem};
+  }
+  return {(const void*)a2a_exec_kernel<0, 1024>, 1024, 0};
+}
 
 // arena flag region: entry[G] u32 | step flags [T'][G][nC] u32
 static inline int64_t entry_flags_off() { return 0; }
@@ -315,9 +472,12 @@ static int bind_plan(Plan& P, int gpu, int dev, int nC) {
   int coop = 0;
   CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
   if (!coop) return fail(A2A_ERR_CUDA, "device does not support cooperative launch");
+  const EngineCfg ec = engine_cfg(P);
+  P.nT = ec.threads;
+  if (ec.smem > 48 * 1024)
+    CK(cudaFuncSetAttribute(ec.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ec.smem));
   int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, a2a_exec_kernel<kUnrollDefault>,
-                                                   P.nT, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ec.fn, P.nT, ec.smem));
   const int max_ctas = per_sm * prop.multiProcessorCount;
   if (nC <= 0) nC = prop.multiProcessorCount;
   if (nC > max_ctas) return fail(A2A_ERR_INVALID, "num_ctas exceeds co-resident capacity");
@@ -464,6 +624,23 @@ int a2a_plan_recv_buffer(const a2a_plan* plan, void** out_ptr) {
   return A2A_OK;
 }
 
+int a2a_plan_set_engine(a2a_plan* plan, int32_t engine, int32_t tma_chunk, int32_t tma_stages) {
+  if (!plan) return fail(A2A_ERR_INVALID, "null plan");
+  if (plan->p.bound) return fail(A2A_ERR_STATE, "set the copy engine before a2a_plan_bind");
+  if (engine != 0 && engine != 1) return fail(A2A_ERR_INVALID, "engine must be 0 (LSU) or 1 (TMA)");
+  if (engine == 1) {
+    if (tma_chunk <= 0) tma_chunk = 32768;
+    if (tma_stages <= 0) tma_stages = 6;
+    if (tma_chunk % 16 || tma_chunk > (1 << 19) || tma_stages > 32 ||
+        (size_t)tma_chunk * tma_stages > 220 * 1024)
+      return fail(A2A_ERR_INVALID, "bad TMA ring (chunk % 16, chunk*stages <= 220 KiB)");
+    plan->p.tma_chunk = tma_chunk;
+    plan->p.tma_stages = tma_stages;
+  }
+  plan->p.engine = engine;
+  return A2A_OK;
+}
+
 int a2a_plan_set_timeout(a2a_plan* plan, int64_t timeout_ns) {
   if (!plan || timeout_ns <= 0) return fail(A2A_ERR_INVALID, "bad argument");
   plan->p.timeout_ns = timeout_ns;
@@ -512,8 +689,10 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
   kp.E = P.E;
   kp.count_links = (options & A2A_EXEC_COUNT_LINKS) ? 1 : 0;
   void* args[] = {&kp};
-  cudaError_t e = cudaLaunchCooperativeKernel((const void*)a2a_exec_kernel<kUnrollDefault>,
-                                              dim3(P.nC), dim3(P.nT), args, 0,
+  kp.tma_chunk = P.tma_chunk;
+  kp.tma_stages = P.engine == 1 ? P.tma_stages : 0;
+  const EngineCfg ec = engine_cfg(P);
+  cudaError_t e = cudaLaunchCooperativeKernel(ec.fn, dim3(P.nC), dim3(ec.threads), args, ec.smem,
                                               (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchCooperativeKernel");
   P.last_stream = stream;

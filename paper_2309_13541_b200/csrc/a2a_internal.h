@@ -81,6 +81,7 @@ struct Plan {
   // ---- device binding (a2a_exec.cu)
   bool bound = false, imported = false;
   int32_t rank = -1, device = -1, nC = 0, nT = 1024;
+  int32_t engine = 0, tma_chunk = 32768, tma_stages = 6;   // copy engine (a2a_plan_set_engine)
   int64_t flags_bytes = 0;                      // arena flag region size
   std::vector<int64_t> recv_off, scratch_off;   // per gpu, inside that gpu's arena
   std::vector<int64_t> arena_bytes;             // per gpu

@@ -108,6 +108,7 @@ class Plan:
         self._h = h
         self.rank = None
         self.device = None
+        self.engine = None
 
     # ---- lifetime
     def close(self):
@@ -182,8 +183,23 @@ class Plan:
         return recvs
 
     # ---- device side
+    def set_engine(self, engine: str = "lsu", tma_chunk: int = 0, tma_stages: int = 0):
+        """Copy engine before bind: "lsu" (SM 128-bit loads/stores) or "tma"
+        (cp.async.bulk ring).  Default from $A2A_ENGINE, else "lsu"."""
+        code = {"lsu": 0, "tma": 1}[engine]
+        self._ck(N.lib.a2a_plan_set_engine(self._h, code, int(tma_chunk), int(tma_stages)),
+                 "a2a_plan_set_engine")
+        self.engine = engine
+        return self
+
     def bind(self, gpu: int = 0, device: int | None = None, num_ctas: int = 0):
         device = gpu if device is None else device
+        if getattr(self, "engine", None) is None:
+            import os
+            env = os.environ.get("A2A_ENGINE", "").strip().lower()
+            if env:
+                parts = env.split(":")      # tma[:chunk[:stages]]
+                self.set_engine(parts[0], *(int(x) for x in parts[1:]))
         self._ck(N.lib.a2a_plan_bind(self._h, int(gpu), int(device), int(num_ctas)),
                  "a2a_plan_bind")
         self.rank, self.device = int(gpu), int(device)

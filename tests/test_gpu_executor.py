@@ -132,3 +132,42 @@ def test_execute_rejects_wrong_buffers(artifacts):
             p.execute(s.float())
         with pytest.raises(TypeError):
             p.execute(s.cpu())
+
+
+@pytest.mark.parametrize("name", ["torus2x4", "gk8_2", "torus2x4_h2", "ts_hypercube3"])
+@pytest.mark.parametrize("m,ring", [(7, (0, 0)), (4096 + 5, (0, 0)), (65536, (4096, 2)),
+                                    ((1 << 20) + 48, (32768, 6)), (300000, (16, 1))])
+def test_tma_engine_bit_exact(name, m, ring, artifacts):
+    """TMA bulk-copy engine (cp.async.bulk ring) == oracle, incl. odd sizes and
+    degenerate rings (1 stage of 16 bytes)."""
+    from paper_2309_13541_b200.executor import Plan
+    from replay_bytes import replay_bytes
+    a = artifacts(name)
+    send = _send(a.g.n, m, seed=m % 97)
+    _, want, _ = replay_bytes(a.g, a.sched, send, m)
+    with Plan(a.g, a.sched, m=m) as p:
+        p.set_engine("tma", *ring)
+        p.bind(0)
+        s = torch.from_numpy(send).cuda()
+        for rep in range(2):
+            r = torch.zeros_like(s)
+            p.execute(s, r, count_links=True)
+            p.sync()
+            assert np.array_equal(r.cpu().numpy(), want)
+        dev = p.read_link_counters()
+        assert np.array_equal(dev, 2 * p.link_bytes())
+
+
+def test_tma_engine_n64(artifacts):
+    from paper_2309_13541_b200.executor import Plan
+    a = artifacts("torus4x4x4")
+    m = 65536 + 16
+    g = torch.Generator(device="cuda").manual_seed(3)
+    s = torch.randint(0, 256, (64, 64, m), dtype=torch.uint8, device="cuda", generator=g)
+    r = torch.zeros_like(s)
+    with Plan(a.g, a.sched, m=m) as p:
+        p.set_engine("tma")
+        p.bind(0)
+        p.execute(s, r)
+        p.sync()
+    assert torch.equal(r, s.transpose(0, 1).contiguous())

@@ -34,7 +34,7 @@ def _port():
     return p
 
 
-def _rank_main(rank, world, port, name, m, reps, q):
+def _rank_main(rank, world, port, name, m, reps, q, engine="lsu"):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     try:
@@ -50,6 +50,7 @@ def _rank_main(rank, world, port, name, m, reps, q):
                                 rank=rank, world_size=world)
         a = load_artifact(name)
         plan = Plan(a.g, a.sched, m=m, n_gpus=world)
+        plan.set_engine(engine)
         plan.bind(rank, device=rank)
         plan.set_timeout(20.0)
         connect(plan)
@@ -80,17 +81,18 @@ def _rank_main(rank, world, port, name, m, reps, q):
         q.put((rank, f"{ex!r}\n{traceback.format_exc()}"))
 
 
+@pytest.mark.parametrize("engine", ["lsu", "tma"])
 @pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("name,m", [("torus2x4", 4096 + 7), ("gk8_2", 65536),
-                                    ("hypercube3", 1 << 20)])
-def test_multiprocess_ipc(world, name, m):
+                                    ("hypercube3", 1 << 20), ("torus4x4x4", 8192)])
+def test_multiprocess_ipc(world, name, m, engine):
     if _ngpu() < world:
         pytest.skip(f"needs {world} GPUs")
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_rank_main, args=(r, world, port, name, m, 3, q))
+    ps = [ctx.Process(target=_rank_main, args=(r, world, port, name, m, 3, q, engine))
           for r in range(world)]
     for p in ps:
         p.start()
