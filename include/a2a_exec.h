@@ -123,6 +123,11 @@ int a2a_plan_import_pointers(a2a_plan* plan, void* const* arenas);
 /* pointer to this rank's arena recv buffer ([V_g][N][m]); with n_gpus > 1
  * peers store into it directly, so execute must be given this buffer */
 int a2a_plan_recv_buffer(const a2a_plan* plan, void** out_ptr);
+/* before bind: number of arena recv buffers (1..4, default 1) so consecutive
+ * all-to-alls can alternate buffers (overlap D2H of one with the next); every
+ * rank must pass the same buffer index to the same execute */
+int a2a_plan_set_recv_buffers(a2a_plan* plan, int32_t count);
+int a2a_plan_recv_buffer_at(const a2a_plan* plan, int32_t index, void** out_ptr);
 
 /* execute options */
 #define A2A_EXEC_COUNT_LINKS 1 /* accumulate device per-(step,edge) byte counters */

@@ -432,6 +432,10 @@ static inline int64_t flag_region_bytes(int G, int TE, int nC) {
   return (step_flags_off() + (int64_t)TE * G * nC * 4 + 65535) & ~65535LL;
 }
 
+static inline int64_t recv_stride(const Plan& P, int g) {
+  return (P.info[g].recv_bytes + 4095) & ~4095LL;
+}
+
 static void free_device(Plan& P) {
   if (P.device < 0) return;
   DeviceGuard dg(P.device);
@@ -498,7 +502,7 @@ static int bind_plan(Plan& P, int gpu, int dev, int nC) {
   P.arena_bytes.assign(G, 0);
   for (int g = 0; g < G; ++g) {
     P.recv_off[g] = P.flags_bytes;
-    P.scratch_off[g] = P.recv_off[g] + ((P.info[g].recv_bytes + 4095) & ~4095LL);
+    P.scratch_off[g] = P.recv_off[g] + (int64_t)P.n_recv * recv_stride(P, g);
     P.arena_bytes[g] = P.scratch_off[g] + P.info[g].scratch_bytes;
   }
   cudaError_t e = cudaMalloc(&P.arena, (size_t)P.arena_bytes[gpu]);
@@ -624,6 +628,15 @@ int a2a_plan_recv_buffer(const a2a_plan* plan, void** out_ptr) {
   return A2A_OK;
 }
 
+int a2a_plan_recv_buffer_at(const a2a_plan* plan, int32_t index, void** out_ptr) {
+  if (!plan || !out_ptr) return fail(A2A_ERR_INVALID, "null argument");
+  const Plan& P = plan->p;
+  if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound");
+  if (index < 0 || index >= P.n_recv) return fail(A2A_ERR_INVALID, "recv buffer index out of range");
+  *out_ptr = (char*)P.arena + P.recv_off[P.rank] + (int64_t)index * recv_stride(P, P.rank);
+  return A2A_OK;
+}
+
 int a2a_plan_set_engine(a2a_plan* plan, int32_t engine, int32_t tma_chunk, int32_t tma_stages) {
   if (!plan) return fail(A2A_ERR_INVALID, "null plan");
   if (plan->p.bound) return fail(A2A_ERR_STATE, "set the copy engine before a2a_plan_bind");
@@ -641,6 +654,14 @@ int a2a_plan_set_engine(a2a_plan* plan, int32_t engine, int32_t tma_chunk, int32
   return A2A_OK;
 }
 
+int a2a_plan_set_recv_buffers(a2a_plan* plan, int32_t count) {
+  if (!plan) return fail(A2A_ERR_INVALID, "null plan");
+  if (plan->p.bound) return fail(A2A_ERR_STATE, "set the recv buffer count before a2a_plan_bind");
+  if (count < 1 || count > 4) return fail(A2A_ERR_INVALID, "recv buffer count must be 1..4");
+  plan->p.n_recv = count;
+  return A2A_OK;
+}
+
 int a2a_plan_set_timeout(a2a_plan* plan, int64_t timeout_ns) {
   if (!plan || timeout_ns <= 0) return fail(A2A_ERR_INVALID, "bad argument");
   plan->p.timeout_ns = timeout_ns;
@@ -655,8 +676,15 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
   if (*P.h_err != 0) return fail(*P.h_err, "a previous execute failed on the device (timeout)");
   char* own_recv = (char*)P.arena + P.recv_off[P.rank];
   if (!recv) recv = own_recv;
-  if (P.G > 1 && recv != own_recv)
-    return fail(A2A_ERR_INVALID, "multi-GPU plans must receive into the arena recv buffer");
+  int32_t ridx = 0;
+  if (P.G > 1) {
+    const int64_t st = recv_stride(P, P.rank);
+    ridx = -1;
+    for (int i = 0; i < P.n_recv; ++i)
+      if ((char*)recv == own_recv + i * st) ridx = i;
+    if (ridx < 0)
+      return fail(A2A_ERR_INVALID, "multi-GPU plans must receive into an arena recv buffer");
+  }
   if (!send && P.info[P.rank].send_bytes > 0) return fail(A2A_ERR_INVALID, "null send buffer");
   DeviceGuard dg(P.device);
   KParams kp;
@@ -664,7 +692,8 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
   kp.base[loc_send()] = (char*)send;
   for (int g = 0; g < P.G; ++g) {
     char* ar = (char*)P.peer_arena[g];
-    kp.base[loc_recv(g)] = (g == P.rank) ? (char*)recv : ar + P.recv_off[g];
+    kp.base[loc_recv(g)] =
+        (g == P.rank) ? (char*)recv : ar + P.recv_off[g] + (int64_t)ridx * recv_stride(P, g);
     kp.base[loc_scratch(g, P.G)] = ar + P.scratch_off[g];
     kp.entry_flags[g] = (uint32_t*)(ar + entry_flags_off());
     kp.step_flags[g] = (uint32_t*)(ar + step_flags_off());

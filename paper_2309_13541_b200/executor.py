@@ -226,11 +226,17 @@ class Plan:
         arr = (C.c_void_p * self.n_gpus)(*ptrs)
         self._ck(N.lib.a2a_plan_import_pointers(self._h, arr), "a2a_plan_import_pointers")
 
-    def recv_buffer(self):
-        """torch uint8 view [V_g, N, m] of this rank's arena recv buffer."""
+    def set_recv_buffers(self, count: int):
+        """Before bind: arena recv buffers to alternate between (1..4)."""
+        self._ck(N.lib.a2a_plan_set_recv_buffers(self._h, int(count)), "a2a_plan_set_recv_buffers")
+        return self
+
+    def recv_buffer(self, index: int = 0):
+        """torch uint8 view [V_g, N, m] of this rank's arena recv buffer `index`."""
         import torch
         p = C.c_void_p()
-        self._ck(N.lib.a2a_plan_recv_buffer(self._h, C.byref(p)), "a2a_plan_recv_buffer")
+        self._ck(N.lib.a2a_plan_recv_buffer_at(self._h, int(index), C.byref(p)),
+                 "a2a_plan_recv_buffer_at")
         V = self.gpu_info(self.rank)["n_local_nodes"]
         return _device_tensor(p.value, (V, self.n, self.m), self.device, torch)
 

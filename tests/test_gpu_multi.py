@@ -135,3 +135,60 @@ def test_single_process_peer_pointers():
         assert np.array_equal(recvs[r].cpu().numpy(), want)
     for p in plans:
         p.close()
+
+
+def _alt_main(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    try:
+        import torch
+        import torch.distributed as dist
+        from replay_bytes import make_send
+
+        from paper_2309_13541_b200.artifacts import load_artifact
+        from paper_2309_13541_b200.dist import connect, local_nodes
+        from paper_2309_13541_b200.executor import Plan
+        torch.cuda.set_device(rank)
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}",
+                                rank=rank, world_size=world)
+        a = load_artifact("gk8_2")
+        m = 20000
+        plan = Plan(a.g, a.sched, m=m, n_gpus=world).set_recv_buffers(2)
+        plan.bind(rank, device=rank)
+        connect(plan)
+        nodes = local_nodes(plan, rank)
+        bufs = [plan.recv_buffer(0), plan.recv_buffer(1)]
+        ok = True
+        wants = []
+        for k in range(4):
+            send_all = make_send(8, m, seed=50 + k)
+            send = torch.from_numpy(np.ascontiguousarray(send_all[nodes])).cuda(rank)
+            plan.execute(send, bufs[k & 1])
+            wants.append(np.swapaxes(send_all, 0, 1)[nodes])
+            plan.sync()
+            if k >= 1:  # the other buffer still holds the previous all-to-all
+                ok &= bool(np.array_equal(bufs[(k - 1) & 1].cpu().numpy(), wants[k - 1]))
+            ok &= bool(np.array_equal(bufs[k & 1].cpu().numpy(), wants[k]))
+        q.put((rank, ok))
+        plan.close()
+        dist.destroy_process_group()
+    except Exception as ex:
+        import traceback
+        q.put((rank, f"{ex!r}\n{traceback.format_exc()}"))
+
+
+def test_alternating_recv_buffers():
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_alt_main, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=300) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    for r in res:
+        assert r[1] is True, r

@@ -18,13 +18,17 @@ from replay_bytes import make_send, replay_bytes
 
 ALL = ["torus2x4", "hypercube3", "gk8_2", "torus2x4_h1", "torus2x4_h2", "gk8_2_h1",
        "ts_ring3", "ts_torus2x4", "ts_hypercube3", "ts_gk8_2", "ts_torus3x3",
-       "torus4x4x4", "gk64_4", "gk64_4_h2"]
+       "torus4x4x4", "gk64_4", "gk64_4_h2", "gk256_4", "gk256_4_h2"]
 
 
 def _available(names):
+    import json
+    import os
     from paper_2309_13541_b200.artifacts import list_artifacts
     have = set(list_artifacts())
-    return [n for n in names if n in have]
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden.json")) as fh:
+        gold = set(json.load(fh)["configs"])
+    return [n for n in names if n in have and n in gold]
 
 
 @pytest.mark.parametrize("name", _available(ALL))
