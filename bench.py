@@ -261,6 +261,9 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     torch.cuda.synchronize(dev)
     clock_rec = clk.stop() if clk else None
     ctx.barrier()
+    from paper_2309_13541_b200.executor import timeline_summary
+    tls = timeline_summary(plan.read_timeline())            # last timed launch, this rank
+    tls["kernel_us"] = ctx.allmax([tls["kernel_us"]])[0]
     per = ctx.allmax([a.elapsed_time(b) for a, b in zip(e0, e1)])
     T = sum(per) / len(per) / 1e3                      # s per all-to-all (max over ranks)
     payload = n * (n - 1) * m
@@ -394,6 +397,7 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     res = {"T": T, "per_step_ms": per, "value": value, "per_gpu": value / G,
            "t_lb": t_lb, "bound_frac": t_lb / T, "roofline": roof, "nccl": nres, "e2e": eres,
            "recv_ok": bool(ok), "clocks": clock_rec, "sync": plan.sync_stats(rank),
+           "kernel_timeline": tls,
            "num_ctas": plan_ctas(plan, num_ctas), "egress_max": max(i["egress_bytes"] for i in infos),
            "scratch_bytes": info["scratch_bytes"]}
     plan.close()
@@ -468,6 +472,7 @@ def main(argv=None):
             "e2e": r["e2e"],
             "nccl": r["nccl"],
             "gpu_launches": args.steps,
+            "kernel_timeline_last_step": r["kernel_timeline"],
             "clocks": r["clocks"],
         }
         print(json.dumps(line), flush=True)

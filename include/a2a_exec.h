@@ -141,10 +141,14 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
 int a2a_plan_sync(a2a_plan* plan);
 /* device byte counters of this rank, out[t * n_edges + e]; then zeroes them */
 int a2a_plan_read_link_counters(a2a_plan* plan, int64_t* out);
-/* copy engine, before bind: 0 = SM 128-bit load/store loop (default),
- * 1 = TMA bulk copies (cp.async.bulk global->smem->global, mbarrier ring of
- * `tma_stages` x `tma_chunk` bytes per CTA; 0 = defaults 6 x 32 KiB) */
+/* copy engine, before bind: 0 = SM 128-bit load/store loop,
+ * 1 = TMA bulk copies (default; cp.async.bulk global->smem->global, mbarrier
+ * ring of `tma_stages` x `tma_chunk` bytes per CTA; 0 = defaults 6 x 32 KiB) */
 int a2a_plan_set_engine(a2a_plan* plan, int32_t engine, int32_t tma_chunk, int32_t tma_stages);
+/* per-CTA %globaltimer timeline of the last execute: out[c][j], j = 0 start,
+ * 1 entry barrier passed, 2+t step t published (0 = no work), 2+T' exit;
+ * *out_cols = T'+3 (call with out = NULL to get the width) */
+int a2a_plan_read_timeline(a2a_plan* plan, uint64_t* out, int32_t* out_cols);
 /* device-side flag-wait timeout (ns, default 10 s) */
 int a2a_plan_set_timeout(a2a_plan* plan, int64_t timeout_ns);
 

@@ -58,6 +58,7 @@ struct KParams {
   uint32_t epoch;
   int32_t G, rank, nC, T, E, count_links;
   int32_t tma_chunk, tma_stages;           // TMA engine: bytes per bulk copy, ring depth
+  unsigned long long* timeline;            // [nC][T'+3] %globaltimer: start, entry done, steps.., end
 };
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -230,7 +231,9 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
   uint32_t* ring_n = reinterpret_cast<uint32_t*>(dsmem + 16 * S);
   char* stages = reinterpret_cast<char*>(dsmem + ((20 * S + 127) & ~127));
   uint32_t gi = 0;  // TMA chunks consumed so far (thread 0): stage/phase bookkeeping
+  unsigned long long* tl = p.timeline + (int64_t)c * (p.T + 3);
   if (tid == 0) {
+    tl[0] = globaltimer();
     s_abort = 0;
     if (kEngine == 1) {
       for (int i = 0; i < S; ++i) mbar_init(&bars[i], 1);
@@ -266,11 +269,15 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
     __syncthreads();
     if (s_abort) return;
   }
+  if (tid == 0) tl[1] = globaltimer();
 
   for (int t = 0; t < p.T; ++t) {
     const int64_t B = p.step_bytes[t];
     const int64_t lo = cta_lo(B, c, p.nC), hi = cta_lo(B, c + 1, p.nC);
-    if (hi <= lo) continue;
+    if (hi <= lo) {
+      if (tid == 0) tl[2 + t] = 0;
+      continue;
+    }
     const int32_t w0 = p.wait_off[t * p.nC + c], w1 = p.wait_off[t * p.nC + c + 1];
     if (w1 > w0) {
       if (warp == 0) {
@@ -364,6 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
         mask &= mask - 1;
         st_release_sys(p.step_flags[h] + slot, p.epoch);
       }
+      tl[2 + t] = globaltimer();
     }
   }
   // ---- exit: all incoming stores of every step have landed (multi-GPU)
@@ -382,7 +390,9 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
       }
     }
     if (!ok) atomicCAS(p.err, 0, (int32_t)A2A_ERR_TIMEOUT);
+    __syncthreads();
   }
+  if (tid == 0) tl[2 + p.T] = globaltimer();
 }
 
 static int cuda_fail(cudaError_t e, const char* what) {
@@ -445,7 +455,7 @@ static void free_device(Plan& P) {
     P.peer_arena[g] = nullptr;
   }
   void** bufs[] = {&P.arena, &P.d_items, &P.d_step_begin, &P.d_step_bytes, &P.d_dst_mask, &P.d_exit_idx,
-                   &P.d_wait_off, &P.d_wait_idx, &P.d_counters};
+                   &P.d_wait_off, &P.d_wait_idx, &P.d_counters, &P.d_timeline};
   for (void** b : bufs) {
     if (*b) cudaFree(*b);
     *b = nullptr;
@@ -521,6 +531,8 @@ static int bind_plan(Plan& P, int gpu, int dev, int nC) {
   if ((rc = upload(&P.d_wait_off, S.wait_off[gpu])) != A2A_OK) return rc;
   if ((rc = upload(&P.d_wait_idx, S.wait_idx[gpu])) != A2A_OK) return rc;
   if ((rc = upload(&P.d_exit_idx, S.exit_idx[gpu])) != A2A_OK) return rc;
+  CK(cudaMalloc(&P.d_timeline, (size_t)nC * (TE + 3) * 8));
+  CK(cudaMemset(P.d_timeline, 0, (size_t)nC * (TE + 3) * 8));
   size_t cbytes = std::max<size_t>((size_t)TE * std::max(P.E, 1) * 8, 16);
   CK(cudaMalloc(&P.d_counters, cbytes));
   CK(cudaMemset(P.d_counters, 0, cbytes));
@@ -718,6 +730,7 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
   kp.E = P.E;
   kp.count_links = (options & A2A_EXEC_COUNT_LINKS) ? 1 : 0;
   void* args[] = {&kp};
+  kp.timeline = (unsigned long long*)P.d_timeline;
   kp.tma_chunk = P.tma_chunk;
   kp.tma_stages = P.engine == 1 ? P.tma_stages : 0;
   const EngineCfg ec = engine_cfg(P);
@@ -738,6 +751,18 @@ int a2a_plan_sync(a2a_plan* plan) {
   if (*P.h_err != 0) {
     return fail(*P.h_err, "device-side flag wait timed out (a peer did not arrive)");
   }
+  return A2A_OK;
+}
+
+int a2a_plan_read_timeline(a2a_plan* plan, uint64_t* out, int32_t* out_cols) {
+  if (!plan || !out_cols) return fail(A2A_ERR_INVALID, "null argument");
+  Plan& P = plan->p;
+  if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound");
+  *out_cols = P.T_exec + 3;
+  if (!out) return A2A_OK;
+  DeviceGuard dg(P.device);
+  CK(cudaStreamSynchronize((cudaStream_t)P.last_stream));
+  CK(cudaMemcpy(out, P.d_timeline, (size_t)P.nC * (P.T_exec + 3) * 8, cudaMemcpyDeviceToHost));
   return A2A_OK;
 }
 

@@ -81,7 +81,7 @@ struct Plan {
   // ---- device binding (a2a_exec.cu)
   bool bound = false, imported = false;
   int32_t rank = -1, device = -1, nC = 0, nT = 1024;
-  int32_t engine = 0, tma_chunk = 32768, tma_stages = 6;   // copy engine (a2a_plan_set_engine)
+  int32_t engine = 1, tma_chunk = 32768, tma_stages = 6;   // copy engine (a2a_plan_set_engine)
   int32_t n_recv = 1;                                        // arena recv buffers (multi-buffering)
   int64_t flags_bytes = 0;                      // arena flag region size
   std::vector<int64_t> recv_off, scratch_off;   // per gpu, inside that gpu's arena
@@ -97,6 +97,7 @@ struct Plan {
   void* d_wait_off = nullptr;
   void* d_wait_idx = nullptr;
   void* d_counters = nullptr;
+  void* d_timeline = nullptr;
   int32_t* h_err = nullptr;                     // mapped pinned error word
   int32_t* d_err = nullptr;
   uint32_t epoch = 0;

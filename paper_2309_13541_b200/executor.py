@@ -25,7 +25,21 @@ import numpy as np
 from . import _native as N
 
 __all__ = ["EvalError", "ExecutorError", "Plan", "replay_timestep_schedule",
-           "execute_timestep_schedule", "contiguous_placement"]
+           "execute_timestep_schedule", "contiguous_placement", "timeline_summary"]
+
+
+def timeline_summary(tl: np.ndarray) -> dict:
+    """Kernel-internal timing from Plan.read_timeline(): microseconds from the
+    earliest CTA start to the entry barrier, each step's last publication and
+    the last CTA exit."""
+    t0 = int(tl[:, 0].min())
+    us = lambda x: round((int(x) - t0) / 1e3, 3)  # noqa: E731
+    steps = []
+    for j in range(2, tl.shape[1] - 1):
+        col = tl[:, j][tl[:, j] > 0]
+        steps.append(us(col.max()) if col.size else None)
+    return {"kernel_us": us(tl[:, -1].max()), "start_spread_us": us(tl[:, 0].max()),
+            "entry_us": us(tl[:, 1].max()), "step_done_us": steps}
 
 
 class EvalError(RuntimeError):
@@ -109,6 +123,8 @@ class Plan:
         self.rank = None
         self.device = None
         self.engine = None
+        self._bufcheck = None
+        self._num_ctas = 0
 
     # ---- lifetime
     def close(self):
@@ -184,8 +200,8 @@ class Plan:
 
     # ---- device side
     def set_engine(self, engine: str = "lsu", tma_chunk: int = 0, tma_stages: int = 0):
-        """Copy engine before bind: "lsu" (SM 128-bit loads/stores) or "tma"
-        (cp.async.bulk ring).  Default from $A2A_ENGINE, else "lsu"."""
+        """Copy engine before bind: "tma" (cp.async.bulk ring, the default) or
+        "lsu" (SM 128-bit loads/stores).  Default from $A2A_ENGINE, else "tma"."""
         code = {"lsu": 0, "tma": 1}[engine]
         self._ck(N.lib.a2a_plan_set_engine(self._h, code, int(tma_chunk), int(tma_stages)),
                  "a2a_plan_set_engine")
@@ -202,6 +218,8 @@ class Plan:
                 self.set_engine(parts[0], *(int(x) for x in parts[1:]))
         self._ck(N.lib.a2a_plan_bind(self._h, int(gpu), int(device), int(num_ctas)),
                  "a2a_plan_bind")
+        self._num_ctas = int(num_ctas)
+        self._bufcheck = None
         self.rank, self.device = int(gpu), int(device)
         return self
 
@@ -244,20 +262,41 @@ class Plan:
         self._ck(N.lib.a2a_plan_set_timeout(self._h, int(seconds * 1e9)), "a2a_plan_set_timeout")
 
     def execute(self, send, recv=None, stream=None, count_links: bool = False):
-        """Launch one all-to-all (asynchronous on ``stream``)."""
+        """Launch one all-to-all (asynchronous on ``stream``, default: current)."""
         import torch
-        info = self.gpu_info(self.rank)
-        _check_buf(send, info["send_bytes"], self.device, "send", torch)
+        ck = self._bufcheck
+        if ck is None:
+            info = self.gpu_info(self.rank)
+            ck = self._bufcheck = (info["send_bytes"], info["recv_bytes"])
+        _check_buf(send, ck[0], self.device, "send", torch)
         rp = None
         if recv is not None:
-            _check_buf(recv, info["recv_bytes"], self.device, "recv", torch)
+            _check_buf(recv, ck[1], self.device, "recv", torch)
             rp = recv.data_ptr()
         if stream is None:
             stream = torch.cuda.current_stream(self.device)
         sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
-        self._ck(N.lib.a2a_plan_execute(
-            self._h, C.c_void_p(send.data_ptr()), C.c_void_p(rp), C.c_void_p(sp),
-            N.A2A_EXEC_COUNT_LINKS if count_links else 0), "a2a_plan_execute")
+        rc = N.lib.a2a_plan_execute(self._h, send.data_ptr(), rp, sp,
+                                    N.A2A_EXEC_COUNT_LINKS if count_links else 0)
+        if rc:
+            _raise(rc, "a2a_plan_execute")
+
+    def read_timeline(self) -> np.ndarray:
+        """Per-CTA %globaltimer stamps of the last execute, uint64 [nC, T'+3]:
+        start, entry barrier passed, step t published (0 = idle), exit."""
+        cols = C.c_int32()
+        self._ck(N.lib.a2a_plan_read_timeline(self._h, None, C.byref(cols)), "a2a_plan_read_timeline")
+        n_cta = self._n_ctas()
+        out = np.zeros((n_cta, cols.value), dtype=np.uint64)
+        self._ck(N.lib.a2a_plan_read_timeline(self._h, out.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                              C.byref(cols)), "a2a_plan_read_timeline")
+        return out
+
+    def _n_ctas(self):
+        if self._num_ctas:
+            return self._num_ctas
+        import torch
+        return torch.cuda.get_device_properties(self.device).multi_processor_count
 
     def sync(self):
         self._ck(N.lib.a2a_plan_sync(self._h), "a2a_plan_sync")

@@ -76,6 +76,7 @@ def main(argv=None):
                     "t_lb_ms": round(r["t_lb"] * 1e3, 4), "bound_frac": round(r["bound_frac"], 4),
                     "roofline": r["roofline"], "nccl": r["nccl"], "recv_ok": r["recv_ok"],
                     "clocks": r["clocks"], "sync_flags": r["sync"],
+                    "kernel_timeline": r["kernel_timeline"],
                     "egress_max_bytes": r["egress_max"], "scratch_bytes": r["scratch_bytes"],
                     "wall_s": round(time.time() - t0, 1)})
         if ctx.rank == 0:
