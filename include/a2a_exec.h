@@ -47,7 +47,8 @@ typedef struct {
 } a2a_op;
 
 /* descriptor flags */
-#define A2A_COPY_SELF 1 /* also copy the self shard send[v][v] -> recv[v][v] */
+#define A2A_COPY_SELF 1  /* also copy the self shard send[v][v] -> recv[v][v] */
+#define A2A_INTERLEAVE 2 /* split items (split_bytes) and interleave destination GPUs */
 
 typedef struct {
   int32_t n_nodes;         /* Digraph.n (must equal ChunkedSchedule.n)      */
@@ -61,7 +62,8 @@ typedef struct {
   int64_t n_ops;
   const int32_t* node_gpu; /* [n_nodes] virtual node -> GPU rank; NULL = all on 0 */
   int32_t n_gpus;          /* >= 1                                           */
-  int32_t flags;           /* A2A_COPY_SELF ...                              */
+  int32_t flags;           /* A2A_COPY_SELF | A2A_INTERLEAVE                 */
+  int64_t split_bytes;     /* piece size for A2A_INTERLEAVE (0 = 256 KiB)    */
 } a2a_schedule_desc;
 
 typedef struct a2a_plan a2a_plan;

@@ -14,6 +14,7 @@ __all__ = ["lib", "A2AOp", "ScheduleDesc", "GpuInfo", "LIB_PATH", "STATUS",
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_a2a_exec.so")
 
 A2A_COPY_SELF = 1
+A2A_INTERLEAVE = 2
 A2A_EXEC_COUNT_LINKS = 1
 STATUS = {0: "OK", 1: "INVALID", 2: "EVAL", 3: "CUDA", 4: "TIMEOUT", 5: "STATE", 6: "NOMEM"}
 
@@ -29,7 +30,7 @@ class ScheduleDesc(C.Structure):
         ("edge_uv", C.POINTER(C.c_int32)), ("edge_cap", C.POINTER(C.c_double)),
         ("ops", C.POINTER(A2AOp)), ("n_ops", C.c_int64),
         ("node_gpu", C.POINTER(C.c_int32)), ("n_gpus", C.c_int32),
-        ("flags", C.c_int32),
+        ("flags", C.c_int32), ("split_bytes", C.c_int64),
     ]
 
 

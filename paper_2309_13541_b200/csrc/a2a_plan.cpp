@@ -305,8 +305,13 @@ static int build_plan(Plan& P, const a2a_schedule_desc* D) {
       P.info[g].local_bytes += m;
     }
   }
-  // order each (gpu, step) list by destination GPU (stable): CTAs then cover
-  // few destinations each (fewer flags) while all destinations stay busy.
+  // Order each (gpu, step) list.  Default: grouped by destination GPU
+  // (stable), so CTAs cover few destinations each.  A2A_INTERLEAVE: items are
+  // split into <= split_bytes pieces (multiples of 64 B, alignment kept) and
+  // the destination classes are merged in proportion to their byte totals, so
+  // every CTA range drives every NVLink peer (and local HBM) at once.
+  const bool interleave = (P.flags & A2A_INTERLEAVE) && G > 1;
+  const int64_t split = std::max<int64_t>(64, (D->split_bytes > 0 ? D->split_bytes : 262144) & ~63LL);
   for (int g = 0; g < G; ++g) {
     auto& tb = P.tables[g];
     tb.step_begin.assign(TE + 1, 0);
@@ -317,6 +322,37 @@ static int build_plan(Plan& P, const a2a_schedule_desc* D) {
         int ka = (a.dst_gpu - g + G) % G, kb = (b.dst_gpu - g + G) % G;
         return ka < kb;
       });
+      if (interleave) {
+        std::vector<std::vector<DevItem>> bucket(G);
+        std::vector<int64_t> total(G, 0), emitted(G, 0);
+        std::vector<size_t> pos(G, 0);
+        for (auto& it : L) {
+          for (int64_t x = 0; x < it.nbytes; x += split) {
+            DevItem pc = it;
+            pc.src_off += x;
+            pc.dst_off += x;
+            pc.nbytes = std::min(split, it.nbytes - x);
+            bucket[it.dst_gpu].push_back(pc);
+          }
+          total[it.dst_gpu] += it.nbytes;
+        }
+        std::vector<DevItem> out;
+        out.reserve(L.size() * 2);
+        for (;;) {
+          int best = -1;
+          double bf = 2.0;
+          for (int h = 0; h < G; ++h) {
+            if (pos[h] >= bucket[h].size()) continue;
+            double f = (double)emitted[h] / (double)total[h];
+            if (f < bf) { bf = f; best = h; }
+          }
+          if (best < 0) break;
+          const DevItem& pc = bucket[best][pos[best]++];
+          emitted[best] += pc.nbytes;
+          out.push_back(pc);
+        }
+        L.swap(out);
+      }
       tb.step_begin[t] = (int64_t)tb.items.size();
       int64_t pre = 0;
       for (auto& it : L) {

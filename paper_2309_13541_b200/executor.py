@@ -89,7 +89,8 @@ class Plan:
     """Validated, laid-out execution plan of one ts schedule at shard size m."""
 
     def __init__(self, g, sched, m: int, placement=None, n_gpus: int = 1,
-                 copy_self: bool = True, ops: np.ndarray | None = None):
+                 copy_self: bool = True, ops: np.ndarray | None = None,
+                 order: str | None = None, split_bytes: int = 0):
         _check_mode(g, sched)
         if int(m) != m or m < 0:
             raise ValueError(f"shard size m must be a non-negative integer, got {m}")
@@ -114,7 +115,15 @@ class Plan:
         d.n_ops = self._ops.shape[0]
         d.node_gpu = self.placement.ctypes.data_as(C.POINTER(C.c_int32))
         d.n_gpus = self.n_gpus
-        d.flags = N.A2A_COPY_SELF if copy_self else 0
+        if order is None:
+            import os
+            order = os.environ.get("A2A_ORDER", "grouped")
+        if order not in ("grouped", "interleaved"):
+            raise ValueError("order must be 'grouped' or 'interleaved'")
+        self.order = order
+        d.flags = (N.A2A_COPY_SELF if copy_self else 0) | \
+            (N.A2A_INTERLEAVE if order == "interleaved" else 0)
+        d.split_bytes = int(split_bytes)
         h = C.c_void_p()
         rc = N.lib.a2a_plan_create(C.byref(d), C.byref(h))
         if rc:

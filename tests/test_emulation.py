@@ -56,3 +56,23 @@ def test_dependency_lists_are_needed(artifacts):
         p.prepare(8)
         st = p.sync_stats(0)
     assert st["wait_flags"] > 0
+
+
+@pytest.mark.parametrize("name,G", [("gk8_2", 2), ("gk8_2", 8), ("torus4x4x4", 4),
+                                    ("hypercube3", 4), ("torus2x4_h2", 2)])
+@pytest.mark.parametrize("split", [64, 4096, 0])
+def test_interleaved_order_interleavings(name, G, split, artifacts):
+    """Destination-interleaved item order (split pieces) keeps bytes and deps exact."""
+    a = artifacts(name)
+    m = 5000 if a.g.n <= 8 else 1024
+    send = make_send(a.g.n, m, seed=2)
+    with Plan(a.g, a.sched, m=m, n_gpus=G, order="interleaved", split_bytes=split) as p:
+        nodes = [local_nodes(p, g) for g in range(G)]
+        for seed in range(2):
+            recvs = p.emulate([send[ns] for ns in nodes], num_ctas=37, seed=seed)
+            want = np.swapaxes(send, 0, 1)
+            for g in range(G):
+                assert np.array_equal(recvs[g], want[nodes[g]])
+        lb = p.link_bytes()
+    with Plan(a.g, a.sched, m=m, n_gpus=G) as q:
+        assert np.array_equal(lb, q.link_bytes())
