@@ -151,6 +151,10 @@ int a2a_plan_set_engine(a2a_plan* plan, int32_t engine, int32_t tma_chunk, int32
  * 1 entry barrier passed, 2+t step t published (0 = no work), 2+T' exit;
  * *out_cols = T'+3 (call with out = NULL to get the width) */
 int a2a_plan_read_timeline(a2a_plan* plan, uint64_t* out, int32_t* out_cols);
+/* step-flag publication variant (tuning/diagnostics): bit0 = fence.acq_rel
+ * instead of fence.sc before the release store, bit1 = no explicit fence
+ * (bar.sync + st.release cumulativity), bit2 = system scope even on one GPU */
+int a2a_plan_set_sync_mode(a2a_plan* plan, int32_t mode);
 /* device-side flag-wait timeout (ns, default 10 s) */
 int a2a_plan_set_timeout(a2a_plan* plan, int64_t timeout_ns);
 

@@ -58,6 +58,8 @@ struct KParams {
   uint32_t epoch;
   int32_t G, rank, nC, T, E, count_links;
   int32_t tma_chunk, tma_stages;           // TMA engine: bytes per bulk copy, ring depth
+  int32_t sync_mode;                       // bit0: acq_rel (not sc) publish fence; bit1: no
+                                           // explicit publish fence; bit2: force .sys at G=1
   unsigned long long* timeline;            // [nC][T'+3] %globaltimer: start, entry done, steps.., end
 };
 
@@ -73,6 +75,26 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 }
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p, bool sys) {
+  uint32_t v;
+  if (sys)
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  else
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v, bool sys) {
+  if (sys)
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  else
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel(bool sys) {
+  if (sys)
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+  else
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 __device__ __forceinline__ int4 ld_stream(const int4* p) {
   int4 r;
@@ -166,14 +188,14 @@ __device__ __forceinline__ void fence_proxy_async() {
 
 // Warp 0 waits until every listed flag reached `epoch`.  Returns false on timeout.
 __device__ bool warp_wait_flags(const uint32_t* flags, const int32_t* idx, int32_t lo, int32_t hi,
-                                uint32_t epoch, int64_t timeout_ns, int32_t* err) {
+                                uint32_t epoch, int64_t timeout_ns, int32_t* err, bool sys) {
   const int lane = threadIdx.x & 31;
   bool ok = true;
   uint64_t t0 = 0;
   for (int32_t i = lo + lane; i < hi; i += 32) {
     const uint32_t* f = flags + idx[i];
     uint32_t spins = 0;
-    while ((int32_t)(ld_acquire_sys(f) - epoch) < 0) {
+    while ((int32_t)(ld_acquire(f, sys) - epoch) < 0) {
       if ((++spins & 255) == 0) {
         uint64_t now = globaltimer();
         if (t0 == 0) t0 = now;
@@ -242,6 +264,8 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
   }
   __syncthreads();
   const uint32_t* my_flags = p.step_flags[p.rank];
+  // one GPU: every producer and consumer is on this GPU -> .gpu scope suffices
+  const bool sys = p.G > 1 || (p.sync_mode & 4);
 
   // ---- entry barrier: announce epoch to every peer, then wait for theirs
   if (p.G > 1) {
@@ -281,9 +305,9 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
     const int32_t w0 = p.wait_off[t * p.nC + c], w1 = p.wait_off[t * p.nC + c + 1];
     if (w1 > w0) {
       if (warp == 0) {
-        bool ok = warp_wait_flags(my_flags, p.wait_idx, w0, w1, p.epoch, p.timeout_ns, p.err);
+        bool ok = warp_wait_flags(my_flags, p.wait_idx, w0, w1, p.epoch, p.timeout_ns, p.err, sys);
         if (!ok && tid == 0) s_abort = 1;
-        if (tid == 0) __threadfence_system();
+        if (tid == 0) fence_acq_rel(sys);
       }
       __syncthreads();
       if (s_abort) return;
@@ -364,12 +388,16 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
     __syncthreads();
     if (tid == 0) {
       uint32_t mask = p.dst_mask[(int64_t)t * p.nC + c];
-      __threadfence_system();
+      if (!(p.sync_mode & 2)) {
+        if (p.sync_mode & 1) fence_acq_rel(sys);
+        else if (sys) __threadfence_system();
+        else __threadfence();
+      }
       const int64_t slot = ((int64_t)t * p.G + p.rank) * p.nC + c;
       while (mask) {
         const int h = __ffs(mask) - 1;
         mask &= mask - 1;
-        st_release_sys(p.step_flags[h] + slot, p.epoch);
+        st_release(p.step_flags[h] + slot, p.epoch, sys);
       }
       tl[2 + t] = globaltimer();
     }
@@ -674,6 +702,12 @@ int a2a_plan_set_recv_buffers(a2a_plan* plan, int32_t count) {
   return A2A_OK;
 }
 
+int a2a_plan_set_sync_mode(a2a_plan* plan, int32_t mode) {
+  if (!plan || mode < 0 || mode > 7) return fail(A2A_ERR_INVALID, "bad sync mode");
+  plan->p.sync_mode = mode;
+  return A2A_OK;
+}
+
 int a2a_plan_set_timeout(a2a_plan* plan, int64_t timeout_ns) {
   if (!plan || timeout_ns <= 0) return fail(A2A_ERR_INVALID, "bad argument");
   plan->p.timeout_ns = timeout_ns;
@@ -731,6 +765,7 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
   kp.count_links = (options & A2A_EXEC_COUNT_LINKS) ? 1 : 0;
   void* args[] = {&kp};
   kp.timeline = (unsigned long long*)P.d_timeline;
+  kp.sync_mode = P.sync_mode;
   kp.tma_chunk = P.tma_chunk;
   kp.tma_stages = P.engine == 1 ? P.tma_stages : 0;
   const EngineCfg ec = engine_cfg(P);

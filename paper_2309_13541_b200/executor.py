@@ -225,6 +225,9 @@ class Plan:
             if env:
                 parts = env.split(":")      # tma[:chunk[:stages]]
                 self.set_engine(parts[0], *(int(x) for x in parts[1:]))
+        import os
+        if os.environ.get("A2A_SYNC_MODE"):
+            self.set_sync_mode(int(os.environ["A2A_SYNC_MODE"]))
         self._ck(N.lib.a2a_plan_bind(self._h, int(gpu), int(device), int(num_ctas)),
                  "a2a_plan_bind")
         self._num_ctas = int(num_ctas)
@@ -266,6 +269,11 @@ class Plan:
                  "a2a_plan_recv_buffer_at")
         V = self.gpu_info(self.rank)["n_local_nodes"]
         return _device_tensor(p.value, (V, self.n, self.m), self.device, torch)
+
+    def set_sync_mode(self, mode: int):
+        """Step-flag publication variant (see a2a_plan_set_sync_mode)."""
+        self._ck(N.lib.a2a_plan_set_sync_mode(self._h, int(mode)), "a2a_plan_set_sync_mode")
+        return self
 
     def set_timeout(self, seconds: float):
         self._ck(N.lib.a2a_plan_set_timeout(self._h, int(seconds * 1e9)), "a2a_plan_set_timeout")
