@@ -44,11 +44,8 @@ struct KParams {
   char* base[1 + 2 * A2A_MAX_GPUS];        // send | recv[G] | scratch[G]
   uint32_t* step_flags[A2A_MAX_GPUS];      // per GPU: [T'][G][nC] u32, slot (t, producer gpu, cta)
   uint32_t* entry_flags[A2A_MAX_GPUS];     // per GPU: [G] u32
-  const DevItem* items;
-  const int64_t* step_begin;               // [T'+1]
-  const int64_t* step_bytes;               // [T']
-  const uint32_t* dst_mask;                // [T'][nC] bit h: CTA wrote to GPU h in step t
-  const int32_t* wait_off;                 // [T'*nC + 1] ranges into wait_idx
+  const DevPiece* pieces;                  // this GPU's pieces, ordered by (cta, step)
+  const CtaStep* prog;                     // [nC][T'] per-CTA step programs
   const int32_t* wait_idx;                 // producer flag indices in own step_flags
   const int32_t* exit_idx;                 // every producer flag of this GPU (exit wait)
   int32_t n_exit;
@@ -60,6 +57,7 @@ struct KParams {
   int32_t tma_chunk, tma_stages;           // TMA engine: bytes per bulk copy, ring depth
   int32_t sync_mode;                       // bit0: acq_rel (not sc) publish fence; bit1: no
                                            // explicit publish fence; bit2: force .sys at G=1
+  int32_t smem_prog, smem_batch, batch;    // dynamic smem offsets, pieces per staged batch
   unsigned long long* timeline;            // [nC][T'+3] %globaltimer: start, entry done, steps.., end
 };
 
@@ -212,28 +210,27 @@ __device__ bool warp_wait_flags(const uint32_t* flags, const int32_t* idx, int32
   return ok;
 }
 
-// Chunk cursor over the 16-byte-aligned bodies of one CTA's pieces in a step
+// Chunk cursor over the 16-byte-aligned bodies of a staged batch of pieces
 // (TMA engine).  Heads/tails and misaligned pieces are copied by threads.
 struct BodyCursor {
-  int64_t k, kend, off, lo, hi;
-  __device__ bool next(const KParams& p, uint32_t ch, const char** src, char** dst, uint32_t* n) {
-    while (k < kend) {
-      const DevItem& it = p.items[k];
-      if (it.prefix >= hi) { k = kend; break; }
-      const int64_t x0 = max(lo, it.prefix) - it.prefix;
-      const int64_t x1 = min(hi, it.prefix + it.nbytes) - it.prefix;
-      const char* s0 = p.base[it.src_loc] + it.src_off + x0;
-      char* d0 = p.base[it.dst_loc] + it.dst_off + x0;
-      const int64_t len = x1 - x0;
-      if (len <= 0 || (((uintptr_t)s0 ^ (uintptr_t)d0) & 15) != 0) { ++k; off = 0; continue; }
+  const DevPiece* pc;
+  int32_t k, n;
+  int64_t off;
+  __device__ bool next(const KParams& p, uint32_t ch, const char** src, char** dst, uint32_t* len) {
+    while (k < n) {
+      const DevPiece& q = pc[k];
+      const char* s0 = p.base[q.src_loc] + q.src_off;
+      char* d0 = p.base[q.dst_loc] + q.dst_off;
+      const int64_t L = q.nbytes;
+      if ((((uintptr_t)s0 ^ (uintptr_t)d0) & 15) != 0) { ++k; off = 0; continue; }
       int64_t head = (16 - ((uintptr_t)d0 & 15)) & 15;
-      if (head > len) head = len;
-      const int64_t body = (len - head) & ~(int64_t)15;
+      if (head > L) head = L;
+      const int64_t body = (L - head) & ~(int64_t)15;
       if (off >= body) { ++k; off = 0; continue; }
       const int64_t c = min((int64_t)ch, body - off);
       *src = s0 + head + off;
       *dst = d0 + head + off;
-      *n = (uint32_t)c;
+      *len = (uint32_t)c;
       off += c;
       return true;
     }
@@ -246,12 +243,14 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
   __shared__ int s_abort;
   extern __shared__ __align__(128) unsigned char dsmem[];
   const int c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5;
-  // TMA ring: [S mbarriers | S dst ptrs | S sizes | pad | S stages of tma_chunk bytes]
+  // dynamic smem: [TMA: S mbarriers | S dst ptrs | S sizes | pad | S stages] [program] [batch]
   const int S = p.tma_stages;
   uint64_t* bars = reinterpret_cast<uint64_t*>(dsmem);
   char** ring_dst = reinterpret_cast<char**>(dsmem + 8 * S);
   uint32_t* ring_n = reinterpret_cast<uint32_t*>(dsmem + 16 * S);
   char* stages = reinterpret_cast<char*>(dsmem + ((20 * S + 127) & ~127));
+  CtaStep* s_prog = reinterpret_cast<CtaStep*>(dsmem + p.smem_prog);
+  DevPiece* s_pc = reinterpret_cast<DevPiece*>(dsmem + p.smem_batch);
   uint32_t gi = 0;  // TMA chunks consumed so far (thread 0): stage/phase bookkeeping
   unsigned long long* tl = p.timeline + (int64_t)c * (p.T + 3);
   if (tid == 0) {
@@ -262,6 +261,8 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
   }
+  // stage this CTA's step program (one parallel load instead of per-step chains)
+  for (int i = tid; i < p.T; i += kThreads) s_prog[i] = p.prog[(int64_t)c * p.T + i];
   __syncthreads();
   const uint32_t* my_flags = p.step_flags[p.rank];
   // one GPU: every producer and consumer is on this GPU -> .gpu scope suffices
@@ -296,103 +297,104 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
   if (tid == 0) tl[1] = globaltimer();
 
   for (int t = 0; t < p.T; ++t) {
-    const int64_t B = p.step_bytes[t];
-    const int64_t lo = cta_lo(B, c, p.nC), hi = cta_lo(B, c + 1, p.nC);
-    if (hi <= lo) {
+    const CtaStep cs = s_prog[t];
+    if (cs.pe <= cs.pb) {
       if (tid == 0) tl[2 + t] = 0;
       continue;
     }
-    const int32_t w0 = p.wait_off[t * p.nC + c], w1 = p.wait_off[t * p.nC + c + 1];
-    if (w1 > w0) {
-      if (warp == 0) {
-        bool ok = warp_wait_flags(my_flags, p.wait_idx, w0, w1, p.epoch, p.timeout_ns, p.err, sys);
-        if (!ok && tid == 0) s_abort = 1;
-        if (tid == 0) fence_acq_rel(sys);
+    bool waited = cs.we <= cs.wb;
+    for (int32_t base = cs.pb; base < cs.pe; base += p.batch) {
+      const int n = min(p.batch, cs.pe - base);
+      // stage the batch first: independent of the flags, so it overlaps the wait
+      for (int i = tid; i < n; i += kThreads) s_pc[i] = p.pieces[base + i];
+      if (!waited) {
+        if (warp == 0) {
+          bool ok = warp_wait_flags(my_flags, p.wait_idx, cs.wb, cs.we, p.epoch, p.timeout_ns,
+                                    p.err, sys);
+          if (!ok && tid == 0) s_abort = 1;
+          if (tid == 0) fence_acq_rel(sys);
+        }
+        waited = true;
       }
       __syncthreads();
       if (s_abort) return;
-    }
-    // items overlapping [lo, hi): binary search the first
-    int64_t a = p.step_begin[t], b = p.step_begin[t + 1] - 1;
-    while (a < b) {
-      int64_t mid = (a + b + 1) >> 1;
-      if (p.items[mid].prefix <= lo) a = mid; else b = mid - 1;
-    }
-    const int64_t kend = p.step_begin[t + 1];
-    for (int64_t k = a; k < kend; ++k) {
-      const DevItem it = p.items[k];
-      if (it.prefix >= hi) break;
-      const int64_t x0 = max(lo, it.prefix) - it.prefix;
-      const int64_t x1 = min(hi, it.prefix + it.nbytes) - it.prefix;
-      if (x1 <= x0) continue;
-      char* d0 = p.base[it.dst_loc] + it.dst_off + x0;
-      const char* s0 = p.base[it.src_loc] + it.src_off + x0;
       if (kEngine == 0) {
-        cta_copy<4>(d0, s0, x1 - x0);
-      } else {  // threads: heads, tails, misaligned pieces; bodies go to the TMA ring
-        const int64_t len = x1 - x0;
-        if ((((uintptr_t)s0 ^ (uintptr_t)d0) & 15) != 0) {
-          for (int64_t i = tid; i < len; i += kThreads) d0[i] = s0[i];
-        } else {
-          int64_t head = (16 - ((uintptr_t)d0 & 15)) & 15;
-          if (head > len) head = len;
-          const int64_t body = (len - head) & ~(int64_t)15, tail = len - head - body;
-          if (tid < head) d0[tid] = s0[tid];
-          if (tid < tail) d0[head + body + tid] = s0[head + body + tid];
+        for (int i = 0; i < n; ++i) {
+          const DevPiece& q = s_pc[i];
+          cta_copy<4>(p.base[q.dst_loc] + q.dst_off, p.base[q.src_loc] + q.src_off, q.nbytes);
         }
-      }
-      if (p.count_links && tid == 0 && it.edge >= 0)
-        atomicAdd(p.counters + (int64_t)t * p.E + it.edge, (unsigned long long)(x1 - x0));
-    }
-    if (kEngine == 1 && tid == 0) {
-      // single-thread TMA pipeline: S loads in flight, stores drained one behind
-      fence_proxy_async();
-      const uint32_t CH = (uint32_t)p.tma_chunk;
-      BodyCursor cur{a, kend, 0, lo, hi};
-      const uint32_t g0 = gi;
-      uint32_t nl = 0, ns = 0;
-      bool more = true;
-      auto issue = [&]() -> bool {
-        const char* src;
-        char* dst;
-        uint32_t n;
-        if (!cur.next(p, CH, &src, &dst, &n)) return false;
-        const uint32_t st = (g0 + nl) % S;
-        ring_dst[st] = dst;
-        ring_n[st] = n;
-        mbar_expect_tx(&bars[st], n);
-        bulk_load(stages + (size_t)st * CH, src, n, &bars[st]);
-        ++nl;
-        return true;
-      };
-      while (more && nl < (uint32_t)S) more = issue();
-      while (ns < nl) {
-        const uint32_t st = (g0 + ns) % S;
-        mbar_wait(&bars[st], ((g0 + ns) / S) & 1);
-        bulk_store(ring_dst[st], stages + (size_t)st * CH, ring_n[st]);
-        ++ns;
-        if (more) {
-          if (S == 1) {
-            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            more = issue();
-          } else if (ns >= 2 && nl - (uint32_t)S == ns - 2) {
-            bulk_wait_read1();
-            more = issue();
+      } else {
+        if (tid != 0) {  // threads 1..: heads, tails, misaligned pieces
+          const int nt = kThreads - 1, me = tid - 1;
+          for (int i = 0; i < n; ++i) {
+            const DevPiece& q = s_pc[i];
+            const char* s0 = p.base[q.src_loc] + q.src_off;
+            char* d0 = p.base[q.dst_loc] + q.dst_off;
+            const int64_t len = q.nbytes;
+            if ((((uintptr_t)s0 ^ (uintptr_t)d0) & 15) != 0) {
+              for (int64_t j = me; j < len; j += nt) d0[j] = s0[j];
+            } else {
+              int64_t head = (16 - ((uintptr_t)d0 & 15)) & 15;
+              if (head > len) head = len;
+              const int64_t body = (len - head) & ~(int64_t)15, tail = len - head - body;
+              if (me < head) d0[me] = s0[me];
+              if (me < tail) d0[head + body + me] = s0[head + body + me];
+            }
           }
+        } else {  // thread 0: TMA pipeline over the batch's bodies
+          fence_proxy_async();
+          const uint32_t CH = (uint32_t)p.tma_chunk;
+          BodyCursor cur{s_pc, 0, n, 0};
+          const uint32_t g0 = gi;
+          uint32_t nl = 0, ns = 0;
+          bool more = true;
+          auto issue = [&]() -> bool {
+            const char* src;
+            char* dst;
+            uint32_t len;
+            if (!cur.next(p, CH, &src, &dst, &len)) return false;
+            const uint32_t st = (g0 + nl) % S;
+            ring_dst[st] = dst;
+            ring_n[st] = len;
+            mbar_expect_tx(&bars[st], len);
+            bulk_load(stages + (size_t)st * CH, src, len, &bars[st]);
+            ++nl;
+            return true;
+          };
+          while (more && nl < (uint32_t)S) more = issue();
+          while (ns < nl) {
+            const uint32_t st = (g0 + ns) % S;
+            mbar_wait(&bars[st], ((g0 + ns) / S) & 1);
+            bulk_store(ring_dst[st], stages + (size_t)st * CH, ring_n[st]);
+            ++ns;
+            if (more) {
+              if (S == 1) {
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                more = issue();
+              } else if (ns >= 2 && nl - (uint32_t)S == ns - 2) {
+                bulk_wait_read1();
+                more = issue();
+              }
+            }
+          }
+          bulk_wait_all();
+          fence_proxy_async();
+          gi = g0 + nl;
         }
       }
-      bulk_wait_all();
-      fence_proxy_async();
-      gi = g0 + nl;
+      if (p.count_links && tid == 0)
+        for (int i = 0; i < n; ++i)
+          if (s_pc[i].edge >= 0)
+            atomicAdd(p.counters + (int64_t)t * p.E + s_pc[i].edge, (unsigned long long)s_pc[i].nbytes);
+      __syncthreads();
     }
-    __syncthreads();
     if (tid == 0) {
-      uint32_t mask = p.dst_mask[(int64_t)t * p.nC + c];
       if (!(p.sync_mode & 2)) {
         if (p.sync_mode & 1) fence_acq_rel(sys);
         else if (sys) __threadfence_system();
         else __threadfence();
       }
+      uint32_t mask = cs.mask;
       const int64_t slot = ((int64_t)t * p.G + p.rank) * p.nC + c;
       while (mask) {
         const int h = __ffs(mask) - 1;
@@ -453,14 +455,26 @@ struct EngineCfg {
   const void* fn;
   int threads;
   size_t smem;
+  int stages, prog_off, batch_off, batch;
 };
 static EngineCfg engine_cfg(const Plan& P) {
+  const int TE = P.T_exec;
+  const size_t prog = ((size_t)TE * sizeof(CtaStep) + 127) & ~(size_t)127;
   if (P.engine == 1) {
-    size_t smem = ((20 * (size_t)P.tma_stages + 127) & ~(size_t)127) +
-                  (size_t)P.tma_stages * P.tma_chunk;
-    return {(const void*)a2a_exec_kernel<1, 256>, 256, smem};
+    const int batch = 64;
+    const size_t fixed = prog + batch * sizeof(DevPiece) + 1024;
+    int S = P.tma_stages;
+    while (S > 1 && ((20 * (size_t)S + 127) & ~(size_t)127) + (size_t)S * P.tma_chunk + fixed >
+                        227 * 1024)
+      --S;
+    const size_t ring = ((20 * (size_t)S + 127) & ~(size_t)127) + (size_t)S * P.tma_chunk;
+    const size_t po = (ring + 127) & ~(size_t)127;
+    return {(const void*)a2a_exec_kernel<1, 256>, 256, po + prog + batch * sizeof(DevPiece), S,
+            (int)po, (int)(po + prog), batch};
   }
-  return {(const void*)a2a_exec_kernel<0, 1024>, 1024, 0};
+  const int batch = 128;
+  return {(const void*)a2a_exec_kernel<0, 1024>, 1024, prog + batch * sizeof(DevPiece), 0, 0,
+          (int)prog, batch};
 }
 
 // arena flag region: entry[G] u32 | step flags [T'][G][nC] u32
@@ -552,11 +566,8 @@ static int bind_plan(Plan& P, int gpu, int dev, int nC) {
     return fail(A2A_ERR_NOMEM, buf);
   }
   CK(cudaMemset(P.arena, 0, (size_t)P.flags_bytes));
-  if ((rc = upload(&P.d_items, P.tables[gpu].items)) != A2A_OK) return rc;
-  if ((rc = upload(&P.d_step_begin, P.tables[gpu].step_begin)) != A2A_OK) return rc;
-  if ((rc = upload(&P.d_step_bytes, P.tables[gpu].step_bytes)) != A2A_OK) return rc;
-  if ((rc = upload(&P.d_dst_mask, S.dst_mask[gpu])) != A2A_OK) return rc;
-  if ((rc = upload(&P.d_wait_off, S.wait_off[gpu])) != A2A_OK) return rc;
+  if ((rc = upload(&P.d_items, S.pieces[gpu])) != A2A_OK) return rc;
+  if ((rc = upload(&P.d_step_begin, S.prog[gpu])) != A2A_OK) return rc;
   if ((rc = upload(&P.d_wait_idx, S.wait_idx[gpu])) != A2A_OK) return rc;
   if ((rc = upload(&P.d_exit_idx, S.exit_idx[gpu])) != A2A_OK) return rc;
   CK(cudaMalloc(&P.d_timeline, (size_t)nC * (TE + 3) * 8));
@@ -744,13 +755,10 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
     kp.entry_flags[g] = (uint32_t*)(ar + entry_flags_off());
     kp.step_flags[g] = (uint32_t*)(ar + step_flags_off());
   }
-  kp.items = (const DevItem*)P.d_items;
-  kp.step_begin = (const int64_t*)P.d_step_begin;
-  kp.step_bytes = (const int64_t*)P.d_step_bytes;
-  kp.dst_mask = (const uint32_t*)P.d_dst_mask;
+  kp.pieces = (const DevPiece*)P.d_items;
+  kp.prog = (const CtaStep*)P.d_step_begin;
   kp.exit_idx = (const int32_t*)P.d_exit_idx;
   kp.n_exit = (int32_t)P.sync.exit_idx[P.rank].size();
-  kp.wait_off = (const int32_t*)P.d_wait_off;
   kp.wait_idx = (const int32_t*)P.d_wait_idx;
   kp.counters = (unsigned long long*)P.d_counters;
   kp.err = P.d_err;
@@ -766,9 +774,12 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
   void* args[] = {&kp};
   kp.timeline = (unsigned long long*)P.d_timeline;
   kp.sync_mode = P.sync_mode;
-  kp.tma_chunk = P.tma_chunk;
-  kp.tma_stages = P.engine == 1 ? P.tma_stages : 0;
   const EngineCfg ec = engine_cfg(P);
+  kp.tma_chunk = P.tma_chunk;
+  kp.tma_stages = ec.stages;
+  kp.smem_prog = ec.prog_off;
+  kp.smem_batch = ec.batch_off;
+  kp.batch = ec.batch;
   cudaError_t e = cudaLaunchCooperativeKernel(ec.fn, dim3(P.nC), dim3(ec.threads), args, ec.smem,
                                               (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchCooperativeKernel");

@@ -47,8 +47,30 @@ struct GpuTables {
 // CTA split + exact producer dependencies for a given CTA count (host-built,
 // identical on every rank).  Flag slot of producer (t, g, c) = (t*G + g)*nC + c
 // in every GPU's step-flag array.
+// One CTA's copy piece (a contiguous sub-range of one item), 32 bytes.
+struct DevPiece {
+  int64_t src_off, dst_off;
+  int32_t nbytes;
+  int32_t edge;
+  int16_t src_loc, dst_loc;
+  int32_t pad;
+};
+static_assert(sizeof(DevPiece) == 32, "DevPiece layout");
+
+// One CTA's program for one step, 32 bytes: piece range, wait-list range,
+// destination-GPU mask of its stores.
+struct CtaStep {
+  int32_t pb, pe;   // [pb, pe) in the GPU's piece array
+  int32_t wb, we;   // [wb, we) in the GPU's wait_idx array
+  uint32_t mask;    // GPUs written in this step (flags to publish)
+  int32_t pad[3];
+};
+static_assert(sizeof(CtaStep) == 32, "CtaStep layout");
+
 struct SyncTables {
   int32_t nC = 0;
+  std::vector<std::vector<DevPiece>> pieces;    // [g] ordered by (cta, step)
+  std::vector<std::vector<CtaStep>> prog;       // [g][c*T' + t]
   std::vector<std::vector<uint32_t>> dst_mask;  // [g][t*nC + c] bit h: (g,c) wrote to h at t
   std::vector<std::vector<int32_t>> wait_off;   // [g][t*nC + c .. +1] into wait_idx[g]
   std::vector<std::vector<int32_t>> wait_idx;   // [g] producer slots to acquire
@@ -83,7 +105,7 @@ struct Plan {
   int32_t rank = -1, device = -1, nC = 0, nT = 1024;
   int32_t engine = 1, tma_chunk = 32768, tma_stages = 6;   // copy engine (a2a_plan_set_engine)
   int32_t n_recv = 1;
-  int32_t sync_mode = 0;                                     // a2a_plan_set_sync_mode                                        // arena recv buffers (multi-buffering)
+  int32_t sync_mode = 2;                                     // a2a_plan_set_sync_mode (2: bar.sync + st.release)                                        // arena recv buffers (multi-buffering)
   int64_t flags_bytes = 0;                      // arena flag region size
   std::vector<int64_t> recv_off, scratch_off;   // per gpu, inside that gpu's arena
   std::vector<int64_t> arena_bytes;             // per gpu

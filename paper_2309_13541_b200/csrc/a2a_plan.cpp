@@ -469,6 +469,38 @@ int build_sync(Plan& P, int nC) {
           if (S.dst_mask[g][(size_t)t * nC + c] & (1u << h))
             S.exit_idx[h].push_back((int32_t)(((int64_t)t * G + g) * nC + c));
   }
+  // per-CTA programs: exact piece lists (split below 1 GiB so nbytes fits int32)
+  S.pieces.assign(G, {});
+  S.prog.assign(G, {});
+  for (int g = 0; g < G; ++g) {
+    std::vector<std::vector<std::vector<DevPiece>>> per_ct(nC, std::vector<std::vector<DevPiece>>(TE));
+    for (int t = 0; t < TE; ++t)
+      for_each_piece(P.tables[g], t, nC, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
+        for (int64_t x = x0; x < x1; x += (1LL << 30)) {
+          DevPiece pc{};
+          pc.src_off = it.src_off + x;
+          pc.dst_off = it.dst_off + x;
+          pc.nbytes = (int32_t)std::min<int64_t>(1LL << 30, x1 - x);
+          pc.edge = it.edge;
+          pc.src_loc = (int16_t)it.src_loc;
+          pc.dst_loc = (int16_t)it.dst_loc;
+          per_ct[c][t].push_back(pc);
+        }
+      });
+    auto& pcs = S.pieces[g];
+    auto& prog = S.prog[g];
+    prog.assign((size_t)nC * TE, CtaStep{});
+    for (int c = 0; c < nC; ++c)
+      for (int t = 0; t < TE; ++t) {
+        CtaStep& cs = prog[(size_t)c * TE + t];
+        cs.pb = (int32_t)pcs.size();
+        pcs.insert(pcs.end(), per_ct[c][t].begin(), per_ct[c][t].end());
+        cs.pe = (int32_t)pcs.size();
+        cs.wb = S.wait_off[g][(size_t)t * nC + c];
+        cs.we = S.wait_off[g][(size_t)t * nC + c + 1];
+        cs.mask = S.dst_mask[g][(size_t)t * nC + c];
+      }
+  }
   P.sync = std::move(S);
   return A2A_OK;
 }
