@@ -148,12 +148,15 @@ int a2a_plan_read_link_counters(a2a_plan* plan, int64_t* out);
  * ring of `tma_stages` x `tma_chunk` bytes per CTA; 0 = defaults 6 x 32 KiB) */
 int a2a_plan_set_engine(a2a_plan* plan, int32_t engine, int32_t tma_chunk, int32_t tma_stages);
 /* per-CTA %globaltimer timeline of the last execute: out[c][j], j = 0 start,
- * 1 entry barrier passed, 2+t step t published (0 = no work), 2+T' exit;
- * *out_cols = T'+3 (call with out = NULL to get the width) */
+ * 1 entry barrier passed, 2+t step t published (0 = no work), 2+T' exit,
+ * 3+T'+t step t dependencies acquired (0 = none); *out_cols = 2T'+3
+ * (call with out = NULL to get the width) */
 int a2a_plan_read_timeline(a2a_plan* plan, uint64_t* out, int32_t* out_cols);
 /* step-flag publication variant (tuning/diagnostics): bit0 = fence.acq_rel
  * instead of fence.sc before the release store, bit1 = no explicit fence
- * (bar.sync + st.release cumulativity), bit2 = system scope even on one GPU */
+ * (bar.sync + st.release cumulativity), bit2 = system scope even on one GPU,
+ * bit3 = __nanosleep backoff while polling, bit4 = ld.acquire polling instead
+ * of ld.relaxed + fence.acq_rel.  Default 2. */
 int a2a_plan_set_sync_mode(a2a_plan* plan, int32_t mode);
 /* device-side flag-wait timeout (ns, default 10 s) */
 int a2a_plan_set_timeout(a2a_plan* plan, int64_t timeout_ns);

@@ -82,6 +82,14 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p, bool sys) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p, bool sys) {
+  uint32_t v;
+  if (sys)
+    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  else
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v, bool sys) {
   if (sys)
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -184,16 +192,23 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// Warp 0 waits until every listed flag reached `epoch`.  Returns false on timeout.
+// Warp 0 waits until every listed flag reached `epoch`: each lane polls its
+// flags with relaxed loads (optionally backing off), then every lane executes
+// fence.acq_rel (the PTX acquire pattern: morally-strong read + fence).
+// Returns false on timeout.
 __device__ bool warp_wait_flags(const uint32_t* flags, const int32_t* idx, int32_t lo, int32_t hi,
-                                uint32_t epoch, int64_t timeout_ns, int32_t* err, bool sys) {
+                                uint32_t epoch, int64_t timeout_ns, int32_t* err, bool sys,
+                                int mode) {
   const int lane = threadIdx.x & 31;
   bool ok = true;
   uint64_t t0 = 0;
   for (int32_t i = lo + lane; i < hi; i += 32) {
     const uint32_t* f = flags + idx[i];
     uint32_t spins = 0;
-    while ((int32_t)(ld_acquire(f, sys) - epoch) < 0) {
+    for (;;) {
+      const uint32_t v = (mode & 16) ? ld_acquire(f, sys) : ld_relaxed(f, sys);
+      if ((int32_t)(v - epoch) >= 0) break;
+      if (mode & 8) __nanosleep(64);
       if ((++spins & 255) == 0) {
         uint64_t now = globaltimer();
         if (t0 == 0) t0 = now;
@@ -205,6 +220,7 @@ __device__ bool warp_wait_flags(const uint32_t* flags, const int32_t* idx, int32
     }
     if (!ok) break;
   }
+  fence_acq_rel(sys);
   ok = __all_sync(0xffffffffu, ok);
   if (!ok && lane == 0) atomicCAS(err, 0, (int32_t)A2A_ERR_TIMEOUT);
   return ok;
@@ -252,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
   CtaStep* s_prog = reinterpret_cast<CtaStep*>(dsmem + p.smem_prog);
   DevPiece* s_pc = reinterpret_cast<DevPiece*>(dsmem + p.smem_batch);
   uint32_t gi = 0;  // TMA chunks consumed so far (thread 0): stage/phase bookkeeping
-  unsigned long long* tl = p.timeline + (int64_t)c * (p.T + 3);
+  unsigned long long* tl = p.timeline + (int64_t)c * (2 * p.T + 3);
   if (tid == 0) {
     tl[0] = globaltimer();
     s_abort = 0;
@@ -299,9 +315,10 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
   for (int t = 0; t < p.T; ++t) {
     const CtaStep cs = s_prog[t];
     if (cs.pe <= cs.pb) {
-      if (tid == 0) tl[2 + t] = 0;
+      if (tid == 0) tl[2 + t] = tl[3 + p.T + t] = 0;
       continue;
     }
+    if (tid == 0 && cs.we <= cs.wb) tl[3 + p.T + t] = 0;
     bool waited = cs.we <= cs.wb;
     for (int32_t base = cs.pb; base < cs.pe; base += p.batch) {
       const int n = min(p.batch, cs.pe - base);
@@ -310,9 +327,9 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
       if (!waited) {
         if (warp == 0) {
           bool ok = warp_wait_flags(my_flags, p.wait_idx, cs.wb, cs.we, p.epoch, p.timeout_ns,
-                                    p.err, sys);
+                                    p.err, sys, p.sync_mode);
           if (!ok && tid == 0) s_abort = 1;
-          if (tid == 0) fence_acq_rel(sys);
+          if (tid == 0) tl[3 + p.T + t] = globaltimer();
         }
         waited = true;
       }
@@ -570,8 +587,8 @@ static int bind_plan(Plan& P, int gpu, int dev, int nC) {
   if ((rc = upload(&P.d_step_begin, S.prog[gpu])) != A2A_OK) return rc;
   if ((rc = upload(&P.d_wait_idx, S.wait_idx[gpu])) != A2A_OK) return rc;
   if ((rc = upload(&P.d_exit_idx, S.exit_idx[gpu])) != A2A_OK) return rc;
-  CK(cudaMalloc(&P.d_timeline, (size_t)nC * (TE + 3) * 8));
-  CK(cudaMemset(P.d_timeline, 0, (size_t)nC * (TE + 3) * 8));
+  CK(cudaMalloc(&P.d_timeline, (size_t)nC * (2 * TE + 3) * 8));
+  CK(cudaMemset(P.d_timeline, 0, (size_t)nC * (2 * TE + 3) * 8));
   size_t cbytes = std::max<size_t>((size_t)TE * std::max(P.E, 1) * 8, 16);
   CK(cudaMalloc(&P.d_counters, cbytes));
   CK(cudaMemset(P.d_counters, 0, cbytes));
@@ -714,7 +731,7 @@ int a2a_plan_set_recv_buffers(a2a_plan* plan, int32_t count) {
 }
 
 int a2a_plan_set_sync_mode(a2a_plan* plan, int32_t mode) {
-  if (!plan || mode < 0 || mode > 7) return fail(A2A_ERR_INVALID, "bad sync mode");
+  if (!plan || mode < 0 || mode > 31) return fail(A2A_ERR_INVALID, "bad sync mode");
   plan->p.sync_mode = mode;
   return A2A_OK;
 }
@@ -804,11 +821,11 @@ int a2a_plan_read_timeline(a2a_plan* plan, uint64_t* out, int32_t* out_cols) {
   if (!plan || !out_cols) return fail(A2A_ERR_INVALID, "null argument");
   Plan& P = plan->p;
   if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound");
-  *out_cols = P.T_exec + 3;
+  *out_cols = 2 * P.T_exec + 3;
   if (!out) return A2A_OK;
   DeviceGuard dg(P.device);
   CK(cudaStreamSynchronize((cudaStream_t)P.last_stream));
-  CK(cudaMemcpy(out, P.d_timeline, (size_t)P.nC * (P.T_exec + 3) * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(out, P.d_timeline, (size_t)P.nC * (2 * P.T_exec + 3) * 8, cudaMemcpyDeviceToHost));
   return A2A_OK;
 }
 

@@ -104,8 +104,8 @@ struct Plan {
   bool bound = false, imported = false;
   int32_t rank = -1, device = -1, nC = 0, nT = 1024;
   int32_t engine = 1, tma_chunk = 32768, tma_stages = 6;   // copy engine (a2a_plan_set_engine)
-  int32_t n_recv = 1;
-  int32_t sync_mode = 2;                                     // a2a_plan_set_sync_mode (2: bar.sync + st.release)                                        // arena recv buffers (multi-buffering)
+  int32_t n_recv = 1;                           // arena recv buffers (multi-buffering)
+  int32_t sync_mode = 2;                        // a2a_plan_set_sync_mode (2: bar.sync + st.release)
   int64_t flags_bytes = 0;                      // arena flag region size
   std::vector<int64_t> recv_off, scratch_off;   // per gpu, inside that gpu's arena
   std::vector<int64_t> arena_bytes;             // per gpu

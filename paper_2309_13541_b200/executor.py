@@ -29,17 +29,20 @@ __all__ = ["EvalError", "ExecutorError", "Plan", "replay_timestep_schedule",
 
 
 def timeline_summary(tl: np.ndarray) -> dict:
-    """Kernel-internal timing from Plan.read_timeline(): microseconds from the
-    earliest CTA start to the entry barrier, each step's last publication and
-    the last CTA exit."""
+    """Kernel-internal timing from Plan.read_timeline() (columns: start, entry,
+    step published [T'], exit, step dependencies acquired [T']): microseconds
+    from the earliest CTA start."""
+    T = (tl.shape[1] - 3) // 2
     t0 = int(tl[:, 0].min())
     us = lambda x: round((int(x) - t0) / 1e3, 3)  # noqa: E731
-    steps = []
-    for j in range(2, tl.shape[1] - 1):
+
+    def last(j):
         col = tl[:, j][tl[:, j] > 0]
-        steps.append(us(col.max()) if col.size else None)
-    return {"kernel_us": us(tl[:, -1].max()), "start_spread_us": us(tl[:, 0].max()),
-            "entry_us": us(tl[:, 1].max()), "step_done_us": steps}
+        return us(col.max()) if col.size else None
+    return {"kernel_us": us(tl[:, 2 + T].max()), "start_spread_us": us(tl[:, 0].max()),
+            "entry_us": us(tl[:, 1].max()),
+            "step_acquired_us": [last(3 + T + t) for t in range(T)],
+            "step_done_us": [last(2 + t) for t in range(T)]}
 
 
 class EvalError(RuntimeError):
