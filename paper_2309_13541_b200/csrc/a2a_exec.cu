@@ -96,6 +96,12 @@ __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v, bool sys) {
   else
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v, bool sys) {
+  if (sys)
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  else
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void fence_acq_rel(bool sys) {
   if (sys)
     asm volatile("fence.acq_rel.sys;" ::: "memory");
@@ -406,17 +412,30 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
       __syncthreads();
     }
     if (tid == 0) {
-      if (!(p.sync_mode & 2)) {
-        if (p.sync_mode & 1) fence_acq_rel(sys);
-        else if (sys) __threadfence_system();
-        else __threadfence();
-      }
-      uint32_t mask = cs.mask;
       const int64_t slot = ((int64_t)t * p.G + p.rank) * p.nC + c;
-      while (mask) {
-        const int h = __ffs(mask) - 1;
-        mask &= mask - 1;
-        st_release(p.step_flags[h] + slot, p.epoch, sys);
+      if (p.sync_mode & 32) {
+        // release pattern: one fence, then relaxed flag stores, peers first
+        fence_acq_rel(sys);
+        const uint32_t own = 1u << p.rank;
+        uint32_t mask = cs.mask & ~own;
+        while (mask) {
+          const int h = __ffs(mask) - 1;
+          mask &= mask - 1;
+          st_relaxed(p.step_flags[h] + slot, p.epoch, sys);
+        }
+        if (cs.mask & own) st_relaxed(p.step_flags[p.rank] + slot, p.epoch, sys);
+      } else {
+        if (!(p.sync_mode & 2)) {
+          if (p.sync_mode & 1) fence_acq_rel(sys);
+          else if (sys) __threadfence_system();
+          else __threadfence();
+        }
+        uint32_t mask = cs.mask;
+        while (mask) {
+          const int h = __ffs(mask) - 1;
+          mask &= mask - 1;
+          st_release(p.step_flags[h] + slot, p.epoch, sys);
+        }
       }
       tl[2 + t] = globaltimer();
     }
@@ -731,7 +750,7 @@ int a2a_plan_set_recv_buffers(a2a_plan* plan, int32_t count) {
 }
 
 int a2a_plan_set_sync_mode(a2a_plan* plan, int32_t mode) {
-  if (!plan || mode < 0 || mode > 31) return fail(A2A_ERR_INVALID, "bad sync mode");
+  if (!plan || mode < 0 || mode > 63) return fail(A2A_ERR_INVALID, "bad sync mode");
   plan->p.sync_mode = mode;
   return A2A_OK;
 }
