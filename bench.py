@@ -197,7 +197,7 @@ class Ctx:
 
 
 def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=True,
-            flush_bytes=512 << 20):
+            flush_bytes=512 << 20, placement="optimized"):
     """Time K all-to-alls of `art` at shard size m on ctx.world GPUs.
 
     Returns a dict (identical on every rank) with T, algBW, bound, roofline,
@@ -210,7 +210,7 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
 
     G, rank, dev = ctx.world, ctx.rank, ctx.dev
     n = art.g.n
-    plan = Plan(art.g, art.sched, m=m, n_gpus=G)
+    plan = Plan(art.g, art.sched, m=m, n_gpus=G, placement=placement)
     if e2e and G > 1:
         plan.set_recv_buffers(2)          # double-buffered recv for the pipelined e2e
     plan.bind(rank, device=ctx.local, num_ctas=num_ctas)
@@ -399,7 +399,7 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
            "recv_ok": bool(ok), "clocks": clock_rec, "sync": plan.sync_stats(rank),
            "kernel_timeline": tls,
            "num_ctas": plan_ctas(plan, num_ctas), "egress_max": max(i["egress_bytes"] for i in infos),
-           "scratch_bytes": info["scratch_bytes"]}
+           "scratch_bytes": info["scratch_bytes"], "placement": plan.placement.tolist()}
     plan.close()
     del send, recv, flush
     torch.cuda.empty_cache()
@@ -419,6 +419,7 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    ap.add_argument("--placement", default="optimized", choices=["optimized", "contiguous"])
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
 
@@ -432,7 +433,7 @@ def main(argv=None):
     if ctx.world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ctx.world}")
     r = measure(ctx, art, m, args.steps, args.warmup, num_ctas=args.num_ctas,
-                nccl=not args.no_nccl, e2e=not args.no_e2e)
+                nccl=not args.no_nccl, e2e=not args.no_e2e, placement=args.placement)
     G, n = ctx.world, art.g.n
 
     # ---- CPU baseline: rank 0, N=1 only, bounded sample
@@ -458,7 +459,8 @@ def main(argv=None):
             "dtype": "u8", "data": "synthetic",
             "config": {"workload": f"{args.config}: frozen decomposed-MCF schedule "
                                    f"(hop i of every route at step i), N={n} virtual nodes, "
-                                   f"m={m} B per pair, placement v*G//N",
+                                   f"m={m} B per pair, placement {args.placement} "
+                                   f"{r['placement'] if G > 1 else ''}",
                        "m_bytes": m, "nodes": n, "hop_ops": len(art.sched.instructions),
                        "nsteps": art.sched.nsteps, "Q": art.sched.Q,
                        "l2": "flushed between timed steps (512 MiB memset, outside events)",

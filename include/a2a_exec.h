@@ -108,6 +108,15 @@ int a2a_plan_sync_stats(const a2a_plan* plan, int32_t gpu, int64_t* n_wait, int6
 int a2a_plan_emulate(a2a_plan* plan, int32_t num_ctas, void* const* send, void* const* recv,
                      uint64_t seed);
 
+/* Placement optimiser (host only): balanced virtual-node -> GPU assignment with
+ * the same per-GPU node counts as `placement` (in/out), minimising the NVLink
+ * term max_g max(egress_g, ingress_g) of the per-edge schedule bytes
+ * (edge_bytes[e], e.g. a2a_plan_link_bytes summed over steps); exhaustive for
+ * n <= 12, sampled best-improvement swaps otherwise (`iters` rounds). */
+int a2a_optimize_placement(int32_t n, int32_t n_edges, const int32_t* edge_uv,
+                           const int64_t* edge_bytes, int32_t n_gpus, int32_t iters,
+                           uint64_t seed, int32_t* placement);
+
 /* ---- device side ---- */
 /* Bind the plan to one GPU: rank `gpu` of the placement on CUDA device
  * `device_ordinal`, with `num_ctas` persistent CTAs (0 = one per SM).  Allocates

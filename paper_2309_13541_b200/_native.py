@@ -77,6 +77,8 @@ def _load():
         "a2a_plan_recv_buffer_at": ([P, C.c_int32, C.POINTER(P)], C.c_int),
         "a2a_plan_read_timeline": ([P, C.POINTER(C.c_uint64), C.POINTER(C.c_int32)], C.c_int),
         "a2a_plan_set_sync_mode": ([P, C.c_int32], C.c_int),
+        "a2a_optimize_placement": ([C.c_int32, C.c_int32, P, P, C.c_int32, C.c_int32,
+                                    C.c_uint64, P], C.c_int),
         "a2a_plan_set_engine": ([P, C.c_int32, C.c_int32, C.c_int32], C.c_int),
     }
     for name, (args, res) in sig.items():

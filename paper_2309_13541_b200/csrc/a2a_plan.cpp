@@ -16,6 +16,7 @@
 #include <array>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <new>
 #include <string>
@@ -661,6 +662,120 @@ int a2a_plan_emulate(a2a_plan* plan, int32_t num_ctas, void* const* send, void* 
   } catch (const std::bad_alloc&) {
     return fail(A2A_ERR_NOMEM, "out of host memory in emulation");
   }
+}
+
+// ---- placement optimiser ---------------------------
+// Objective: max over GPUs of max(egress, ingress) cross-GPU bytes — the
+// NVLink term of the topology bound — then total cross bytes as tie-break.
+// Balanced placements only (node counts per GPU as in `placement`).
+namespace {
+struct PlaceEval {
+  int n, E, G;
+  const int32_t* uv;
+  const int64_t* w;
+  std::vector<std::vector<std::pair<int, int64_t>>> out_e, in_e;  // (nbr, bytes)
+  void init() {
+    out_e.assign(n, {});
+    in_e.assign(n, {});
+    for (int e = 0; e < E; ++e) {
+      if (w[e] == 0) continue;
+      out_e[uv[2 * e]].emplace_back(uv[2 * e + 1], w[e]);
+      in_e[uv[2 * e + 1]].emplace_back(uv[2 * e], w[e]);
+    }
+  }
+  void loads(const std::vector<int>& P, std::vector<int64_t>& eg, std::vector<int64_t>& ing,
+             int64_t& cross) const {
+    eg.assign(G, 0);
+    ing.assign(G, 0);
+    cross = 0;
+    for (int e = 0; e < E; ++e) {
+      int a = P[uv[2 * e]], b = P[uv[2 * e + 1]];
+      if (a != b) { eg[a] += w[e]; ing[b] += w[e]; cross += w[e]; }
+    }
+  }
+  std::pair<int64_t, int64_t> cost(const std::vector<int>& P) const {
+    std::vector<int64_t> eg, ing;
+    int64_t cross;
+    loads(P, eg, ing, cross);
+    int64_t mx = 0;
+    for (int g = 0; g < G; ++g) mx = std::max(mx, std::max(eg[g], ing[g]));
+    return {mx, cross};
+  }
+};
+}  // namespace
+
+int a2a_optimize_placement(int32_t n, int32_t n_edges, const int32_t* edge_uv,
+                           const int64_t* edge_bytes, int32_t n_gpus, int32_t iters,
+                           uint64_t seed, int32_t* placement) {
+  if (n < 1 || n_edges < 0 || !edge_uv || !edge_bytes || !placement || n_gpus < 1 ||
+      n_gpus > A2A_MAX_GPUS)
+    return fail(A2A_ERR_INVALID, "bad placement arguments");
+  PlaceEval ev{n, n_edges, n_gpus, edge_uv, edge_bytes, {}, {}};
+  ev.init();
+  std::vector<int> P(placement, placement + n);
+  for (int v = 0; v < n; ++v)
+    if (P[v] < 0 || P[v] >= n_gpus) return fail(A2A_ERR_INVALID, "placement entry out of range");
+  auto best = ev.cost(P);
+  std::vector<int> bestP = P;
+  if (n <= 12 && n_gpus > 1) {
+    // exhaustive over balanced assignments with the same per-GPU counts,
+    // canonical (GPU labels are interchangeable only if counts match: keep labels)
+    std::vector<int> cnt(n_gpus, 0), cap(n_gpus, 0);
+    for (int v = 0; v < n; ++v) cap[P[v]]++;
+    std::vector<int> cur(n, 0);
+    std::function<void(int)> rec = [&](int v) {
+      if (v == n) {
+        auto c = ev.cost(cur);
+        if (c < best) { best = c; bestP = cur; }
+        return;
+      }
+      for (int g = 0; g < n_gpus; ++g) {
+        if (cnt[g] >= cap[g]) continue;
+        // symmetry: the first node of each empty equal-capacity GPU goes to the lowest one
+        bool skip = false;
+        if (cnt[g] == 0)
+          for (int h = 0; h < g; ++h)
+            if (cnt[h] == 0 && cap[h] == cap[g]) { skip = true; break; }
+        if (skip) continue;
+        cnt[g]++;
+        cur[v] = g;
+        rec(v + 1);
+        cnt[g]--;
+      }
+    };
+    rec(0);
+  } else if (n_gpus > 1) {
+    // local search: best-improvement swaps touching the bottleneck GPU, random restarts of ties
+    uint64_t x = seed * 0x9E3779B97F4A7C15ULL + 7;
+    auto rnd = [&]() { x ^= x << 13; x ^= x >> 7; x ^= x << 17; return x; };
+    std::vector<int64_t> eg, ing;
+    int64_t cross;
+    for (int it = 0; it < std::max(1, iters); ++it) {
+      ev.loads(P, eg, ing, cross);
+      int gw = 0;
+      int64_t mx = -1;
+      for (int g = 0; g < n_gpus; ++g)
+        if (std::max(eg[g], ing[g]) > mx) { mx = std::max(eg[g], ing[g]); gw = g; }
+      std::pair<int64_t, int64_t> cbest = ev.cost(P);
+      int bu = -1, bv = -1;
+      // sample candidate pairs (u on the bottleneck GPU, v elsewhere)
+      std::vector<int> on, off;
+      for (int v = 0; v < n; ++v) (P[v] == gw ? on : off).push_back(v);
+      const int samples = std::min<int64_t>((int64_t)on.size() * off.size(), 4096);
+      for (int k = 0; k < samples; ++k) {
+        int u = on[rnd() % on.size()], v = off[rnd() % off.size()];
+        std::swap(P[u], P[v]);
+        auto c = ev.cost(P);
+        std::swap(P[u], P[v]);
+        if (c < cbest) { cbest = c; bu = u; bv = v; }
+      }
+      if (bu < 0) break;
+      std::swap(P[bu], P[bv]);
+      if (cbest < best) { best = cbest; bestP = P; }
+    }
+  }
+  std::copy(bestP.begin(), bestP.end(), placement);
+  return A2A_OK;
 }
 
 int a2a_plan_gpu_info(const a2a_plan* plan, int32_t gpu, a2a_gpu_info* out) {

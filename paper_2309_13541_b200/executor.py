@@ -104,8 +104,11 @@ class Plan:
             [(u, v) for u, v, _ in g.edges], dtype=np.int32).reshape(-1, 2)
         self._cap = np.ascontiguousarray([c for _, _, c in g.edges], dtype=np.float64)
         self._ops = _ops_array(sched.instructions if ops is None else ops)
-        if placement is None:
+        if placement is None or placement == "contiguous":
             placement = contiguous_placement(self.n, self.n_gpus)
+        elif placement == "optimized":
+            from .placement import optimized_placement
+            placement = optimized_placement(g, sched, self.n_gpus, m=max(int(m), sched.Q))
         self.placement = np.ascontiguousarray(placement, dtype=np.int32)
         if self.placement.shape != (self.n,):
             raise ValueError("placement must list one GPU per node")

@@ -76,3 +76,39 @@ def test_interleaved_order_interleavings(name, G, split, artifacts):
         lb = p.link_bytes()
     with Plan(a.g, a.sched, m=m, n_gpus=G) as q:
         assert np.array_equal(lb, q.link_bytes())
+
+
+@pytest.mark.parametrize("name,G", [("gk8_2", 2), ("gk8_2", 4), ("hypercube3", 4),
+                                    ("gk64_4", 8), ("torus2x4_h2", 4)])
+def test_optimized_placement(name, G, artifacts):
+    """f4: the optimiser keeps per-GPU node counts, never raises the NVLink
+    bound, and the executor stays exact under the new placement."""
+    from paper_2309_13541_b200.executor import contiguous_placement
+    from paper_2309_13541_b200.placement import (cross_gpu_bytes, edge_bytes,
+                                                 optimized_placement)
+    a = artifacts(name)
+    c = contiguous_placement(a.g.n, G)
+    o = optimized_placement(a.g, a.sched, G)
+    assert sorted(np.bincount(o, minlength=G)) == sorted(np.bincount(c, minlength=G))
+    eb = edge_bytes(a.g, a.sched, 1 << 20)
+    bound = lambda pl: max(max(x) for x in cross_gpu_bytes(a.g, eb, pl))  # noqa: E731
+    assert bound(o) <= bound(c)
+    m = 3000
+    send = make_send(a.g.n, m, seed=1)
+    with Plan(a.g, a.sched, m=m, n_gpus=G, placement=o) as p:
+        nodes = [local_nodes(p, g) for g in range(G)]
+        recvs = p.emulate([send[ns] for ns in nodes], num_ctas=29, seed=3)
+    want = np.swapaxes(send, 0, 1)
+    for g in range(G):
+        assert np.array_equal(recvs[g], want[nodes[g]])
+
+
+def test_placement_known_optimum():
+    """GK(8,2) on 2 GPUs: exhaustive search finds the 16-chunk-MiB optimum."""
+    from paper_2309_13541_b200.artifacts import load_artifact
+    from paper_2309_13541_b200.placement import (cross_gpu_bytes, edge_bytes,
+                                                 optimized_placement)
+    a = load_artifact("gk8_2")
+    eb = edge_bytes(a.g, a.sched, 1 << 20)
+    o = optimized_placement(a.g, a.sched, 2)
+    assert max(max(x) for x in cross_gpu_bytes(a.g, eb, o)) == 16 << 20

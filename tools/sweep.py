@@ -41,6 +41,7 @@ def main(argv=None):
     ap.add_argument("--out", default=None)
     ap.add_argument("--mem-limit-gib", type=float, default=150.0)
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--placement", default="optimized", choices=["optimized", "contiguous"])
     a = ap.parse_args(argv)
     cases = list(PRESETS.get(a.preset, [])) if a.preset else []
     for c in filter(None, a.cases.split(",")):
@@ -59,7 +60,7 @@ def main(argv=None):
             rec["skipped"] = "artifact not generated"
         else:
             art = load_artifact(name)
-            with Plan(art.g, art.sched, m=m, n_gpus=ctx.world) as p:
+            with Plan(art.g, art.sched, m=m, n_gpus=ctx.world, placement=a.placement) as p:
                 mem = max(p.gpu_info(g)["send_bytes"] * 2 + p.gpu_info(g)["scratch_bytes"]
                           for g in range(ctx.world))
             if mem > a.mem_limit_gib * 2 ** 30:
@@ -67,7 +68,7 @@ def main(argv=None):
             else:
                 t0 = time.time()
                 r = bench.measure(ctx, art, m, a.steps, a.warmup, nccl=not a.no_nccl,
-                                  e2e=False, clocks=True)
+                                  e2e=False, clocks=True, placement=a.placement)
                 rec.update({
                     "nodes": art.g.n, "hop_ops": len(art.sched.instructions),
                     "nsteps": art.sched.nsteps, "Q": art.sched.Q,
@@ -78,6 +79,7 @@ def main(argv=None):
                     "clocks": r["clocks"], "sync_flags": r["sync"],
                     "kernel_timeline": r["kernel_timeline"],
                     "egress_max_bytes": r["egress_max"], "scratch_bytes": r["scratch_bytes"],
+                    "placement": a.placement,
                     "wall_s": round(time.time() - t0, 1)})
         if ctx.rank == 0:
             line = json.dumps(rec)
