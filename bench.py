@@ -263,7 +263,10 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     ctx.barrier()
     from paper_2309_13541_b200.executor import timeline_summary
     tls = timeline_summary(plan.read_timeline())            # last timed launch, this rank
-    tls["kernel_us"] = ctx.allmax([tls["kernel_us"]])[0]
+    if ctx.pg:
+        alltl = [None] * G
+        ctx.pg.all_gather_object(alltl, tls)
+        tls = {"kernel_us": max(x["kernel_us"] for x in alltl), "ranks": alltl}
     per = ctx.allmax([a.elapsed_time(b) for a, b in zip(e0, e1)])
     T = sum(per) / len(per) / 1e3                      # s per all-to-all (max over ranks)
     payload = n * (n - 1) * m
