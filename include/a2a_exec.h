@@ -82,6 +82,24 @@ typedef struct {
   int64_t local_bytes;     /* hop bytes that stay on this GPU (+ self copies)*/
 } a2a_gpu_info;
 
+/* ---- native loader for the reference's on-disk formats (plain or .gz) ---- */
+typedef struct {
+  int32_t n, nsteps, q;
+  int32_t mode;            /* 0 = "ts", 1 = "path" */
+  double chunk_bytes;
+} a2a_sched_header;
+/* parse_schedule_xml (reference src/schedule.py:349-384): same rejects, the
+ * ScheduleError texts come back as A2A_ERR_EVAL.  *ops is malloc'd: a2a_free. */
+int a2a_load_schedule_xml(const char* path, a2a_sched_header* hdr, a2a_op** ops, int64_t* n_ops);
+/* path-mode XML + `.routes.json` sidecar (reference src/cli.py:289-292) ->
+ * hop-indexed mode="ts" ops (hop i at step i, ts sort key of schedule.py:237).
+ * node_map (optional, length map_len) maps host-augmented ids to physical
+ * nodes (collapse, n_phys nodes). */
+int a2a_lower_path_files(const char* xml_path, const char* routes_path, const int32_t* node_map,
+                         int32_t map_len, int32_t n_phys, a2a_sched_header* hdr, a2a_op** ops,
+                         int64_t* n_ops);
+void a2a_free(void* p);
+
 /* ---- plan construction: validation exactly like the reference replay ---- */
 int a2a_plan_create(const a2a_schedule_desc* desc, a2a_plan** out);
 int a2a_plan_destroy(a2a_plan* plan);

@@ -34,6 +34,11 @@ class ScheduleDesc(C.Structure):
     ]
 
 
+class SchedHeader(C.Structure):
+    _fields_ = [("n", C.c_int32), ("nsteps", C.c_int32), ("q", C.c_int32),
+                ("mode", C.c_int32), ("chunk_bytes", C.c_double)]
+
+
 class GpuInfo(C.Structure):
     _fields_ = [
         ("n_local_nodes", C.c_int32), ("first_node", C.c_int32),
@@ -52,6 +57,12 @@ def _load():
     L = C.CDLL(LIB_PATH)
     P = C.c_void_p
     sig = {
+        "a2a_load_schedule_xml": ([C.c_char_p, C.POINTER(SchedHeader), C.POINTER(P),
+                                   C.POINTER(C.c_int64)], C.c_int),
+        "a2a_lower_path_files": ([C.c_char_p, C.c_char_p, P, C.c_int32, C.c_int32,
+                                  C.POINTER(SchedHeader), C.POINTER(P), C.POINTER(C.c_int64)],
+                                 C.c_int),
+        "a2a_free": ([P], None),
         "a2a_plan_create": ([C.POINTER(ScheduleDesc), C.POINTER(P)], C.c_int),
         "a2a_plan_destroy": ([P], C.c_int),
         "a2a_last_error": ([], C.c_char_p),

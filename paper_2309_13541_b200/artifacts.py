@@ -62,13 +62,25 @@ def list_artifacts() -> list:
                   if os.path.exists(os.path.join(ARTIFACT_DIR, x, "manifest.json")))
 
 
-def load_artifact(name: str, verify: bool = True) -> Artifact:
+def load_artifact(name: str, verify: bool = True, native: bool = False) -> Artifact:
+    """Load a frozen artifact; ``native=True`` parses and lowers in C++
+    (native_io) — identical ops, ~20x faster on GK(256,4)."""
     d = os.path.join(ARTIFACT_DIR, name)
     if verify:
         _verify(d)
     with open(os.path.join(d, "meta.json")) as fh:
         meta = json.load(fh)
     g = load_graph(_find(d, "graph.json"))
+    if native:
+        from .native_io import load_schedule_xml, lower_path_files
+        if meta["kind"] == "ts":
+            return Artifact(name, g, load_schedule_xml(_find(d, "ts.xml")), meta)
+        nm = None
+        if meta.get("host_capacity") is not None:
+            nm = [x // 3 for x in range(3 * g.n)]
+        ts = lower_path_files(_find(d, "path.xml"), _find(d, "path.xml.routes.json"),
+                              node_map=nm, n_phys=g.n)
+        return Artifact(name, g, ts, meta)
     if meta["kind"] == "ts":
         return Artifact(name, g, parse_schedule_xml(_find(d, "ts.xml")), meta)
     path_sched = parse_schedule_xml(_find(d, "path.xml"))

@@ -103,6 +103,8 @@ class Plan:
         self._edge_uv = np.ascontiguousarray(
             [(u, v) for u, v, _ in g.edges], dtype=np.int32).reshape(-1, 2)
         self._cap = np.ascontiguousarray([c for _, _, c in g.edges], dtype=np.float64)
+        if ops is None:
+            ops = getattr(sched, "ops_array", None)   # native-loaded schedules
         self._ops = _ops_array(sched.instructions if ops is None else ops)
         if placement is None or placement == "contiguous":
             placement = contiguous_placement(self.n, self.n_gpus)
