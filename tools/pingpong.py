@@ -58,7 +58,7 @@ def main():
     dist.all_gather_object(hs, h)
     other = hs[1 - rank]
     peer_storage = torch.UntypedStorage._new_shared_cuda(*other)
-    peer = torch.empty(0, dtype=torch.int32, device="cuda").set_(peer_storage)
+    peer = torch.empty(0, dtype=torch.int32, device=peer_storage.device).set_(peer_storage)
     out = torch.zeros(1, dtype=torch.int64, device="cuda")
     iters = 1000
     dist.barrier()
