@@ -49,6 +49,7 @@ typedef struct {
 /* descriptor flags */
 #define A2A_COPY_SELF 1  /* also copy the self shard send[v][v] -> recv[v][v] */
 #define A2A_INTERLEAVE 2 /* split items (split_bytes) and interleave destination GPUs */
+#define A2A_REUSE_SCRATCH 4 /* liveness-based scratch reuse (+ WAR/WAW dependencies) */
 
 typedef struct {
   int32_t n_nodes;         /* Digraph.n (must equal ChunkedSchedule.n)      */

@@ -92,6 +92,7 @@ struct Plan {
   std::vector<std::vector<int64_t>> step_ops;   // op indices per step, list order
   std::vector<int32_t> node_gpu, local_idx;
   int32_t T_exec = 1;                           // max(T, 1): self copies need a step
+  bool reuse = false;                           // scratch liveness reuse (A2A_REUSE_SCRATCH)
 
   // ---- layout / tables (host)
   std::vector<a2a_gpu_info> info;               // per gpu

@@ -221,15 +221,106 @@ static int build_plan(Plan& P, const a2a_schedule_desc* D) {
   std::unordered_map<uint64_t, std::vector<Interval>> slots;
   slots.reserve(keys.size() * 2 + 1);
   std::vector<int64_t> cursor(G, 0);
-  for (uint64_t k : keys) {
-    int v = (int)(k / ((uint64_t)n * n));
-    int g = P.node_gpu[v];
-    auto& out = slots[k];
-    for (auto& x : written[k].iv) {
-      int64_t lo = chunk_off(x.first, m, Q), hi = chunk_off(x.second, m, Q);
-      int64_t base = ((cursor[g] + 63) & ~(int64_t)63) + (lo & 63);
-      out.push_back(Interval{x.first, x.second, base});
-      cursor[g] = base + (hi - lo);
+  const bool reuse = (P.flags & A2A_REUSE_SCRATCH) != 0;
+  P.reuse = reuse;
+  if (!reuse) {
+    for (uint64_t k : keys) {
+      int v = (int)(k / ((uint64_t)n * n));
+      int g = P.node_gpu[v];
+      auto& out = slots[k];
+      for (auto& x : written[k].iv) {
+        int64_t lo = chunk_off(x.first, m, Q), hi = chunk_off(x.second, m, Q);
+        int64_t base = ((cursor[g] + 63) & ~(int64_t)63) + (lo & 63);
+        out.push_back(Interval{x.first, x.second, base});
+        cursor[g] = base + (hi - lo);
+      }
+    }
+  } else {
+    // Liveness reuse (SURVEY.md §7 hard part 4): each slot interval lives from
+    // its first write to its last access; an offline first-fit allocator hands
+    // out regions whose previous occupant is dead (strictly earlier step).
+    // build_sync adds the WAR/WAW dependencies that make reuse safe.
+    struct Ref { uint64_t key; int32_t a, b; int64_t lo, hi; int start, end, gpu; };
+    std::vector<Ref> refs;
+    std::unordered_map<uint64_t, std::vector<int>> by_key;
+    for (uint64_t k : keys) {
+      int v = (int)(k / ((uint64_t)n * n));
+      for (auto& x : written[k].iv) {
+        by_key[k].push_back((int)refs.size());
+        refs.push_back(Ref{k, x.first, x.second, chunk_off(x.first, m, Q), chunk_off(x.second, m, Q),
+                           INT32_MAX, -1, P.node_gpu[v]});
+      }
+    }
+    auto find = [&](int v, int s_, int d_, int32_t c0) -> Ref* {
+      auto it = by_key.find(key3(v, s_, d_, n));
+      if (it == by_key.end()) return nullptr;
+      for (int r : it->second)
+        if (refs[r].a <= c0 && c0 < refs[r].b) return &refs[r];
+      return nullptr;
+    };
+    for (int t = 0; t < T; ++t)
+      for (int64_t i : P.step_ops[t]) {
+        const a2a_op& o = P.ops[i];
+        if (o.c0 >= o.c1) continue;
+        if (o.dst != o.d) {
+          Ref* r = find(o.dst, o.s, o.d, o.c0);
+          if (r) { r->start = std::min(r->start, t); r->end = std::max(r->end, t); }
+        }
+        if (o.src != o.s && o.src != o.d) {
+          Ref* r = find(o.src, o.s, o.d, o.c0);
+          if (r) r->end = std::max(r->end, t);
+        }
+      }
+    std::vector<int> order(refs.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+      if (refs[x].gpu != refs[y].gpu) return refs[x].gpu < refs[y].gpu;
+      return refs[x].start < refs[y].start;
+    });
+    std::vector<std::map<int64_t, int64_t>> freel(G);           // offset -> size
+    std::vector<std::vector<std::array<int64_t, 3>>> active(G);   // {end, off, size}
+    std::unordered_map<int, int64_t> base_of;
+    auto release = [&](int g, int64_t off, int64_t size) {
+      auto& F = freel[g];
+      auto it = F.emplace(off, size).first;
+      auto nx = std::next(it);
+      if (nx != F.end() && it->first + it->second == nx->first) { it->second += nx->second; F.erase(nx); }
+      if (it != F.begin()) {
+        auto pv = std::prev(it);
+        if (pv->first + pv->second == it->first) { pv->second += it->second; F.erase(it); }
+      }
+    };
+    for (int r : order) {
+      Ref& R = refs[r];
+      const int g = R.gpu;
+      auto& A = active[g];
+      for (size_t j = 0; j < A.size();) {
+        if (A[j][0] < R.start) { release(g, A[j][1], A[j][2]); A[j] = A.back(); A.pop_back(); }
+        else ++j;
+      }
+      const int64_t need = R.hi - R.lo, res = R.lo & 63;
+      int64_t base = -1;
+      for (auto it = freel[g].begin(); it != freel[g].end(); ++it) {
+        int64_t b = it->first + (((res - it->first) % 64) + 64) % 64;
+        if (b + need <= it->first + it->second) {
+          const int64_t off = it->first, size = it->second;
+          freel[g].erase(it);
+          if (b > off) freel[g].emplace(off, b - off);
+          if (b + need < off + size) freel[g].emplace(b + need, off + size - (b + need));
+          base = b;
+          break;
+        }
+      }
+      if (base < 0) {
+        base = ((cursor[g] + 63) & ~(int64_t)63) + res;
+        cursor[g] = base + need;
+      }
+      if (need > 0) A.push_back({R.end, base, need});
+      base_of[r] = base;
+    }
+    for (uint64_t k : keys) {
+      auto& out = slots[k];
+      for (int r : by_key[k]) out.push_back(Interval{refs[r].a, refs[r].b, base_of[r]});
     }
   }
   for (int g = 0; g < G; ++g) P.info[g].scratch_bytes = (cursor[g] + 4095) & ~(int64_t)4095;
@@ -405,6 +496,7 @@ int build_sync(Plan& P, int nC) {
   const int G = P.G, TE = P.T_exec;
   SyncTables S;
   S.nC = nC;
+  (void)0;
   S.dst_mask.assign(G, std::vector<uint32_t>((size_t)TE * nC, 0));
   // segs[h][0] = writes into h's recv, segs[h][1] = into h's scratch
   std::vector<std::array<std::vector<Seg>, 2>> segs(G);
@@ -432,12 +524,61 @@ int build_sync(Plan& P, int nC) {
   S.wait_off.assign(G, {});
   S.wait_idx.assign(G, {});
   S.exit_idx.assign(G, {});
-  std::vector<int32_t> deps;
+  // per[g][t*nC + c]: producer slots CTA (g, c) must acquire before step t
+  std::vector<std::vector<std::vector<int32_t>>> per_all(G, std::vector<std::vector<int32_t>>((size_t)TE * nC));
+  if (P.reuse) {
+    // WAR / WAW: a write into reused scratch bytes waits for every earlier
+    // read (local CTAs of the owning GPU) and write of those bytes; the earlier
+    // CTAs also publish their flag to the writer's GPU.
+    std::vector<std::vector<Seg>> rseg(G), wseg(G);
+    std::vector<std::vector<int32_t>> rcta(G), wg(G);   // producer GPU of each segment
+    for (int g = 0; g < G; ++g)
+      for (int t = 0; t < TE; ++t)
+        for_each_piece(P.tables[g], t, nC, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
+          const int32_t slot = (int32_t)(((int64_t)t * G + g) * nC + c);
+          if (it.src_loc == loc_scratch(g, G)) {
+            rseg[g].push_back(Seg{it.src_off + x0, it.src_off + x1, t, slot});
+            rcta[g].push_back(g);
+          }
+          if (it.dst_loc == loc_scratch(it.dst_gpu, G)) {
+            wseg[it.dst_gpu].push_back(Seg{it.dst_off + x0, it.dst_off + x1, t, slot});
+            wg[it.dst_gpu].push_back(g);
+          }
+        });
+    for (int h = 0; h < G; ++h) {
+      // accesses of h's scratch, sorted by start with running max end
+      struct Acc { Seg s; int32_t gpu; };
+      std::vector<Acc> acc;
+      for (size_t i = 0; i < rseg[h].size(); ++i) acc.push_back(Acc{rseg[h][i], rcta[h][i]});
+      for (size_t i = 0; i < wseg[h].size(); ++i) acc.push_back(Acc{wseg[h][i], wg[h][i]});
+      std::sort(acc.begin(), acc.end(), [](const Acc& x, const Acc& y) { return x.s.a < y.s.a; });
+      std::vector<int64_t> me(acc.size());
+      int64_t mx = INT64_MIN;
+      for (size_t i = 0; i < acc.size(); ++i) me[i] = mx = std::max(mx, acc[i].s.b);
+      for (size_t i = 0; i < wseg[h].size(); ++i) {
+        const Seg& w = wseg[h][i];
+        const int g = wg[h][i];
+        const int c = (int)(w.slot % nC);
+        size_t j = std::lower_bound(acc.begin(), acc.end(), w.b,
+                                    [](const Acc& x, int64_t b) { return x.s.a < b; }) - acc.begin();
+        while (j > 0) {
+          --j;
+          if (me[j] <= w.a) break;
+          const Acc& q = acc[j];
+          if (q.s.b > w.a && q.s.t < w.t) {
+            per_all[g][(size_t)w.t * nC + c].push_back(q.s.slot);
+            const int qt = q.s.t, qc = (int)(q.s.slot % nC);
+            S.dst_mask[q.gpu][(size_t)qt * nC + qc] |= 1u << g;
+          }
+        }
+      }
+    }
+  }
   for (int h = 0; h < G; ++h) {
     auto& off = S.wait_off[h];
     auto& idx = S.wait_idx[h];
     off.assign((size_t)TE * nC + 1, 0);
-    std::vector<std::vector<int32_t>> per((size_t)TE * nC);
+    auto& per = per_all[h];
     for (int t = 0; t < TE; ++t) {
       for_each_piece(P.tables[h], t, nC, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
         if (it.src_loc == loc_send()) return;
@@ -515,7 +656,9 @@ static int emulate(Plan& P, int nC, uint8_t* const* send, uint8_t* const* recv, 
   const int G = P.G, TE = P.T_exec;
   std::vector<std::vector<uint8_t>> scratch(G);
   for (int g = 0; g < G; ++g) scratch[g].assign((size_t)P.info[g].scratch_bytes + 64, 0);
-  std::vector<char> flag((size_t)TE * G * nC, 0);
+  // per-GPU flag arrays: a producer's flag is visible on GPU h only if its
+  // destination mask has bit h (exactly what the kernel publishes)
+  std::vector<std::vector<char>> flag(G, std::vector<char>((size_t)TE * G * nC, 0));
   // per (g, c): list of (t, pieces) in step order
   struct Piece { int32_t src_loc, dst_loc; int64_t src, dst, n; };
   std::vector<std::vector<std::vector<std::vector<Piece>>>> work(
@@ -549,7 +692,7 @@ static int emulate(Plan& P, int nC, uint8_t* const* send, uint8_t* const* recv, 
         const auto& off = P.sync.wait_off[g];
         bool ok = true;
         for (int32_t i = off[(size_t)t * nC + c]; i < off[(size_t)t * nC + c + 1] && ok; ++i)
-          ok = flag[P.sync.wait_idx[g][i]];
+          ok = flag[g][P.sync.wait_idx[g][i]];
         if (ok) ready.emplace_back(g, c);
       }
     if (!left) break;
@@ -558,7 +701,9 @@ static int emulate(Plan& P, int nC, uint8_t* const* send, uint8_t* const* recv, 
     int t = next[g][c];
     for (const Piece& pc : work[g][c][t])
       std::memmove(base(g, pc.dst_loc) + pc.dst, base(g, pc.src_loc) + pc.src, (size_t)pc.n);
-    flag[((size_t)t * G + g) * nC + c] = 1;
+    uint32_t mask = P.sync.dst_mask[g][(size_t)t * nC + c];
+    for (int h = 0; h < G; ++h)
+      if (mask & (1u << h)) flag[h][((size_t)t * G + g) * nC + c] = 1;
     ++next[g][c];
   }
   return A2A_OK;

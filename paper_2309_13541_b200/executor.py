@@ -93,7 +93,8 @@ class Plan:
 
     def __init__(self, g, sched, m: int, placement=None, n_gpus: int = 1,
                  copy_self: bool = True, ops: np.ndarray | None = None,
-                 order: str | None = None, split_bytes: int = 0):
+                 order: str | None = None, split_bytes: int = 0,
+                 reuse_scratch: bool | None = None):
         _check_mode(g, sched)
         if int(m) != m or m < 0:
             raise ValueError(f"shard size m must be a non-negative integer, got {m}")
@@ -129,8 +130,13 @@ class Plan:
         if order not in ("grouped", "interleaved"):
             raise ValueError("order must be 'grouped' or 'interleaved'")
         self.order = order
+        if reuse_scratch is None:
+            import os
+            reuse_scratch = os.environ.get("A2A_REUSE_SCRATCH", "0") == "1"
+        self.reuse_scratch = bool(reuse_scratch)
         d.flags = (N.A2A_COPY_SELF if copy_self else 0) | \
-            (N.A2A_INTERLEAVE if order == "interleaved" else 0)
+            (N.A2A_INTERLEAVE if order == "interleaved" else 0) | \
+            (N.A2A_REUSE_SCRATCH if reuse_scratch else 0)
         d.split_bytes = int(split_bytes)
         h = C.c_void_p()
         rc = N.lib.a2a_plan_create(C.byref(d), C.byref(h))

@@ -112,3 +112,36 @@ def test_placement_known_optimum():
     eb = edge_bytes(a.g, a.sched, 1 << 20)
     o = optimized_placement(a.g, a.sched, 2)
     assert max(max(x) for x in cross_gpu_bytes(a.g, eb, o)) == 16 << 20
+
+
+@pytest.mark.parametrize("name,G", [("gk8_2", 1), ("gk8_2", 2), ("gk8_2", 8), ("torus4x4x4", 4),
+                                    ("torus4x4x4", 1), ("gk64_4_h2", 8), ("ts_torus2x4", 2),
+                                    ("ts_hypercube3", 4), ("ts_torus3x3", 1), ("torus2x4_h2", 8)])
+@pytest.mark.parametrize("nC", [7, 148])
+def test_scratch_reuse_interleavings(name, G, nC, artifacts):
+    """Liveness-reused scratch + WAR/WAW dependencies: exact under random
+    interleavings (per-GPU flag visibility), and never larger than static."""
+    a = artifacts(name)
+    m = 4096 if a.g.n <= 9 else 512
+    send = make_send(a.g.n, m, seed=4)
+    with Plan(a.g, a.sched, m=m, n_gpus=G, reuse_scratch=True) as p:
+        nodes = [local_nodes(p, g) for g in range(G)]
+        for seed in range(3):
+            recvs = p.emulate([send[ns] for ns in nodes], num_ctas=nC, seed=seed)
+            want = np.swapaxes(send, 0, 1)
+            for g in range(G):
+                assert np.array_equal(recvs[g], want[nodes[g]]), (seed, g)
+        reused = [p.gpu_info(g)["scratch_bytes"] for g in range(G)]
+    with Plan(a.g, a.sched, m=m, n_gpus=G) as q:
+        static = [q.gpu_info(g)["scratch_bytes"] for g in range(G)]
+    assert all(r <= s for r, s in zip(reused, static))
+
+
+def test_scratch_reuse_saves_memory(artifacts):
+    a = artifacts("torus4x4x4")
+    m = 1 << 20
+    with Plan(a.g, a.sched, m=m, reuse_scratch=True) as p:
+        r = p.gpu_info(0)["scratch_bytes"]
+    with Plan(a.g, a.sched, m=m) as q:
+        s = q.gpu_info(0)["scratch_bytes"]
+    assert r < 0.8 * s
