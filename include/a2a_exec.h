@@ -136,6 +136,15 @@ int a2a_optimize_placement(int32_t n, int32_t n_edges, const int32_t* edge_uv,
                            const int64_t* edge_bytes, int32_t n_gpus, int32_t iters,
                            uint64_t seed, int32_t* placement);
 
+/* Execution schedule, before bind: 0 = static per-CTA step programs (default),
+ * 1 = dynamic units: items cut into units of `unit_bytes` (0 = auto), CTAs grab
+ * units in step-major, readiness-ordered lists from a per-GPU atomic counter and
+ * acquire per-unit producer flags.  a2a_plan_emulate follows the
+ * selected mode.  Stats: units and dependency entries of `gpu`, model makespan. */
+int a2a_plan_set_schedule(a2a_plan* plan, int32_t mode, int64_t unit_bytes);
+int a2a_plan_dyn_stats(a2a_plan* plan, int32_t gpu, int32_t num_ctas, int64_t* n_units,
+                       int64_t* n_wait, double* est_makespan_s);
+
 /* ---- device side ---- */
 /* Bind the plan to one GPU: rank `gpu` of the placement on CUDA device
  * `device_ordinal`, with `num_ctas` persistent CTAs (0 = one per SM).  Allocates

@@ -77,6 +77,29 @@ struct SyncTables {
   std::vector<std::vector<int32_t>> exit_idx;   // [g] every producer slot that writes into g
 };
 
+// Dynamic mode: one unit of work = a contiguous sub-range of
+// one item; CTAs grab units in list order from a per-GPU atomic counter.
+struct DevUnit {
+  int64_t src_off, dst_off;
+  int32_t nbytes;
+  int32_t edge;
+  int16_t src_loc, dst_loc;
+  int32_t wb, we;     // [wb, we) in the GPU's unit wait list
+  uint32_t mask;      // GPUs whose flag array receives this unit's flag
+  int32_t step;
+};
+static_assert(sizeof(DevUnit) == 48, "DevUnit layout");
+
+struct DynTables {
+  int32_t nC = 0;
+  int64_t unit_bytes = 0;                       // target unit size (0 = auto)
+  std::vector<int32_t> unit_base;               // [G+1] global unit id = base[g] + index
+  std::vector<std::vector<DevUnit>> units;      // [g] grab order
+  std::vector<std::vector<int32_t>> wait_idx;   // [g] global unit ids to acquire
+  std::vector<std::vector<int32_t>> exit_idx;   // [g] global unit ids flagged into g
+  double est_makespan = 0;                      // host model estimate (s)
+};
+
 struct Interval {
   int32_t a, b;       // chunk range [a, b)
   int64_t base;       // scratch byte offset of chunk a's first byte
@@ -100,6 +123,9 @@ struct Plan {
   std::vector<int64_t> link_bytes;              // [T * E]
 
   SyncTables sync;
+  DynTables dyn;
+  int32_t sched_mode = 0;                       // 0 static per-CTA programs, 1 dynamic units
+  int64_t dyn_unit_bytes = 0;                   // dynamic unit size (0 = auto)
 
   // ---- device binding (a2a_exec.cu)
   bool bound = false, imported = false;
@@ -137,6 +163,7 @@ inline int64_t chunk_off(int64_t c, int64_t m, int64_t Q) {
 
 void set_error(const std::string& msg);
 int build_sync(Plan& P, int nC);
+int build_dyn(Plan& P, int nC, int64_t unit_bytes);
 int fail(int code, const std::string& msg);
 
 // CTA work split shared by host (flag lists) and device (copy ranges)

@@ -709,6 +709,230 @@ static int emulate(Plan& P, int nC, uint8_t* const* send, uint8_t* const* recv, 
   return A2A_OK;
 }
 
+// ---- dynamic unit schedule --------------------------------
+//
+// Items are cut into units of <= unit_bytes (multiples of 64 B from the item
+// start, so src/dst stay congruent).  A unit depends on every earlier-step
+// unit whose destination bytes overlap its source bytes (RAW) and, with
+// scratch reuse, on earlier readers/writers of the bytes it overwrites
+// (WAR/WAW).  Each GPU's list is step-major (deadlock freedom with in-order
+// grabbing: a unit only waits for units of earlier steps, which precede it in
+// every list); within a step units are ordered by their estimated ready time
+// from a simple pipe model (NVLink egress/ingress and HBM copy per GPU).
+int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
+  DynTables& D = P.dyn;
+  if (D.nC == nC && D.unit_bytes == unit_bytes && !D.units.empty()) return A2A_OK;
+  if (nC < 1) return fail(A2A_ERR_INVALID, "num_ctas must be >= 1");
+  const int G = P.G, TE = P.T_exec;
+  struct TU {
+    DevUnit u;
+    int g, t, dst_gpu;
+    double ready = 0, finish = 0;
+    std::vector<int> deps;
+    uint32_t notify = 0;
+  };
+  std::vector<TU> all;
+  std::vector<std::vector<std::vector<int>>> per(G, std::vector<std::vector<int>>(TE));
+  for (int g = 0; g < G; ++g) {
+    const GpuTables& tb = P.tables[g];
+    for (int t = 0; t < TE; ++t) {
+      int64_t target = unit_bytes > 0 ? unit_bytes
+                                      : std::min<int64_t>(4 << 20, std::max<int64_t>(64 << 10, tb.step_bytes[t] / (4LL * nC)));
+      target = std::max<int64_t>(64, std::min<int64_t>(target, 1LL << 30) & ~63LL);
+      for (int64_t k = tb.step_begin[t]; k < tb.step_begin[t + 1]; ++k) {
+        const DevItem& it = tb.items[k];
+        for (int64_t x = 0; x < it.nbytes; x += target) {
+          TU tu;
+          tu.u = DevUnit{};
+          tu.u.src_off = it.src_off + x;
+          tu.u.dst_off = it.dst_off + x;
+          tu.u.nbytes = (int32_t)std::min(target, it.nbytes - x);
+          tu.u.edge = it.edge;
+          tu.u.src_loc = (int16_t)it.src_loc;
+          tu.u.dst_loc = (int16_t)it.dst_loc;
+          tu.u.step = t;
+          tu.g = g;
+          tu.t = t;
+          tu.dst_gpu = it.dst_gpu;
+          per[g][t].push_back((int)all.size());
+          all.push_back(std::move(tu));
+        }
+      }
+    }
+  }
+  // writes into each GPU's recv (cls 0) / scratch (cls 1), sorted, for overlap queries
+  struct WS { int64_t a, b; int t, id; };
+  std::vector<std::array<std::vector<WS>, 2>> ws(G);
+  std::vector<std::vector<WS>> rs(G);  // scratch reads (for WAR)
+  for (int i = 0; i < (int)all.size(); ++i) {
+    const TU& x = all[i];
+    const int h = x.dst_gpu;
+    const int cls = (x.u.dst_loc == loc_recv(h)) ? 0 : 1;
+    ws[h][cls].push_back(WS{x.u.dst_off, x.u.dst_off + x.u.nbytes, x.t, i});
+    if (x.u.src_loc == loc_scratch(x.g, G)) rs[x.g].push_back(WS{x.u.src_off, x.u.src_off + x.u.nbytes, x.t, i});
+  }
+  auto prep = [](std::vector<WS>& v, std::vector<int64_t>& me) {
+    std::sort(v.begin(), v.end(), [](const WS& p, const WS& q) { return p.a < q.a; });
+    me.resize(v.size());
+    int64_t m = INT64_MIN;
+    for (size_t i = 0; i < v.size(); ++i) me[i] = m = std::max(m, v[i].b);
+  };
+  auto query = [](const std::vector<WS>& v, const std::vector<int64_t>& me, int64_t a, int64_t b,
+                  int tmax, std::vector<int>& out) {
+    size_t j = std::lower_bound(v.begin(), v.end(), b, [](const WS& s, int64_t x) { return s.a < x; }) - v.begin();
+    while (j > 0) {
+      --j;
+      if (me[j] <= a) break;
+      if (v[j].b > a && v[j].t < tmax) out.push_back(v[j].id);
+    }
+  };
+  std::vector<std::array<std::vector<int64_t>, 2>> wme(G);
+  std::vector<std::vector<int64_t>> rme(G);
+  for (int h = 0; h < G; ++h) {
+    prep(ws[h][0], wme[h][0]);
+    prep(ws[h][1], wme[h][1]);
+    prep(rs[h], rme[h]);
+  }
+  for (int i = 0; i < (int)all.size(); ++i) {
+    TU& x = all[i];
+    if (x.u.src_loc != loc_send()) {  // RAW on the executing GPU's own recv/scratch
+      const int cls = (x.u.src_loc == loc_recv(x.g)) ? 0 : 1;
+      query(ws[x.g][cls], wme[x.g][cls], x.u.src_off, x.u.src_off + x.u.nbytes, x.t, x.deps);
+    }
+    if (P.reuse && x.u.dst_loc == loc_scratch(x.dst_gpu, G)) {  // WAR / WAW
+      std::vector<int> q;
+      const int h = x.dst_gpu;
+      query(rs[h], rme[h], x.u.dst_off, x.u.dst_off + x.u.nbytes, x.t, q);
+      query(ws[h][1], wme[h][1], x.u.dst_off, x.u.dst_off + x.u.nbytes, x.t, q);
+      for (int j : q) {
+        x.deps.push_back(j);
+        all[j].notify |= 1u << x.g;
+      }
+    }
+    std::sort(x.deps.begin(), x.deps.end());
+    x.deps.erase(std::unique(x.deps.begin(), x.deps.end()), x.deps.end());
+  }
+  // readiness model: remote bytes at ~700 GB/s per GPU direction, local copies at ~3.2 TB/s
+  const double nv = 700e9, hbm = 3.2e12;
+  std::vector<double> eg_free(G, 0), in_free(G, 0), hbm_free(G, 0);
+  for (int t = 0; t < TE; ++t) {
+    std::vector<int> step_units;
+    for (int g = 0; g < G; ++g) {
+      for (int id : per[g][t]) {
+        TU& x = all[id];
+        x.ready = 0;
+        for (int d : x.deps) x.ready = std::max(x.ready, all[d].finish);
+      }
+      std::stable_sort(per[g][t].begin(), per[g][t].end(), [&](int a, int b) {
+        if (all[a].ready != all[b].ready) return all[a].ready < all[b].ready;
+        const bool ra = all[a].dst_gpu != all[a].g, rb = all[b].dst_gpu != all[b].g;
+        return ra > rb;  // remote first: NVLink is the scarce pipe
+      });
+      step_units.insert(step_units.end(), per[g][t].begin(), per[g][t].end());
+    }
+    std::stable_sort(step_units.begin(), step_units.end(),
+                     [&](int a, int b) { return all[a].ready < all[b].ready; });
+    for (int id : step_units) {
+      TU& x = all[id];
+      if (x.dst_gpu != x.g) {
+        double st = std::max(x.ready, std::max(eg_free[x.g], in_free[x.dst_gpu]));
+        x.finish = st + x.u.nbytes / nv;
+        eg_free[x.g] = in_free[x.dst_gpu] = x.finish;
+      } else {
+        double st = std::max(x.ready, hbm_free[x.g]);
+        x.finish = st + x.u.nbytes / hbm;
+        hbm_free[x.g] = x.finish;
+      }
+      D.est_makespan = std::max(D.est_makespan, x.finish);
+    }
+  }
+  // global ids in grab order
+  D.unit_base.assign(G + 1, 0);
+  std::vector<int> gid(all.size(), -1);
+  D.units.assign(G, {});
+  for (int g = 0; g < G; ++g) {
+    int k = 0;
+    for (int t = 0; t < TE; ++t)
+      for (int id : per[g][t]) gid[id] = D.unit_base[g] + k++;
+    D.unit_base[g + 1] = D.unit_base[g] + k;
+  }
+  D.wait_idx.assign(G, {});
+  D.exit_idx.assign(G, {});
+  for (int g = 0; g < G; ++g)
+    for (int t = 0; t < TE; ++t)
+      for (int id : per[g][t]) {
+        TU& x = all[id];
+        DevUnit u = x.u;
+        u.wb = (int32_t)D.wait_idx[g].size();
+        for (int d : x.deps) D.wait_idx[g].push_back(gid[d]);
+        u.we = (int32_t)D.wait_idx[g].size();
+        u.mask = (1u << x.dst_gpu) | x.notify;
+        D.units[g].push_back(u);
+        for (int h = 0; h < G; ++h)
+          if (u.mask & (1u << h)) D.exit_idx[h].push_back(gid[id]);
+      }
+  D.nC = nC;
+  D.unit_bytes = unit_bytes;
+  return A2A_OK;
+}
+
+// Host emulation of the dynamic protocol: CTAs grab units in list order and
+// execute them once their producers' flags are visible on their GPU; random
+// interleavings; a stuck state is a deadlock error.
+static int emulate_dyn(Plan& P, int nC, uint8_t* const* send, uint8_t* const* recv, uint64_t seed,
+                       int64_t unit_bytes) {
+  int rc = build_dyn(P, nC, unit_bytes);
+  if (rc) return rc;
+  const DynTables& D = P.dyn;
+  const int G = P.G;
+  std::vector<std::vector<uint8_t>> scratch(G);
+  for (int g = 0; g < G; ++g) scratch[g].assign((size_t)P.info[g].scratch_bytes + 64, 0);
+  const int total = D.unit_base[G];
+  std::vector<std::vector<char>> flag(G, std::vector<char>((size_t)total, 0));
+  std::vector<int> next(G, 0);
+  std::vector<std::vector<int>> held(G, std::vector<int>(nC, -1));
+  auto base = [&](int g, int loc) -> uint8_t* {
+    if (loc == loc_send()) return send[g];
+    if (loc >= 1 && loc < 1 + G) return recv[loc - 1];
+    return scratch[loc - 1 - G].data();
+  };
+  uint64_t x = seed * 0x9E3779B97F4A7C15ULL + 3;
+  auto rnd = [&]() { x ^= x << 13; x ^= x >> 7; x ^= x << 17; return x; };
+  for (;;) {
+    std::vector<std::pair<int, int>> act;  // (g, c): grab or run
+    bool busy = false;
+    for (int g = 0; g < G; ++g)
+      for (int c = 0; c < nC; ++c) {
+        int u = held[g][c];
+        if (u < 0) {
+          if (next[g] < (int)D.units[g].size()) act.emplace_back(g, c);
+          continue;
+        }
+        busy = true;
+        const DevUnit& du = D.units[g][u];
+        bool ok = true;
+        for (int32_t i = du.wb; i < du.we && ok; ++i) ok = flag[g][D.wait_idx[g][i]];
+        if (ok) act.emplace_back(g, c);
+      }
+    if (act.empty()) {
+      if (busy) return fail(A2A_ERR_INVALID, "dynamic emulation deadlock");
+      break;
+    }
+    auto [g, c] = act[rnd() % act.size()];
+    if (held[g][c] < 0) {
+      held[g][c] = next[g]++;
+    } else {
+      const DevUnit& du = D.units[g][held[g][c]];
+      std::memmove(base(g, du.dst_loc) + du.dst_off, base(g, du.src_loc) + du.src_off, (size_t)du.nbytes);
+      const int id = D.unit_base[g] + held[g][c];
+      for (int h = 0; h < G; ++h)
+        if (du.mask & (1u << h)) flag[h][id] = 1;
+      held[g][c] = -1;
+    }
+  }
+  return A2A_OK;
+}
+
 }  // namespace a2a
 
 using namespace a2a;
@@ -789,6 +1013,27 @@ int a2a_plan_prepare(a2a_plan* plan, int32_t num_ctas) {
   }
 }
 
+int a2a_plan_set_schedule(a2a_plan* plan, int32_t mode, int64_t unit_bytes) {
+  if (!plan || (mode != 0 && mode != 1) || unit_bytes < 0) return fail(A2A_ERR_INVALID, "bad schedule mode");
+  if (plan->p.bound) return fail(A2A_ERR_STATE, "set the schedule mode before a2a_plan_bind");
+  plan->p.sched_mode = mode;
+  plan->p.dyn_unit_bytes = unit_bytes;
+  plan->p.dyn = DynTables{};
+  return A2A_OK;
+}
+
+int a2a_plan_dyn_stats(a2a_plan* plan, int32_t gpu, int32_t num_ctas, int64_t* n_units,
+                       int64_t* n_wait, double* est_makespan_s) {
+  if (!plan || !n_units || !n_wait || !est_makespan_s) return fail(A2A_ERR_INVALID, "null argument");
+  if (gpu < 0 || gpu >= plan->p.G) return fail(A2A_ERR_INVALID, "gpu out of range");
+  int rc = build_dyn(plan->p, num_ctas, plan->p.dyn_unit_bytes);
+  if (rc) return rc;
+  *n_units = (int64_t)plan->p.dyn.units[gpu].size();
+  *n_wait = (int64_t)plan->p.dyn.wait_idx[gpu].size();
+  *est_makespan_s = plan->p.dyn.est_makespan;
+  return A2A_OK;
+}
+
 int a2a_plan_sync_stats(const a2a_plan* plan, int32_t gpu, int64_t* n_wait, int64_t* n_exit) {
   if (!plan || !n_wait || !n_exit) return fail(A2A_ERR_INVALID, "null argument");
   const SyncTables& S = plan->p.sync;
@@ -803,6 +1048,9 @@ int a2a_plan_emulate(a2a_plan* plan, int32_t num_ctas, void* const* send, void* 
                      uint64_t seed) {
   if (!plan || !send || !recv) return fail(A2A_ERR_INVALID, "null argument");
   try {
+    if (plan->p.sched_mode == 1)
+      return emulate_dyn(plan->p, num_ctas, (uint8_t* const*)send, (uint8_t* const*)recv, seed,
+                         plan->p.dyn_unit_bytes);
     return emulate(plan->p, num_ctas, (uint8_t* const*)send, (uint8_t* const*)recv, seed);
   } catch (const std::bad_alloc&) {
     return fail(A2A_ERR_NOMEM, "out of host memory in emulation");

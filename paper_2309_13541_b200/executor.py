@@ -148,6 +148,7 @@ class Plan:
         self.engine = None
         self._bufcheck = None
         self._num_ctas = 0
+        self.schedule = None
 
     # ---- lifetime
     def close(self):
@@ -198,6 +199,20 @@ class Plan:
         self._ck(N.lib.a2a_plan_prepare(self._h, int(num_ctas)), "a2a_plan_prepare")
         return self
 
+    def set_schedule(self, mode: str = "static", unit_bytes: int = 0):
+        """Before bind: "static" per-CTA step programs or "dynamic" units
+        grabbed from a per-GPU queue."""
+        code = {"static": 0, "dynamic": 1}[mode]
+        self._ck(N.lib.a2a_plan_set_schedule(self._h, code, int(unit_bytes)), "a2a_plan_set_schedule")
+        self.schedule = mode
+        return self
+
+    def dyn_stats(self, gpu: int, num_ctas: int) -> dict:
+        nu, nw, est = C.c_int64(), C.c_int64(), C.c_double()
+        self._ck(N.lib.a2a_plan_dyn_stats(self._h, int(gpu), int(num_ctas), C.byref(nu),
+                                          C.byref(nw), C.byref(est)), "a2a_plan_dyn_stats")
+        return {"units": nu.value, "wait_entries": nw.value, "model_makespan_s": est.value}
+
     def sync_stats(self, gpu: int) -> dict:
         w, e = C.c_int64(), C.c_int64()
         self._ck(N.lib.a2a_plan_sync_stats(self._h, int(gpu), C.byref(w), C.byref(e)),
@@ -240,6 +255,9 @@ class Plan:
                 parts = env.split(":")      # tma[:chunk[:stages]]
                 self.set_engine(parts[0], *(int(x) for x in parts[1:]))
         import os
+        if getattr(self, "schedule", None) is None and os.environ.get("A2A_SCHED"):
+            parts = os.environ["A2A_SCHED"].split(":")   # dynamic[:unit_bytes]
+            self.set_schedule(parts[0], *(int(x) for x in parts[1:]))
         if os.environ.get("A2A_SYNC_MODE"):
             self.set_sync_mode(int(os.environ["A2A_SYNC_MODE"]))
         self._ck(N.lib.a2a_plan_bind(self._h, int(gpu), int(device), int(num_ctas)),

@@ -145,3 +145,27 @@ def test_scratch_reuse_saves_memory(artifacts):
     with Plan(a.g, a.sched, m=m) as q:
         s = q.gpu_info(0)["scratch_bytes"]
     assert r < 0.8 * s
+
+
+@pytest.mark.parametrize("name,G", [("gk8_2", 1), ("gk8_2", 2), ("gk8_2", 8), ("hypercube3", 4),
+                                    ("torus4x4x4", 4), ("gk64_4_h2", 8), ("ts_torus2x4", 2),
+                                    ("ts_torus3x3", 1), ("torus2x4_h2", 4)])
+@pytest.mark.parametrize("unit", [0, 256, 1000 * 64])
+@pytest.mark.parametrize("reuse", [False, True])
+def test_dynamic_schedule_interleavings(name, G, unit, reuse, artifacts):
+    """Dynamic unit queues (f2): in-order grabbing + per-unit producer flags
+    deliver the transpose under random interleavings, with and without
+    scratch reuse, and never deadlock."""
+    a = artifacts(name)
+    m = 5000 if a.g.n <= 9 else 640
+    send = make_send(a.g.n, m, seed=6)
+    with Plan(a.g, a.sched, m=m, n_gpus=G, reuse_scratch=reuse) as p:
+        p.set_schedule("dynamic", unit)
+        nodes = [local_nodes(p, g) for g in range(G)]
+        for seed in range(2):
+            recvs = p.emulate([send[ns] for ns in nodes], num_ctas=11, seed=seed)
+            want = np.swapaxes(send, 0, 1)
+            for g in range(G):
+                assert np.array_equal(recvs[g], want[nodes[g]]), (seed, g)
+        st = p.dyn_stats(0, 11)
+        assert st["units"] > 0
