@@ -58,7 +58,13 @@ struct KParams {
   int32_t sync_mode;                       // bit0: acq_rel (not sc) publish fence; bit1: no
                                            // explicit publish fence; bit2: force .sys at G=1
   int32_t smem_prog, smem_batch, batch;    // dynamic smem offsets, pieces per staged batch
-  unsigned long long* timeline;            // [nC][T'+3] %globaltimer: start, entry done, steps.., end
+  unsigned long long* timeline;            // [nC][2T'+3] %globaltimer stamps (see read_timeline)
+  // dynamic mode (a2a_dyn_kernel)
+  const DevUnit* units;                    // this GPU's units in grab order
+  const int32_t* unit_wait;                // global unit ids to acquire
+  int32_t n_units, unit_base;              // this GPU's units; global id of its first
+  unsigned long long* grab;                // per-GPU grab counter (own arena)
+  unsigned long long grab_base;            // counter value at the start of this execute
 };
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -461,6 +467,177 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
   if (tid == 0) tl[2 + p.T] = globaltimer();
 }
 
+// ---- dynamic mode: CTAs grab units from a per-GPU counter ----
+template <int kEngine, int kThreads>
+__global__ void __launch_bounds__(kThreads, 1) a2a_dyn_kernel(const KParams p) {
+  __shared__ int s_abort;
+  __shared__ long long s_idx;
+  __shared__ DevUnit s_u;
+  __shared__ DevPiece s_pc[1];
+  extern __shared__ __align__(128) unsigned char dsmem[];
+  const int c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5;
+  const int S = p.tma_stages;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dsmem);
+  char** ring_dst = reinterpret_cast<char**>(dsmem + 8 * S);
+  uint32_t* ring_n = reinterpret_cast<uint32_t*>(dsmem + 16 * S);
+  char* stages = reinterpret_cast<char*>(dsmem + ((20 * S + 127) & ~127));
+  uint32_t gi = 0;
+  unsigned long long* tl = p.timeline + (int64_t)c * (2 * p.T + 3);
+  if (tid == 0) {
+    tl[0] = globaltimer();
+    s_abort = 0;
+    if (kEngine == 1) {
+      for (int i = 0; i < S; ++i) mbar_init(&bars[i], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
+  __syncthreads();
+  const uint32_t* my_flags = p.step_flags[p.rank];
+  const bool sys = p.G > 1 || (p.sync_mode & 4);
+  if (p.G > 1) {  // entry barrier (same protocol as the static kernel)
+    if (c == 0 && tid < p.G && tid != p.rank) st_release_sys(p.entry_flags[tid] + p.rank, p.epoch);
+    if (warp == 0) {
+      const int lane = tid & 31;
+      bool ok = true;
+      if (lane < p.G && lane != p.rank) {
+        const uint32_t* f = p.entry_flags[p.rank] + lane;
+        uint64_t t0 = globaltimer();
+        uint32_t spins = 0;
+        while ((int32_t)(ld_acquire_sys(f) - p.epoch) < 0) {
+          if ((++spins & 255) == 0 && ((int64_t)(globaltimer() - t0) > p.timeout_ns ||
+                                       *(volatile int32_t*)p.err != 0)) {
+            ok = false;
+            break;
+          }
+        }
+      }
+      ok = __all_sync(0xffffffffu, ok);
+      if (!ok && lane == 0) { atomicCAS(p.err, 0, (int32_t)A2A_ERR_TIMEOUT); s_abort = 1; }
+    }
+    __syncthreads();
+    if (s_abort) return;
+  }
+  if (tid == 0) tl[1] = globaltimer();
+  unsigned long long waited_ns = 0, done = 0;
+  for (;;) {
+    if (tid == 0) {
+      const long long idx = (long long)(atomicAdd(p.grab, 1ull) - p.grab_base);
+      s_idx = idx;
+      if (idx < p.n_units) {
+        const DevUnit u = p.units[idx];
+        s_u = u;
+        s_pc[0] = DevPiece{u.src_off, u.dst_off, u.nbytes, u.edge, u.src_loc, u.dst_loc, 0};
+      }
+    }
+    __syncthreads();
+    const long long idx = s_idx;
+    if (idx >= p.n_units) break;
+    const DevUnit u = s_u;
+    if (u.we > u.wb) {
+      if (warp == 0) {
+        const uint64_t w0 = globaltimer();
+        bool ok = warp_wait_flags(my_flags, p.unit_wait, u.wb, u.we, p.epoch, p.timeout_ns, p.err,
+                                  sys, p.sync_mode);
+        if (!ok && tid == 0) s_abort = 1;
+        if (tid == 0) waited_ns += globaltimer() - w0;
+      }
+      __syncthreads();
+      if (s_abort) return;
+    }
+    const char* s0 = p.base[u.src_loc] + u.src_off;
+    char* d0 = p.base[u.dst_loc] + u.dst_off;
+    if (kEngine == 0) {
+      cta_copy<4>(d0, s0, u.nbytes);
+    } else if (tid != 0) {
+      const int nt = kThreads - 1, me = tid - 1;
+      const int64_t len = u.nbytes;
+      if ((((uintptr_t)s0 ^ (uintptr_t)d0) & 15) != 0) {
+        for (int64_t j = me; j < len; j += nt) d0[j] = s0[j];
+      } else {
+        int64_t head = (16 - ((uintptr_t)d0 & 15)) & 15;
+        if (head > len) head = len;
+        const int64_t body = (len - head) & ~(int64_t)15, tail = len - head - body;
+        if (me < head) d0[me] = s0[me];
+        if (me < tail) d0[head + body + me] = s0[head + body + me];
+      }
+    } else {
+      fence_proxy_async();
+      const uint32_t CH = (uint32_t)p.tma_chunk;
+      BodyCursor cur{s_pc, 0, 1, 0};
+      const uint32_t g0 = gi;
+      uint32_t nl = 0, ns = 0;
+      bool more = true;
+      auto issue = [&]() -> bool {
+        const char* src;
+        char* dst;
+        uint32_t len;
+        if (!cur.next(p, CH, &src, &dst, &len)) return false;
+        const uint32_t st = (g0 + nl) % S;
+        ring_dst[st] = dst;
+        ring_n[st] = len;
+        mbar_expect_tx(&bars[st], len);
+        bulk_load(stages + (size_t)st * CH, src, len, &bars[st]);
+        ++nl;
+        return true;
+      };
+      while (more && nl < (uint32_t)S) more = issue();
+      while (ns < nl) {
+        const uint32_t st = (g0 + ns) % S;
+        mbar_wait(&bars[st], ((g0 + ns) / S) & 1);
+        bulk_store(ring_dst[st], stages + (size_t)st * CH, ring_n[st]);
+        ++ns;
+        if (more) {
+          if (S == 1) {
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            more = issue();
+          } else if (ns >= 2 && nl - (uint32_t)S == ns - 2) {
+            bulk_wait_read1();
+            more = issue();
+          }
+        }
+      }
+      bulk_wait_all();
+      fence_proxy_async();
+      gi = g0 + nl;
+    }
+    if (p.count_links && tid == 0 && u.edge >= 0)
+      atomicAdd(p.counters + (int64_t)u.step * p.E + u.edge, (unsigned long long)u.nbytes);
+    __syncthreads();
+    if (tid == 0) {
+      const int64_t slot = (int64_t)p.unit_base + idx;
+      uint32_t mask = u.mask;
+      while (mask) {
+        const int h = __ffs(mask) - 1;
+        mask &= mask - 1;
+        st_release(p.step_flags[h] + slot, p.epoch, sys);
+      }
+      ++done;
+    }
+  }
+  if (c == 0 && p.G > 1) {  // exit: every unit flagged into this GPU has landed
+    bool ok = true;
+    for (int32_t i = tid; i < p.n_exit && ok; i += kThreads) {
+      const uint32_t* f = my_flags + p.exit_idx[i];
+      uint64_t t0 = globaltimer();
+      uint32_t spins = 0;
+      while ((int32_t)(ld_acquire_sys(f) - p.epoch) < 0) {
+        if ((++spins & 255) == 0 && ((int64_t)(globaltimer() - t0) > p.timeout_ns ||
+                                     *(volatile int32_t*)p.err != 0)) {
+          ok = false;
+          break;
+        }
+      }
+    }
+    if (!ok) atomicCAS(p.err, 0, (int32_t)A2A_ERR_TIMEOUT);
+    __syncthreads();
+  }
+  if (tid == 0) {
+    tl[2] = done;
+    tl[3] = waited_ns;
+    tl[2 + p.T] = globaltimer();
+  }
+}
+
 static int cuda_fail(cudaError_t e, const char* what) {
   char buf[256];
   snprintf(buf, sizeof buf, "%s: %s", what, cudaGetErrorString(e));
@@ -495,6 +672,15 @@ struct EngineCfg {
 };
 static EngineCfg engine_cfg(const Plan& P) {
   const int TE = P.T_exec;
+  if (P.sched_mode == 1) {
+    if (P.engine == 1) {
+      int S = P.tma_stages;
+      while (S > 1 && ((20 * (size_t)S + 127) & ~(size_t)127) + (size_t)S * P.tma_chunk > 220 * 1024) --S;
+      const size_t ring = ((20 * (size_t)S + 127) & ~(size_t)127) + (size_t)S * P.tma_chunk;
+      return {(const void*)a2a_dyn_kernel<1, 256>, 256, ring, S, 0, 0, 0};
+    }
+    return {(const void*)a2a_dyn_kernel<0, 1024>, 1024, 0, 0, 0, 0, 0};
+  }
   const size_t prog = ((size_t)TE * sizeof(CtaStep) + 127) & ~(size_t)127;
   if (P.engine == 1) {
     const int batch = 64;
@@ -513,11 +699,13 @@ static EngineCfg engine_cfg(const Plan& P) {
           (int)prog, batch};
 }
 
-// arena flag region: entry[G] u32 | step flags [T'][G][nC] u32
+// arena flag region: entry[G] u32 | grab counter u64 @128 | flags @256:
+//   static: [T'][G][nC] u32 (slot (t, gpu, cta)); dynamic: [total units] u32
 static inline int64_t entry_flags_off() { return 0; }
+static inline int64_t grab_off() { return 128; }
 static inline int64_t step_flags_off() { return 256; }
-static inline int64_t flag_region_bytes(int G, int TE, int nC) {
-  return (step_flags_off() + (int64_t)TE * G * nC * 4 + 65535) & ~65535LL;
+static inline int64_t flag_region_bytes(int64_t n_flags) {
+  return (step_flags_off() + n_flags * 4 + 65535) & ~65535LL;
 }
 
 static inline int64_t recv_stride(const Plan& P, int g) {
@@ -579,12 +767,14 @@ static int bind_plan(Plan& P, int gpu, int dev, int nC) {
   const int G = P.G, TE = P.T_exec;
 
   // ---- CTA split + producer dependency lists (host, identical on all ranks)
-  int rc = build_sync(P, nC);
+  int rc = P.sched_mode == 1 ? build_dyn(P, nC, P.dyn_unit_bytes) : build_sync(P, nC);
   if (rc != A2A_OK) return rc;
   const SyncTables& S = P.sync;
+  const DynTables& Dy = P.dyn;
 
   // ---- arena layout, identical on every rank: flags | recv | scratch
-  P.flags_bytes = flag_region_bytes(G, TE, nC);
+  P.flags_bytes = flag_region_bytes(P.sched_mode == 1 ? (int64_t)Dy.unit_base[G]
+                                                      : (int64_t)TE * G * nC);
   P.recv_off.assign(G, 0);
   P.scratch_off.assign(G, 0);
   P.arena_bytes.assign(G, 0);
@@ -602,10 +792,17 @@ static int bind_plan(Plan& P, int gpu, int dev, int nC) {
     return fail(A2A_ERR_NOMEM, buf);
   }
   CK(cudaMemset(P.arena, 0, (size_t)P.flags_bytes));
-  if ((rc = upload(&P.d_items, S.pieces[gpu])) != A2A_OK) return rc;
-  if ((rc = upload(&P.d_step_begin, S.prog[gpu])) != A2A_OK) return rc;
-  if ((rc = upload(&P.d_wait_idx, S.wait_idx[gpu])) != A2A_OK) return rc;
-  if ((rc = upload(&P.d_exit_idx, S.exit_idx[gpu])) != A2A_OK) return rc;
+  if (P.sched_mode == 1) {
+    if ((rc = upload(&P.d_items, Dy.units[gpu])) != A2A_OK) return rc;
+    if ((rc = upload(&P.d_wait_idx, Dy.wait_idx[gpu])) != A2A_OK) return rc;
+    if ((rc = upload(&P.d_exit_idx, Dy.exit_idx[gpu])) != A2A_OK) return rc;
+  } else {
+    if ((rc = upload(&P.d_items, S.pieces[gpu])) != A2A_OK) return rc;
+    if ((rc = upload(&P.d_step_begin, S.prog[gpu])) != A2A_OK) return rc;
+    if ((rc = upload(&P.d_wait_idx, S.wait_idx[gpu])) != A2A_OK) return rc;
+    if ((rc = upload(&P.d_exit_idx, S.exit_idx[gpu])) != A2A_OK) return rc;
+  }
+  P.dyn_execs = 0;
   CK(cudaMalloc(&P.d_timeline, (size_t)nC * (2 * TE + 3) * 8));
   CK(cudaMemset(P.d_timeline, 0, (size_t)nC * (2 * TE + 3) * 8));
   size_t cbytes = std::max<size_t>((size_t)TE * std::max(P.E, 1) * 8, 16);
@@ -794,7 +991,18 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
   kp.pieces = (const DevPiece*)P.d_items;
   kp.prog = (const CtaStep*)P.d_step_begin;
   kp.exit_idx = (const int32_t*)P.d_exit_idx;
-  kp.n_exit = (int32_t)P.sync.exit_idx[P.rank].size();
+  if (P.sched_mode == 1) {
+    const DynTables& Dy = P.dyn;
+    kp.n_exit = (int32_t)Dy.exit_idx[P.rank].size();
+    kp.units = (const DevUnit*)P.d_items;
+    kp.unit_wait = (const int32_t*)P.d_wait_idx;
+    kp.n_units = (int32_t)Dy.units[P.rank].size();
+    kp.unit_base = Dy.unit_base[P.rank];
+    kp.grab = (unsigned long long*)((char*)P.arena + grab_off());
+    kp.grab_base = (unsigned long long)P.dyn_execs * (unsigned long long)(kp.n_units + P.nC);
+  } else {
+    kp.n_exit = (int32_t)P.sync.exit_idx[P.rank].size();
+  }
   kp.wait_idx = (const int32_t*)P.d_wait_idx;
   kp.counters = (unsigned long long*)P.d_counters;
   kp.err = P.d_err;
@@ -819,6 +1027,7 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
   cudaError_t e = cudaLaunchCooperativeKernel(ec.fn, dim3(P.nC), dim3(ec.threads), args, ec.smem,
                                               (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchCooperativeKernel");
+  if (P.sched_mode == 1) ++P.dyn_execs;
   P.last_stream = stream;
   P.launched = true;
   return A2A_OK;

@@ -126,6 +126,7 @@ struct Plan {
   DynTables dyn;
   int32_t sched_mode = 0;                       // 0 static per-CTA programs, 1 dynamic units
   int64_t dyn_unit_bytes = 0;                   // dynamic unit size (0 = auto)
+  int64_t dyn_execs = 0;                        // dynamic executes so far (grab counter base)
 
   // ---- device binding (a2a_exec.cu)
   bool bound = false, imported = false;

@@ -171,3 +171,45 @@ def test_tma_engine_n64(artifacts):
         p.execute(s, r)
         p.sync()
     assert torch.equal(r, s.transpose(0, 1).contiguous())
+
+
+@pytest.mark.parametrize("name", ["torus2x4", "gk8_2", "torus2x4_h2", "ts_hypercube3", "ts_torus3x3"])
+@pytest.mark.parametrize("engine", ["tma", "lsu"])
+@pytest.mark.parametrize("m,unit", [(7, 0), (4096 + 5, 0), (65536, 4096), ((1 << 20) + 48, 0)])
+@pytest.mark.parametrize("reuse", [False, True])
+def test_dynamic_schedule_bit_exact(name, engine, m, unit, reuse, artifacts):
+    """Dynamic unit queues (f2) on the device: exact over repeated executes
+    (the grab counter carries across epochs), with and without scratch reuse."""
+    from paper_2309_13541_b200.executor import Plan
+    from replay_bytes import replay_bytes
+    a = artifacts(name)
+    with Plan(a.g, a.sched, m=m, reuse_scratch=reuse) as p:
+        p.set_schedule("dynamic", unit)
+        p.set_engine(engine)
+        p.bind(0)
+        for rep in range(3):
+            send = _send(a.g.n, m, seed=rep + m % 13)
+            _, want, _ = replay_bytes(a.g, a.sched, send, m)
+            s = torch.from_numpy(send).cuda()
+            r = torch.zeros_like(s)
+            p.execute(s, r, count_links=True)
+            p.sync()
+            assert np.array_equal(r.cpu().numpy(), want), rep
+        assert np.array_equal(p.read_link_counters(), 3 * p.link_bytes())
+
+
+@pytest.mark.parametrize("reuse", [False, True])
+def test_dynamic_n64(reuse, artifacts):
+    from paper_2309_13541_b200.executor import Plan
+    a = artifacts("gk64_4_h2")
+    m = 32768 + 16
+    g = torch.Generator(device="cuda").manual_seed(5)
+    s = torch.randint(0, 256, (64, 64, m), dtype=torch.uint8, device="cuda", generator=g)
+    with Plan(a.g, a.sched, m=m, reuse_scratch=reuse) as p:
+        p.set_schedule("dynamic")
+        p.bind(0)
+        for _ in range(2):
+            r = torch.zeros_like(s)
+            p.execute(s, r)
+            p.sync()
+            assert torch.equal(r, s.transpose(0, 1).contiguous())

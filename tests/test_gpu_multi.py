@@ -34,7 +34,7 @@ def _port():
     return p
 
 
-def _rank_main(rank, world, port, name, m, reps, q, engine="lsu"):
+def _rank_main(rank, world, port, name, m, reps, q, engine="lsu", sched="static", reuse=False):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     try:
@@ -49,8 +49,9 @@ def _rank_main(rank, world, port, name, m, reps, q, engine="lsu"):
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}",
                                 rank=rank, world_size=world)
         a = load_artifact(name)
-        plan = Plan(a.g, a.sched, m=m, n_gpus=world)
+        plan = Plan(a.g, a.sched, m=m, n_gpus=world, reuse_scratch=reuse, placement="optimized")
         plan.set_engine(engine)
+        plan.set_schedule(sched)
         plan.bind(rank, device=rank)
         plan.set_timeout(20.0)
         connect(plan)
@@ -175,6 +176,32 @@ def _alt_main(rank, world, port, q):
     except Exception as ex:
         import traceback
         q.put((rank, f"{ex!r}\n{traceback.format_exc()}"))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("engine", ["tma", "lsu"])
+@pytest.mark.parametrize("reuse", [False, True])
+@pytest.mark.parametrize("name,m", [("gk8_2", 65536 + 64), ("torus4x4x4", 8192), ("torus2x4_h2", 4099)])
+def test_multiprocess_dynamic(world, engine, reuse, name, m):
+    """Dynamic unit queues across GPUs (+ scratch reuse, optimized placement)."""
+    if _ngpu() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_rank_main,
+                      args=(r, world, port, name, m, 3, q, engine, "dynamic", reuse))
+          for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=300) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    for r in sorted(res, key=lambda x: x[0]):
+        assert len(r) == 3, r
+        assert r[1], f"rank {r[0]}: recv mismatch"
+        assert r[2], f"rank {r[0]}: link counters differ from schedule"
 
 
 def test_alternating_recv_buffers():
