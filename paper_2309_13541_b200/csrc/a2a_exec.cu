@@ -63,8 +63,9 @@ struct KParams {
   const DevUnit* units;                    // this GPU's units in grab order
   const int32_t* unit_wait;                // global unit ids to acquire
   int32_t n_units, unit_base;              // this GPU's units; global id of its first
-  unsigned long long* grab;                // per-GPU grab counter (own arena)
-  unsigned long long grab_base;            // counter value at the start of this execute
+  int32_t n_remote, remote_ctas;           // remote queue = units [0, n_remote); CTAs starting on it
+  unsigned long long* grab;                // per-GPU grab counters [2] (remote, local queue)
+  unsigned long long grab_base[2];         // counter values at the start of this execute
 };
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -519,11 +520,19 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_dyn_kernel(const KParams p) {
   }
   if (tid == 0) tl[1] = globaltimer();
   unsigned long long waited_ns = 0, done = 0;
+  int q = c < p.remote_ctas ? 0 : 1, visited = 0;  // queue of thread 0
   for (;;) {
     if (tid == 0) {
-      const long long idx = (long long)(atomicAdd(p.grab, 1ull) - p.grab_base);
+      long long idx = -1;
+      for (;;) {  // own queue first, then the other; one failing grab per queue
+        const long long qn = q == 0 ? p.n_remote : (long long)p.n_units - p.n_remote;
+        const long long j = (long long)(atomicAdd(p.grab + q, 1ull) - p.grab_base[q]);
+        if (j < qn) { idx = (q == 0 ? 0 : p.n_remote) + j; break; }
+        if (++visited == 2) break;
+        q ^= 1;
+      }
       s_idx = idx;
-      if (idx < p.n_units) {
+      if (idx >= 0) {
         const DevUnit u = p.units[idx];
         s_u = u;
         s_pc[0] = DevPiece{u.src_off, u.dst_off, u.nbytes, u.edge, u.src_loc, u.dst_loc, 0};
@@ -531,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_dyn_kernel(const KParams p) {
     }
     __syncthreads();
     const long long idx = s_idx;
-    if (idx >= p.n_units) break;
+    if (idx < 0) break;
     const DevUnit u = s_u;
     if (u.we > u.wb) {
       if (warp == 0) {
@@ -999,7 +1008,11 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
     kp.n_units = (int32_t)Dy.units[P.rank].size();
     kp.unit_base = Dy.unit_base[P.rank];
     kp.grab = (unsigned long long*)((char*)P.arena + grab_off());
-    kp.grab_base = (unsigned long long)P.dyn_execs * (unsigned long long)(kp.n_units + P.nC);
+    kp.n_remote = Dy.n_remote[P.rank];
+    kp.remote_ctas = Dy.remote_ctas[P.rank];
+    kp.grab_base[0] = (unsigned long long)P.dyn_execs * (unsigned long long)(kp.n_remote + P.nC);
+    kp.grab_base[1] =
+        (unsigned long long)P.dyn_execs * (unsigned long long)(kp.n_units - kp.n_remote + P.nC);
   } else {
     kp.n_exit = (int32_t)P.sync.exit_idx[P.rank].size();
   }

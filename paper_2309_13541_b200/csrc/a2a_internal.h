@@ -94,7 +94,9 @@ struct DynTables {
   int32_t nC = 0;
   int64_t unit_bytes = 0;                       // target unit size (0 = auto)
   std::vector<int32_t> unit_base;               // [G+1] global unit id = base[g] + index
-  std::vector<std::vector<DevUnit>> units;      // [g] grab order
+  std::vector<std::vector<DevUnit>> units;      // [g] grab order: remote queue, then local queue
+  std::vector<int32_t> n_remote;                // [g] units in the remote (NVLink) queue
+  std::vector<int32_t> remote_ctas;             // [g] CTAs that start on the remote queue
   std::vector<std::vector<int32_t>> wait_idx;   // [g] global unit ids to acquire
   std::vector<std::vector<int32_t>> exit_idx;   // [g] global unit ids flagged into g
   double est_makespan = 0;                      // host model estimate (s)

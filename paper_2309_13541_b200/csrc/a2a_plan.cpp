@@ -14,6 +14,7 @@
 // elsewhere), resolve every op's source and destination address.
 #include <algorithm>
 #include <array>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <functional>
@@ -737,7 +738,7 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
     const GpuTables& tb = P.tables[g];
     for (int t = 0; t < TE; ++t) {
       int64_t target = unit_bytes > 0 ? unit_bytes
-                                      : std::min<int64_t>(4 << 20, std::max<int64_t>(64 << 10, tb.step_bytes[t] / (4LL * nC)));
+                                      : std::min<int64_t>(2 << 20, std::max<int64_t>(256 << 10, tb.step_bytes[t] / (2LL * nC)));
       target = std::max<int64_t>(64, std::min<int64_t>(target, 1LL << 30) & ~63LL);
       for (int64_t k = tb.step_begin[t]; k < tb.step_begin[t + 1]; ++k) {
         const DevItem& it = tb.items[k];
@@ -846,21 +847,42 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
       D.est_makespan = std::max(D.est_makespan, x.finish);
     }
   }
-  // global ids in grab order
+  // global ids in grab order: per GPU the remote (NVLink) queue, then the local
+  // (HBM) queue, each step-major; CTAs split between the queues so both pipes
+  // stay busy (a CTA moves to the other queue when its own drains)
   D.unit_base.assign(G + 1, 0);
+  D.n_remote.assign(G, 0);
+  D.remote_ctas.assign(G, 0);
   std::vector<int> gid(all.size(), -1);
+  std::vector<std::vector<int>> qorder(G);
   D.units.assign(G, {});
   for (int g = 0; g < G; ++g) {
+    double rb = 0, lb = 0;
+    for (int pass = 0; pass < 2; ++pass)
+      for (int t = 0; t < TE; ++t)
+        for (int id : per[g][t]) {
+          const bool remote = all[id].dst_gpu != g;
+          if (remote != (pass == 0)) continue;
+          qorder[g].push_back(id);
+          (remote ? rb : lb) += all[id].u.nbytes;
+          if (remote) D.n_remote[g]++;
+        }
     int k = 0;
-    for (int t = 0; t < TE; ++t)
-      for (int id : per[g][t]) gid[id] = D.unit_base[g] + k++;
+    for (int id : qorder[g]) gid[id] = D.unit_base[g] + k++;
     D.unit_base[g + 1] = D.unit_base[g] + k;
+    // CTAs on the remote queue: proportional to the pipe times, at least 1/4
+    // of the CTAs when there is NVLink work (remote stores need many in flight)
+    const double tr = rb / nv, tl = lb / hbm;
+    int nr = (tr + tl) > 0 ? (int)std::lround(nC * tr / (tr + tl)) : 0;
+    if (D.n_remote[g] > 0) nr = std::max(nr, std::max(1, nC / 4));
+    if (D.n_remote[g] < (int)qorder[g].size()) nr = std::min(nr, nC - std::max(1, nC / 8));
+    D.remote_ctas[g] = std::max(0, std::min(nr, nC));
   }
   D.wait_idx.assign(G, {});
   D.exit_idx.assign(G, {});
   for (int g = 0; g < G; ++g)
-    for (int t = 0; t < TE; ++t)
-      for (int id : per[g][t]) {
+    for (int id : qorder[g]) {
+      {
         TU& x = all[id];
         DevUnit u = x.u;
         u.wb = (int32_t)D.wait_idx[g].size();
@@ -871,6 +893,7 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
         for (int h = 0; h < G; ++h)
           if (u.mask & (1u << h)) D.exit_idx[h].push_back(gid[id]);
       }
+    }
   D.nC = nC;
   D.unit_bytes = unit_bytes;
   return A2A_OK;
@@ -889,12 +912,24 @@ static int emulate_dyn(Plan& P, int nC, uint8_t* const* send, uint8_t* const* re
   for (int g = 0; g < G; ++g) scratch[g].assign((size_t)P.info[g].scratch_bytes + 64, 0);
   const int total = D.unit_base[G];
   std::vector<std::vector<char>> flag(G, std::vector<char>((size_t)total, 0));
-  std::vector<int> next(G, 0);
+  // two queues per GPU: [0, n_remote) and [n_remote, n); CTA c starts on the
+  // remote queue iff c < remote_ctas[g] and switches when its queue drains
+  std::vector<std::array<int, 2>> next(G), qend(G);
+  for (int g = 0; g < G; ++g) {
+    next[g] = {0, D.n_remote[g]};
+    qend[g] = {D.n_remote[g], (int)D.units[g].size()};
+  }
   std::vector<std::vector<int>> held(G, std::vector<int>(nC, -1));
   auto base = [&](int g, int loc) -> uint8_t* {
     if (loc == loc_send()) return send[g];
     if (loc >= 1 && loc < 1 + G) return recv[loc - 1];
     return scratch[loc - 1 - G].data();
+  };
+  auto pick_queue = [&](int g, int c) -> int {  // queue a CTA grabs from, -1 if both drained
+    const int own = c < D.remote_ctas[g] ? 0 : 1;
+    if (next[g][own] < qend[g][own]) return own;
+    if (next[g][1 - own] < qend[g][1 - own]) return 1 - own;
+    return -1;
   };
   uint64_t x = seed * 0x9E3779B97F4A7C15ULL + 3;
   auto rnd = [&]() { x ^= x << 13; x ^= x >> 7; x ^= x << 17; return x; };
@@ -905,7 +940,7 @@ static int emulate_dyn(Plan& P, int nC, uint8_t* const* send, uint8_t* const* re
       for (int c = 0; c < nC; ++c) {
         int u = held[g][c];
         if (u < 0) {
-          if (next[g] < (int)D.units[g].size()) act.emplace_back(g, c);
+          if (pick_queue(g, c) >= 0) act.emplace_back(g, c);
           continue;
         }
         busy = true;
@@ -920,7 +955,8 @@ static int emulate_dyn(Plan& P, int nC, uint8_t* const* send, uint8_t* const* re
     }
     auto [g, c] = act[rnd() % act.size()];
     if (held[g][c] < 0) {
-      held[g][c] = next[g]++;
+      const int q = pick_queue(g, c);
+      held[g][c] = next[g][q]++;
     } else {
       const DevUnit& du = D.units[g][held[g][c]];
       std::memmove(base(g, du.dst_loc) + du.dst_off, base(g, du.src_loc) + du.src_off, (size_t)du.nbytes);
