@@ -313,6 +313,8 @@ class Plan:
     def execute(self, send, recv=None, stream=None, count_links: bool = False):
         """Launch one all-to-all (asynchronous on ``stream``, default: current)."""
         import torch
+        if self.rank is None:
+            raise ExecutorError("a2a_plan_execute: [STATE] plan not bound to a device")
         ck = self._bufcheck
         if ck is None:
             info = self.gpu_info(self.rank)

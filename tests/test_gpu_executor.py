@@ -213,3 +213,40 @@ def test_dynamic_n64(reuse, artifacts):
             p.execute(s, r)
             p.sync()
             assert torch.equal(r, s.transpose(0, 1).contiguous())
+
+
+def test_missing_peer_times_out_instead_of_hanging(artifacts):
+    """A 2-GPU plan whose peer never launches: the entry barrier spin is bounded
+    by the device timeout and reports A2A_ERR_TIMEOUT (no hang); the plan then
+    refuses further executes."""
+    from paper_2309_13541_b200.executor import ExecutorError, Plan
+    a = artifacts("gk8_2")
+    m = 4096
+    p0 = Plan(a.g, a.sched, m=m, n_gpus=2).bind(0, device=0)
+    p1 = Plan(a.g, a.sched, m=m, n_gpus=2).bind(1, device=0)   # never executes
+    ptrs = [p0.arena_ptr(), p1.arena_ptr()]
+    p0.import_pointers(ptrs)
+    p0.set_timeout(0.3)
+    info = p0.gpu_info(0)
+    s = torch.zeros(info["send_bytes"], dtype=torch.uint8, device="cuda")
+    p0.execute(s, p0.recv_buffer().reshape(-1))
+    with pytest.raises(ExecutorError, match="TIMEOUT"):
+        p0.sync()
+    with pytest.raises(ExecutorError):
+        p0.execute(s, p0.recv_buffer().reshape(-1))
+    p0.close()
+    p1.close()
+
+
+def test_call_order_errors(artifacts):
+    from paper_2309_13541_b200.executor import ExecutorError, Plan
+    a = artifacts("torus2x4")
+    with Plan(a.g, a.sched, m=64) as p:
+        s = torch.zeros((8, 8, 64), dtype=torch.uint8, device="cuda")
+        with pytest.raises((ExecutorError, TypeError)):
+            p.execute(s)                      # not bound
+        p.bind(0)
+        with pytest.raises(ExecutorError):
+            p.set_engine("lsu")               # after bind
+        with pytest.raises(ExecutorError):
+            p.bind(0)                         # twice
