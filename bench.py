@@ -44,31 +44,65 @@ def _peaks():
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """SM clock + throttle-reason sampler running during the timed region.
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    Uses NVML directly (~ms per sample, so even a ~15 ms timed region gets
+    samples); falls back to polling nvidia-smi."""
+
+    NAMES = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+             "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+             "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+             "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
+        self.sm, self.mx, self.reasons = [], [], set()
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            pr = torch.cuda.get_device_properties(index)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            self._h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            self._nvml = pynvml
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        n = self._nvml
+        self.sm.append(n.nvmlDeviceGetClockInfo(self._h, n.NVML_CLOCK_SM))
+        self.mx.append(n.nvmlDeviceGetMaxClockInfo(self._h, n.NVML_CLOCK_SM))
+        r = n.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        for name, attr in self.NAMES.items():
+            if r & getattr(n, attr):
+                self.reasons.add(name)
+
+    def _sample_smi(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        r = [x.strip() for x in out.split(",")]
+        if len(r) >= 6 and r[0].replace(".", "").isdigit():
+            self.sm.append(float(r[0]))
+            self.mx.append(float(r[1]))
+            for i, name in enumerate(self.NAMES):
+                if r[2 + i].lower() == "active":
+                    self.reasons.add(name)
 
     def start(self):
         def run():
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(
-                        ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                         "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                        timeout=5).stdout.strip()
-                    if out:
-                        self.rows.append([x.strip() for x in out.split(",")])
+                    self._sample_nvml() if self._nvml else self._sample_smi()
                 except Exception:
                     pass
-                self._stop.wait(0.1)
+                self._stop.wait(0.002 if self._nvml else 0.1)
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
 
@@ -76,15 +110,11 @@ class Clocks:
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
-        sm = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) >= 8 and r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows if len(r) >= 8
-                          for i in range(4) if r[4 + i].lower() == "active"})
-        sm.sort()
+        sm = sorted(self.sm)
         return {"sm_mhz": sm[len(sm) // 2] if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "sm_max_mhz": max(self.mx) if self.mx else None,
+                "reasons": sorted(self.reasons), "samples": len(sm),
+                "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 def _dist():
@@ -233,8 +263,6 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     stream = torch.cuda.current_stream(dev)
 
     clk = Clocks(ctx.local) if clocks else None
-    if clk:
-        clk.start()
     # ---- warm-up + correctness of the exact buffers we time
     for _ in range(warmup):
         plan.execute(send, recv, stream=stream)
@@ -252,6 +280,8 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     e1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     ctx.barrier()
     torch.cuda.synchronize(dev)
+    if clk:
+        clk.start()
     for k in range(steps):
         flush.zero_()
         e0[k].record(stream)
