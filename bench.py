@@ -226,8 +226,52 @@ class Ctx:
             self.pg.destroy_process_group()
 
 
+def autotune_schedule(ctx, art, m, placement="optimized", num_ctas=0, trials=5,
+                      candidates=("static", "dynamic:1048576")):
+    """Time a few executes of each execution schedule (same placement, same
+    buffers) and return (best, {candidate: ms}); identical on every rank."""
+    import torch
+
+    from paper_2309_13541_b200.dist import connect, local_nodes
+    from paper_2309_13541_b200.executor import Plan
+    G, dev = ctx.world, ctx.dev
+    times = {}
+    for cand in candidates:
+        mode, *ub = cand.split(":")
+        plan = Plan(art.g, art.sched, m=m, n_gpus=G, placement=placement)
+        plan.set_schedule(mode, *(int(x) for x in ub))
+        plan.bind(ctx.rank, device=ctx.local, num_ctas=num_ctas)
+        if G > 1:
+            connect(plan)
+        V = plan.gpu_info(ctx.rank)["n_local_nodes"]
+        send = torch.zeros((V, art.g.n, m), dtype=torch.uint8, device=dev)
+        recv = plan.recv_buffer() if G > 1 else torch.empty_like(send)
+        stream = torch.cuda.current_stream(dev)
+        for _ in range(3):
+            plan.execute(send, recv, stream=stream)
+        plan.sync()
+        ctx.barrier()
+        ev = []
+        for _ in range(trials):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            plan.execute(send, recv, stream=stream)
+            b.record(stream)
+            ev.append((a, b))
+        plan.sync()
+        torch.cuda.synchronize(dev)
+        t = ctx.allmax([x.elapsed_time(y) for x, y in ev])
+        times[cand] = round(sorted(t)[len(t) // 2], 4)
+        plan.close()
+        del send, recv
+        torch.cuda.empty_cache()
+        ctx.barrier()
+    best = min(times, key=lambda k: (times[k], k))
+    return best, times
+
+
 def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=True,
-            flush_bytes=512 << 20, placement="optimized"):
+            flush_bytes=512 << 20, placement="optimized", schedule="static"):
     """Time K all-to-alls of `art` at shard size m on ctx.world GPUs.
 
     Returns a dict (identical on every rank) with T, algBW, bound, roofline,
@@ -241,6 +285,9 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     G, rank, dev = ctx.world, ctx.rank, ctx.dev
     n = art.g.n
     plan = Plan(art.g, art.sched, m=m, n_gpus=G, placement=placement)
+    if schedule:
+        mode, *ub = schedule.split(":")
+        plan.set_schedule(mode, *(int(x) for x in ub))
     if e2e and G > 1:
         plan.set_recv_buffers(2)          # double-buffered recv for the pipelined e2e
     plan.bind(rank, device=ctx.local, num_ctas=num_ctas)
@@ -434,7 +481,8 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
                     else plan.sync_stats(rank)),
            "kernel_timeline": tls,
            "num_ctas": plan_ctas(plan, num_ctas), "egress_max": max(i["egress_bytes"] for i in infos),
-           "scratch_bytes": info["scratch_bytes"], "placement": plan.placement.tolist()}
+           "scratch_bytes": info["scratch_bytes"], "placement": plan.placement.tolist(),
+           "schedule": schedule}
     plan.close()
     del send, recv, flush
     torch.cuda.empty_cache()
@@ -455,6 +503,8 @@ def main(argv=None):
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--placement", default="optimized", choices=["optimized", "contiguous"])
+    ap.add_argument("--schedule", default="auto",
+                    help="static | dynamic[:unit_bytes] | auto (time both, keep the faster)")
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
 
@@ -467,8 +517,14 @@ def main(argv=None):
     ctx = Ctx()
     if ctx.world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ctx.world}")
+    tune = None
+    schedule = args.schedule
+    if schedule == "auto":
+        schedule, tune = autotune_schedule(ctx, art, m, placement=args.placement,
+                                           num_ctas=args.num_ctas)
     r = measure(ctx, art, m, args.steps, args.warmup, num_ctas=args.num_ctas,
-                nccl=not args.no_nccl, e2e=not args.no_e2e, placement=args.placement)
+                nccl=not args.no_nccl, e2e=not args.no_e2e, placement=args.placement,
+                schedule=schedule)
     G, n = ctx.world, art.g.n
 
     # ---- CPU baseline: rank 0, N=1 only, bounded sample
@@ -499,7 +555,8 @@ def main(argv=None):
                        "m_bytes": m, "nodes": n, "hop_ops": len(art.sched.instructions),
                        "nsteps": art.sched.nsteps, "Q": art.sched.Q,
                        "l2": "flushed between timed steps (512 MiB memset, outside events)",
-                       "num_ctas": r["num_ctas"]},
+                       "num_ctas": r["num_ctas"], "schedule": schedule,
+                       "schedule_autotune_ms": tune},
             "per_gpu": round(r["per_gpu"], 3),
             "bound": {"t_lb_ms": round(r["t_lb"] * 1e3, 4), "frac": round(r["bound_frac"], 4),
                       "def": "G=1: 2*m*sum(dist)/HBM; G>1: max_g max(egress,ingress)/900 GB/s"},

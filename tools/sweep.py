@@ -42,6 +42,8 @@ def main(argv=None):
     ap.add_argument("--mem-limit-gib", type=float, default=150.0)
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--placement", default="optimized", choices=["optimized", "contiguous"])
+    ap.add_argument("--schedule", default=None,
+                    help="static | dynamic[:bytes] | auto; default: $A2A_SCHED or static")
     a = ap.parse_args(argv)
     cases = list(PRESETS.get(a.preset, [])) if a.preset else []
     for c in filter(None, a.cases.split(",")):
@@ -67,8 +69,14 @@ def main(argv=None):
                 rec["skipped"] = f"needs {mem / 2**30:.1f} GiB per GPU"
             else:
                 t0 = time.time()
+                sched = a.schedule or os.environ.get("A2A_SCHED") or "static"
+                tune = None
+                if sched == "auto":
+                    sched, tune = bench.autotune_schedule(ctx, art, m, placement=a.placement)
                 r = bench.measure(ctx, art, m, a.steps, a.warmup, nccl=not a.no_nccl,
-                                  e2e=False, clocks=True, placement=a.placement)
+                                  e2e=False, clocks=True, placement=a.placement, schedule=sched)
+                rec["schedule"] = sched
+                rec["schedule_autotune_ms"] = tune
                 rec.update({
                     "nodes": art.g.n, "hop_ops": len(art.sched.instructions),
                     "nsteps": art.sched.nsteps, "Q": art.sched.Q,
