@@ -95,7 +95,15 @@ class Clocks:
                 if r[2 + i].lower() == "active":
                     self.reasons.add(name)
 
+    def sample(self):
+        try:
+            self._sample_nvml() if self._nvml else self._sample_smi()
+        except Exception:
+            pass
+
     def start(self):
+        self.sample()
+
         def run():
             while not self._stop.is_set():
                 try:
@@ -107,6 +115,7 @@ class Clocks:
         self._t.start()
 
     def stop(self):
+        self.sample()
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
@@ -334,12 +343,14 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
         e0[k].record(stream)
         plan.execute(send, recv, stream=stream)
         e1[k].record(stream)
+        if clk and k % 8 == 7:
+            clk.sample()          # the GPU runs ahead of this host loop: sample while it works
     plan.sync()
     torch.cuda.synchronize(dev)
     clock_rec = clk.stop() if clk else None
     ctx.barrier()
     from paper_2309_13541_b200.executor import timeline_summary
-    tls = timeline_summary(plan.read_timeline())            # last timed launch, this rank
+    tls = timeline_summary(plan.read_timeline(), schedule)    # last timed launch, this rank
     if ctx.pg:
         alltl = [None] * G
         ctx.pg.all_gather_object(alltl, tls)
@@ -492,7 +503,7 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="gk8_2")

@@ -28,13 +28,19 @@ __all__ = ["EvalError", "ExecutorError", "Plan", "replay_timestep_schedule",
            "execute_timestep_schedule", "contiguous_placement", "timeline_summary"]
 
 
-def timeline_summary(tl: np.ndarray) -> dict:
+def timeline_summary(tl: np.ndarray, schedule: str | None = "static") -> dict:
     """Kernel-internal timing from Plan.read_timeline() (columns: start, entry,
     step published [T'], exit, step dependencies acquired [T']): microseconds
-    from the earliest CTA start."""
+    from the earliest CTA start.  Dynamic schedules store per-CTA unit counts
+    and flag-wait nanoseconds in columns 2 and 3 instead of step stamps."""
     T = (tl.shape[1] - 3) // 2
     t0 = int(tl[:, 0].min())
     us = lambda x: round((int(x) - t0) / 1e3, 3)  # noqa: E731
+    if schedule and schedule.startswith("dynamic"):
+        units = tl[:, 2].astype(np.int64)
+        return {"kernel_us": us(tl[:, 2 + T].max()), "start_spread_us": us(tl[:, 0].max()),
+                "entry_us": us(tl[:, 1].max()), "units_per_cta": [int(units.min()), int(units.max())],
+                "max_cta_wait_us": round(int(tl[:, 3].max()) / 1e3, 3)}
 
     def last(j):
         col = tl[:, j][tl[:, j] > 0]
