@@ -236,7 +236,7 @@ class Ctx:
 
 
 def autotune_schedule(ctx, art, m, placement="optimized", num_ctas=0, trials=5,
-                      candidates=("static", "dynamic:1048576")):
+                      candidates=("static", "dynamic:1048576", "list:1048576")):
     """Time a few executes of each execution schedule (same placement, same
     buffers) and return (best, {candidate: ms}); identical on every rank."""
     import torch
@@ -488,7 +488,7 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     res = {"T": T, "per_step_ms": per, "value": value, "per_gpu": value / G,
            "t_lb": t_lb, "bound_frac": t_lb / T, "roofline": roof, "nccl": nres, "e2e": eres,
            "recv_ok": bool(ok), "clocks": clock_rec,
-           "sync": (plan.dyn_stats(rank, plan_ctas(plan, num_ctas)) if plan.schedule == "dynamic"
+           "sync": (plan.dyn_stats(rank, plan_ctas(plan, num_ctas)) if plan.schedule in ("dynamic", "list")
                     else plan.sync_stats(rank)),
            "kernel_timeline": tls,
            "num_ctas": plan_ctas(plan, num_ctas), "egress_max": max(i["egress_bytes"] for i in infos),

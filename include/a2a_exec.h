@@ -139,7 +139,9 @@ int a2a_optimize_placement(int32_t n, int32_t n_edges, const int32_t* edge_uv,
 /* Execution schedule, before bind: 0 = static per-CTA step programs (default),
  * 1 = dynamic units: items cut into units of `unit_bytes` (0 = auto), CTAs grab
  * units in step-major, readiness-ordered lists from a per-GPU atomic counter and
- * acquire per-unit producer flags.  a2a_plan_emulate follows the
+ * acquire per-unit producer flags; 2 = dynamic units ordered by
+ * an event-driven list schedule (start times) instead of step-major, so routes
+ * pipeline hop by hop at unit granularity.  a2a_plan_emulate follows the
  * selected mode.  Stats: units and dependency entries of `gpu`, model makespan. */
 int a2a_plan_set_schedule(a2a_plan* plan, int32_t mode, int64_t unit_bytes);
 int a2a_plan_dyn_stats(a2a_plan* plan, int32_t gpu, int32_t num_ctas, int64_t* n_units,

@@ -681,7 +681,7 @@ struct EngineCfg {
 };
 static EngineCfg engine_cfg(const Plan& P) {
   const int TE = P.T_exec;
-  if (P.sched_mode == 1) {
+  if (P.sched_mode >= 1) {
     if (P.engine == 1) {
       int S = P.tma_stages;
       while (S > 1 && ((20 * (size_t)S + 127) & ~(size_t)127) + (size_t)S * P.tma_chunk > 220 * 1024) --S;
@@ -776,13 +776,13 @@ static int bind_plan(Plan& P, int gpu, int dev, int nC) {
   const int G = P.G, TE = P.T_exec;
 
   // ---- CTA split + producer dependency lists (host, identical on all ranks)
-  int rc = P.sched_mode == 1 ? build_dyn(P, nC, P.dyn_unit_bytes) : build_sync(P, nC);
+  int rc = P.sched_mode >= 1 ? build_dyn(P, nC, P.dyn_unit_bytes) : build_sync(P, nC);
   if (rc != A2A_OK) return rc;
   const SyncTables& S = P.sync;
   const DynTables& Dy = P.dyn;
 
   // ---- arena layout, identical on every rank: flags | recv | scratch
-  P.flags_bytes = flag_region_bytes(P.sched_mode == 1 ? (int64_t)Dy.unit_base[G]
+  P.flags_bytes = flag_region_bytes(P.sched_mode >= 1 ? (int64_t)Dy.unit_base[G]
                                                       : (int64_t)TE * G * nC);
   P.recv_off.assign(G, 0);
   P.scratch_off.assign(G, 0);
@@ -801,7 +801,7 @@ static int bind_plan(Plan& P, int gpu, int dev, int nC) {
     return fail(A2A_ERR_NOMEM, buf);
   }
   CK(cudaMemset(P.arena, 0, (size_t)P.flags_bytes));
-  if (P.sched_mode == 1) {
+  if (P.sched_mode >= 1) {
     if ((rc = upload(&P.d_items, Dy.units[gpu])) != A2A_OK) return rc;
     if ((rc = upload(&P.d_wait_idx, Dy.wait_idx[gpu])) != A2A_OK) return rc;
     if ((rc = upload(&P.d_exit_idx, Dy.exit_idx[gpu])) != A2A_OK) return rc;
@@ -1000,7 +1000,7 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
   kp.pieces = (const DevPiece*)P.d_items;
   kp.prog = (const CtaStep*)P.d_step_begin;
   kp.exit_idx = (const int32_t*)P.d_exit_idx;
-  if (P.sched_mode == 1) {
+  if (P.sched_mode >= 1) {
     const DynTables& Dy = P.dyn;
     kp.n_exit = (int32_t)Dy.exit_idx[P.rank].size();
     kp.units = (const DevUnit*)P.d_items;
@@ -1040,7 +1040,7 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
   cudaError_t e = cudaLaunchCooperativeKernel(ec.fn, dim3(P.nC), dim3(ec.threads), args, ec.smem,
                                               (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchCooperativeKernel");
-  if (P.sched_mode == 1) ++P.dyn_execs;
+  if (P.sched_mode >= 1) ++P.dyn_execs;
   P.last_stream = stream;
   P.launched = true;
   return A2A_OK;

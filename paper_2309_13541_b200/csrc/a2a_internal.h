@@ -126,7 +126,7 @@ struct Plan {
 
   SyncTables sync;
   DynTables dyn;
-  int32_t sched_mode = 0;                       // 0 static per-CTA programs, 1 dynamic units
+  int32_t sched_mode = 0;                       // 0 static programs, 1 dynamic step-major, 2 dynamic list-scheduled
   int64_t dyn_unit_bytes = 0;                   // dynamic unit size (0 = auto)
   int64_t dyn_execs = 0;                        // dynamic executes so far (grab counter base)
 

@@ -20,6 +20,7 @@
 #include <functional>
 #include <map>
 #include <new>
+#include <queue>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -816,35 +817,80 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
   // readiness model: remote bytes at ~700 GB/s per GPU direction, local copies at ~3.2 TB/s
   const double nv = 700e9, hbm = 3.2e12;
   std::vector<double> eg_free(G, 0), in_free(G, 0), hbm_free(G, 0);
-  for (int t = 0; t < TE; ++t) {
-    std::vector<int> step_units;
-    for (int g = 0; g < G; ++g) {
-      for (int id : per[g][t]) {
-        TU& x = all[id];
-        x.ready = 0;
-        for (int d : x.deps) x.ready = std::max(x.ready, all[d].finish);
-      }
-      std::stable_sort(per[g][t].begin(), per[g][t].end(), [&](int a, int b) {
-        if (all[a].ready != all[b].ready) return all[a].ready < all[b].ready;
-        const bool ra = all[a].dst_gpu != all[a].g, rb = all[b].dst_gpu != all[b].g;
-        return ra > rb;  // remote first: NVLink is the scarce pipe
-      });
-      step_units.insert(step_units.end(), per[g][t].begin(), per[g][t].end());
+  std::vector<double> key(all.size(), 0);   // queue order key (step-major or start time)
+  auto place = [&](TU& x) {
+    if (x.dst_gpu != x.g) {
+      // egress pipe only: NVSwitch shares a GPU's ingress among its senders
+      // fluidly, so an exclusive ingress pipe would invent idle gaps
+      double st = std::max(x.ready, eg_free[x.g]);
+      x.finish = st + x.u.nbytes / nv;
+      eg_free[x.g] = x.finish;
+      (void)in_free;
+      return st;
     }
-    std::stable_sort(step_units.begin(), step_units.end(),
-                     [&](int a, int b) { return all[a].ready < all[b].ready; });
-    for (int id : step_units) {
+    double st = std::max(x.ready, hbm_free[x.g]);
+    x.finish = st + x.u.nbytes / hbm;
+    hbm_free[x.g] = x.finish;
+    return st;
+  };
+  if (P.sched_mode == 2) {
+    // event-driven list schedule over the unit DAG: pop the unit that becomes
+    // ready first, place it on its pipe; the queue order is the start time,
+    // which is a topological order (start >= ready >= producers' finish).
+    // Routes then pipeline hop by hop at unit granularity (cut-through).
+    std::vector<std::vector<int>> succ(all.size());
+    std::vector<int> indeg(all.size(), 0);
+    for (int i = 0; i < (int)all.size(); ++i)
+      for (int d : all[i].deps) { succ[d].push_back(i); ++indeg[i]; }
+    typedef std::pair<double, int> KI;
+    std::priority_queue<KI, std::vector<KI>, std::greater<KI>> pq;
+    for (int i = 0; i < (int)all.size(); ++i) {
+      all[i].ready = 0;
+      if (indeg[i] == 0) pq.emplace(0.0, i);
+    }
+    while (!pq.empty()) {
+      const int id = pq.top().second;
+      pq.pop();
       TU& x = all[id];
-      if (x.dst_gpu != x.g) {
-        double st = std::max(x.ready, std::max(eg_free[x.g], in_free[x.dst_gpu]));
-        x.finish = st + x.u.nbytes / nv;
-        eg_free[x.g] = in_free[x.dst_gpu] = x.finish;
-      } else {
-        double st = std::max(x.ready, hbm_free[x.g]);
-        x.finish = st + x.u.nbytes / hbm;
-        hbm_free[x.g] = x.finish;
-      }
+      key[id] = place(x);
       D.est_makespan = std::max(D.est_makespan, x.finish);
+      for (int sx : succ[id]) {
+        all[sx].ready = std::max(all[sx].ready, x.finish);
+        if (--indeg[sx] == 0) pq.emplace(all[sx].ready, sx);
+      }
+    }
+    for (int g = 0; g < G; ++g)
+      for (int t = 0; t < TE; ++t)
+        std::stable_sort(per[g][t].begin(), per[g][t].end(),
+                         [&](int a, int b) { return key[a] < key[b]; });
+  } else {
+    for (int t = 0; t < TE; ++t) {
+      std::vector<int> step_units;
+      for (int g = 0; g < G; ++g) {
+        for (int id : per[g][t]) {
+          TU& x = all[id];
+          x.ready = 0;
+          for (int d : x.deps) x.ready = std::max(x.ready, all[d].finish);
+        }
+        std::stable_sort(per[g][t].begin(), per[g][t].end(), [&](int a, int b) {
+          if (all[a].ready != all[b].ready) return all[a].ready < all[b].ready;
+          const bool ra = all[a].dst_gpu != all[a].g, rb = all[b].dst_gpu != all[b].g;
+          return ra > rb;  // remote first: NVLink is the scarce pipe
+        });
+        step_units.insert(step_units.end(), per[g][t].begin(), per[g][t].end());
+      }
+      std::stable_sort(step_units.begin(), step_units.end(),
+                       [&](int a, int b) { return all[a].ready < all[b].ready; });
+      for (int id : step_units) {
+        place(all[id]);
+        D.est_makespan = std::max(D.est_makespan, all[id].finish);
+      }
+    }
+    // step-major key
+    for (int g = 0; g < G; ++g) {
+      double k = 0;
+      for (int t = 0; t < TE; ++t)
+        for (int id : per[g][t]) key[id] = k++;
     }
   }
   // global ids in grab order: per GPU the remote (NVLink) queue, then the local
@@ -858,15 +904,19 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
   D.units.assign(G, {});
   for (int g = 0; g < G; ++g) {
     double rb = 0, lb = 0;
-    for (int pass = 0; pass < 2; ++pass)
+    for (int pass = 0; pass < 2; ++pass) {
+      std::vector<int> q;
       for (int t = 0; t < TE; ++t)
         for (int id : per[g][t]) {
           const bool remote = all[id].dst_gpu != g;
           if (remote != (pass == 0)) continue;
-          qorder[g].push_back(id);
+          q.push_back(id);
           (remote ? rb : lb) += all[id].u.nbytes;
           if (remote) D.n_remote[g]++;
         }
+      std::stable_sort(q.begin(), q.end(), [&](int a, int b) { return key[a] < key[b]; });
+      qorder[g].insert(qorder[g].end(), q.begin(), q.end());
+    }
     int k = 0;
     for (int id : qorder[g]) gid[id] = D.unit_base[g] + k++;
     D.unit_base[g + 1] = D.unit_base[g] + k;
@@ -1050,7 +1100,7 @@ int a2a_plan_prepare(a2a_plan* plan, int32_t num_ctas) {
 }
 
 int a2a_plan_set_schedule(a2a_plan* plan, int32_t mode, int64_t unit_bytes) {
-  if (!plan || (mode != 0 && mode != 1) || unit_bytes < 0) return fail(A2A_ERR_INVALID, "bad schedule mode");
+  if (!plan || mode < 0 || mode > 2 || unit_bytes < 0) return fail(A2A_ERR_INVALID, "bad schedule mode");
   if (plan->p.bound) return fail(A2A_ERR_STATE, "set the schedule mode before a2a_plan_bind");
   plan->p.sched_mode = mode;
   plan->p.dyn_unit_bytes = unit_bytes;
@@ -1084,7 +1134,7 @@ int a2a_plan_emulate(a2a_plan* plan, int32_t num_ctas, void* const* send, void* 
                      uint64_t seed) {
   if (!plan || !send || !recv) return fail(A2A_ERR_INVALID, "null argument");
   try {
-    if (plan->p.sched_mode == 1)
+    if (plan->p.sched_mode >= 1)
       return emulate_dyn(plan->p, num_ctas, (uint8_t* const*)send, (uint8_t* const*)recv, seed,
                          plan->p.dyn_unit_bytes);
     return emulate(plan->p, num_ctas, (uint8_t* const*)send, (uint8_t* const*)recv, seed);

@@ -152,7 +152,8 @@ def test_scratch_reuse_saves_memory(artifacts):
                                     ("ts_torus3x3", 1), ("torus2x4_h2", 4)])
 @pytest.mark.parametrize("unit", [0, 256, 1000 * 64])
 @pytest.mark.parametrize("reuse", [False, True])
-def test_dynamic_schedule_interleavings(name, G, unit, reuse, artifacts):
+@pytest.mark.parametrize("mode", ["dynamic", "list"])
+def test_dynamic_schedule_interleavings(name, G, unit, reuse, mode, artifacts):
     """Dynamic unit queues (f2): in-order grabbing + per-unit producer flags
     deliver the transpose under random interleavings, with and without
     scratch reuse, and never deadlock."""
@@ -160,7 +161,7 @@ def test_dynamic_schedule_interleavings(name, G, unit, reuse, artifacts):
     m = 5000 if a.g.n <= 9 else 640
     send = make_send(a.g.n, m, seed=6)
     with Plan(a.g, a.sched, m=m, n_gpus=G, reuse_scratch=reuse) as p:
-        p.set_schedule("dynamic", unit)
+        p.set_schedule(mode, unit)
         nodes = [local_nodes(p, g) for g in range(G)]
         for seed in range(2):
             recvs = p.emulate([send[ns] for ns in nodes], num_ctas=11, seed=seed)

@@ -177,14 +177,15 @@ def test_tma_engine_n64(artifacts):
 @pytest.mark.parametrize("engine", ["tma", "lsu"])
 @pytest.mark.parametrize("m,unit", [(7, 0), (4096 + 5, 0), (65536, 4096), ((1 << 20) + 48, 0)])
 @pytest.mark.parametrize("reuse", [False, True])
-def test_dynamic_schedule_bit_exact(name, engine, m, unit, reuse, artifacts):
+@pytest.mark.parametrize("mode", ["dynamic", "list"])
+def test_dynamic_schedule_bit_exact(name, engine, m, unit, reuse, mode, artifacts):
     """Dynamic unit queues (f2) on the device: exact over repeated executes
     (the grab counter carries across epochs), with and without scratch reuse."""
     from paper_2309_13541_b200.executor import Plan
     from replay_bytes import replay_bytes
     a = artifacts(name)
     with Plan(a.g, a.sched, m=m, reuse_scratch=reuse) as p:
-        p.set_schedule("dynamic", unit)
+        p.set_schedule(mode, unit)
         p.set_engine(engine)
         p.bind(0)
         for rep in range(3):

@@ -182,7 +182,8 @@ def _alt_main(rank, world, port, q):
 @pytest.mark.parametrize("engine", ["tma", "lsu"])
 @pytest.mark.parametrize("reuse", [False, True])
 @pytest.mark.parametrize("name,m", [("gk8_2", 65536 + 64), ("torus4x4x4", 8192), ("torus2x4_h2", 4099)])
-def test_multiprocess_dynamic(world, engine, reuse, name, m):
+@pytest.mark.parametrize("mode", ["dynamic", "list"])
+def test_multiprocess_dynamic(world, engine, reuse, name, m, mode):
     """Dynamic unit queues across GPUs (+ scratch reuse, optimized placement)."""
     if _ngpu() < world:
         pytest.skip(f"needs {world} GPUs")
@@ -191,7 +192,7 @@ def test_multiprocess_dynamic(world, engine, reuse, name, m):
     q = ctx.Queue()
     port = _port()
     ps = [ctx.Process(target=_rank_main,
-                      args=(r, world, port, name, m, 3, q, engine, "dynamic", reuse))
+                      args=(r, world, port, name, m, 3, q, engine, mode, reuse))
           for r in range(world)]
     for p in ps:
         p.start()
