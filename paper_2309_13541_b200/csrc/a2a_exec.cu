@@ -472,9 +472,9 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
 template <int kEngine, int kThreads>
 __global__ void __launch_bounds__(kThreads, 1) a2a_dyn_kernel(const KParams p) {
   __shared__ int s_abort;
-  __shared__ long long s_idx;
-  __shared__ DevUnit s_u;
-  __shared__ DevPiece s_pc[1];
+  __shared__ long long s_idx[2];
+  __shared__ DevUnit s_u[2];
+  __shared__ DevPiece s_pc[2];
   extern __shared__ __align__(128) unsigned char dsmem[];
   const int c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5;
   const int S = p.tma_stages;
@@ -520,45 +520,60 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_dyn_kernel(const KParams p) {
   }
   if (tid == 0) tl[1] = globaltimer();
   unsigned long long waited_ns = 0, done = 0;
-  int q = c < p.remote_ctas ? 0 : 1, visited = 0;  // queue of thread 0
+  int q = c < p.remote_ctas ? 0 : 1, visited = 0;  // queue state, owned by the fetching thread
+  // fetch (grab + descriptor) of the next unit into slot `sl`; thread `fetcher`
+  auto fetch = [&](int sl) {
+    long long idx = -1;
+    for (;;) {  // own queue first, then the other; one failing grab per queue
+      const long long qn = q == 0 ? p.n_remote : (long long)p.n_units - p.n_remote;
+      const long long j = (long long)(atomicAdd(p.grab + q, 1ull) - p.grab_base[q]);
+      if (j < qn) { idx = (q == 0 ? 0 : p.n_remote) + j; break; }
+      if (++visited == 2) break;
+      q ^= 1;
+    }
+    s_idx[sl] = idx;
+    if (idx >= 0) {
+      const DevUnit u = p.units[idx];
+      s_u[sl] = u;
+      s_pc[sl] = DevPiece{u.src_off, u.dst_off, u.nbytes, u.edge, u.src_loc, u.dst_loc, 0};
+    }
+  };
+  // acquire the producers of the unit in slot `sl` (one warp)
+  auto acquire = [&](int sl) -> bool {
+    const DevUnit& u = s_u[sl];
+    if (s_idx[sl] < 0 || u.we <= u.wb) return true;
+    const uint64_t w0 = globaltimer();
+    bool ok = warp_wait_flags(my_flags, p.unit_wait, u.wb, u.we, p.epoch, p.timeout_ns, p.err,
+                              sys, p.sync_mode);
+    if ((tid & 31) == 0) waited_ns += globaltimer() - w0;
+    return ok;
+  };
+  // TMA engine: warp 1 prefetches unit k+1 (grab, descriptor, dependency wait)
+  // while thread 0 streams unit k and threads 64.. copy its heads/tails.
+  const int fw = kEngine == 1 ? 1 : 0;  // fetching warp
+  if (warp == fw) {
+    if ((tid & 31) == 0) fetch(0);
+    __syncwarp();
+    if (!acquire(0) && (tid & 31) == 0) s_abort = 1;
+  }
+  __syncthreads();
+  if (s_abort) return;
+  int cur = 0;
   for (;;) {
-    if (tid == 0) {
-      long long idx = -1;
-      for (;;) {  // own queue first, then the other; one failing grab per queue
-        const long long qn = q == 0 ? p.n_remote : (long long)p.n_units - p.n_remote;
-        const long long j = (long long)(atomicAdd(p.grab + q, 1ull) - p.grab_base[q]);
-        if (j < qn) { idx = (q == 0 ? 0 : p.n_remote) + j; break; }
-        if (++visited == 2) break;
-        q ^= 1;
-      }
-      s_idx = idx;
-      if (idx >= 0) {
-        const DevUnit u = p.units[idx];
-        s_u = u;
-        s_pc[0] = DevPiece{u.src_off, u.dst_off, u.nbytes, u.edge, u.src_loc, u.dst_loc, 0};
-      }
-    }
-    __syncthreads();
-    const long long idx = s_idx;
+    const long long idx = s_idx[cur];
     if (idx < 0) break;
-    const DevUnit u = s_u;
-    if (u.we > u.wb) {
-      if (warp == 0) {
-        const uint64_t w0 = globaltimer();
-        bool ok = warp_wait_flags(my_flags, p.unit_wait, u.wb, u.we, p.epoch, p.timeout_ns, p.err,
-                                  sys, p.sync_mode);
-        if (!ok && tid == 0) s_abort = 1;
-        if (tid == 0) waited_ns += globaltimer() - w0;
-      }
-      __syncthreads();
-      if (s_abort) return;
-    }
+    const DevUnit u = s_u[cur];
     const char* s0 = p.base[u.src_loc] + u.src_off;
     char* d0 = p.base[u.dst_loc] + u.dst_off;
+    // the next unit is only grabbed here; its dependency wait comes after this
+    // unit's flag is published, so a CTA never withholds a finished unit
     if (kEngine == 0) {
       cta_copy<4>(d0, s0, u.nbytes);
-    } else if (tid != 0) {
-      const int nt = kThreads - 1, me = tid - 1;
+      if (tid == 0) fetch(cur ^ 1);
+    } else if (warp == fw) {
+      if ((tid & 31) == 0) fetch(cur ^ 1);
+    } else if (tid >= 64) {
+      const int nt = kThreads - 64, me = tid - 64;
       const int64_t len = u.nbytes;
       if ((((uintptr_t)s0 ^ (uintptr_t)d0) & 15) != 0) {
         for (int64_t j = me; j < len; j += nt) d0[j] = s0[j];
@@ -569,10 +584,10 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_dyn_kernel(const KParams p) {
         if (me < head) d0[me] = s0[me];
         if (me < tail) d0[head + body + me] = s0[head + body + me];
       }
-    } else {
+    } else if (tid == 0) {
       fence_proxy_async();
       const uint32_t CH = (uint32_t)p.tma_chunk;
-      BodyCursor cur{s_pc, 0, 1, 0};
+      BodyCursor bc{&s_pc[cur], 0, 1, 0};
       const uint32_t g0 = gi;
       uint32_t nl = 0, ns = 0;
       bool more = true;
@@ -580,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_dyn_kernel(const KParams p) {
         const char* src;
         char* dst;
         uint32_t len;
-        if (!cur.next(p, CH, &src, &dst, &len)) return false;
+        if (!bc.next(p, CH, &src, &dst, &len)) return false;
         const uint32_t st = (g0 + nl) % S;
         ring_dst[st] = dst;
         ring_n[st] = len;
@@ -622,6 +637,10 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_dyn_kernel(const KParams p) {
       }
       ++done;
     }
+    if (warp == fw && !acquire(cur ^ 1) && (tid & 31) == 0) s_abort = 1;
+    __syncthreads();
+    if (s_abort) return;
+    cur ^= 1;
   }
   if (c == 0 && p.G > 1) {  // exit: every unit flagged into this GPU has landed
     bool ok = true;
@@ -642,9 +661,9 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_dyn_kernel(const KParams p) {
   }
   if (tid == 0) {
     tl[2] = done;
-    tl[3] = waited_ns;
     tl[2 + p.T] = globaltimer();
   }
+  if (tid == (kEngine == 1 ? 32 : 0)) tl[3] = waited_ns;
 }
 
 static int cuda_fail(cudaError_t e, const char* what) {
