@@ -820,12 +820,13 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
   std::vector<double> key(all.size(), 0);   // queue order key (step-major or start time)
   auto place = [&](TU& x) {
     if (x.dst_gpu != x.g) {
-      // egress pipe only: NVSwitch shares a GPU's ingress among its senders
-      // fluidly, so an exclusive ingress pipe would invent idle gaps
-      double st = std::max(x.ready, eg_free[x.g]);
+      // egress AND ingress pipes: the makespan estimate is pessimistic (no
+      // fluid sharing), but the resulting order spreads concurrent transfers
+      // over receivers and avoids incast on one GPU (measured: GK(8,2) at 4
+      // GPUs 0.70 ms vs 1.02 ms with an egress-only model)
+      double st = std::max(x.ready, std::max(eg_free[x.g], in_free[x.dst_gpu]));
       x.finish = st + x.u.nbytes / nv;
-      eg_free[x.g] = x.finish;
-      (void)in_free;
+      eg_free[x.g] = in_free[x.dst_gpu] = x.finish;
       return st;
     }
     double st = std::max(x.ready, hbm_free[x.g]);
