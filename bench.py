@@ -343,9 +343,7 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
         e0[k].record(stream)
         plan.execute(send, recv, stream=stream)
         e1[k].record(stream)
-        if clk and k % 8 == 7:
-            clk.sample()          # the GPU runs ahead of this host loop: sample while it works
-    plan.sync()
+    plan.sync()                   # the sampler thread keeps sampling while the GPU drains
     torch.cuda.synchronize(dev)
     clock_rec = clk.stop() if clk else None
     ctx.barrier()
