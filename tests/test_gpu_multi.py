@@ -220,3 +220,70 @@ def test_alternating_recv_buffers():
         p.join(timeout=60)
     for r in res:
         assert r[1] is True, r
+
+
+def _gk256_main(rank, world, port, name, sched, q):
+    sys.path.insert(0, ROOT)
+    try:
+        import torch
+        import torch.distributed as dist
+
+        from paper_2309_13541_b200.artifacts import load_artifact
+        from paper_2309_13541_b200.dist import connect, local_nodes
+        from paper_2309_13541_b200.executor import Plan
+        torch.cuda.set_device(rank)
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}",
+                                rank=rank, world_size=world)
+        a = load_artifact(name, native=True)
+        m = 8192 + 64
+        plan = Plan(a.g, a.sched, m=m, n_gpus=world, placement="optimized")
+        plan.set_schedule(sched)
+        plan.bind(rank, device=rank)
+        plan.set_timeout(30.0)
+        connect(plan)
+        nodes = local_nodes(plan, rank)
+        n = a.g.n
+
+        def row(s):   # deterministic shard rows of node s, generated on the device
+            gen = torch.Generator(device="cuda").manual_seed(977 * (s + 1))
+            return torch.randint(0, 256, (n, m), dtype=torch.uint8, device="cuda", generator=gen)
+        send = torch.stack([row(v) for v in nodes])
+        recv = plan.recv_buffer()
+        plan.execute(send, recv, count_links=True)
+        plan.sync()
+        ok = True
+        for s in range(n):
+            r = row(s)
+            ok &= bool(torch.equal(recv[:, s], r[nodes]))
+        counters = plan.read_link_counters()
+        tot = [None] * world
+        dist.all_gather_object(tot, counters)
+        q.put((rank, ok, bool(np.array_equal(sum(tot), plan.link_bytes()))))
+        plan.close()
+        dist.destroy_process_group()
+    except Exception as ex:
+        import traceback
+        q.put((rank, f"{ex!r}\n{traceback.format_exc()}"))
+
+
+@pytest.mark.parametrize("name", ["gk256_4", "gk256_4_h2"])
+@pytest.mark.parametrize("sched", ["static", "dynamic"])
+def test_gk256_four_gpus(name, sched):
+    """Config 4 (GenKautz N=256, with / without extra NIC forwarding) on 4 GPUs:
+    transpose of device-generated shards, device link counters == schedule."""
+    if _ngpu() < 4:
+        pytest.skip("needs 4 GPUs")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_gk256_main, args=(r, 4, port, name, sched, q)) for r in range(4)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=600) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    for r in sorted(res, key=lambda x: x[0]):
+        assert len(r) == 3, r
+        assert r[1], f"rank {r[0]}: recv mismatch"
+        assert r[2], f"rank {r[0]}: link counters differ from schedule"
