@@ -279,8 +279,11 @@ def autotune_schedule(ctx, art, m, placement="optimized", num_ctas=0, trials=5,
     return best, times
 
 
+L2_BYTES = 126 << 20
+
+
 def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=True,
-            flush_bytes=512 << 20, placement="optimized", schedule="static"):
+            flush_bytes=512 << 20, placement="optimized", schedule="static", flush=None):
     """Time K all-to-alls of `art` at shard size m on ctx.world GPUs.
 
     Returns a dict (identical on every rank) with T, algBW, bound, roofline,
@@ -315,7 +318,15 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     for i, s in enumerate(nodes):
         send[i] = node_send(s)
     recv = plan.recv_buffer() if G > 1 else torch.empty_like(send)
-    flush = torch.empty(flush_bytes, dtype=torch.uint8, device=dev)
+    # L2 policy: flush (512 MiB memset outside the events) unless every GPU's
+    # send buffer alone exceeds L2 (126 MB), in which case inputs are larger
+    # than L2 and back-to-back all-to-alls avoid per-rank flush skew
+    if flush is None:
+        flush = min(i["send_bytes"] for i in infos) < L2_BYTES
+    l2_policy = ("flushed between timed steps (512 MiB memset, outside events)" if flush else
+                 f"inputs larger than L2 ({min(i['send_bytes'] for i in infos) >> 20} MiB send per GPU "
+                 f"> 126 MB), no flush")
+    flush_buf = torch.empty(flush_bytes if flush else 1, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     clk = Clocks(ctx.local) if clocks else None
@@ -339,7 +350,8 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     if clk:
         clk.start()
     for k in range(steps):
-        flush.zero_()
+        if flush:
+            flush_buf.zero_()
         e0[k].record(stream)
         plan.execute(send, recv, stream=stream)
         e1[k].record(stream)
@@ -394,7 +406,8 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
         torch.cuda.synchronize(dev)
         ts = []
         for _ in range(steps):
-            flush.zero_()
+            if flush:
+                flush_buf.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             ctx.pg.all_to_all_single(out, inp)
@@ -491,9 +504,9 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
            "kernel_timeline": tls,
            "num_ctas": plan_ctas(plan, num_ctas), "egress_max": max(i["egress_bytes"] for i in infos),
            "scratch_bytes": info["scratch_bytes"], "placement": plan.placement.tolist(),
-           "schedule": schedule}
+           "schedule": schedule, "l2": l2_policy}
     plan.close()
-    del send, recv, flush
+    del send, recv, flush_buf
     torch.cuda.empty_cache()
     return res
 
@@ -563,7 +576,7 @@ def main(argv=None):
                                    f"{r['placement'] if G > 1 else ''}",
                        "m_bytes": m, "nodes": n, "hop_ops": len(art.sched.instructions),
                        "nsteps": art.sched.nsteps, "Q": art.sched.Q,
-                       "l2": "flushed between timed steps (512 MiB memset, outside events)",
+                       "l2": r["l2"],
                        "num_ctas": r["num_ctas"], "schedule": schedule,
                        "schedule_autotune_ms": tune},
             "per_gpu": round(r["per_gpu"], 3),

@@ -87,7 +87,7 @@ def main(argv=None):
                     "clocks": r["clocks"], "sync_flags": r["sync"],
                     "kernel_timeline": r["kernel_timeline"],
                     "egress_max_bytes": r["egress_max"], "scratch_bytes": r["scratch_bytes"],
-                    "placement": a.placement,
+                    "placement": a.placement, "l2": r["l2"],
                     "wall_s": round(time.time() - t0, 1)})
         if ctx.rank == 0:
             line = json.dumps(rec)
