@@ -12,8 +12,9 @@ i; the 8 virtual nodes are placed v*G//8 on G GPUs (one per GPU at G=8).
 A "step" = one complete all-to-all.  value = whole-job algBW
 N(N-1)m / T (GB/s); per_gpu = value / G.
 Timing: W warm-up steps, then K steps each bracketed by CUDA events on the
-launching stream, L2 flushed (512 MiB memset) between steps outside the
-events; barrier + synchronize around the timed region; per-step max over ranks.
+launching stream; L2 flushed (512 MiB memset, outside the events) between steps unless
+every GPU's send buffer exceeds L2 (then inputs are larger than L2, recorded in config.l2);
+barrier + synchronize around the timed region; per-step max over ranks.
 """
 from __future__ import annotations
 
