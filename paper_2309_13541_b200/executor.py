@@ -19,6 +19,7 @@ objects as well as this package's mirrors (duck typing on ``n``, ``edges``,
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
@@ -131,13 +132,11 @@ class Plan:
         d.node_gpu = self.placement.ctypes.data_as(C.POINTER(C.c_int32))
         d.n_gpus = self.n_gpus
         if order is None:
-            import os
             order = os.environ.get("A2A_ORDER", "grouped")
         if order not in ("grouped", "interleaved"):
             raise ValueError("order must be 'grouped' or 'interleaved'")
         self.order = order
         if reuse_scratch is None:
-            import os
             reuse_scratch = os.environ.get("A2A_REUSE_SCRATCH", "0") == "1"
         self.reuse_scratch = bool(reuse_scratch)
         d.flags = (N.A2A_COPY_SELF if copy_self else 0) | \
@@ -254,14 +253,13 @@ class Plan:
 
     def bind(self, gpu: int = 0, device: int | None = None, num_ctas: int = 0):
         device = gpu if device is None else device
-        if getattr(self, "engine", None) is None:
-            import os
+        # environment overrides for experiments (explicit setters win)
+        if self.engine is None:
             env = os.environ.get("A2A_ENGINE", "").strip().lower()
             if env:
                 parts = env.split(":")      # tma[:chunk[:stages]]
                 self.set_engine(parts[0], *(int(x) for x in parts[1:]))
-        import os
-        if getattr(self, "schedule", None) is None and os.environ.get("A2A_SCHED"):
+        if self.schedule is None and os.environ.get("A2A_SCHED"):
             parts = os.environ["A2A_SCHED"].split(":")   # dynamic[:unit_bytes]
             self.set_schedule(parts[0], *(int(x) for x in parts[1:]))
         if os.environ.get("A2A_SYNC_MODE"):
@@ -300,7 +298,8 @@ class Plan:
         return self
 
     def recv_buffer(self, index: int = 0):
-        """torch uint8 view [V_g, N, m] of this rank's arena recv buffer `index`."""
+        """torch uint8 view [V_g, N, m] of this rank's arena recv buffer `index`
+        (plan-owned memory: valid until ``close()``)."""
         import torch
         p = C.c_void_p()
         self._ck(N.lib.a2a_plan_recv_buffer_at(self._h, int(index), C.byref(p)),
