@@ -136,6 +136,10 @@ int a2a_optimize_placement(int32_t n, int32_t n_edges, const int32_t* edge_uv,
                            const int64_t* edge_bytes, int32_t n_gpus, int32_t iters,
                            uint64_t seed, int32_t* placement);
 
+/* Static CTA split, before bind: each step's items are cut into equal-cost CTA
+ * ranges where a byte bound for another GPU costs `remote_weight` (1..64,
+ * default 1) and a local byte 1. */
+int a2a_plan_set_split(a2a_plan* plan, int32_t remote_weight);
 /* Execution schedule, before bind: 0 = static per-CTA step programs (default),
  * 1 = dynamic units: items cut into units of `unit_bytes` (0 = auto), CTAs grab
  * units in step-major, readiness-ordered lists from a per-GPU atomic counter and

@@ -69,6 +69,7 @@ static_assert(sizeof(CtaStep) == 32, "CtaStep layout");
 
 struct SyncTables {
   int32_t nC = 0;
+  int32_t weight = 0;                           // remote_weight the split was built with
   std::vector<std::vector<DevPiece>> pieces;    // [g] ordered by (cta, step)
   std::vector<std::vector<CtaStep>> prog;       // [g][c*T' + t]
   std::vector<std::vector<uint32_t>> dst_mask;  // [g][t*nC + c] bit h: (g,c) wrote to h at t
@@ -126,6 +127,7 @@ struct Plan {
 
   SyncTables sync;
   DynTables dyn;
+  int32_t remote_weight = 1;                    // CTA split cost of an NVLink byte vs a local byte
   int32_t sched_mode = 0;                       // 0 static programs, 1 dynamic step-major, 2 dynamic list-scheduled
   int64_t dyn_unit_bytes = 0;                   // dynamic unit size (0 = auto)
   int64_t dyn_execs = 0;                        // dynamic executes so far (grab counter base)

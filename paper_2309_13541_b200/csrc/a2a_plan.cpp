@@ -474,37 +474,55 @@ struct Seg {
   int64_t a, b;
   int32_t t, slot;
 };
+// CTA split of one step: the step's items are cut into nC contiguous ranges of
+// equal *cost*, where a byte bound for another GPU (NVLink) costs `wr` and a
+// local byte (HBM) costs 1 -- an SM moves local bytes several times faster
+// than it can push them over NVLink, so equal-byte ranges would leave the
+// NVLink CTAs finishing last.  Boundaries inside an item fall on 64-byte
+// multiples (the item end excepted), so every piece keeps src == dst (mod 64).
 template <typename F>
-void for_each_piece(const GpuTables& tb, int t, int nC, F&& f) {
-  const int64_t B = tb.step_bytes[t];
-  int64_t k = tb.step_begin[t];
+void for_each_piece(const GpuTables& tb, int g, int t, int nC, int wr, F&& f) {
+  const int64_t b0 = tb.step_begin[t], b1 = tb.step_begin[t + 1];
+  if (b1 <= b0) return;
+  std::vector<int64_t> pw(b1 - b0 + 1, 0);  // weighted prefix
+  for (int64_t j = b0; j < b1; ++j) {
+    const DevItem& it = tb.items[j];
+    pw[j - b0 + 1] = pw[j - b0] + (it.dst_gpu != g ? wr : 1) * it.nbytes;
+  }
+  const int64_t W = pw[b1 - b0];
+  auto pos = [&](int64_t j, int64_t b) -> int64_t {  // byte position of cost b in item j
+    const DevItem& it = tb.items[j];
+    const int64_t w = it.dst_gpu != g ? wr : 1, P0 = pw[j - b0];
+    if (b <= P0) return 0;
+    if (b >= P0 + w * it.nbytes) return it.nbytes;
+    return std::min<int64_t>(it.nbytes, ((b - P0) / w) & ~(int64_t)63);
+  };
+  int64_t k = b0;
   for (int c = 0; c < nC; ++c) {
-    const int64_t lo = cta_lo(B, c, nC), hi = cta_lo(B, c + 1, nC);
+    const int64_t lo = (int64_t)(((__int128)W * c) / nC), hi = (int64_t)(((__int128)W * (c + 1)) / nC);
     if (hi <= lo) continue;
-    while (k < tb.step_begin[t + 1] && tb.items[k].prefix + tb.items[k].nbytes <= lo) ++k;
-    for (int64_t j = k; j < tb.step_begin[t + 1] && tb.items[j].prefix < hi; ++j) {
-      const DevItem& it = tb.items[j];
-      const int64_t x0 = std::max(lo, it.prefix) - it.prefix;
-      const int64_t x1 = std::min(hi, it.prefix + it.nbytes) - it.prefix;
-      if (x1 > x0) f(c, it, x0, x1);
+    while (k < b1 && pw[k - b0 + 1] <= lo) ++k;
+    for (int64_t j = k; j < b1 && pw[j - b0] < hi; ++j) {
+      const int64_t x0 = pos(j, lo), x1 = pos(j, hi);
+      if (x1 > x0) f(c, tb.items[j], x0, x1);
     }
   }
 }
 }  // namespace
 
 int build_sync(Plan& P, int nC) {
-  if (P.sync.nC == nC) return A2A_OK;
+  if (P.sync.nC == nC && P.sync.weight == P.remote_weight) return A2A_OK;
   if (nC < 1) return fail(A2A_ERR_INVALID, "num_ctas must be >= 1");
   const int G = P.G, TE = P.T_exec;
   SyncTables S;
   S.nC = nC;
-  (void)0;
+  S.weight = P.remote_weight;
   S.dst_mask.assign(G, std::vector<uint32_t>((size_t)TE * nC, 0));
   // segs[h][0] = writes into h's recv, segs[h][1] = into h's scratch
   std::vector<std::array<std::vector<Seg>, 2>> segs(G);
   for (int g = 0; g < G; ++g) {
     for (int t = 0; t < TE; ++t) {
-      for_each_piece(P.tables[g], t, nC, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
+      for_each_piece(P.tables[g], g, t, nC, P.remote_weight, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
         S.dst_mask[g][(size_t)t * nC + c] |= 1u << it.dst_gpu;
         const int cls = (it.dst_loc == loc_recv(it.dst_gpu)) ? 0 : 1;
         segs[it.dst_gpu][cls].push_back(
@@ -536,7 +554,7 @@ int build_sync(Plan& P, int nC) {
     std::vector<std::vector<int32_t>> rcta(G), wg(G);   // producer GPU of each segment
     for (int g = 0; g < G; ++g)
       for (int t = 0; t < TE; ++t)
-        for_each_piece(P.tables[g], t, nC, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
+        for_each_piece(P.tables[g], g, t, nC, P.remote_weight, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
           const int32_t slot = (int32_t)(((int64_t)t * G + g) * nC + c);
           if (it.src_loc == loc_scratch(g, G)) {
             rseg[g].push_back(Seg{it.src_off + x0, it.src_off + x1, t, slot});
@@ -582,7 +600,7 @@ int build_sync(Plan& P, int nC) {
     off.assign((size_t)TE * nC + 1, 0);
     auto& per = per_all[h];
     for (int t = 0; t < TE; ++t) {
-      for_each_piece(P.tables[h], t, nC, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
+      for_each_piece(P.tables[h], h, t, nC, P.remote_weight, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
         if (it.src_loc == loc_send()) return;
         const int cls = (it.src_loc == loc_recv(h)) ? 0 : 1;
         const int64_t a = it.src_off + x0, b = it.src_off + x1;
@@ -619,7 +637,7 @@ int build_sync(Plan& P, int nC) {
   for (int g = 0; g < G; ++g) {
     std::vector<std::vector<std::vector<DevPiece>>> per_ct(nC, std::vector<std::vector<DevPiece>>(TE));
     for (int t = 0; t < TE; ++t)
-      for_each_piece(P.tables[g], t, nC, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
+      for_each_piece(P.tables[g], g, t, nC, P.remote_weight, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
         for (int64_t x = x0; x < x1; x += (1LL << 30)) {
           DevPiece pc{};
           pc.src_off = it.src_off + x;
@@ -668,10 +686,9 @@ static int emulate(Plan& P, int nC, uint8_t* const* send, uint8_t* const* recv, 
   std::vector<std::vector<std::vector<char>>> has(G, std::vector<std::vector<char>>(nC, std::vector<char>(TE, 0)));
   for (int g = 0; g < G; ++g)
     for (int t = 0; t < TE; ++t) {
-      const int64_t B = P.tables[g].step_bytes[t];
-      for (int c = 0; c < nC; ++c) has[g][c][t] = cta_lo(B, c + 1, nC) > cta_lo(B, c, nC);
-      for_each_piece(P.tables[g], t, nC, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
+      for_each_piece(P.tables[g], g, t, nC, P.remote_weight, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
         work[g][c][t].push_back(Piece{it.src_loc, it.dst_loc, it.src_off + x0, it.dst_off + x0, x1 - x0});
+        has[g][c][t] = 1;
       });
     }
   auto base = [&](int g, int loc) -> uint8_t* {
@@ -1098,6 +1115,13 @@ int a2a_plan_prepare(a2a_plan* plan, int32_t num_ctas) {
   } catch (const std::bad_alloc&) {
     return fail(A2A_ERR_NOMEM, "out of host memory building the CTA tables");
   }
+}
+
+int a2a_plan_set_split(a2a_plan* plan, int32_t remote_weight) {
+  if (!plan || remote_weight < 1 || remote_weight > 64) return fail(A2A_ERR_INVALID, "bad remote weight");
+  if (plan->p.bound) return fail(A2A_ERR_STATE, "set the CTA split before a2a_plan_bind");
+  plan->p.remote_weight = remote_weight;
+  return A2A_OK;
 }
 
 int a2a_plan_set_schedule(a2a_plan* plan, int32_t mode, int64_t unit_bytes) {

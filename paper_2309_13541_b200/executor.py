@@ -204,6 +204,12 @@ class Plan:
         self._ck(N.lib.a2a_plan_prepare(self._h, int(num_ctas)), "a2a_plan_prepare")
         return self
 
+    def set_split(self, remote_weight: int):
+        """Before bind: cost weight of an NVLink byte in the static CTA split."""
+        self._ck(N.lib.a2a_plan_set_split(self._h, int(remote_weight)), "a2a_plan_set_split")
+        self.remote_weight = int(remote_weight)
+        return self
+
     def set_schedule(self, mode: str = "static", unit_bytes: int = 0):
         """Before bind: "static" per-CTA step programs or "dynamic" units
         grabbed from a per-GPU queue."""
@@ -262,6 +268,8 @@ class Plan:
         if self.schedule is None and os.environ.get("A2A_SCHED"):
             parts = os.environ["A2A_SCHED"].split(":")   # dynamic[:unit_bytes]
             self.set_schedule(parts[0], *(int(x) for x in parts[1:]))
+        if os.environ.get("A2A_SPLIT_W") and getattr(self, "remote_weight", None) is None:
+            self.set_split(int(os.environ["A2A_SPLIT_W"]))
         if os.environ.get("A2A_SYNC_MODE"):
             self.set_sync_mode(int(os.environ["A2A_SYNC_MODE"]))
         self._ck(N.lib.a2a_plan_bind(self._h, int(gpu), int(device), int(num_ctas)),

@@ -170,3 +170,22 @@ def test_dynamic_schedule_interleavings(name, G, unit, reuse, mode, artifacts):
                 assert np.array_equal(recvs[g], want[nodes[g]]), (seed, g)
         st = p.dyn_stats(0, 11)
         assert st["units"] > 0
+
+
+@pytest.mark.parametrize("name,G", [("gk8_2", 2), ("gk8_2", 4), ("torus4x4x4", 4), ("hypercube3", 8),
+                                    ("torus2x4_h2", 4), ("ts_hypercube3", 2)])
+@pytest.mark.parametrize("w", [1, 3, 8])
+def test_weighted_split_interleavings(name, G, w, artifacts):
+    """Cost-weighted CTA split (NVLink bytes weighted w): still an exact
+    partition of every step's bytes, dependencies still sufficient."""
+    a = artifacts(name)
+    m = 5000 if a.g.n <= 8 else 1024
+    send = make_send(a.g.n, m, seed=8)
+    with Plan(a.g, a.sched, m=m, n_gpus=G, placement="optimized") as p:
+        p.set_split(w)
+        nodes = [local_nodes(p, g) for g in range(G)]
+        for seed in range(2):
+            recvs = p.emulate([send[ns] for ns in nodes], num_ctas=23, seed=seed)
+            want = np.swapaxes(send, 0, 1)
+            for g in range(G):
+                assert np.array_equal(recvs[g], want[nodes[g]])
