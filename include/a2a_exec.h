@@ -145,7 +145,8 @@ int a2a_plan_set_split(a2a_plan* plan, int32_t remote_weight);
  * units in step-major, readiness-ordered lists from a per-GPU atomic counter and
  * acquire per-unit producer flags; 2 = dynamic units ordered by
  * an event-driven list schedule (start times) instead of step-major, so routes
- * pipeline hop by hop at unit granularity.  a2a_plan_emulate follows the
+ * pipeline hop by hop at unit granularity; 3 = dynamic units, step-major with
+ * critical-path (bottom-level) priority within a step.  a2a_plan_emulate follows the
  * selected mode.  Stats: units and dependency entries of `gpu`, model makespan. */
 int a2a_plan_set_schedule(a2a_plan* plan, int32_t mode, int64_t unit_bytes);
 int a2a_plan_dyn_stats(a2a_plan* plan, int32_t gpu, int32_t num_ctas, int64_t* n_units,

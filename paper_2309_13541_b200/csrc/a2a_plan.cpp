@@ -881,6 +881,30 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
       for (int t = 0; t < TE; ++t)
         std::stable_sort(per[g][t].begin(), per[g][t].end(),
                          [&](int a, int b) { return key[a] < key[b]; });
+  } else if (P.sched_mode == 3) {
+    // critical-path priorities (HLFET): bottom level = own cost + the longest
+    // cost chain through successors; within a step, larger bottom level first
+    // (early hops of long routes before units that end a route)
+    std::vector<std::vector<int>> succ(all.size());
+    for (int i = 0; i < (int)all.size(); ++i)
+      for (int d : all[i].deps) succ[d].push_back(i);
+    std::vector<double> bl(all.size(), 0.0);
+    for (int t = TE - 1; t >= 0; --t)
+      for (int g = 0; g < G; ++g)
+        for (int id : per[g][t]) {
+          const TU& x = all[id];
+          double best = 0;
+          for (int sx : succ[id]) best = std::max(best, bl[sx]);
+          bl[id] = best + x.u.nbytes / (x.dst_gpu != x.g ? nv : hbm);
+        }
+    for (int g = 0; g < G; ++g) {
+      double k = 0;
+      for (int t = 0; t < TE; ++t) {
+        std::stable_sort(per[g][t].begin(), per[g][t].end(),
+                         [&](int a, int b) { return bl[a] > bl[b]; });
+        for (int id : per[g][t]) key[id] = k++;
+      }
+    }
   } else {
     for (int t = 0; t < TE; ++t) {
       std::vector<int> step_units;
@@ -1125,7 +1149,7 @@ int a2a_plan_set_split(a2a_plan* plan, int32_t remote_weight) {
 }
 
 int a2a_plan_set_schedule(a2a_plan* plan, int32_t mode, int64_t unit_bytes) {
-  if (!plan || mode < 0 || mode > 2 || unit_bytes < 0) return fail(A2A_ERR_INVALID, "bad schedule mode");
+  if (!plan || mode < 0 || mode > 3 || unit_bytes < 0) return fail(A2A_ERR_INVALID, "bad schedule mode");
   if (plan->p.bound) return fail(A2A_ERR_STATE, "set the schedule mode before a2a_plan_bind");
   plan->p.sched_mode = mode;
   plan->p.dyn_unit_bytes = unit_bytes;
