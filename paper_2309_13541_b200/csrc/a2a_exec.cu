@@ -241,6 +241,10 @@ __device__ bool warp_wait_flags(const uint32_t* flags, const int32_t* idx, int32
 
 // Chunk cursor over the 16-byte-aligned bodies of a staged batch of pieces
 // (TMA engine).  Heads/tails and misaligned pieces are copied by threads.
+// pieces at most this long are copied with 128-bit loads/stores by all threads
+// even in the TMA engine: no bulk-group completion round trip before publishing
+constexpr int64_t kSmallPiece = 32768;
+
 struct BodyCursor {
   const DevPiece* pc;
   int32_t k, n;
@@ -248,6 +252,7 @@ struct BodyCursor {
   __device__ bool next(const KParams& p, uint32_t ch, const char** src, char** dst, uint32_t* len) {
     while (k < n) {
       const DevPiece& q = pc[k];
+      if (q.nbytes <= kSmallPiece) { ++k; off = 0; continue; }
       const char* s0 = p.base[q.src_loc] + q.src_off;
       char* d0 = p.base[q.dst_loc] + q.dst_off;
       const int64_t L = q.nbytes;
@@ -354,10 +359,20 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
           cta_copy<4>(p.base[q.dst_loc] + q.dst_off, p.base[q.src_loc] + q.src_off, q.nbytes);
         }
       } else {
-        if (tid != 0) {  // threads 1..: heads, tails, misaligned pieces
+        for (int i = 0; i < n; ++i) {  // small pieces: all threads, 128-bit LSU
+          const DevPiece& q = s_pc[i];
+          if (q.nbytes <= kSmallPiece)
+            cta_copy<4>(p.base[q.dst_loc] + q.dst_off, p.base[q.src_loc] + q.src_off, q.nbytes);
+        }
+        bool any_big = false;
+        for (int i = 0; i < n && !any_big; ++i) any_big = s_pc[i].nbytes > kSmallPiece;
+        if (!any_big) {
+          // nothing for the TMA ring in this batch
+        } else if (tid != 0) {  // threads 1..: heads, tails, misaligned big pieces
           const int nt = kThreads - 1, me = tid - 1;
           for (int i = 0; i < n; ++i) {
             const DevPiece& q = s_pc[i];
+            if (q.nbytes <= kSmallPiece) continue;
             const char* s0 = p.base[q.src_loc] + q.src_off;
             char* d0 = p.base[q.dst_loc] + q.dst_off;
             const int64_t len = q.nbytes;
@@ -570,6 +585,9 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_dyn_kernel(const KParams p) {
     if (kEngine == 0) {
       cta_copy<4>(d0, s0, u.nbytes);
       if (tid == 0) fetch(cur ^ 1);
+    } else if (u.nbytes <= kSmallPiece) {  // small unit: all threads, no bulk round trip
+      cta_copy<4>(d0, s0, u.nbytes);
+      if (warp == fw && (tid & 31) == 0) fetch(cur ^ 1);
     } else if (warp == fw) {
       if ((tid & 31) == 0) fetch(cur ^ 1);
     } else if (tid >= 64) {
