@@ -497,7 +497,10 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
                         "value = pipelined (double-buffered, 3 streams), sequential also given"}
         del hs, hr, sends, recvs
     plan.sync()
-    res = {"T": T, "per_step_ms": per, "value": value, "per_gpu": value / G,
+    sp = sorted(per)
+    dist = {"p50": round(sp[len(sp) // 2], 4), "p90": round(sp[min(len(sp) - 1, int(0.9 * len(sp)))], 4),
+            "max": round(sp[-1], 4), "min": round(sp[0], 4)}
+    res = {"T": T, "per_step_ms": per, "step_ms_dist": dist, "value": value, "per_gpu": value / G,
            "t_lb": t_lb, "bound_frac": t_lb / T, "roofline": roof, "nccl": nres, "e2e": eres,
            "recv_ok": bool(ok), "clocks": clock_rec,
            "sync": (plan.dyn_stats(rank, plan_ctas(plan, num_ctas)) if plan.schedule in ("dynamic", "list", "cp")
@@ -581,6 +584,7 @@ def main(argv=None):
                        "num_ctas": r["num_ctas"], "schedule": schedule,
                        "schedule_autotune_ms": tune},
             "per_gpu": round(r["per_gpu"], 3),
+            "step_ms_dist": r["step_ms_dist"],
             "bound": {"t_lb_ms": round(r["t_lb"] * 1e3, 4), "frac": round(r["bound_frac"], 4),
                       "def": "G=1: 2*m*sum(dist)/HBM; G>1: max_g max(egress,ingress)/900 GB/s"},
             "recv_ok": r["recv_ok"],

@@ -80,7 +80,8 @@ def main(argv=None):
                 rec.update({
                     "nodes": art.g.n, "hop_ops": len(art.sched.instructions),
                     "nsteps": art.sched.nsteps, "Q": art.sched.Q,
-                    "ms": round(r["T"] * 1e3, 4), "algbw_gbs": round(r["value"], 2),
+                    "ms": round(r["T"] * 1e3, 4), "step_ms_dist": r["step_ms_dist"],
+                    "algbw_gbs": round(r["value"], 2),
                     "algbw_per_gpu_gbs": round(r["per_gpu"], 2),
                     "t_lb_ms": round(r["t_lb"] * 1e3, 4), "bound_frac": round(r["bound_frac"], 4),
                     "roofline": r["roofline"], "nccl": r["nccl"], "recv_ok": r["recv_ok"],
