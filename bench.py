@@ -503,7 +503,7 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     res = {"T": T, "per_step_ms": per, "step_ms_dist": dist, "value": value, "per_gpu": value / G,
            "t_lb": t_lb, "bound_frac": t_lb / T, "roofline": roof, "nccl": nres, "e2e": eres,
            "recv_ok": bool(ok), "clocks": clock_rec,
-           "sync": (plan.dyn_stats(rank, plan_ctas(plan, num_ctas)) if plan.schedule in ("dynamic", "list", "cp")
+           "sync": (plan.dyn_stats(rank, plan_ctas(plan, num_ctas)) if plan.schedule in ("dynamic", "list", "cp", "mix")
                     else plan.sync_stats(rank)),
            "kernel_timeline": tls,
            "num_ctas": plan_ctas(plan, num_ctas), "egress_max": max(i["egress_bytes"] for i in infos),

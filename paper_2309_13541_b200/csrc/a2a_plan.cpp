@@ -881,6 +881,47 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
       for (int t = 0; t < TE; ++t)
         std::stable_sort(per[g][t].begin(), per[g][t].end(),
                          [&](int a, int b) { return key[a] < key[b]; });
+  } else if (P.sched_mode == 4) {
+    // single queue, step-major; within a step the NVLink and HBM units are
+    // merged in proportion to their estimated time (remote byte ~ hbm/nv local
+    // bytes), each class ordered by critical path, so both pipes stay busy and
+    // neither class runs ahead of the other
+    std::vector<std::vector<int>> succ(all.size());
+    for (int i = 0; i < (int)all.size(); ++i)
+      for (int d : all[i].deps) succ[d].push_back(i);
+    std::vector<double> bl(all.size(), 0.0);
+    for (int t = TE - 1; t >= 0; --t)
+      for (int g = 0; g < G; ++g)
+        for (int id : per[g][t]) {
+          double best = 0;
+          for (int sx : succ[id]) best = std::max(best, bl[sx]);
+          bl[id] = best + all[id].u.nbytes / (all[id].dst_gpu != all[id].g ? nv : hbm);
+        }
+    for (int g = 0; g < G; ++g) {
+      double k = 0;
+      for (int t = 0; t < TE; ++t) {
+        std::vector<int> rq, lq;
+        double rt = 0, lt = 0;
+        for (int id : per[g][t]) {
+          if (all[id].dst_gpu != g) { rq.push_back(id); rt += all[id].u.nbytes / nv; }
+          else { lq.push_back(id); lt += all[id].u.nbytes / hbm; }
+        }
+        auto bysl = [&](int a, int b) { return bl[a] > bl[b]; };
+        std::stable_sort(rq.begin(), rq.end(), bysl);
+        std::stable_sort(lq.begin(), lq.end(), bysl);
+        std::vector<int> merged;
+        size_t i = 0, j = 0;
+        double er = 0, el = 0;
+        while (i < rq.size() || j < lq.size()) {
+          const bool take_r = j >= lq.size() ||
+                              (i < rq.size() && (rt > 0 ? er / rt : 1.0) <= (lt > 0 ? el / lt : 1.0));
+          if (take_r) { er += all[rq[i]].u.nbytes / nv; merged.push_back(rq[i++]); }
+          else { el += all[lq[j]].u.nbytes / hbm; merged.push_back(lq[j++]); }
+        }
+        per[g][t] = merged;
+        for (int id : per[g][t]) key[id] = k++;
+      }
+    }
   } else if (P.sched_mode == 3) {
     // critical-path priorities (HLFET): bottom level = own cost + the longest
     // cost chain through successors; within a step, larger bottom level first
@@ -946,6 +987,18 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
   D.units.assign(G, {});
   for (int g = 0; g < G; ++g) {
     double rb = 0, lb = 0;
+    if (P.sched_mode == 4) {  // one queue in key order; n_remote = 0, no CTA on queue 0
+      std::vector<int> q;
+      for (int t = 0; t < TE; ++t)
+        for (int id : per[g][t]) q.push_back(id);
+      std::stable_sort(q.begin(), q.end(), [&](int a, int b) { return key[a] < key[b]; });
+      qorder[g] = q;
+      int k = 0;
+      for (int id : qorder[g]) gid[id] = D.unit_base[g] + k++;
+      D.unit_base[g + 1] = D.unit_base[g] + k;
+      D.remote_ctas[g] = 0;
+      continue;
+    }
     for (int pass = 0; pass < 2; ++pass) {
       std::vector<int> q;
       for (int t = 0; t < TE; ++t)
@@ -1149,7 +1202,7 @@ int a2a_plan_set_split(a2a_plan* plan, int32_t remote_weight) {
 }
 
 int a2a_plan_set_schedule(a2a_plan* plan, int32_t mode, int64_t unit_bytes) {
-  if (!plan || mode < 0 || mode > 3 || unit_bytes < 0) return fail(A2A_ERR_INVALID, "bad schedule mode");
+  if (!plan || mode < 0 || mode > 4 || unit_bytes < 0) return fail(A2A_ERR_INVALID, "bad schedule mode");
   if (plan->p.bound) return fail(A2A_ERR_STATE, "set the schedule mode before a2a_plan_bind");
   plan->p.sched_mode = mode;
   plan->p.dyn_unit_bytes = unit_bytes;
