@@ -237,7 +237,7 @@ class Ctx:
 
 
 def autotune_schedule(ctx, art, m, placement="optimized", num_ctas=0, trials=5,
-                      candidates=("static", "dynamic:1048576", "list:1048576")):
+                      candidates=("static", "cp:1048576", "dynamic:1048576")):
     """Time a few executes of each execution schedule (same placement, same
     buffers) and return (best, {candidate: ms}); identical on every rank."""
     import torch
@@ -261,6 +261,7 @@ def autotune_schedule(ctx, art, m, placement="optimized", num_ctas=0, trials=5,
             plan.execute(send, recv, stream=stream)
         plan.sync()
         ctx.barrier()
+        plan.execute(send, recv, stream=stream)   # skew absorber (see measure)
         ev = []
         for _ in range(trials):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -350,6 +351,10 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     torch.cuda.synchronize(dev)
     if clk:
         clk.start()
+    # one untimed all-to-all right before the timed ones (no host sync between):
+    # it absorbs the ranks' host launch skew in its entry barrier, so the
+    # first timed step measures the pipeline and not process start-up skew
+    plan.execute(send, recv, stream=stream)
     for k in range(steps):
         if flush:
             flush_buf.zero_()
@@ -405,6 +410,8 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
         for _ in range(3):
             ctx.pg.all_to_all_single(out, inp)
         torch.cuda.synchronize(dev)
+        ctx.barrier()
+        ctx.pg.all_to_all_single(out, inp)      # same skew absorber as for our kernel
         ts = []
         for _ in range(steps):
             if flush:
