@@ -182,7 +182,7 @@ def _alt_main(rank, world, port, q):
 @pytest.mark.parametrize("engine", ["tma", "lsu"])
 @pytest.mark.parametrize("reuse", [False, True])
 @pytest.mark.parametrize("name,m", [("gk8_2", 65536 + 64), ("torus4x4x4", 8192), ("torus2x4_h2", 4099)])
-@pytest.mark.parametrize("mode", ["dynamic", "list"])
+@pytest.mark.parametrize("mode", ["dynamic", "list", "cp", "mix"])
 def test_multiprocess_dynamic(world, engine, reuse, name, m, mode):
     """Dynamic unit queues across GPUs (+ scratch reuse, optimized placement)."""
     if _ngpu() < world:
