@@ -237,7 +237,7 @@ class Ctx:
 
 
 def autotune_schedule(ctx, art, m, placement="optimized", num_ctas=0, trials=5,
-                      candidates=("static", "cp:1048576", "dynamic:1048576")):
+                      candidates=("static", "mix:1048576", "cp:1048576")):
     """Time a few executes of each execution schedule (same placement, same
     buffers) and return (best, {candidate: ms}); identical on every rank."""
     import torch
