@@ -136,6 +136,10 @@ int a2a_optimize_placement(int32_t n, int32_t n_edges, const int32_t* edge_uv,
                            const int64_t* edge_bytes, int32_t n_gpus, int32_t iters,
                            uint64_t seed, int32_t* placement);
 
+/* Host audit: every piece / unit of every GPU (for `num_ctas` CTAs and the
+ * selected schedule) reads inside its source buffer on the executing GPU and
+ * writes inside its destination buffer (the address-math part of memcheck). */
+int a2a_plan_check_bounds(a2a_plan* plan, int32_t num_ctas);
 /* Static CTA split, before bind: each step's items are cut into equal-cost CTA
  * ranges where a byte bound for another GPU costs `remote_weight` (1..64,
  * default 1) and a local byte 1. */

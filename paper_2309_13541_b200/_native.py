@@ -91,6 +91,7 @@ def _load():
         "a2a_plan_set_sync_mode": ([P, C.c_int32], C.c_int),
         "a2a_optimize_placement": ([C.c_int32, C.c_int32, P, P, C.c_int32, C.c_int32,
                                     C.c_uint64, P], C.c_int),
+        "a2a_plan_check_bounds": ([P, C.c_int32], C.c_int),
         "a2a_plan_set_split": ([P, C.c_int32], C.c_int),
         "a2a_plan_set_schedule": ([P, C.c_int32, C.c_int64], C.c_int),
         "a2a_plan_dyn_stats": ([P, C.c_int32, C.c_int32, C.POINTER(C.c_int64),

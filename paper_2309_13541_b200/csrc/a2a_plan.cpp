@@ -1194,6 +1194,48 @@ int a2a_plan_prepare(a2a_plan* plan, int32_t num_ctas) {
   }
 }
 
+// Host audit of every device copy range (what memcheck would catch in the
+// address math): each piece / unit reads inside its source buffer and writes
+// inside its destination buffer on the owning GPU.
+int a2a_plan_check_bounds(a2a_plan* plan, int32_t num_ctas) {
+  if (!plan) return fail(A2A_ERR_INVALID, "null plan");
+  Plan& P = plan->p;
+  const int G = P.G;
+  int rc = P.sched_mode >= 1 ? build_dyn(P, num_ctas, P.dyn_unit_bytes) : build_sync(P, num_ctas);
+  if (rc) return rc;
+  auto size_of = [&](int g, int loc) -> int64_t {
+    if (loc == loc_send()) return P.info[g].send_bytes;
+    if (loc >= 1 && loc < 1 + G) return P.info[loc - 1].recv_bytes;
+    if (loc >= 1 + G && loc < 1 + 2 * G) return P.info[loc - 1 - G].scratch_bytes;
+    return -1;
+  };
+  auto check = [&](int g, int sl, int64_t so, int dl, int64_t dof, int64_t n) -> bool {
+    const int64_t ss = size_of(g, sl), ds = size_of(g, dl);
+    return n > 0 && ss >= 0 && ds >= 0 && so >= 0 && dof >= 0 && so + n <= ss && dof + n <= ds;
+  };
+  char buf[200];
+  for (int g = 0; g < G; ++g) {
+    if (P.sched_mode >= 1) {
+      for (const DevUnit& u : P.dyn.units[g])
+        if (!check(g, u.src_loc, u.src_off, u.dst_loc, u.dst_off, u.nbytes) ||
+            !(u.src_loc == loc_send() || u.src_loc == loc_recv(g) || u.src_loc == loc_scratch(g, G))) {
+          snprintf(buf, sizeof buf, "gpu %d: unit out of bounds (src %d+%lld, dst %d+%lld, %d B)", g,
+                   u.src_loc, (long long)u.src_off, u.dst_loc, (long long)u.dst_off, u.nbytes);
+          return fail(A2A_ERR_INVALID, buf);
+        }
+    } else {
+      for (const DevPiece& q : P.sync.pieces[g])
+        if (!check(g, q.src_loc, q.src_off, q.dst_loc, q.dst_off, q.nbytes) ||
+            !(q.src_loc == loc_send() || q.src_loc == loc_recv(g) || q.src_loc == loc_scratch(g, G))) {
+          snprintf(buf, sizeof buf, "gpu %d: piece out of bounds (src %d+%lld, dst %d+%lld, %d B)", g,
+                   q.src_loc, (long long)q.src_off, q.dst_loc, (long long)q.dst_off, q.nbytes);
+          return fail(A2A_ERR_INVALID, buf);
+        }
+    }
+  }
+  return A2A_OK;
+}
+
 int a2a_plan_set_split(a2a_plan* plan, int32_t remote_weight) {
   if (!plan || remote_weight < 1 || remote_weight > 64) return fail(A2A_ERR_INVALID, "bad remote weight");
   if (plan->p.bound) return fail(A2A_ERR_STATE, "set the CTA split before a2a_plan_bind");

@@ -204,6 +204,11 @@ class Plan:
         self._ck(N.lib.a2a_plan_prepare(self._h, int(num_ctas)), "a2a_plan_prepare")
         return self
 
+    def check_bounds(self, num_ctas: int = 148):
+        """Host audit of every device copy range against its buffer (raises)."""
+        self._ck(N.lib.a2a_plan_check_bounds(self._h, int(num_ctas)), "a2a_plan_check_bounds")
+        return True
+
     def set_split(self, remote_weight: int):
         """Before bind: cost weight of an NVLink byte in the static CTA split."""
         self._ck(N.lib.a2a_plan_set_split(self._h, int(remote_weight)), "a2a_plan_set_split")

@@ -1,0 +1,34 @@
+"""Host bounds audit of every device copy range (compute-sanitizer is closed on
+this GPU pool; this is its address-math half): all artifacts, 1/2/4/8 GPUs,
+static and dynamic schedules, scratch reuse on/off, odd shard sizes."""
+from __future__ import annotations
+
+import pytest
+
+from paper_2309_13541_b200.artifacts import list_artifacts
+from paper_2309_13541_b200.executor import Plan
+
+NAMES = [n for n in list_artifacts() if not n.startswith("gk256")]
+
+
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+@pytest.mark.parametrize("sched", ["static", "cp", "mix"])
+@pytest.mark.parametrize("reuse", [False, True])
+def test_every_copy_range_in_bounds(name, G, sched, reuse, artifacts):
+    a = artifacts(name)
+    if G > a.g.n:
+        pytest.skip("more GPUs than nodes")
+    for m in (1, 1000 + 7, 65536):
+        with Plan(a.g, a.sched, m=m, n_gpus=G, reuse_scratch=reuse, placement="optimized") as p:
+            p.set_schedule(sched, 0 if sched == "static" else 4096)
+            assert p.check_bounds(37)
+
+
+def test_gk256_in_bounds(artifacts):
+    if "gk256_4" not in list_artifacts():
+        pytest.skip("artifact missing")
+    from paper_2309_13541_b200.artifacts import load_artifact
+    a = load_artifact("gk256_4", native=True, verify=False)
+    with Plan(a.g, a.sched, m=4096 + 64, n_gpus=8, reuse_scratch=True) as p:
+        assert p.check_bounds(148)
