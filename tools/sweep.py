@@ -42,6 +42,7 @@ def main(argv=None):
     ap.add_argument("--mem-limit-gib", type=float, default=150.0)
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--placement", default="optimized", choices=["optimized", "contiguous"])
+    ap.add_argument("--num-ctas", type=int, default=0)
     ap.add_argument("--schedule", default=None,
                     help="static | dynamic[:bytes] | auto; default: $A2A_SCHED or static")
     a = ap.parse_args(argv)
@@ -72,9 +73,11 @@ def main(argv=None):
                 sched = a.schedule or os.environ.get("A2A_SCHED") or "static"
                 tune = None
                 if sched == "auto":
-                    sched, tune = bench.autotune_schedule(ctx, art, m, placement=a.placement)
+                    sched, tune = bench.autotune_schedule(ctx, art, m, placement=a.placement,
+                                                          num_ctas=a.num_ctas)
                 r = bench.measure(ctx, art, m, a.steps, a.warmup, nccl=not a.no_nccl,
-                                  e2e=False, clocks=True, placement=a.placement, schedule=sched)
+                                  e2e=False, clocks=True, placement=a.placement, schedule=sched,
+                                  num_ctas=a.num_ctas)
                 rec["schedule"] = sched
                 rec["schedule_autotune_ms"] = tune
                 rec.update({
@@ -88,7 +91,7 @@ def main(argv=None):
                     "clocks": r["clocks"], "sync_flags": r["sync"],
                     "kernel_timeline": r["kernel_timeline"],
                     "egress_max_bytes": r["egress_max"], "scratch_bytes": r["scratch_bytes"],
-                    "placement": a.placement, "l2": r["l2"],
+                    "placement": a.placement, "l2": r["l2"], "num_ctas": r["num_ctas"],
                     "wall_s": round(time.time() - t0, 1)})
         if ctx.rank == 0:
             line = json.dumps(rec)
