@@ -59,13 +59,19 @@ def main():
     torch.cuda.empty_cache()
 
     g = Digraph.from_edges(2, [(0, 1, 1.0), (1, 0, 1.0)])
-    sched = ChunkedSchedule(n=2, nsteps=1, chunk_bytes=1.0, Q=1, mode="ts",
-                            instructions=[Instruction(0, 0, 1, 0, 1, 0, 1),
-                                          Instruction(0, 1, 0, 1, 0, 0, 1)])
     m = 512 << 20
-    for engine in ("tma", "lsu"):
-        plans = [Plan(g, sched, m=m, n_gpus=2, copy_self=False).set_engine(engine).bind(r, device=r)
-                 for r in range(2)]
+    both_ways = [Instruction(0, 0, 1, 0, 1, 0, 1), Instruction(0, 1, 0, 1, 0, 0, 1)]
+    # one-way: shard (1,0) travels 1 -> 0 at step 0 as before, shard (0,1) only at step 1
+    # (the timed step-0 traffic of the first all-to-all is then one direction at a time)
+    variants = [("tma", (0, 0), "bidir"), ("lsu", (0, 0), "bidir"), ("tma", (65536, 3), "bidir"),
+                ("tma", (16384, 12), "bidir"), ("tma", (0, 0), "oneway")]
+    for engine, ring, mode in variants:
+        ins = both_ways if mode == "bidir" else [Instruction(0, 0, 1, 0, 1, 0, 1),
+                                                 Instruction(1, 1, 0, 1, 0, 0, 1)]
+        sched = ChunkedSchedule(n=2, nsteps=1 if mode == "bidir" else 2, chunk_bytes=1.0, Q=1,
+                                mode="ts", instructions=ins)
+        plans = [Plan(g, sched, m=m, n_gpus=2, copy_self=False).set_engine(engine, *ring)
+                 .bind(r, device=r) for r in range(2)]
         ptrs = [p.arena_ptr() for p in plans]
         for p in plans:
             p.import_pointers(ptrs)
@@ -80,8 +86,10 @@ def main():
         for p in plans:
             p.sync()
         ok = all(torch.equal(recvs[r][0, 1 - r].cpu(), sends[1 - r][0, r].cpu()) for r in range(2))
-        out[f"a2a_exec_{engine}_bidir_per_direction_gbs"] = round(m / t / 1e9, 1)
-        out[f"a2a_exec_{engine}_ok"] = ok
+        tag = f"a2a_exec_{engine}{'' if ring == (0, 0) else f'_{ring[0]}x{ring[1]}'}_{mode}"
+        # bidir: m bytes each way in t; oneway: 2 sequential one-way transfers of m in t
+        out[tag + "_gbs_per_direction"] = round((m if mode == "bidir" else 2 * m) / t / 1e9, 1)
+        out[tag + "_ok"] = ok
         for p in plans:
             p.close()
         del sends, recvs
