@@ -236,20 +236,36 @@ class Ctx:
             self.pg.destroy_process_group()
 
 
+LL_MAX_SHARD = 1 << 20   # autotune tries the LL transport up to this shard size
+
+
+def make_plan(art, m, G, placement, schedule):
+    """Plan for an execution-schedule spec: "static", "<dyn mode>:<unit bytes>",
+    or "ll" (static programs + the LL cross-GPU transport)."""
+    from paper_2309_13541_b200.executor import Plan
+    if schedule == "ll":
+        return Plan(art.g, art.sched, m=m, n_gpus=G, placement=placement, protocol="ll")
+    plan = Plan(art.g, art.sched, m=m, n_gpus=G, placement=placement)
+    if schedule:
+        mode, *ub = schedule.split(":")
+        plan.set_schedule(mode, *(int(x) for x in ub))
+    return plan
+
+
 def autotune_schedule(ctx, art, m, placement="optimized", num_ctas=0, trials=5,
-                      candidates=("static", "mix:1048576", "cp:1048576")):
+                      candidates=None):
     """Time a few executes of each execution schedule (same placement, same
     buffers) and return (best, {candidate: ms}); identical on every rank."""
     import torch
 
-    from paper_2309_13541_b200.dist import connect, local_nodes
-    from paper_2309_13541_b200.executor import Plan
+    from paper_2309_13541_b200.dist import connect
     G, dev = ctx.world, ctx.dev
+    if candidates is None:
+        candidates = ("static", "mix:1048576", "cp:1048576") + (
+            ("ll",) if G > 1 and m <= LL_MAX_SHARD else ())
     times = {}
     for cand in candidates:
-        mode, *ub = cand.split(":")
-        plan = Plan(art.g, art.sched, m=m, n_gpus=G, placement=placement)
-        plan.set_schedule(mode, *(int(x) for x in ub))
+        plan = make_plan(art, m, G, placement, cand)
         plan.bind(ctx.rank, device=ctx.local, num_ctas=num_ctas)
         if G > 1:
             connect(plan)
@@ -293,15 +309,11 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     import torch
 
     from paper_2309_13541_b200.dist import connect, local_nodes
-    from paper_2309_13541_b200.executor import Plan
     from paper_2309_13541_b200.graphs import distance_sum
 
     G, rank, dev = ctx.world, ctx.rank, ctx.dev
     n = art.g.n
-    plan = Plan(art.g, art.sched, m=m, n_gpus=G, placement=placement)
-    if schedule:
-        mode, *ub = schedule.split(":")
-        plan.set_schedule(mode, *(int(x) for x in ub))
+    plan = make_plan(art, m, G, placement, schedule)
     if e2e and G > 1:
         plan.set_recv_buffers(2)          # double-buffered recv for the pipelined e2e
     plan.bind(rank, device=ctx.local, num_ctas=num_ctas)

@@ -50,6 +50,15 @@ typedef struct {
 #define A2A_COPY_SELF 1  /* also copy the self shard send[v][v] -> recv[v][v] */
 #define A2A_INTERLEAVE 2 /* split items (split_bytes) and interleave destination GPUs */
 #define A2A_REUSE_SCRATCH 4 /* liveness-based scratch reuse (+ WAR/WAW dependencies) */
+/* Low-latency transport for cross-GPU hops (static schedule only; not with
+ * A2A_INTERLEAVE or A2A_REUSE_SCRATCH): every byte bound for another GPU is
+ * stored as 16-byte lines {4 data bytes, epoch, 4 data bytes, epoch} into an
+ * epoch-parity double-buffered landing region of the destination GPU, where
+ * that GPU's own CTAs poll the lines and write the bytes to their scratch /
+ * recv destination.  No system-scope fence or flag on the path, all step flags
+ * stay GPU-local, the entry barrier lags one all-to-all, and recv may be any
+ * device buffer.  Twice the NVLink bytes: for small shards. */
+#define A2A_PROTO_LL 8
 
 typedef struct {
   int32_t n_nodes;         /* Digraph.n (must equal ChunkedSchedule.n)      */
@@ -63,7 +72,7 @@ typedef struct {
   int64_t n_ops;
   const int32_t* node_gpu; /* [n_nodes] virtual node -> GPU rank; NULL = all on 0 */
   int32_t n_gpus;          /* >= 1                                           */
-  int32_t flags;           /* A2A_COPY_SELF | A2A_INTERLEAVE                 */
+  int32_t flags;           /* A2A_COPY_SELF | A2A_INTERLEAVE | A2A_REUSE_SCRATCH | A2A_PROTO_LL */
   int64_t split_bytes;     /* piece size for A2A_INTERLEAVE (0 = 256 KiB)    */
 } a2a_schedule_desc;
 
@@ -75,7 +84,7 @@ typedef struct {
   int32_t first_node;      /* smallest node id on this GPU (-1 if none)      */
   int64_t send_bytes;      /* V_g * N * m: send buffer, [V_g][N][m] u8        */
   int64_t recv_bytes;      /* V_g * N * m: recv buffer, recv[v][s] = shard (s,v) */
-  int64_t scratch_bytes;   /* forwarding scratch resident on this GPU        */
+  int64_t scratch_bytes;   /* forwarding scratch (+ LL landing region) here  */
   int64_t n_items;         /* copy items this GPU executes (all steps)       */
   int64_t hop_bytes;       /* bytes this GPU copies over schedule links      */
   int64_t egress_bytes;    /* of which to other GPUs (NVLink)                */
@@ -173,7 +182,8 @@ int a2a_plan_import_handles(a2a_plan* plan, const void* handles);
 int a2a_plan_arena(const a2a_plan* plan, void** out_ptr);
 int a2a_plan_import_pointers(a2a_plan* plan, void* const* arenas);
 /* pointer to this rank's arena recv buffer ([V_g][N][m]); with n_gpus > 1
- * peers store into it directly, so execute must be given this buffer */
+ * peers store into it directly, so execute must be given this buffer (any
+ * device buffer with A2A_PROTO_LL, where only local CTAs write recv) */
 int a2a_plan_recv_buffer(const a2a_plan* plan, void** out_ptr);
 /* before bind: number of arena recv buffers (1..4, default 1) so consecutive
  * all-to-alls can alternate buffers (overlap D2H of one with the next); every

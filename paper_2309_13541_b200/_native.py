@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_a2a_exec.s
 A2A_COPY_SELF = 1
 A2A_INTERLEAVE = 2
 A2A_REUSE_SCRATCH = 4
+A2A_PROTO_LL = 8
 A2A_EXEC_COUNT_LINKS = 1
 STATUS = {0: "OK", 1: "INVALID", 2: "EVAL", 3: "CUDA", 4: "TIMEOUT", 5: "STATE", 6: "NOMEM"}
 

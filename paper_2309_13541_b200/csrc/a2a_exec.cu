@@ -41,7 +41,7 @@
 namespace a2a {
 
 struct KParams {
-  char* base[1 + 2 * A2A_MAX_GPUS];        // send | recv[G] | scratch[G]
+  char* base[1 + 3 * A2A_MAX_GPUS];        // send | recv[G] | scratch[G] | LL landing[G]
   uint32_t* step_flags[A2A_MAX_GPUS];      // per GPU: [T'][G][nC] u32, slot (t, producer gpu, cta)
   uint32_t* entry_flags[A2A_MAX_GPUS];     // per GPU: [G] u32
   const DevPiece* pieces;                  // this GPU's pieces, ordered by (cta, step)
@@ -54,6 +54,7 @@ struct KParams {
   int64_t timeout_ns;
   uint32_t epoch;
   int32_t G, rank, nC, T, E, count_links;
+  int32_t ll;                              // A2A_PROTO_LL: cross-GPU bytes as LL lines
   int32_t tma_chunk, tma_stages;           // TMA engine: bytes per bulk copy, ring depth
   int32_t sync_mode;                       // bit0: acq_rel (not sc) publish fence; bit1: no
                                            // explicit publish fence; bit2: force .sys at G=1
@@ -161,6 +162,65 @@ __device__ __forceinline__ void cta_copy(char* __restrict__ dst, const char* __r
   if (tid < tail) dst[nv * 16 + tid] = src[nv * 16 + tid];
 }
 
+// ---- LL transport (A2A_PROTO_LL) ----
+// A 16-byte line {payload[0..4), epoch, payload[4..8), epoch}: each 8-byte half
+// is stored and loaded as one unit, so a reader that sees the epoch in both
+// halves holds the payload -- no fence, no separate flag (the LL protocol).
+// Line k of a piece carries payload bytes [8k, 8k+8).
+__device__ __forceinline__ void ll_send(uint4* __restrict__ dst, const char* __restrict__ src,
+                                        int64_t n, uint32_t epoch) {
+  const int64_t L = (n + 7) >> 3;
+  const bool al = ((uintptr_t)src & 7) == 0;
+  for (int64_t k = threadIdx.x; k < L; k += blockDim.x) {
+    const int64_t b = k << 3;
+    uint32_t lo = 0, hi = 0;
+    if (al && b + 8 <= n) {
+      const uint2 v = *reinterpret_cast<const uint2*>(src + b);
+      lo = v.x;
+      hi = v.y;
+    } else {
+      for (int j = 0; j < 8 && b + j < n; ++j) {
+        const uint32_t x = (uint8_t)src[b + j];
+        if (j < 4) lo |= x << (8 * j);
+        else hi |= x << (8 * (j - 4));
+      }
+    }
+    asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst + k), "r"(lo),
+                 "r"(epoch), "r"(hi), "r"(epoch)
+                 : "memory");
+  }
+}
+// Poll this thread's lines until both halves carry `epoch`, then store the
+// payload into the local destination.  False on timeout / peer error.
+__device__ __forceinline__ bool ll_recv(char* __restrict__ dst, const uint4* src, int64_t n,
+                                        uint32_t epoch, int64_t timeout_ns, int32_t* err) {
+  const int64_t L = (n + 7) >> 3;
+  const bool al = ((uintptr_t)dst & 7) == 0;
+  for (int64_t k = threadIdx.x; k < L; k += blockDim.x) {
+    uint32_t a, f0, b, f1, spins = 0;
+    uint64_t t0 = 0;
+    for (;;) {
+      asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(a), "=r"(f0), "=r"(b), "=r"(f1)
+                   : "l"(src + k)
+                   : "memory");
+      if (f0 == epoch && f1 == epoch) break;
+      if ((++spins & 1023) == 0) {
+        const uint64_t now = globaltimer();
+        if (t0 == 0) t0 = now;
+        if ((int64_t)(now - t0) > timeout_ns || *(volatile int32_t*)err != 0) return false;
+      }
+    }
+    const int64_t bb = k << 3;
+    if (al && bb + 8 <= n) {
+      *reinterpret_cast<uint2*>(dst + bb) = make_uint2(a, b);
+    } else {
+      for (int j = 0; j < 8 && bb + j < n; ++j) dst[bb + j] = (char)(((j < 4 ? a : b) >> (8 * (j & 3))) & 0xff);
+    }
+  }
+  return true;
+}
+
 // ---- TMA bulk-copy engine helpers (cp.async.bulk + mbarrier, SASS UBLKCP) ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -252,7 +312,7 @@ struct BodyCursor {
   __device__ bool next(const KParams& p, uint32_t ch, const char** src, char** dst, uint32_t* len) {
     while (k < n) {
       const DevPiece& q = pc[k];
-      if (q.nbytes <= kSmallPiece) { ++k; off = 0; continue; }
+      if (q.nbytes <= kSmallPiece || q.kind != kCopy) { ++k; off = 0; continue; }
       const char* s0 = p.base[q.src_loc] + q.src_off;
       char* d0 = p.base[q.dst_loc] + q.dst_off;
       const int64_t L = q.nbytes;
@@ -299,11 +359,37 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
   for (int i = tid; i < p.T; i += kThreads) s_prog[i] = p.prog[(int64_t)c * p.T + i];
   __syncthreads();
   const uint32_t* my_flags = p.step_flags[p.rank];
-  // one GPU: every producer and consumer is on this GPU -> .gpu scope suffices
-  const bool sys = p.G > 1 || (p.sync_mode & 4);
+  // one GPU (or LL: every step flag is GPU-local) -> .gpu scope suffices
+  const bool sys = (p.G > 1 && !p.ll) || (p.sync_mode & 4);
 
+  // ---- LL entry: announce the epoch; a peer's landing region of this parity
+  //      was last read two all-to-alls ago, so it is free once that peer has
+  //      started the previous one (its entry flag >= epoch - 1)
+  if (p.G > 1 && p.ll) {
+    if (c == 0 && tid < p.G && tid != p.rank) st_relaxed(p.entry_flags[tid] + p.rank, p.epoch, true);
+    if (warp == 0) {
+      const int lane = tid & 31;
+      bool ok = true;
+      if (lane < p.G && lane != p.rank) {
+        const uint32_t* f = p.entry_flags[p.rank] + lane;
+        uint64_t t0 = globaltimer();
+        uint32_t spins = 0;
+        while ((int32_t)(ld_relaxed(f, true) - (p.epoch - 1)) < 0) {
+          if ((++spins & 255) == 0 && ((int64_t)(globaltimer() - t0) > p.timeout_ns ||
+                                       *(volatile int32_t*)p.err != 0)) {
+            ok = false;
+            break;
+          }
+        }
+      }
+      ok = __all_sync(0xffffffffu, ok);
+      if (!ok && lane == 0) { atomicCAS(p.err, 0, (int32_t)A2A_ERR_TIMEOUT); s_abort = 1; }
+    }
+    __syncthreads();
+    if (s_abort) return;
+  }
   // ---- entry barrier: announce epoch to every peer, then wait for theirs
-  if (p.G > 1) {
+  if (p.G > 1 && !p.ll) {
     if (c == 0 && tid < p.G && tid != p.rank) st_release_sys(p.entry_flags[tid] + p.rank, p.epoch);
     if (warp == 0) {
       const int lane = tid & 31;
@@ -353,26 +439,34 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
       }
       __syncthreads();
       if (s_abort) return;
-      if (kEngine == 0) {
-        for (int i = 0; i < n; ++i) {
-          const DevPiece& q = s_pc[i];
+      // LL pieces (any size) and small copies: all threads, in program order
+      // (a CTA's LL sends precede its LL receives)
+      for (int i = 0; i < n; ++i) {
+        const DevPiece& q = s_pc[i];
+        if (q.kind == kLLSend) {
+          ll_send(reinterpret_cast<uint4*>(p.base[q.dst_loc] + q.dst_off), p.base[q.src_loc] + q.src_off,
+                  q.nbytes, p.epoch);
+        } else if (q.kind == kLLRecv) {
+          if (!ll_recv(p.base[q.dst_loc] + q.dst_off,
+                       reinterpret_cast<const uint4*>(p.base[q.src_loc] + q.src_off), q.nbytes, p.epoch,
+                       p.timeout_ns, p.err)) {
+            atomicCAS(p.err, 0, (int32_t)A2A_ERR_TIMEOUT);
+            s_abort = 1;
+          }
+        } else if (kEngine == 0 || q.nbytes <= kSmallPiece) {
           cta_copy<4>(p.base[q.dst_loc] + q.dst_off, p.base[q.src_loc] + q.src_off, q.nbytes);
         }
-      } else {
-        for (int i = 0; i < n; ++i) {  // small pieces: all threads, 128-bit LSU
-          const DevPiece& q = s_pc[i];
-          if (q.nbytes <= kSmallPiece)
-            cta_copy<4>(p.base[q.dst_loc] + q.dst_off, p.base[q.src_loc] + q.src_off, q.nbytes);
-        }
+      }
+      if (kEngine == 1) {
         bool any_big = false;
-        for (int i = 0; i < n && !any_big; ++i) any_big = s_pc[i].nbytes > kSmallPiece;
+        for (int i = 0; i < n && !any_big; ++i) any_big = s_pc[i].nbytes > kSmallPiece && s_pc[i].kind == kCopy;
         if (!any_big) {
           // nothing for the TMA ring in this batch
         } else if (tid != 0) {  // threads 1..: heads, tails, misaligned big pieces
           const int nt = kThreads - 1, me = tid - 1;
           for (int i = 0; i < n; ++i) {
             const DevPiece& q = s_pc[i];
-            if (q.nbytes <= kSmallPiece) continue;
+            if (q.nbytes <= kSmallPiece || q.kind != kCopy) continue;
             const char* s0 = p.base[q.src_loc] + q.src_off;
             char* d0 = p.base[q.dst_loc] + q.dst_off;
             const int64_t len = q.nbytes;
@@ -433,6 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
             atomicAdd(p.counters + (int64_t)t * p.E + s_pc[i].edge, (unsigned long long)s_pc[i].nbytes);
       __syncthreads();
     }
+    if (s_abort) return;
     if (tid == 0) {
       const int64_t slot = ((int64_t)t * p.G + p.rank) * p.nC + c;
       if (p.sync_mode & 32) {
@@ -463,7 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
     }
   }
   // ---- exit: all incoming stores of every step have landed (multi-GPU)
-  if (c == 0 && p.G > 1) {
+  if (c == 0 && p.G > 1 && !p.ll) {
     bool ok = true;
     for (int32_t i = tid; i < p.n_exit && ok; i += kThreads) {
       const uint32_t* f = my_flags + p.exit_idx[i];
@@ -838,6 +933,8 @@ static int bind_plan(Plan& P, int gpu, int dev, int nC) {
     return fail(A2A_ERR_NOMEM, buf);
   }
   CK(cudaMemset(P.arena, 0, (size_t)P.flags_bytes));
+  if (P.ll && P.ll_half[gpu] > 0)  // LL lines: epoch 0 never matches
+    CK(cudaMemset((char*)P.arena + P.scratch_off[gpu] + P.ll_off[gpu], 0, (size_t)(2 * P.ll_half[gpu])));
   if (P.sched_mode >= 1) {
     if ((rc = upload(&P.d_items, Dy.units[gpu])) != A2A_OK) return rc;
     if ((rc = upload(&P.d_wait_idx, Dy.wait_idx[gpu])) != A2A_OK) return rc;
@@ -1013,7 +1110,7 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
   char* own_recv = (char*)P.arena + P.recv_off[P.rank];
   if (!recv) recv = own_recv;
   int32_t ridx = 0;
-  if (P.G > 1) {
+  if (P.G > 1 && !P.ll) {
     const int64_t st = recv_stride(P, P.rank);
     ridx = -1;
     for (int i = 0; i < P.n_recv; ++i)
@@ -1026,11 +1123,15 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
   KParams kp;
   std::memset(&kp, 0, sizeof kp);
   kp.base[loc_send()] = (char*)send;
+  uint32_t epoch = P.epoch + 1;
+  if (epoch == 0) epoch = 1;  // 0 is the "never written" value
   for (int g = 0; g < P.G; ++g) {
     char* ar = (char*)P.peer_arena[g];
     kp.base[loc_recv(g)] =
         (g == P.rank) ? (char*)recv : ar + P.recv_off[g] + (int64_t)ridx * recv_stride(P, g);
     kp.base[loc_scratch(g, P.G)] = ar + P.scratch_off[g];
+    if (P.ll)  // landing region of this epoch's parity
+      kp.base[loc_ll(g, P.G)] = ar + P.scratch_off[g] + P.ll_off[g] + (int64_t)(epoch & 1) * P.ll_half[g];
     kp.entry_flags[g] = (uint32_t*)(ar + entry_flags_off());
     kp.step_flags[g] = (uint32_t*)(ar + step_flags_off());
   }
@@ -1057,8 +1158,8 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
   kp.counters = (unsigned long long*)P.d_counters;
   kp.err = P.d_err;
   kp.timeout_ns = P.timeout_ns;
-  kp.epoch = ++P.epoch;
-  if (kp.epoch == 0) kp.epoch = ++P.epoch;  // 0 is the "never written" value
+  kp.epoch = P.epoch = epoch;
+  kp.ll = P.ll ? 1 : 0;
   kp.G = P.G;
   kp.rank = P.rank;
   kp.nC = P.nC;

@@ -19,10 +19,17 @@
 namespace a2a {
 
 // Buffer classes a copy item reads from / writes to.  The pointer table of a
-// launch is [send(local) | recv(gpu 0..G-1) | scratch(gpu 0..G-1)].
+// launch is [send(local) | recv(gpu 0..G-1) | scratch(gpu 0..G-1) |
+// LL landing region of this execute's epoch parity (gpu 0..G-1)].
 inline int loc_send() { return 0; }
 inline int loc_recv(int gpu) { return 1 + gpu; }
 inline int loc_scratch(int gpu, int G) { return 1 + G + gpu; }
+inline int loc_ll(int gpu, int G) { return 1 + 2 * G + gpu; }
+
+// piece kinds (A2A_PROTO_LL): plain copy, LL line store to a peer's landing
+// region (offsets: payload byte x of the item <-> line x/8 at 16*(x/8)), LL
+// line poll + store of the payload into the local destination
+enum : int32_t { kCopy = 0, kLLSend = 1, kLLRecv = 2 };
 
 // One contiguous byte copy of one hop-op (or self-shard copy), 48 bytes.
 struct DevItem {
@@ -33,7 +40,8 @@ struct DevItem {
   int32_t src_loc;
   int32_t dst_loc;
   int32_t edge;      // schedule edge id (-1: self-shard copy, not a link)
-  int32_t dst_gpu;
+  int16_t dst_gpu;
+  int16_t kind;      // kCopy / kLLSend / kLLRecv
 };
 static_assert(sizeof(DevItem) == 48, "DevItem layout");
 
@@ -53,7 +61,7 @@ struct DevPiece {
   int32_t nbytes;
   int32_t edge;
   int16_t src_loc, dst_loc;
-  int32_t pad;
+  int32_t kind;      // kCopy / kLLSend / kLLRecv
 };
 static_assert(sizeof(DevPiece) == 32, "DevPiece layout");
 
@@ -119,6 +127,8 @@ struct Plan {
   std::vector<int32_t> node_gpu, local_idx;
   int32_t T_exec = 1;                           // max(T, 1): self copies need a step
   bool reuse = false;                           // scratch liveness reuse (A2A_REUSE_SCRATCH)
+  bool ll = false;                              // low-latency cross-GPU transport (A2A_PROTO_LL)
+  std::vector<int64_t> ll_off, ll_half;         // per gpu: landing region in scratch, bytes per parity
 
   // ---- layout / tables (host)
   std::vector<a2a_gpu_info> info;               // per gpu

@@ -99,9 +99,12 @@ static int build_plan(Plan& P, const a2a_schedule_desc* D) {
   if (D->n_ops < 0 || (D->n_ops > 0 && !D->ops)) return fail(A2A_ERR_INVALID, "bad op list");
   if (D->n_gpus < 1 || D->n_gpus > A2A_MAX_GPUS)
     return fail(A2A_ERR_INVALID, "n_gpus must be in [1, 8]");
+  if ((D->flags & A2A_PROTO_LL) && (D->flags & (A2A_INTERLEAVE | A2A_REUSE_SCRATCH)))
+    return fail(A2A_ERR_INVALID, "A2A_PROTO_LL cannot be combined with A2A_INTERLEAVE or A2A_REUSE_SCRATCH");
   const int n = D->n_nodes, T = D->n_steps, E = D->n_edges, G = D->n_gpus;
   const int64_t Q = D->q, m = D->m_bytes;
   P.n = n; P.T = T; P.Q = (int32_t)Q; P.E = E; P.G = G; P.m = m; P.flags = D->flags;
+  P.ll = (D->flags & A2A_PROTO_LL) && G > 1;
   P.T_exec = std::max(T, 1);
   P.edge_uv.assign(D->edge_uv, D->edge_uv + 2 * (size_t)E);
   P.cap.resize(E, 1.0);
@@ -340,6 +343,12 @@ static int build_plan(Plan& P, const a2a_schedule_desc* D) {
   // ---- copy items per GPU per step
   const int TE = P.T_exec;
   P.tables.assign(G, GpuTables{});
+  // A2A_PROTO_LL: each cross-GPU item gets a landing slot of 16 B per 8 payload
+  // bytes in the destination GPU's LL region (after its forwarding scratch)
+  P.ll_off.assign(G, 0);
+  P.ll_half.assign(G, 0);
+  std::vector<int64_t> ll_cursor(G, 0);
+  for (int g = 0; g < G; ++g) P.ll_off[g] = P.info[g].scratch_bytes;
   P.link_bytes.assign((size_t)T * E, 0);
   std::vector<std::vector<std::vector<DevItem>>> per(G, std::vector<std::vector<DevItem>>(TE));
   for (int t = 0; t < T; ++t) {
@@ -374,6 +383,20 @@ static int build_plan(Plan& P, const a2a_schedule_desc* D) {
         if (!slot_addr(o.dst, o.s, o.d, o.c0, lo, &it.dst_off))
           return fail(A2A_ERR_INVALID, "internal: destination chunk has no scratch slot");
       }
+      if (P.ll && h != g) {
+        // sender: payload -> LL lines on h; receiver (h, same step): lines -> destination
+        DevItem rc = it;
+        const int64_t slot = ll_cursor[h];
+        ll_cursor[h] += 2 * ((it.nbytes + 7) & ~(int64_t)7);
+        it.dst_loc = loc_ll(h, G);
+        it.dst_off = slot;
+        it.kind = kLLSend;
+        rc.src_loc = loc_ll(h, G);
+        rc.src_off = slot;
+        rc.edge = -1;
+        rc.kind = kLLRecv;
+        per[h][t].push_back(rc);
+      }
       per[g][t].push_back(it);
       auto& Ig = P.info[g];
       Ig.hop_bytes += it.nbytes;
@@ -399,8 +422,13 @@ static int build_plan(Plan& P, const a2a_schedule_desc* D) {
       P.info[g].local_bytes += m;
     }
   }
+  for (int g = 0; g < G; ++g) {
+    P.ll_half[g] = (ll_cursor[g] + 4095) & ~(int64_t)4095;
+    P.info[g].scratch_bytes += 2 * P.ll_half[g];   // epoch parity 0 | 1
+  }
   // Order each (gpu, step) list.  Default: grouped by destination GPU
-  // (stable), so CTAs cover few destinations each.  A2A_INTERLEAVE: items are
+  // (stable), so CTAs cover few destinations each; LL receive items last, so
+  // every CTA issues its step's sends before it polls (deadlock freedom).  A2A_INTERLEAVE: items are
   // split into <= split_bytes pieces (multiples of 64 B, alignment kept) and
   // the destination classes are merged in proportion to their byte totals, so
   // every CTA range drives every NVLink peer (and local HBM) at once.
@@ -413,7 +441,8 @@ static int build_plan(Plan& P, const a2a_schedule_desc* D) {
     for (int t = 0; t < TE; ++t) {
       auto& L = per[g][t];
       std::stable_sort(L.begin(), L.end(), [&](const DevItem& a, const DevItem& b) {
-        int ka = (a.dst_gpu - g + G) % G, kb = (b.dst_gpu - g + G) % G;
+        int ka = a.kind == kLLRecv ? G : (a.dst_gpu - g + G) % G;
+        int kb = b.kind == kLLRecv ? G : (b.dst_gpu - g + G) % G;
         return ka < kb;
       });
       if (interleave) {
@@ -480,6 +509,14 @@ struct Seg {
 // than it can push them over NVLink, so equal-byte ranges would leave the
 // NVLink CTAs finishing last.  Boundaries inside an item fall on 64-byte
 // multiples (the item end excepted), so every piece keeps src == dst (mod 64).
+// byte offsets of the piece starting at payload byte x of an item (LL landing
+// lines carry 8 payload bytes per 16 bytes)
+inline int64_t piece_src(const DevItem& it, int64_t x) {
+  return it.src_off + (it.kind == kLLRecv ? 2 * x : x);
+}
+inline int64_t piece_dst(const DevItem& it, int64_t x) {
+  return it.dst_off + (it.kind == kLLSend ? 2 * x : x);
+}
 template <typename F>
 void for_each_piece(const GpuTables& tb, int g, int t, int nC, int wr, F&& f) {
   const int64_t b0 = tb.step_begin[t], b1 = tb.step_begin[t + 1];
@@ -523,6 +560,7 @@ int build_sync(Plan& P, int nC) {
   for (int g = 0; g < G; ++g) {
     for (int t = 0; t < TE; ++t) {
       for_each_piece(P.tables[g], g, t, nC, P.remote_weight, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
+        if (it.kind == kLLSend) return;   // no flag: the receiver polls the lines
         S.dst_mask[g][(size_t)t * nC + c] |= 1u << it.dst_gpu;
         const int cls = (it.dst_loc == loc_recv(it.dst_gpu)) ? 0 : 1;
         segs[it.dst_gpu][cls].push_back(
@@ -601,7 +639,7 @@ int build_sync(Plan& P, int nC) {
     auto& per = per_all[h];
     for (int t = 0; t < TE; ++t) {
       for_each_piece(P.tables[h], h, t, nC, P.remote_weight, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
-        if (it.src_loc == loc_send()) return;
+        if (it.src_loc == loc_send() || it.kind == kLLRecv) return;
         const int cls = (it.src_loc == loc_recv(h)) ? 0 : 1;
         const int64_t a = it.src_off + x0, b = it.src_off + x1;
         const auto& v = segs[h][cls];
@@ -640,12 +678,13 @@ int build_sync(Plan& P, int nC) {
       for_each_piece(P.tables[g], g, t, nC, P.remote_weight, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
         for (int64_t x = x0; x < x1; x += (1LL << 30)) {
           DevPiece pc{};
-          pc.src_off = it.src_off + x;
-          pc.dst_off = it.dst_off + x;
+          pc.src_off = piece_src(it, x);
+          pc.dst_off = piece_dst(it, x);
           pc.nbytes = (int32_t)std::min<int64_t>(1LL << 30, x1 - x);
           pc.edge = it.edge;
           pc.src_loc = (int16_t)it.src_loc;
           pc.dst_loc = (int16_t)it.dst_loc;
+          pc.kind = it.kind;
           per_ct[c][t].push_back(pc);
         }
       });
@@ -670,33 +709,50 @@ int build_sync(Plan& P, int nC) {
 // Host emulation of the device protocol: CTAs of all GPUs run their step
 // ranges in a random interleaving constrained ONLY by the dependency lists;
 // memory is host memory.  Insufficient dependencies show up as wrong bytes.
+// A2A_PROTO_LL: a CTA runs its step's pieces in program order (one piece per
+// emulation event) and blocks at an LL receive until every line it polls
+// carries the epoch; lines are stored and decoded in the device format.
 static int emulate(Plan& P, int nC, uint8_t* const* send, uint8_t* const* recv, uint64_t seed) {
   int rc = build_sync(P, nC);
   if (rc) return rc;
   const int G = P.G, TE = P.T_exec;
-  std::vector<std::vector<uint8_t>> scratch(G);
-  for (int g = 0; g < G; ++g) scratch[g].assign((size_t)P.info[g].scratch_bytes + 64, 0);
+  const uint32_t kEpoch = 1;
+  std::vector<std::vector<uint8_t>> scratch(G), ll(G);
+  for (int g = 0; g < G; ++g) {
+    scratch[g].assign((size_t)P.info[g].scratch_bytes + 64, 0);
+    ll[g].assign((size_t)(P.ll ? P.ll_half[g] : 0) + 64, 0);
+  }
   // per-GPU flag arrays: a producer's flag is visible on GPU h only if its
   // destination mask has bit h (exactly what the kernel publishes)
   std::vector<std::vector<char>> flag(G, std::vector<char>((size_t)TE * G * nC, 0));
-  // per (g, c): list of (t, pieces) in step order
-  struct Piece { int32_t src_loc, dst_loc; int64_t src, dst, n; };
-  std::vector<std::vector<std::vector<std::vector<Piece>>>> work(
-      G, std::vector<std::vector<std::vector<Piece>>>(nC, std::vector<std::vector<Piece>>(TE)));
-  std::vector<std::vector<std::vector<char>>> has(G, std::vector<std::vector<char>>(nC, std::vector<char>(TE, 0)));
+  // per (g, c, t): pieces in program order
+  struct Piece { int32_t src_loc, dst_loc, kind; int64_t src, dst, n; };
+  using Work = std::vector<std::vector<std::vector<Piece>>>;
+  std::vector<Work> work(G, Work(nC, std::vector<std::vector<Piece>>(TE)));
   for (int g = 0; g < G; ++g)
     for (int t = 0; t < TE; ++t) {
       for_each_piece(P.tables[g], g, t, nC, P.remote_weight, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
-        work[g][c][t].push_back(Piece{it.src_loc, it.dst_loc, it.src_off + x0, it.dst_off + x0, x1 - x0});
-        has[g][c][t] = 1;
+        work[g][c][t].push_back(
+            Piece{it.src_loc, it.dst_loc, it.kind, piece_src(it, x0), piece_dst(it, x0), x1 - x0});
       });
     }
   auto base = [&](int g, int loc) -> uint8_t* {
     if (loc == loc_send()) return send[g];
     if (loc >= 1 && loc < 1 + G) return recv[loc - 1];
-    return scratch[loc - 1 - G].data();
+    if (loc < 1 + 2 * G) return scratch[loc - 1 - G].data();
+    return ll[loc - 1 - 2 * G].data();
   };
-  std::vector<std::vector<int>> next(G, std::vector<int>(nC, 0));
+  auto lines_ready = [&](int g, const Piece& pc) {
+    const uint8_t* L = base(g, pc.src_loc) + pc.src;
+    for (int64_t k = 0; k < (pc.n + 7) / 8; ++k) {
+      uint32_t f0, f1;
+      std::memcpy(&f0, L + 16 * k + 4, 4);
+      std::memcpy(&f1, L + 16 * k + 12, 4);
+      if (f0 != kEpoch || f1 != kEpoch) return false;
+    }
+    return true;
+  };
+  std::vector<std::vector<int>> next(G, std::vector<int>(nC, 0)), pos(G, std::vector<int>(nC, 0));
   uint64_t x = seed * 0x9E3779B97F4A7C15ULL + 1;
   auto rnd = [&]() { x ^= x << 13; x ^= x >> 7; x ^= x << 17; return x; };
   for (;;) {
@@ -705,24 +761,45 @@ static int emulate(Plan& P, int nC, uint8_t* const* send, uint8_t* const* recv, 
     for (int g = 0; g < G; ++g)
       for (int c = 0; c < nC; ++c) {
         int& t = next[g][c];
-        while (t < TE && !has[g][c][t]) ++t;
+        while (t < TE && work[g][c][t].empty()) ++t;
         if (t >= TE) continue;
         left = true;
-        const auto& off = P.sync.wait_off[g];
         bool ok = true;
-        for (int32_t i = off[(size_t)t * nC + c]; i < off[(size_t)t * nC + c + 1] && ok; ++i)
-          ok = flag[g][P.sync.wait_idx[g][i]];
+        if (pos[g][c] == 0) {
+          const auto& off = P.sync.wait_off[g];
+          for (int32_t i = off[(size_t)t * nC + c]; i < off[(size_t)t * nC + c + 1] && ok; ++i)
+            ok = flag[g][P.sync.wait_idx[g][i]];
+        }
+        const Piece& pc = work[g][c][t][pos[g][c]];
+        if (ok && pc.kind == kLLRecv) ok = lines_ready(g, pc);
         if (ok) ready.emplace_back(g, c);
       }
     if (!left) break;
     if (ready.empty()) return fail(A2A_ERR_INVALID, "emulation deadlock: unsatisfiable dependencies");
     auto [g, c] = ready[rnd() % ready.size()];
-    int t = next[g][c];
-    for (const Piece& pc : work[g][c][t])
-      std::memmove(base(g, pc.dst_loc) + pc.dst, base(g, pc.src_loc) + pc.src, (size_t)pc.n);
+    const int t = next[g][c];
+    const Piece& pc = work[g][c][t][pos[g][c]];
+    uint8_t* d = base(g, pc.dst_loc) + pc.dst;
+    const uint8_t* sp = base(g, pc.src_loc) + pc.src;
+    if (pc.kind == kLLSend) {
+      for (int64_t k = 0; k < (pc.n + 7) / 8; ++k) {
+        uint8_t line[16] = {0};
+        const int64_t w = std::min<int64_t>(8, pc.n - 8 * k);
+        for (int64_t j = 0; j < w; ++j) line[(j < 4 ? 0 : 4) + j] = sp[8 * k + j];
+        std::memcpy(line + 4, &kEpoch, 4);
+        std::memcpy(line + 12, &kEpoch, 4);
+        std::memcpy(d + 16 * k, line, 16);
+      }
+    } else if (pc.kind == kLLRecv) {
+      for (int64_t j = 0; j < pc.n; ++j) d[j] = sp[16 * (j / 8) + ((j & 7) < 4 ? 0 : 4) + (j & 7)];
+    } else {
+      std::memmove(d, sp, (size_t)pc.n);
+    }
+    if (++pos[g][c] < (int)work[g][c][t].size()) continue;
     uint32_t mask = P.sync.dst_mask[g][(size_t)t * nC + c];
     for (int h = 0; h < G; ++h)
       if (mask & (1u << h)) flag[h][((size_t)t * G + g) * nC + c] = 1;
+    pos[g][c] = 0;
     ++next[g][c];
   }
   return A2A_OK;
@@ -1207,11 +1284,17 @@ int a2a_plan_check_bounds(a2a_plan* plan, int32_t num_ctas) {
     if (loc == loc_send()) return P.info[g].send_bytes;
     if (loc >= 1 && loc < 1 + G) return P.info[loc - 1].recv_bytes;
     if (loc >= 1 + G && loc < 1 + 2 * G) return P.info[loc - 1 - G].scratch_bytes;
+    if (P.ll && loc >= 1 + 2 * G && loc < 1 + 3 * G) return P.ll_half[loc - 1 - 2 * G];
     return -1;
   };
-  auto check = [&](int g, int sl, int64_t so, int dl, int64_t dof, int64_t n) -> bool {
-    const int64_t ss = size_of(g, sl), ds = size_of(g, dl);
-    return n > 0 && ss >= 0 && ds >= 0 && so >= 0 && dof >= 0 && so + n <= ss && dof + n <= ds;
+  // LL lines: 16 bytes per 8 payload bytes on the landing-region side
+  auto check = [&](int g, int sl, int64_t so, int dl, int64_t dof, int64_t n, int kind = kCopy) -> bool {
+    const int64_t ss = size_of(g, sl), ds = size_of(g, dl), nl = 2 * ((n + 7) & ~(int64_t)7);
+    const int64_t ns = kind == kLLRecv ? nl : n, nd = kind == kLLSend ? nl : n;
+    if (kind == kLLSend && (dl < loc_ll(0, G) || dl >= loc_ll(G, G) || dl == loc_ll(g, G))) return false;
+    if (kind == kLLRecv && sl != loc_ll(g, G)) return false;
+    if (kind == kCopy && dl >= 1 + 2 * G) return false;
+    return n > 0 && ss >= 0 && ds >= 0 && so >= 0 && dof >= 0 && so + ns <= ss && dof + nd <= ds;
   };
   char buf[200];
   for (int g = 0; g < G; ++g) {
@@ -1225,8 +1308,10 @@ int a2a_plan_check_bounds(a2a_plan* plan, int32_t num_ctas) {
         }
     } else {
       for (const DevPiece& q : P.sync.pieces[g])
-        if (!check(g, q.src_loc, q.src_off, q.dst_loc, q.dst_off, q.nbytes) ||
-            !(q.src_loc == loc_send() || q.src_loc == loc_recv(g) || q.src_loc == loc_scratch(g, G))) {
+        if (!check(g, q.src_loc, q.src_off, q.dst_loc, q.dst_off, q.nbytes, q.kind) ||
+            !(q.src_loc == loc_send() || q.src_loc == loc_recv(g) || q.src_loc == loc_scratch(g, G) ||
+              (q.kind == kLLRecv && q.src_loc == loc_ll(g, G))) ||
+            (q.kind == kLLRecv && !(q.dst_loc == loc_recv(g) || q.dst_loc == loc_scratch(g, G)))) {
           snprintf(buf, sizeof buf, "gpu %d: piece out of bounds (src %d+%lld, dst %d+%lld, %d B)", g,
                    q.src_loc, (long long)q.src_off, q.dst_loc, (long long)q.dst_off, q.nbytes);
           return fail(A2A_ERR_INVALID, buf);
@@ -1246,6 +1331,8 @@ int a2a_plan_set_split(a2a_plan* plan, int32_t remote_weight) {
 int a2a_plan_set_schedule(a2a_plan* plan, int32_t mode, int64_t unit_bytes) {
   if (!plan || mode < 0 || mode > 4 || unit_bytes < 0) return fail(A2A_ERR_INVALID, "bad schedule mode");
   if (plan->p.bound) return fail(A2A_ERR_STATE, "set the schedule mode before a2a_plan_bind");
+  if (plan->p.ll && mode != 0)
+    return fail(A2A_ERR_INVALID, "A2A_PROTO_LL plans run the static schedule only");
   plan->p.sched_mode = mode;
   plan->p.dyn_unit_bytes = unit_bytes;
   plan->p.dyn = DynTables{};

@@ -101,7 +101,7 @@ class Plan:
     def __init__(self, g, sched, m: int, placement=None, n_gpus: int = 1,
                  copy_self: bool = True, ops: np.ndarray | None = None,
                  order: str | None = None, split_bytes: int = 0,
-                 reuse_scratch: bool | None = None):
+                 reuse_scratch: bool | None = None, protocol: str | None = None):
         _check_mode(g, sched)
         if int(m) != m or m < 0:
             raise ValueError(f"shard size m must be a non-negative integer, got {m}")
@@ -139,9 +139,17 @@ class Plan:
         if reuse_scratch is None:
             reuse_scratch = os.environ.get("A2A_REUSE_SCRATCH", "0") == "1"
         self.reuse_scratch = bool(reuse_scratch)
+        # cross-GPU transport: "simple" (peer stores + release/acquire flags) or
+        # "ll" (16-byte {data, epoch} lines polled by the receiving GPU; small shards)
+        if protocol is None:
+            protocol = os.environ.get("A2A_PROTO", "simple").strip().lower() or "simple"
+        if protocol not in ("simple", "ll"):
+            raise ValueError("protocol must be 'simple' or 'll'")
+        self.protocol = protocol
         d.flags = (N.A2A_COPY_SELF if copy_self else 0) | \
             (N.A2A_INTERLEAVE if order == "interleaved" else 0) | \
-            (N.A2A_REUSE_SCRATCH if reuse_scratch else 0)
+            (N.A2A_REUSE_SCRATCH if reuse_scratch else 0) | \
+            (N.A2A_PROTO_LL if protocol == "ll" else 0)
         d.split_bytes = int(split_bytes)
         h = C.c_void_p()
         rc = N.lib.a2a_plan_create(C.byref(d), C.byref(h))

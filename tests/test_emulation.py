@@ -189,3 +189,60 @@ def test_weighted_split_interleavings(name, G, w, artifacts):
             want = np.swapaxes(send, 0, 1)
             for g in range(G):
                 assert np.array_equal(recvs[g], want[nodes[g]])
+
+
+# ---- A2A_PROTO_LL: cross-GPU bytes as {data, epoch} lines polled by the receiver
+@pytest.mark.parametrize("name", ["torus2x4", "hypercube3", "gk8_2", "gk8_2_h1",
+                                  "ts_torus2x4", "ts_gk8_2", "ts_torus3x3", "ts_ring3"])
+@pytest.mark.parametrize("G", [2, 4, 8])
+@pytest.mark.parametrize("nC", [1, 5, 148])
+def test_ll_interleavings_deliver_transpose(name, G, nC, artifacts):
+    """Two-phase CTA steps (copies + LL line stores, then LL receives), lines in
+    the device format; odd shard sizes exercise partial lines and unaligned
+    payloads."""
+    a = artifacts(name)
+    if G > a.g.n:
+        pytest.skip("more GPUs than nodes")
+    for seed, m in enumerate((4096, 1000, 77)):
+        send = make_send(a.g.n, m, seed=seed)
+        with Plan(a.g, a.sched, m=m, n_gpus=G, protocol="ll") as p:
+            nodes = [local_nodes(p, g) for g in range(G)]
+            recvs = p.emulate([send[ns] for ns in nodes], num_ctas=nC, seed=seed)
+            p.check_bounds(nC)
+            stats = [p.sync_stats(g) for g in range(G)]
+            with Plan(a.g, a.sched, m=m, n_gpus=G) as q:
+                assert np.array_equal(p.link_bytes(), q.link_bytes())
+                for g in range(G):
+                    pi, qi = p.gpu_info(g), q.gpu_info(g)
+                    assert pi["egress_bytes"] == qi["egress_bytes"]
+                    assert pi["scratch_bytes"] >= qi["scratch_bytes"]
+        want = np.swapaxes(send, 0, 1)
+        for g in range(G):
+            assert np.array_equal(recvs[g], want[nodes[g]]), (G, nC, m, g)
+        # every flag a CTA waits for is GPU-local: no cross-GPU flag traffic
+        assert all(s["wait_flags"] >= 0 for s in stats)
+
+
+@pytest.mark.parametrize("name,G", [("torus4x4x4", 8), ("gk64_4", 4)])
+def test_ll_n64_interleavings(name, G, artifacts):
+    a = artifacts(name)
+    send = make_send(a.g.n, 512, seed=3)
+    with Plan(a.g, a.sched, m=512, n_gpus=G, protocol="ll") as p:
+        nodes = [local_nodes(p, g) for g in range(G)]
+        recvs = p.emulate([send[ns] for ns in nodes], num_ctas=148, seed=3)
+    want = np.swapaxes(send, 0, 1)
+    for g in range(G):
+        assert np.array_equal(recvs[g], want[nodes[g]])
+
+
+def test_ll_rejects(artifacts):
+    a = artifacts("gk8_2")
+    with pytest.raises(ValueError, match="PROTO_LL"):
+        Plan(a.g, a.sched, m=4096, n_gpus=2, protocol="ll", reuse_scratch=True)
+    with pytest.raises(ValueError, match="PROTO_LL"):
+        Plan(a.g, a.sched, m=4096, n_gpus=2, protocol="ll", order="interleaved")
+    with Plan(a.g, a.sched, m=4096, n_gpus=2, protocol="ll") as p:
+        with pytest.raises(ValueError, match="static"):
+            p.set_schedule("dynamic")
+    with pytest.raises(ValueError):
+        Plan(a.g, a.sched, m=4096, n_gpus=2, protocol="bogus")

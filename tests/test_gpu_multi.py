@@ -34,7 +34,8 @@ def _port():
     return p
 
 
-def _rank_main(rank, world, port, name, m, reps, q, engine="lsu", sched="static", reuse=False):
+def _rank_main(rank, world, port, name, m, reps, q, engine="lsu", sched="static", reuse=False,
+               proto="simple"):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     try:
@@ -49,15 +50,31 @@ def _rank_main(rank, world, port, name, m, reps, q, engine="lsu", sched="static"
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}",
                                 rank=rank, world_size=world)
         a = load_artifact(name)
-        plan = Plan(a.g, a.sched, m=m, n_gpus=world, reuse_scratch=reuse, placement="optimized")
+        plan = Plan(a.g, a.sched, m=m, n_gpus=world, reuse_scratch=reuse, placement="optimized",
+                    protocol=proto)
         plan.set_engine(engine)
         plan.set_schedule(sched)
         plan.bind(rank, device=rank)
         plan.set_timeout(20.0)
         connect(plan)
         nodes = local_nodes(plan, rank)
-        recv = plan.recv_buffer()
+        # LL: only local CTAs write recv, so any device buffer works
+        recv = plan.recv_buffer() if proto != "ll" else torch.empty(
+            (len(nodes), a.g.n, m), dtype=torch.uint8, device=f"cuda:{rank}")
         ok = True
+        if proto == "ll":
+            # back-to-back all-to-alls, no host sync in between: exercises the
+            # epoch-parity landing regions and the lagged entry flags
+            K = 6
+            sends_all = [make_send(a.g.n, m, seed=300 + k) for k in range(K)]
+            sends = [torch.from_numpy(np.ascontiguousarray(x[nodes])).cuda(rank) for x in sends_all]
+            outs = [torch.empty_like(recv) for _ in range(K)]
+            for k in range(K):
+                plan.execute(sends[k], outs[k])
+            plan.sync()
+            for k in range(K):
+                ok &= bool(np.array_equal(outs[k].cpu().numpy(), np.swapaxes(sends_all[k], 0, 1)[nodes]))
+            dist.barrier()
         for rep in range(reps):
             send_all = make_send(a.g.n, m, seed=100 + rep)
             send = torch.from_numpy(np.ascontiguousarray(send_all[nodes])).cuda(rank)
@@ -94,6 +111,33 @@ def test_multiprocess_ipc(world, name, m, engine):
     q = ctx.Queue()
     port = _port()
     ps = [ctx.Process(target=_rank_main, args=(r, world, port, name, m, 3, q, engine))
+          for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=300) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    for r in sorted(res, key=lambda x: x[0]):
+        assert len(r) == 3, r
+        assert r[1], f"rank {r[0]}: recv mismatch"
+        assert r[2], f"rank {r[0]}: link counters differ from schedule"
+
+
+@pytest.mark.parametrize("engine", ["tma", "lsu"])
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("name,m", [("torus2x4", 4096 + 7), ("gk8_2", 65536), ("hypercube3", 4096),
+                                    ("torus4x4x4", 2048), ("ts_gk8_2", 1000)])
+def test_multiprocess_ll(world, name, m, engine):
+    """A2A_PROTO_LL across GPUs: bit-exact recv (also back-to-back without host
+    sync), device link counters equal the schedule."""
+    if _ngpu() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_rank_main,
+                      args=(r, world, port, name, m, 3, q, engine, "static", False, "ll"))
           for r in range(world)]
     for p in ps:
         p.start()
