@@ -367,12 +367,14 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     # it absorbs the ranks' host launch skew in its entry barrier, so the
     # first timed step measures the pipeline and not process start-up skew
     plan.execute(send, recv, stream=stream)
+    h0 = time.perf_counter()
     for k in range(steps):
         if flush:
             flush_buf.zero_()
         e0[k].record(stream)
         plan.execute(send, recv, stream=stream)
         e1[k].record(stream)
+    host_us = (time.perf_counter() - h0) / steps * 1e6   # host enqueue time per step
     plan.sync()                   # the sampler thread keeps sampling while the GPU drains
     torch.cuda.synchronize(dev)
     clock_rec = clk.stop() if clk else None
@@ -522,6 +524,7 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     res = {"T": T, "per_step_ms": per, "step_ms_dist": dist, "value": value, "per_gpu": value / G,
            "t_lb": t_lb, "bound_frac": t_lb / T, "roofline": roof, "nccl": nres, "e2e": eres,
            "recv_ok": bool(ok), "clocks": clock_rec,
+           "host_enqueue_us_per_step": round(ctx.allmax([host_us])[0], 2),
            "sync": (plan.dyn_stats(rank, plan_ctas(plan, num_ctas)) if plan.schedule in ("dynamic", "list", "cp", "mix")
                     else plan.sync_stats(rank)),
            "kernel_timeline": tls,

@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -52,7 +53,8 @@ struct KParams {
   unsigned long long* counters;            // [T'][E]
   int32_t* err;
   int64_t timeout_ns;
-  uint32_t epoch;
+  uint32_t* ctl;                           // [nC] last completed epoch of each CTA (device memory)
+  int64_t ll_half[A2A_MAX_GPUS];           // LL landing region bytes per epoch parity
   int32_t G, rank, nC, T, E, count_links;
   int32_t ll;                              // A2A_PROTO_LL: cross-GPU bytes as LL lines
   int32_t tma_chunk, tma_stages;           // TMA engine: bytes per bulk copy, ring depth
@@ -66,7 +68,6 @@ struct KParams {
   int32_t n_units, unit_base;              // this GPU's units; global id of its first
   int32_t n_remote, remote_ctas;           // remote queue = units [0, n_remote); CTAs starting on it
   unsigned long long* grab;                // per-GPU grab counters [2] (remote, local queue)
-  unsigned long long grab_base[2];         // counter values at the start of this execute
 };
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -167,37 +168,46 @@ __device__ __forceinline__ void cta_copy(char* __restrict__ dst, const char* __r
 // is stored and loaded as one unit, so a reader that sees the epoch in both
 // halves holds the payload -- no fence, no separate flag (the LL protocol).
 // Line k of a piece carries payload bytes [8k, 8k+8).
+__device__ __forceinline__ uint2 ll_load8(const char* __restrict__ src, int64_t b, int64_t n, bool al) {
+  if (al && b + 8 <= n) return *reinterpret_cast<const uint2*>(src + b);
+  uint32_t lo = 0, hi = 0;
+  for (int j = 0; j < 8 && b + j < n; ++j) {
+    const uint32_t x = (uint8_t)src[b + j];
+    if (j < 4) lo |= x << (8 * j);
+    else hi |= x << (8 * (j - 4));
+  }
+  return make_uint2(lo, hi);
+}
+__device__ __forceinline__ void ll_store(uint4* dst, uint2 v, uint32_t epoch) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "r"(v.x), "r"(epoch),
+               "r"(v.y), "r"(epoch)
+               : "memory");
+}
 __device__ __forceinline__ void ll_send(uint4* __restrict__ dst, const char* __restrict__ src,
                                         int64_t n, uint32_t epoch) {
-  const int64_t L = (n + 7) >> 3;
+  constexpr int kU = 4;  // lines in flight per thread
+  const int64_t L = (n + 7) >> 3, nt = blockDim.x;
   const bool al = ((uintptr_t)src & 7) == 0;
-  for (int64_t k = threadIdx.x; k < L; k += blockDim.x) {
-    const int64_t b = k << 3;
-    uint32_t lo = 0, hi = 0;
-    if (al && b + 8 <= n) {
-      const uint2 v = *reinterpret_cast<const uint2*>(src + b);
-      lo = v.x;
-      hi = v.y;
-    } else {
-      for (int j = 0; j < 8 && b + j < n; ++j) {
-        const uint32_t x = (uint8_t)src[b + j];
-        if (j < 4) lo |= x << (8 * j);
-        else hi |= x << (8 * (j - 4));
-      }
-    }
-    asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst + k), "r"(lo),
-                 "r"(epoch), "r"(hi), "r"(epoch)
-                 : "memory");
+  int64_t k = threadIdx.x;
+  for (; k + (kU - 1) * nt < L; k += kU * nt) {
+    uint2 v[kU];
+#pragma unroll
+    for (int j = 0; j < kU; ++j) v[j] = ll_load8(src, (k + j * nt) << 3, n, al);
+#pragma unroll
+    for (int j = 0; j < kU; ++j) ll_store(dst + k + j * nt, v[j], epoch);
   }
+  for (; k < L; k += nt) ll_store(dst + k, ll_load8(src, k << 3, n, al), epoch);
 }
 // Poll this thread's lines until both halves carry `epoch`, then store the
-// payload into the local destination.  False on timeout / peer error.
+// payload into the local destination.  Polls back off (up to ~0.5 us) so that
+// CTAs waiting on large landing regions do not flood L2 with requests while
+// the NVLink writes are arriving.  False on timeout / peer error.
 __device__ __forceinline__ bool ll_recv(char* __restrict__ dst, const uint4* src, int64_t n,
                                         uint32_t epoch, int64_t timeout_ns, int32_t* err) {
   const int64_t L = (n + 7) >> 3;
   const bool al = ((uintptr_t)dst & 7) == 0;
   for (int64_t k = threadIdx.x; k < L; k += blockDim.x) {
-    uint32_t a, f0, b, f1, spins = 0;
+    uint32_t a, f0, b, f1, spins = 0, nap = 0;
     uint64_t t0 = 0;
     for (;;) {
       asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -205,7 +215,11 @@ __device__ __forceinline__ bool ll_recv(char* __restrict__ dst, const uint4* src
                    : "l"(src + k)
                    : "memory");
       if (f0 == epoch && f1 == epoch) break;
-      if ((++spins & 1023) == 0) {
+      if (++spins > 4) {
+        nap = nap ? min(2 * nap, 512u) : 32u;
+        __nanosleep(nap);
+      }
+      if ((spins & 255) == 0) {
         const uint64_t now = globaltimer();
         if (t0 == 0) t0 = now;
         if ((int64_t)(now - t0) > timeout_ns || *(volatile int32_t*)err != 0) return false;
@@ -332,8 +346,22 @@ struct BodyCursor {
   }
 };
 
+// ---- device-side epochs (graph-capturable executes) ----
+// Every CTA keeps the epoch of its last all-to-all in its own device word: it
+// reads it at kernel start (+1) and writes it back at its end.  All CTAs run
+// every execute, so the words agree, no cross-CTA synchronisation is needed,
+// and a replayed CUDA graph runs a fresh epoch each time without the host.
+__device__ __forceinline__ uint32_t begin_epoch(const KParams& p) {
+  const uint32_t e = *(volatile const uint32_t*)(p.ctl + blockIdx.x) + 1;
+  return e == 0 ? 1 : e;
+}
+__device__ __forceinline__ void end_epoch(const KParams& p, uint32_t epoch) {
+  __syncthreads();  // every thread has read the old value
+  if (threadIdx.x == 0) p.ctl[blockIdx.x] = epoch;
+}
+
 template <int kEngine, int kThreads>
-__global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) {
+__device__ __forceinline__ void exec_body(const KParams& p, const uint32_t epoch) {
   __shared__ int s_abort;
   extern __shared__ __align__(128) unsigned char dsmem[];
   const int c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5;
@@ -366,7 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
   //      was last read two all-to-alls ago, so it is free once that peer has
   //      started the previous one (its entry flag >= epoch - 1)
   if (p.G > 1 && p.ll) {
-    if (c == 0 && tid < p.G && tid != p.rank) st_relaxed(p.entry_flags[tid] + p.rank, p.epoch, true);
+    if (c == 0 && tid < p.G && tid != p.rank) st_relaxed(p.entry_flags[tid] + p.rank, epoch, true);
     if (warp == 0) {
       const int lane = tid & 31;
       bool ok = true;
@@ -374,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
         const uint32_t* f = p.entry_flags[p.rank] + lane;
         uint64_t t0 = globaltimer();
         uint32_t spins = 0;
-        while ((int32_t)(ld_relaxed(f, true) - (p.epoch - 1)) < 0) {
+        while ((int32_t)(ld_relaxed(f, true) - (epoch - 1)) < 0) {
           if ((++spins & 255) == 0 && ((int64_t)(globaltimer() - t0) > p.timeout_ns ||
                                        *(volatile int32_t*)p.err != 0)) {
             ok = false;
@@ -390,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
   }
   // ---- entry barrier: announce epoch to every peer, then wait for theirs
   if (p.G > 1 && !p.ll) {
-    if (c == 0 && tid < p.G && tid != p.rank) st_release_sys(p.entry_flags[tid] + p.rank, p.epoch);
+    if (c == 0 && tid < p.G && tid != p.rank) st_release_sys(p.entry_flags[tid] + p.rank, epoch);
     if (warp == 0) {
       const int lane = tid & 31;
       bool ok = true;
@@ -398,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
         const uint32_t* f = p.entry_flags[p.rank] + lane;
         uint64_t t0 = globaltimer();
         uint32_t spins = 0;
-        while ((int32_t)(ld_acquire_sys(f) - p.epoch) < 0) {
+        while ((int32_t)(ld_acquire_sys(f) - epoch) < 0) {
           if ((++spins & 255) == 0 && ((int64_t)(globaltimer() - t0) > p.timeout_ns ||
                                        *(volatile int32_t*)p.err != 0)) {
             ok = false;
@@ -430,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
       for (int i = tid; i < n; i += kThreads) s_pc[i] = p.pieces[base + i];
       if (!waited) {
         if (warp == 0) {
-          bool ok = warp_wait_flags(my_flags, p.wait_idx, cs.wb, cs.we, p.epoch, p.timeout_ns,
+          bool ok = warp_wait_flags(my_flags, p.wait_idx, cs.wb, cs.we, epoch, p.timeout_ns,
                                     p.err, sys, p.sync_mode);
           if (!ok && tid == 0) s_abort = 1;
           if (tid == 0) tl[3 + p.T + t] = globaltimer();
@@ -443,13 +471,15 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
       // (a CTA's LL sends precede its LL receives)
       for (int i = 0; i < n; ++i) {
         const DevPiece& q = s_pc[i];
-        if (q.kind == kLLSend) {
-          ll_send(reinterpret_cast<uint4*>(p.base[q.dst_loc] + q.dst_off), p.base[q.src_loc] + q.src_off,
-                  q.nbytes, p.epoch);
+        if (q.kind == kLLSend) {  // landing region of this epoch's parity on GPU h
+          const int h = q.dst_loc - (1 + 2 * p.G);
+          ll_send(reinterpret_cast<uint4*>(p.base[q.dst_loc] + q.dst_off + (epoch & 1) * p.ll_half[h]),
+                  p.base[q.src_loc] + q.src_off, q.nbytes, epoch);
         } else if (q.kind == kLLRecv) {
           if (!ll_recv(p.base[q.dst_loc] + q.dst_off,
-                       reinterpret_cast<const uint4*>(p.base[q.src_loc] + q.src_off), q.nbytes, p.epoch,
-                       p.timeout_ns, p.err)) {
+                       reinterpret_cast<const uint4*>(p.base[q.src_loc] + q.src_off +
+                                                      (epoch & 1) * p.ll_half[p.rank]),
+                       q.nbytes, epoch, p.timeout_ns, p.err)) {
             atomicCAS(p.err, 0, (int32_t)A2A_ERR_TIMEOUT);
             s_abort = 1;
           }
@@ -538,9 +568,9 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
         while (mask) {
           const int h = __ffs(mask) - 1;
           mask &= mask - 1;
-          st_relaxed(p.step_flags[h] + slot, p.epoch, sys);
+          st_relaxed(p.step_flags[h] + slot, epoch, sys);
         }
-        if (cs.mask & own) st_relaxed(p.step_flags[p.rank] + slot, p.epoch, sys);
+        if (cs.mask & own) st_relaxed(p.step_flags[p.rank] + slot, epoch, sys);
       } else {
         if (!(p.sync_mode & 2)) {
           if (p.sync_mode & 1) fence_acq_rel(sys);
@@ -551,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
         while (mask) {
           const int h = __ffs(mask) - 1;
           mask &= mask - 1;
-          st_release(p.step_flags[h] + slot, p.epoch, sys);
+          st_release(p.step_flags[h] + slot, epoch, sys);
         }
       }
       tl[2 + t] = globaltimer();
@@ -564,7 +594,7 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
       const uint32_t* f = my_flags + p.exit_idx[i];
       uint64_t t0 = globaltimer();
       uint32_t spins = 0;
-      while ((int32_t)(ld_acquire_sys(f) - p.epoch) < 0) {
+      while ((int32_t)(ld_acquire_sys(f) - epoch) < 0) {
         if ((++spins & 255) == 0 && ((int64_t)(globaltimer() - t0) > p.timeout_ns ||
                                      *(volatile int32_t*)p.err != 0)) {
           ok = false;
@@ -578,9 +608,16 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
   if (tid == 0) tl[2 + p.T] = globaltimer();
 }
 
+template <int kEngine, int kThreads>
+__global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) {
+  const uint32_t epoch = begin_epoch(p);
+  exec_body<kEngine, kThreads>(p, epoch);
+  end_epoch(p, epoch);
+}
+
 // ---- dynamic mode: CTAs grab units from a per-GPU counter ----
 template <int kEngine, int kThreads>
-__global__ void __launch_bounds__(kThreads, 1) a2a_dyn_kernel(const KParams p) {
+__device__ __forceinline__ void dyn_body(const KParams& p, const uint32_t epoch) {
   __shared__ int s_abort;
   __shared__ long long s_idx[2];
   __shared__ DevUnit s_u[2];
@@ -606,7 +643,7 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_dyn_kernel(const KParams p) {
   const uint32_t* my_flags = p.step_flags[p.rank];
   const bool sys = p.G > 1 || (p.sync_mode & 4);
   if (p.G > 1) {  // entry barrier (same protocol as the static kernel)
-    if (c == 0 && tid < p.G && tid != p.rank) st_release_sys(p.entry_flags[tid] + p.rank, p.epoch);
+    if (c == 0 && tid < p.G && tid != p.rank) st_release_sys(p.entry_flags[tid] + p.rank, epoch);
     if (warp == 0) {
       const int lane = tid & 31;
       bool ok = true;
@@ -614,7 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_dyn_kernel(const KParams p) {
         const uint32_t* f = p.entry_flags[p.rank] + lane;
         uint64_t t0 = globaltimer();
         uint32_t spins = 0;
-        while ((int32_t)(ld_acquire_sys(f) - p.epoch) < 0) {
+        while ((int32_t)(ld_acquire_sys(f) - epoch) < 0) {
           if ((++spins & 255) == 0 && ((int64_t)(globaltimer() - t0) > p.timeout_ns ||
                                        *(volatile int32_t*)p.err != 0)) {
             ok = false;
@@ -636,7 +673,8 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_dyn_kernel(const KParams p) {
     long long idx = -1;
     for (;;) {  // own queue first, then the other; one failing grab per queue
       const long long qn = q == 0 ? p.n_remote : (long long)p.n_units - p.n_remote;
-      const long long j = (long long)(atomicAdd(p.grab + q, 1ull) - p.grab_base[q]);
+      const long long j = (long long)(atomicAdd(p.grab + q, 1ull) -
+                                      (unsigned long long)(epoch - 1) * (unsigned long long)(qn + p.nC));
       if (j < qn) { idx = (q == 0 ? 0 : p.n_remote) + j; break; }
       if (++visited == 2) break;
       q ^= 1;
@@ -653,7 +691,7 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_dyn_kernel(const KParams p) {
     const DevUnit& u = s_u[sl];
     if (s_idx[sl] < 0 || u.we <= u.wb) return true;
     const uint64_t w0 = globaltimer();
-    bool ok = warp_wait_flags(my_flags, p.unit_wait, u.wb, u.we, p.epoch, p.timeout_ns, p.err,
+    bool ok = warp_wait_flags(my_flags, p.unit_wait, u.wb, u.we, epoch, p.timeout_ns, p.err,
                               sys, p.sync_mode);
     if ((tid & 31) == 0) waited_ns += globaltimer() - w0;
     return ok;
@@ -746,7 +784,7 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_dyn_kernel(const KParams p) {
       while (mask) {
         const int h = __ffs(mask) - 1;
         mask &= mask - 1;
-        st_release(p.step_flags[h] + slot, p.epoch, sys);
+        st_release(p.step_flags[h] + slot, epoch, sys);
       }
       ++done;
     }
@@ -761,7 +799,7 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_dyn_kernel(const KParams p) {
       const uint32_t* f = my_flags + p.exit_idx[i];
       uint64_t t0 = globaltimer();
       uint32_t spins = 0;
-      while ((int32_t)(ld_acquire_sys(f) - p.epoch) < 0) {
+      while ((int32_t)(ld_acquire_sys(f) - epoch) < 0) {
         if ((++spins & 255) == 0 && ((int64_t)(globaltimer() - t0) > p.timeout_ns ||
                                      *(volatile int32_t*)p.err != 0)) {
           ok = false;
@@ -777,6 +815,13 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_dyn_kernel(const KParams p) {
     tl[2 + p.T] = globaltimer();
   }
   if (tid == (kEngine == 1 ? 32 : 0)) tl[3] = waited_ns;
+}
+
+template <int kEngine, int kThreads>
+__global__ void __launch_bounds__(kThreads, 1) a2a_dyn_kernel(const KParams p) {
+  const uint32_t epoch = begin_epoch(p);
+  dyn_body<kEngine, kThreads>(p, epoch);
+  end_epoch(p, epoch);
 }
 
 static int cuda_fail(cudaError_t e, const char* what) {
@@ -840,7 +885,7 @@ static EngineCfg engine_cfg(const Plan& P) {
           (int)prog, batch};
 }
 
-// arena flag region: entry[G] u32 | grab counter u64 @128 | flags @256:
+// arena flag region: entry[G] u32 | grab counters u64 @128 | flags @256:
 //   static: [T'][G][nC] u32 (slot (t, gpu, cta)); dynamic: [total units] u32
 static inline int64_t entry_flags_off() { return 0; }
 static inline int64_t grab_off() { return 128; }
@@ -862,7 +907,7 @@ static void free_device(Plan& P) {
     P.peer_arena[g] = nullptr;
   }
   void** bufs[] = {&P.arena, &P.d_items, &P.d_step_begin, &P.d_step_bytes, &P.d_dst_mask, &P.d_exit_idx,
-                   &P.d_wait_off, &P.d_wait_idx, &P.d_counters, &P.d_timeline};
+                   &P.d_wait_off, &P.d_wait_idx, &P.d_counters, &P.d_timeline, &P.d_ctl};
   for (void** b : bufs) {
     if (*b) cudaFree(*b);
     *b = nullptr;
@@ -905,6 +950,10 @@ static int bind_plan(Plan& P, int gpu, int dev, int nC) {
   P.rank = gpu;
   P.device = dev;
   P.nC = nC;
+  {  // experiments only: plain launch (co-residency then rests on 1 CTA/SM and an idle GPU)
+    const char* nc = getenv("A2A_NONCOOP");
+    P.coop = !(nc && nc[0] == '1');
+  }
   const int G = P.G, TE = P.T_exec;
 
   // ---- CTA split + producer dependency lists (host, identical on all ranks)
@@ -945,7 +994,8 @@ static int bind_plan(Plan& P, int gpu, int dev, int nC) {
     if ((rc = upload(&P.d_wait_idx, S.wait_idx[gpu])) != A2A_OK) return rc;
     if ((rc = upload(&P.d_exit_idx, S.exit_idx[gpu])) != A2A_OK) return rc;
   }
-  P.dyn_execs = 0;
+  CK(cudaMalloc(&P.d_ctl, (size_t)nC * 4));
+  CK(cudaMemset(P.d_ctl, 0, (size_t)nC * 4));
   CK(cudaMalloc(&P.d_timeline, (size_t)nC * (2 * TE + 3) * 8));
   CK(cudaMemset(P.d_timeline, 0, (size_t)nC * (2 * TE + 3) * 8));
   size_t cbytes = std::max<size_t>((size_t)TE * std::max(P.E, 1) * 8, 16);
@@ -1123,15 +1173,15 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
   KParams kp;
   std::memset(&kp, 0, sizeof kp);
   kp.base[loc_send()] = (char*)send;
-  uint32_t epoch = P.epoch + 1;
-  if (epoch == 0) epoch = 1;  // 0 is the "never written" value
   for (int g = 0; g < P.G; ++g) {
     char* ar = (char*)P.peer_arena[g];
     kp.base[loc_recv(g)] =
         (g == P.rank) ? (char*)recv : ar + P.recv_off[g] + (int64_t)ridx * recv_stride(P, g);
     kp.base[loc_scratch(g, P.G)] = ar + P.scratch_off[g];
-    if (P.ll)  // landing region of this epoch's parity
-      kp.base[loc_ll(g, P.G)] = ar + P.scratch_off[g] + P.ll_off[g] + (int64_t)(epoch & 1) * P.ll_half[g];
+    if (P.ll) {  // parity 0; the kernel adds (epoch & 1) * ll_half
+      kp.base[loc_ll(g, P.G)] = ar + P.scratch_off[g] + P.ll_off[g];
+      kp.ll_half[g] = P.ll_half[g];
+    }
     kp.entry_flags[g] = (uint32_t*)(ar + entry_flags_off());
     kp.step_flags[g] = (uint32_t*)(ar + step_flags_off());
   }
@@ -1148,9 +1198,6 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
     kp.grab = (unsigned long long*)((char*)P.arena + grab_off());
     kp.n_remote = Dy.n_remote[P.rank];
     kp.remote_ctas = Dy.remote_ctas[P.rank];
-    kp.grab_base[0] = (unsigned long long)P.dyn_execs * (unsigned long long)(kp.n_remote + P.nC);
-    kp.grab_base[1] =
-        (unsigned long long)P.dyn_execs * (unsigned long long)(kp.n_units - kp.n_remote + P.nC);
   } else {
     kp.n_exit = (int32_t)P.sync.exit_idx[P.rank].size();
   }
@@ -1158,7 +1205,7 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
   kp.counters = (unsigned long long*)P.d_counters;
   kp.err = P.d_err;
   kp.timeout_ns = P.timeout_ns;
-  kp.epoch = P.epoch = epoch;
+  kp.ctl = (uint32_t*)P.d_ctl;
   kp.ll = P.ll ? 1 : 0;
   kp.G = P.G;
   kp.rank = P.rank;
@@ -1175,10 +1222,20 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
   kp.smem_prog = ec.prog_off;
   kp.smem_batch = ec.batch_off;
   kp.batch = ec.batch;
-  cudaError_t e = cudaLaunchCooperativeKernel(ec.fn, dim3(P.nC), dim3(ec.threads), args, ec.smem,
-                                              (cudaStream_t)stream);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchCooperativeKernel");
-  if (P.sched_mode >= 1) ++P.dyn_execs;
+  // cooperative launch (all CTAs co-resident: CTAs spin on each other's flags);
+  // cudaLaunchKernelExC with the cooperative attribute is stream-capturable
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P.nC);
+  cfg.blockDim = dim3(ec.threads);
+  cfg.dynamicSmemBytes = ec.smem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = P.coop ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelExC(&cfg, ec.fn, args);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernelExC (cooperative)");
   P.last_stream = stream;
   P.launched = true;
   return A2A_OK;

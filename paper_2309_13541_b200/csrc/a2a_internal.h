@@ -140,7 +140,6 @@ struct Plan {
   int32_t remote_weight = 1;                    // CTA split cost of an NVLink byte vs a local byte
   int32_t sched_mode = 0;                       // 0 static programs, 1 dynamic step-major, 2 dynamic list-scheduled
   int64_t dyn_unit_bytes = 0;                   // dynamic unit size (0 = auto)
-  int64_t dyn_execs = 0;                        // dynamic executes so far (grab counter base)
 
   // ---- device binding (a2a_exec.cu)
   bool bound = false, imported = false;
@@ -148,6 +147,7 @@ struct Plan {
   int32_t engine = 1, tma_chunk = 32768, tma_stages = 6;   // copy engine (a2a_plan_set_engine)
   int32_t n_recv = 1;                           // arena recv buffers (multi-buffering)
   int32_t sync_mode = 2;                        // a2a_plan_set_sync_mode (2: bar.sync + st.release)
+  bool coop = true;                             // cooperative launch (A2A_NONCOOP=1: plain, experiments)
   int64_t flags_bytes = 0;                      // arena flag region size
   std::vector<int64_t> recv_off, scratch_off;   // per gpu, inside that gpu's arena
   std::vector<int64_t> arena_bytes;             // per gpu
@@ -163,9 +163,9 @@ struct Plan {
   void* d_wait_idx = nullptr;
   void* d_counters = nullptr;
   void* d_timeline = nullptr;
+  void* d_ctl = nullptr;                        // [nC] u32 per-CTA epoch (device-side, graph-safe)
   int32_t* h_err = nullptr;                     // mapped pinned error word
   int32_t* d_err = nullptr;
-  uint32_t epoch = 0;
   int64_t timeout_ns = 10000000000LL;
   void* last_stream = nullptr;
   bool launched = false;

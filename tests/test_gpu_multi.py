@@ -35,7 +35,7 @@ def _port():
 
 
 def _rank_main(rank, world, port, name, m, reps, q, engine="lsu", sched="static", reuse=False,
-               proto="simple"):
+               proto="simple", graph=False):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     try:
@@ -83,6 +83,21 @@ def _rank_main(rank, world, port, name, m, reps, q, engine="lsu", sched="static"
             want = np.swapaxes(send_all, 0, 1)[nodes]
             ok &= bool(np.array_equal(recv.cpu().numpy(), want))
             dist.barrier()
+        if graph:
+            # one execute captured into a CUDA graph, replayed with new send
+            # contents: device-side epochs keep the ranks in step
+            send = torch.empty((len(nodes), a.g.n, m), dtype=torch.uint8, device=f"cuda:{rank}")
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                plan.execute(send, recv)
+            for rep in range(4):
+                send_all = make_send(a.g.n, m, seed=700 + rep)
+                send.copy_(torch.from_numpy(np.ascontiguousarray(send_all[nodes])))
+                dist.barrier()
+                g.replay()
+                torch.cuda.synchronize(rank)
+                ok &= bool(np.array_equal(recv.cpu().numpy(), np.swapaxes(send_all, 0, 1)[nodes]))
+                dist.barrier()
         counters = plan.read_link_counters()
         tot = [None] * world
         dist.all_gather_object(tot, counters)
@@ -123,10 +138,11 @@ def test_multiprocess_ipc(world, name, m, engine):
         assert r[2], f"rank {r[0]}: link counters differ from schedule"
 
 
-@pytest.mark.parametrize("engine", ["tma", "lsu"])
 @pytest.mark.parametrize("world", [2, 4, 8])
-@pytest.mark.parametrize("name,m", [("torus2x4", 4096 + 7), ("gk8_2", 65536), ("hypercube3", 4096),
-                                    ("torus4x4x4", 2048), ("ts_gk8_2", 1000)])
+@pytest.mark.parametrize("name,m,engine", [
+    ("torus2x4", 4096 + 7, "tma"), ("gk8_2", 65536, "tma"), ("hypercube3", 4096, "tma"),
+    ("torus4x4x4", 2048, "tma"), ("ts_gk8_2", 1000, "tma"), ("gk8_2", 20000, "lsu"),
+    ("torus2x4", 333, "lsu")])
 def test_multiprocess_ll(world, name, m, engine):
     """A2A_PROTO_LL across GPUs: bit-exact recv (also back-to-back without host
     sync), device link counters equal the schedule."""
@@ -138,6 +154,30 @@ def test_multiprocess_ll(world, name, m, engine):
     port = _port()
     ps = [ctx.Process(target=_rank_main,
                       args=(r, world, port, name, m, 3, q, engine, "static", False, "ll"))
+          for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=300) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    for r in sorted(res, key=lambda x: x[0]):
+        assert len(r) == 3, r
+        assert r[1], f"rank {r[0]}: recv mismatch"
+        assert r[2], f"rank {r[0]}: link counters differ from schedule"
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("proto,sched", [("simple", "static"), ("ll", "static"), ("simple", "cp")])
+def test_multiprocess_cuda_graph(world, proto, sched):
+    """Executes captured into CUDA graphs on every rank, replayed repeatedly."""
+    if _ngpu() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_rank_main,
+                      args=(r, world, port, "gk8_2", 20000, 1, q, "tma", sched, False, proto, True))
           for r in range(world)]
     for p in ps:
         p.start()
@@ -222,10 +262,10 @@ def _alt_main(rank, world, port, q):
         q.put((rank, f"{ex!r}\n{traceback.format_exc()}"))
 
 
-@pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("engine", ["tma", "lsu"])
-@pytest.mark.parametrize("reuse", [False, True])
-@pytest.mark.parametrize("name,m", [("gk8_2", 65536 + 64), ("torus4x4x4", 8192), ("torus2x4_h2", 4099)])
+@pytest.mark.parametrize("world,engine,reuse,name,m", [
+    (2, "tma", False, "gk8_2", 65536 + 64), (4, "tma", True, "torus4x4x4", 8192),
+    (2, "lsu", True, "torus2x4_h2", 4099), (4, "lsu", False, "gk8_2", 65536 + 64),
+    (4, "tma", False, "torus2x4_h2", 4099)])
 @pytest.mark.parametrize("mode", ["dynamic", "list", "cp", "mix"])
 def test_multiprocess_dynamic(world, engine, reuse, name, m, mode):
     """Dynamic unit queues across GPUs (+ scratch reuse, optimized placement)."""

@@ -89,6 +89,7 @@ def main(argv=None):
                     "t_lb_ms": round(r["t_lb"] * 1e3, 4), "bound_frac": round(r["bound_frac"], 4),
                     "roofline": r["roofline"], "nccl": r["nccl"], "recv_ok": r["recv_ok"],
                     "clocks": r["clocks"], "sync_flags": r["sync"],
+                    "host_enqueue_us_per_step": r["host_enqueue_us_per_step"],
                     "kernel_timeline": r["kernel_timeline"],
                     "egress_max_bytes": r["egress_max"], "scratch_bytes": r["scratch_bytes"],
                     "placement": a.placement, "l2": r["l2"], "num_ctas": r["num_ctas"],
