@@ -262,7 +262,7 @@ def autotune_schedule(ctx, art, m, placement="optimized", num_ctas=0, trials=5,
     G, dev = ctx.world, ctx.dev
     if candidates is None:
         candidates = ("static", "mix:1048576", "cp:1048576") + (
-            ("ll",) if G > 1 and m <= LL_MAX_SHARD else ())
+            ("ll",) if m <= LL_MAX_SHARD else ())
     times = {}
     for cand in candidates:
         plan = make_plan(art, m, G, placement, cand)
@@ -359,6 +359,7 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     # ---- timed region: K all-to-alls, L2 flushed between them (outside the events)
     e0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     e1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ef = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]   # before the flush
     ctx.barrier()
     torch.cuda.synchronize(dev)
     if clk:
@@ -369,6 +370,7 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     plan.execute(send, recv, stream=stream)
     h0 = time.perf_counter()
     for k in range(steps):
+        ef[k].record(stream)
         if flush:
             flush_buf.zero_()
         e0[k].record(stream)
@@ -386,6 +388,16 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
         ctx.pg.all_gather_object(alltl, tls)
         tls = {"kernel_us": max(x["kernel_us"] for x in alltl), "ranks": alltl}
     per = ctx.allmax([a.elapsed_time(b) for a, b in zip(e0, e1)])
+    # per-rank GPU time of the flush + of the whole step (diagnostics: a rank
+    # whose stream lags shows up here, not in its kernel span)
+    fl = sorted(a.elapsed_time(b) for a, b in zip(ef, e0))
+    gap = sorted(a.elapsed_time(b) for a, b in zip(ef[:-1], ef[1:])) or [0.0]
+    diag = [fl[len(fl) // 2], gap[len(gap) // 2]]
+    if ctx.pg:
+        alld = [None] * G
+        ctx.pg.all_gather_object(alld, diag)
+    else:
+        alld = [diag]
     T = sum(per) / len(per) / 1e3                      # s per all-to-all (max over ranks)
     payload = n * (n - 1) * m
     value = payload / T / 1e9
@@ -525,6 +537,8 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
            "t_lb": t_lb, "bound_frac": t_lb / T, "roofline": roof, "nccl": nres, "e2e": eres,
            "recv_ok": bool(ok), "clocks": clock_rec,
            "host_enqueue_us_per_step": round(ctx.allmax([host_us])[0], 2),
+           "flush_ms_p50_by_rank": [round(x[0], 4) for x in alld],
+           "step_period_ms_p50_by_rank": [round(x[1], 4) for x in alld],
            "sync": (plan.dyn_stats(rank, plan_ctas(plan, num_ctas)) if plan.schedule in ("dynamic", "list", "cp", "mix")
                     else plan.sync_stats(rank)),
            "kernel_timeline": tls,

@@ -167,70 +167,103 @@ __device__ __forceinline__ void cta_copy(char* __restrict__ dst, const char* __r
 // A 16-byte line {payload[0..4), epoch, payload[4..8), epoch}: each 8-byte half
 // is stored and loaded as one unit, so a reader that sees the epoch in both
 // halves holds the payload -- no fence, no separate flag (the LL protocol).
-// Line k of a piece carries payload bytes [8k, 8k+8).
-__device__ __forceinline__ uint2 ll_load8(const char* __restrict__ src, int64_t b, int64_t n, bool al) {
-  if (al && b + 8 <= n) return *reinterpret_cast<const uint2*>(src + b);
-  uint32_t lo = 0, hi = 0;
-  for (int j = 0; j < 8 && b + j < n; ++j) {
-    const uint32_t x = (uint8_t)src[b + j];
-    if (j < 4) lo |= x << (8 * j);
-    else hi |= x << (8 * (j - 4));
-  }
-  return make_uint2(lo, hi);
+// LL offsets are payload addresses: payload byte x of a landing region lives
+// in line x/8.
+__device__ __forceinline__ uint64_t plain_load8(const char* __restrict__ s, int nb) {
+  if (nb == 8 && ((uintptr_t)s & 7) == 0) return *reinterpret_cast<const uint64_t*>(s);
+  uint64_t v = 0;
+  for (int j = 0; j < nb; ++j) v |= (uint64_t)(uint8_t)s[j] << (8 * j);
+  return v;
 }
-__device__ __forceinline__ void ll_store(uint4* dst, uint2 v, uint32_t epoch) {
-  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "r"(v.x), "r"(epoch),
-               "r"(v.y), "r"(epoch)
+__device__ __forceinline__ void plain_store8(char* __restrict__ d, uint64_t v, int nb) {
+  if (nb == 8 && ((uintptr_t)d & 7) == 0) {
+    *reinterpret_cast<uint64_t*>(d) = v;
+    return;
+  }
+  for (int j = 0; j < nb; ++j) d[j] = (char)((v >> (8 * j)) & 0xff);
+}
+__device__ __forceinline__ void ll_store(uint4* dst, uint64_t v, uint32_t epoch) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "r"((uint32_t)v),
+               "r"(epoch), "r"((uint32_t)(v >> 32)), "r"(epoch)
                : "memory");
 }
-__device__ __forceinline__ void ll_send(uint4* __restrict__ dst, const char* __restrict__ src,
-                                        int64_t n, uint32_t epoch) {
-  constexpr int kU = 4;  // lines in flight per thread
-  const int64_t L = (n + 7) >> 3, nt = blockDim.x;
-  const bool al = ((uintptr_t)src & 7) == 0;
-  int64_t k = threadIdx.x;
-  for (; k + (kU - 1) * nt < L; k += kU * nt) {
-    uint2 v[kU];
-#pragma unroll
-    for (int j = 0; j < kU; ++j) v[j] = ll_load8(src, (k + j * nt) << 3, n, al);
-#pragma unroll
-    for (int j = 0; j < kU; ++j) ll_store(dst + k + j * nt, v[j], epoch);
+// Poll one line until both halves carry `epoch`.  Polls back off (up to
+// ~0.5 us) so that CTAs waiting on large landing regions do not flood L2 with
+// requests while the NVLink writes are arriving.  False on timeout / error.
+__device__ __forceinline__ bool ll_poll(const uint4* line, uint32_t epoch, int64_t timeout_ns,
+                                        int32_t* err, uint64_t* out) {
+  uint32_t a, f0, b, f1, spins = 0, nap = 0;
+  uint64_t t0 = 0;
+  for (;;) {
+    asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(a), "=r"(f0), "=r"(b), "=r"(f1)
+                 : "l"(line)
+                 : "memory");
+    if (f0 == epoch && f1 == epoch) {
+      *out = (uint64_t)a | ((uint64_t)b << 32);
+      return true;
+    }
+    if (++spins > 4) {
+      nap = nap ? min(2 * nap, 512u) : 32u;
+      __nanosleep(nap);
+    }
+    if ((spins & 255) == 0) {
+      const uint64_t now = globaltimer();
+      if (t0 == 0) t0 = now;
+      if ((int64_t)(now - t0) > timeout_ns || *(volatile int32_t*)err != 0) return false;
+    }
   }
-  for (; k < L; k += nt) ll_store(dst + k, ll_load8(src, k << 3, n, al), epoch);
 }
-// Poll this thread's lines until both halves carry `epoch`, then store the
-// payload into the local destination.  Polls back off (up to ~0.5 us) so that
-// CTAs waiting on large landing regions do not flood L2 with requests while
-// the NVLink writes are arriving.  False on timeout / peer error.
-__device__ __forceinline__ bool ll_recv(char* __restrict__ dst, const uint4* src, int64_t n,
-                                        uint32_t epoch, int64_t timeout_ns, int32_t* err) {
-  const int64_t L = (n + 7) >> 3;
-  const bool al = ((uintptr_t)dst & 7) == 0;
-  for (int64_t k = threadIdx.x; k < L; k += blockDim.x) {
-    uint32_t a, f0, b, f1, spins = 0, nap = 0;
-    uint64_t t0 = 0;
-    for (;;) {
-      asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(a), "=r"(f0), "=r"(b), "=r"(f1)
-                   : "l"(src + k)
-                   : "memory");
-      if (f0 == epoch && f1 == epoch) break;
-      if (++spins > 4) {
-        nap = nap ? min(2 * nap, 512u) : 32u;
-        __nanosleep(nap);
+// One LL-mode piece, all threads: thread k produces payload bytes [8k, 8k+8)
+// -- gathered from plain memory or from the one or two source lines they span
+// (polled) -- and stores them as one destination line (8-aligned payload
+// address) or as plain bytes.  Plain sources: 4 lines in flight per thread.
+__device__ __forceinline__ bool ll_piece(const char* sbase, char* dbase, const DevPiece& q,
+                                         uint32_t epoch, int64_t timeout_ns, int32_t* err) {
+  const bool sll = q.kind & kLLSrc, dll = q.kind & kLLDst;
+  const int64_t n = q.nbytes, L = (n + 7) >> 3, nt = blockDim.x;
+  const uint4* sl = reinterpret_cast<const uint4*>(sbase);
+  uint4* dl = reinterpret_cast<uint4*>(dbase) + (q.dst_off >> 3);
+  char* dp = dbase + q.dst_off;
+  int64_t k = threadIdx.x;
+  if (!sll) {
+    const char* sp = sbase + q.src_off;
+    constexpr int kU = 4;
+    for (; k + (kU - 1) * nt < L; k += kU * nt) {
+      uint64_t v[kU];
+#pragma unroll
+      for (int j = 0; j < kU; ++j) {
+        const int64_t b = (k + j * nt) << 3;
+        v[j] = plain_load8(sp + b, (int)min((int64_t)8, n - b));
       }
-      if ((spins & 255) == 0) {
-        const uint64_t now = globaltimer();
-        if (t0 == 0) t0 = now;
-        if ((int64_t)(now - t0) > timeout_ns || *(volatile int32_t*)err != 0) return false;
+#pragma unroll
+      for (int j = 0; j < kU; ++j) {
+        const int64_t b = (k + j * nt) << 3;
+        if (dll) ll_store(dl + k + j * nt, v[j], epoch);
+        else plain_store8(dp + b, v[j], (int)min((int64_t)8, n - b));
       }
     }
-    const int64_t bb = k << 3;
-    if (al && bb + 8 <= n) {
-      *reinterpret_cast<uint2*>(dst + bb) = make_uint2(a, b);
+  }
+  for (; k < L; k += nt) {
+    const int64_t b = k << 3;
+    const int nb = (int)min((int64_t)8, n - b);
+    uint64_t v;
+    if (sll) {
+      const int64_t pa = q.src_off + b;
+      const int sh = (int)(pa & 7);
+      uint64_t x;
+      if (!ll_poll(sl + (pa >> 3), epoch, timeout_ns, err, &x)) return false;
+      v = x >> (8 * sh);
+      if (sh && sh + nb > 8) {
+        uint64_t y;
+        if (!ll_poll(sl + (pa >> 3) + 1, epoch, timeout_ns, err, &y)) return false;
+        v |= y << (64 - 8 * sh);
+      }
     } else {
-      for (int j = 0; j < 8 && bb + j < n; ++j) dst[bb + j] = (char)(((j < 4 ? a : b) >> (8 * (j & 3))) & 0xff);
+      v = plain_load8(sbase + q.src_off + b, nb);
     }
+    if (dll) ll_store(dl + k, v, epoch);
+    else plain_store8(dp + b, v, nb);
   }
   return true;
 }
@@ -468,18 +501,15 @@ __device__ __forceinline__ void exec_body(const KParams& p, const uint32_t epoch
       __syncthreads();
       if (s_abort) return;
       // LL pieces (any size) and small copies: all threads, in program order
-      // (a CTA's LL sends precede its LL receives)
+      // (same-step decodes are last in every CTA's step)
       for (int i = 0; i < n; ++i) {
         const DevPiece& q = s_pc[i];
-        if (q.kind == kLLSend) {  // landing region of this epoch's parity on GPU h
-          const int h = q.dst_loc - (1 + 2 * p.G);
-          ll_send(reinterpret_cast<uint4*>(p.base[q.dst_loc] + q.dst_off + (epoch & 1) * p.ll_half[h]),
-                  p.base[q.src_loc] + q.src_off, q.nbytes, epoch);
-        } else if (q.kind == kLLRecv) {
-          if (!ll_recv(p.base[q.dst_loc] + q.dst_off,
-                       reinterpret_cast<const uint4*>(p.base[q.src_loc] + q.src_off +
-                                                      (epoch & 1) * p.ll_half[p.rank]),
-                       q.nbytes, epoch, p.timeout_ns, p.err)) {
+        if (q.kind != kCopy) {  // LL regions: this epoch's parity
+          const char* sb = p.base[q.src_loc];
+          char* db = p.base[q.dst_loc];
+          if (q.kind & kLLSrc) sb += (epoch & 1) * p.ll_half[p.rank];
+          if (q.kind & kLLDst) db += (epoch & 1) * p.ll_half[q.dst_loc - (1 + 2 * p.G)];
+          if (!ll_piece(sb, db, q, epoch, p.timeout_ns, p.err)) {
             atomicCAS(p.err, 0, (int32_t)A2A_ERR_TIMEOUT);
             s_abort = 1;
           }

@@ -26,10 +26,12 @@ inline int loc_recv(int gpu) { return 1 + gpu; }
 inline int loc_scratch(int gpu, int G) { return 1 + G + gpu; }
 inline int loc_ll(int gpu, int G) { return 1 + 2 * G + gpu; }
 
-// piece kinds (A2A_PROTO_LL): plain copy, LL line store to a peer's landing
-// region (offsets: payload byte x of the item <-> line x/8 at 16*(x/8)), LL
-// line poll + store of the payload into the local destination
-enum : int32_t { kCopy = 0, kLLSend = 1, kLLRecv = 2 };
+// piece kinds (bits): kLLDst = the destination is LL lines of a landing region,
+// kLLSrc = the source is LL lines (polled until they carry the epoch); LL
+// offsets are payload addresses: payload byte x of a region lives in line x/8
+// (bytes 16*(x/8) .. +16).  kDecode marks a same-step decode of remote lines
+// into recv (ordering only: last in its step).
+enum : int32_t { kCopy = 0, kLLDst = 1, kLLSrc = 2, kDecode = 4 };
 
 // One contiguous byte copy of one hop-op (or self-shard copy), 48 bytes.
 struct DevItem {
@@ -41,7 +43,7 @@ struct DevItem {
   int32_t dst_loc;
   int32_t edge;      // schedule edge id (-1: self-shard copy, not a link)
   int16_t dst_gpu;
-  int16_t kind;      // kCopy / kLLSend / kLLRecv
+  int16_t kind;      // kCopy or kLLDst / kLLSrc / kDecode bits
 };
 static_assert(sizeof(DevItem) == 48, "DevItem layout");
 
@@ -61,7 +63,7 @@ struct DevPiece {
   int32_t nbytes;
   int32_t edge;
   int16_t src_loc, dst_loc;
-  int32_t kind;      // kCopy / kLLSend / kLLRecv
+  int32_t kind;      // kCopy or kLLDst / kLLSrc / kDecode bits
 };
 static_assert(sizeof(DevPiece) == 32, "DevPiece layout");
 

@@ -88,6 +88,9 @@ std::string fmt_missing(int t, int src, int64_t c, int s, int d) {
 
 }  // namespace
 
+static int order_items(Plan& P, std::vector<std::vector<std::vector<DevItem>>>& per, int64_t split_bytes);
+static int build_ll_items(Plan& P, const std::function<int32_t(int32_t, int32_t)>& edge_of);
+
 static int build_plan(Plan& P, const a2a_schedule_desc* D) {
   if (!D) return fail(A2A_ERR_INVALID, "null descriptor");
   if (D->n_nodes < 1) return fail(A2A_ERR_INVALID, "n_nodes must be >= 1");
@@ -104,7 +107,7 @@ static int build_plan(Plan& P, const a2a_schedule_desc* D) {
   const int n = D->n_nodes, T = D->n_steps, E = D->n_edges, G = D->n_gpus;
   const int64_t Q = D->q, m = D->m_bytes;
   P.n = n; P.T = T; P.Q = (int32_t)Q; P.E = E; P.G = G; P.m = m; P.flags = D->flags;
-  P.ll = (D->flags & A2A_PROTO_LL) && G > 1;
+  P.ll = (D->flags & A2A_PROTO_LL) != 0;
   P.T_exec = std::max(T, 1);
   P.edge_uv.assign(D->edge_uv, D->edge_uv + 2 * (size_t)E);
   P.cap.resize(E, 1.0);
@@ -215,6 +218,7 @@ static int build_plan(Plan& P, const a2a_schedule_desc* D) {
     P.info[g].send_bytes = (int64_t)P.info[g].n_local_nodes * n * m;
     P.info[g].recv_bytes = P.info[g].send_bytes;
   }
+  if (P.ll) return build_ll_items(P, edge_of);
 
   // ---- scratch layout: per (v,s,d) the merged intervals ever written there.
   // A slot starts at the same residue mod 64 as the shard offset of its first
@@ -343,12 +347,6 @@ static int build_plan(Plan& P, const a2a_schedule_desc* D) {
   // ---- copy items per GPU per step
   const int TE = P.T_exec;
   P.tables.assign(G, GpuTables{});
-  // A2A_PROTO_LL: each cross-GPU item gets a landing slot of 16 B per 8 payload
-  // bytes in the destination GPU's LL region (after its forwarding scratch)
-  P.ll_off.assign(G, 0);
-  P.ll_half.assign(G, 0);
-  std::vector<int64_t> ll_cursor(G, 0);
-  for (int g = 0; g < G; ++g) P.ll_off[g] = P.info[g].scratch_bytes;
   P.link_bytes.assign((size_t)T * E, 0);
   std::vector<std::vector<std::vector<DevItem>>> per(G, std::vector<std::vector<DevItem>>(TE));
   for (int t = 0; t < T; ++t) {
@@ -383,20 +381,6 @@ static int build_plan(Plan& P, const a2a_schedule_desc* D) {
         if (!slot_addr(o.dst, o.s, o.d, o.c0, lo, &it.dst_off))
           return fail(A2A_ERR_INVALID, "internal: destination chunk has no scratch slot");
       }
-      if (P.ll && h != g) {
-        // sender: payload -> LL lines on h; receiver (h, same step): lines -> destination
-        DevItem rc = it;
-        const int64_t slot = ll_cursor[h];
-        ll_cursor[h] += 2 * ((it.nbytes + 7) & ~(int64_t)7);
-        it.dst_loc = loc_ll(h, G);
-        it.dst_off = slot;
-        it.kind = kLLSend;
-        rc.src_loc = loc_ll(h, G);
-        rc.src_off = slot;
-        rc.edge = -1;
-        rc.kind = kLLRecv;
-        per[h][t].push_back(rc);
-      }
       per[g][t].push_back(it);
       auto& Ig = P.info[g];
       Ig.hop_bytes += it.nbytes;
@@ -422,18 +406,18 @@ static int build_plan(Plan& P, const a2a_schedule_desc* D) {
       P.info[g].local_bytes += m;
     }
   }
-  for (int g = 0; g < G; ++g) {
-    P.ll_half[g] = (ll_cursor[g] + 4095) & ~(int64_t)4095;
-    P.info[g].scratch_bytes += 2 * P.ll_half[g];   // epoch parity 0 | 1
-  }
-  // Order each (gpu, step) list.  Default: grouped by destination GPU
-  // (stable), so CTAs cover few destinations each; LL receive items last, so
-  // every CTA issues its step's sends before it polls (deadlock freedom).  A2A_INTERLEAVE: items are
-  // split into <= split_bytes pieces (multiples of 64 B, alignment kept) and
-  // the destination classes are merged in proportion to their byte totals, so
-  // every CTA range drives every NVLink peer (and local HBM) at once.
+  return order_items(P, per, D->split_bytes);
+}
+
+// Per (gpu, step) item order + byte prefixes.  Default: grouped by destination
+// GPU (stable), so CTAs cover few destinations each.  A2A_INTERLEAVE: items are
+// split into <= split_bytes pieces (multiples of 64 B, alignment kept) and
+// the destination classes are merged in proportion to their byte totals, so
+// every CTA range drives every NVLink peer (and local HBM) at once.
+static int order_items(Plan& P, std::vector<std::vector<std::vector<DevItem>>>& per, int64_t split_bytes) {
+  const int G = P.G, TE = P.T_exec;
   const bool interleave = (P.flags & A2A_INTERLEAVE) && G > 1;
-  const int64_t split = std::max<int64_t>(64, (D->split_bytes > 0 ? D->split_bytes : 262144) & ~63LL);
+  const int64_t split = std::max<int64_t>(64, (split_bytes > 0 ? split_bytes : 262144) & ~63LL);
   for (int g = 0; g < G; ++g) {
     auto& tb = P.tables[g];
     tb.step_begin.assign(TE + 1, 0);
@@ -441,8 +425,10 @@ static int build_plan(Plan& P, const a2a_schedule_desc* D) {
     for (int t = 0; t < TE; ++t) {
       auto& L = per[g][t];
       std::stable_sort(L.begin(), L.end(), [&](const DevItem& a, const DevItem& b) {
-        int ka = a.kind == kLLRecv ? G : (a.dst_gpu - g + G) % G;
-        int kb = b.kind == kLLRecv ? G : (b.dst_gpu - g + G) % G;
+        // LL same-step decodes last: every CTA stores its step's lines before
+        // it polls lines of the same step (deadlock freedom)
+        int ka = (a.kind & kDecode) ? G : (a.dst_gpu - g + G) % G;
+        int kb = (b.kind & kDecode) ? G : (b.dst_gpu - g + G) % G;
         return ka < kb;
       });
       if (interleave) {
@@ -491,6 +477,125 @@ static int build_plan(Plan& P, const a2a_schedule_desc* D) {
   return A2A_OK;
 }
 
+// ---- A2A_PROTO_LL items ------------------------------------------------------
+//
+// Every hop lands as LL lines (16-byte {4 data bytes, epoch, 4 data bytes,
+// epoch}) in a fresh slot of the destination node's GPU, and every forwarding
+// hop polls its source lines directly: no scratch copy, no step flag, no
+// fence anywhere on the path.  Hop 0 reads the caller's send buffer, the last
+// hop writes plain bytes into recv.  LL offsets are payload addresses (byte x
+// of a region's payload lives in line x/8); slots start at multiples of 8.  A
+// forwarding op whose chunks arrived through several earlier ops is split at
+// those arrivals, so each item reads one slot.  The landing region of each GPU
+// is double-buffered by epoch parity (see the kernel's lagged entry).
+static int build_ll_items(Plan& P, const std::function<int32_t(int32_t, int32_t)>& edge_of) {
+  const int n = P.n, T = P.T, G = P.G, TE = P.T_exec;
+  const int64_t Q = P.Q, m = P.m;
+  struct Arrival { int32_t c0, c1, t; int64_t pa; };   // chunks [c0,c1) at payload address pa
+  std::unordered_map<uint64_t, std::vector<Arrival>> at;   // (node, s, d) -> arrivals
+  std::vector<int64_t> cursor(G, 0);                        // landing payload bytes per GPU
+  std::vector<std::vector<std::vector<DevItem>>> per(G, std::vector<std::vector<DevItem>>(TE));
+  P.tables.assign(G, GpuTables{});
+  P.link_bytes.assign((size_t)T * P.E, 0);
+  for (int t = 0; t < T; ++t) {
+    std::vector<std::pair<uint64_t, Arrival>> fresh;   // usable from step t + 1 on
+    for (int64_t i : P.step_ops[t]) {
+      const a2a_op& o = P.ops[i];
+      if (o.c0 >= o.c1) continue;
+      const int e = edge_of(o.src, o.dst);
+      P.link_bytes[(size_t)t * P.E + e] += chunk_off(o.c1, m, Q) - chunk_off(o.c0, m, Q);
+      if (o.src == o.d && o.src != o.s)
+        return fail(A2A_ERR_INVALID, "A2A_PROTO_LL: the schedule forwards chunks out of their destination");
+      const int g = P.node_gpu[o.src], h = P.node_gpu[o.dst];
+      // source segments: [ca, cb) read from send (hop 0) or from one arrival slot
+      for (int32_t ca = o.c0; ca < o.c1;) {
+        int32_t cb = o.c1;
+        int src_loc = loc_send();
+        int64_t src_off = 0, lo = chunk_off(ca, m, Q);
+        if (o.src == o.s) {
+          src_off = ((int64_t)P.local_idx[o.src] * n + o.d) * m + lo;
+        } else {
+          const Arrival* best = nullptr;
+          auto it = at.find(key3(o.src, o.s, o.d, n));
+          if (it != at.end())
+            for (const Arrival& a : it->second)
+              if (a.t < t && a.c0 <= ca && ca < a.c1 && (!best || a.c1 > best->c1)) best = &a;
+          if (!best) return fail(A2A_ERR_INVALID, "internal: LL source chunk has no arrival");
+          cb = std::min(cb, best->c1);
+          src_loc = loc_ll(g, G);
+          src_off = best->pa + (lo - chunk_off(best->c0, m, Q));
+        }
+        const int64_t hi = chunk_off(cb, m, Q);
+        if (o.dst != o.d)   // arrival record even for empty byte ranges (m < Q)
+          fresh.push_back({key3(o.dst, o.s, o.d, n), Arrival{ca, cb, t, cursor[h]}});
+        if (hi > lo) {
+          DevItem it{};
+          it.nbytes = hi - lo;
+          it.edge = e;
+          it.dst_gpu = (int16_t)h;
+          it.src_loc = src_loc;
+          it.src_off = src_off;
+          it.kind = src_loc == loc_send() ? kCopy : kLLSrc;
+          const int64_t recv_off = ((int64_t)P.local_idx[o.dst] * n + o.s) * m + lo;
+          if (o.dst == o.d && h == g) {   // local final hop: plain bytes into recv
+            it.dst_loc = loc_recv(h);
+            it.dst_off = recv_off;
+          } else {
+            it.dst_loc = loc_ll(h, G);
+            it.dst_off = cursor[h];
+            it.kind |= kLLDst;
+            if (o.dst == o.d) {   // remote final hop: h decodes the lines into recv in the same step
+              DevItem dc{};
+              dc.nbytes = it.nbytes;
+              dc.edge = -1;
+              dc.dst_gpu = (int16_t)h;
+              dc.src_loc = loc_ll(h, G);
+              dc.src_off = cursor[h];
+              dc.dst_loc = loc_recv(h);
+              dc.dst_off = recv_off;
+              dc.kind = kLLSrc | kDecode;
+              per[h][t].push_back(dc);
+            }
+            cursor[h] += (it.nbytes + 7) & ~(int64_t)7;
+          }
+          per[g][t].push_back(it);
+          auto& Ig = P.info[g];
+          Ig.hop_bytes += it.nbytes;
+          if (h != g) {
+            Ig.egress_bytes += it.nbytes;
+            P.info[h].ingress_bytes += it.nbytes;
+          } else {
+            Ig.local_bytes += it.nbytes;
+          }
+        }
+        ca = cb;
+      }
+    }
+    for (auto& f : fresh) at[f.first].push_back(f.second);
+  }
+  if ((P.flags & A2A_COPY_SELF) && m > 0) {
+    for (int v = 0; v < n; ++v) {
+      const int g = P.node_gpu[v];
+      DevItem it{};
+      it.src_loc = loc_send();
+      it.dst_loc = loc_recv(g);
+      it.src_off = it.dst_off = ((int64_t)P.local_idx[v] * n + v) * m;
+      it.nbytes = m;
+      it.edge = -1;
+      it.dst_gpu = (int16_t)g;
+      per[g][0].push_back(it);
+      P.info[g].local_bytes += m;
+    }
+  }
+  P.ll_off.assign(G, 0);
+  P.ll_half.assign(G, 0);
+  for (int g = 0; g < G; ++g) {
+    P.ll_half[g] = (2 * cursor[g] + 4095) & ~(int64_t)4095;   // line bytes per parity
+    P.info[g].scratch_bytes = 2 * P.ll_half[g];               // epoch parity 0 | 1
+  }
+  return order_items(P, per, 0);
+}
+
 // ---- CTA split and exact producer dependencies ---------------------------
 //
 // Every GPU splits each step's concatenated item bytes into nC contiguous
@@ -509,14 +614,9 @@ struct Seg {
 // than it can push them over NVLink, so equal-byte ranges would leave the
 // NVLink CTAs finishing last.  Boundaries inside an item fall on 64-byte
 // multiples (the item end excepted), so every piece keeps src == dst (mod 64).
-// byte offsets of the piece starting at payload byte x of an item (LL landing
-// lines carry 8 payload bytes per 16 bytes)
-inline int64_t piece_src(const DevItem& it, int64_t x) {
-  return it.src_off + (it.kind == kLLRecv ? 2 * x : x);
-}
-inline int64_t piece_dst(const DevItem& it, int64_t x) {
-  return it.dst_off + (it.kind == kLLSend ? 2 * x : x);
-}
+// offsets of the piece starting at byte x of an item (LL: payload addresses)
+inline int64_t piece_src(const DevItem& it, int64_t x) { return it.src_off + x; }
+inline int64_t piece_dst(const DevItem& it, int64_t x) { return it.dst_off + x; }
 template <typename F>
 void for_each_piece(const GpuTables& tb, int g, int t, int nC, int wr, F&& f) {
   const int64_t b0 = tb.step_begin[t], b1 = tb.step_begin[t + 1];
@@ -560,7 +660,7 @@ int build_sync(Plan& P, int nC) {
   for (int g = 0; g < G; ++g) {
     for (int t = 0; t < TE; ++t) {
       for_each_piece(P.tables[g], g, t, nC, P.remote_weight, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
-        if (it.kind == kLLSend) return;   // no flag: the receiver polls the lines
+        if (P.ll) return;   // LL: no flags, consumers poll the lines
         S.dst_mask[g][(size_t)t * nC + c] |= 1u << it.dst_gpu;
         const int cls = (it.dst_loc == loc_recv(it.dst_gpu)) ? 0 : 1;
         segs[it.dst_gpu][cls].push_back(
@@ -639,7 +739,7 @@ int build_sync(Plan& P, int nC) {
     auto& per = per_all[h];
     for (int t = 0; t < TE; ++t) {
       for_each_piece(P.tables[h], h, t, nC, P.remote_weight, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
-        if (it.src_loc == loc_send() || it.kind == kLLRecv) return;
+        if (it.src_loc == loc_send() || P.ll) return;
         const int cls = (it.src_loc == loc_recv(h)) ? 0 : 1;
         const int64_t a = it.src_off + x0, b = it.src_off + x1;
         const auto& v = segs[h][cls];
@@ -709,9 +809,9 @@ int build_sync(Plan& P, int nC) {
 // Host emulation of the device protocol: CTAs of all GPUs run their step
 // ranges in a random interleaving constrained ONLY by the dependency lists;
 // memory is host memory.  Insufficient dependencies show up as wrong bytes.
-// A2A_PROTO_LL: a CTA runs its step's pieces in program order (one piece per
-// emulation event) and blocks at an LL receive until every line it polls
-// carries the epoch; lines are stored and decoded in the device format.
+// A CTA runs its step's pieces in program order (one piece per emulation
+// event).  A2A_PROTO_LL: a piece with an LL source blocks until every line it
+// polls carries the epoch; lines are stored and decoded in the device format.
 static int emulate(Plan& P, int nC, uint8_t* const* send, uint8_t* const* recv, uint64_t seed) {
   int rc = build_sync(P, nC);
   if (rc) return rc;
@@ -742,9 +842,11 @@ static int emulate(Plan& P, int nC, uint8_t* const* send, uint8_t* const* recv, 
     if (loc < 1 + 2 * G) return scratch[loc - 1 - G].data();
     return ll[loc - 1 - 2 * G].data();
   };
+  // LL payload address x -> byte of the line region
+  auto ll_byte = [](int64_t x) -> int64_t { return 16 * (x >> 3) + ((x & 7) < 4 ? (x & 7) : (x & 7) + 4); };
   auto lines_ready = [&](int g, const Piece& pc) {
-    const uint8_t* L = base(g, pc.src_loc) + pc.src;
-    for (int64_t k = 0; k < (pc.n + 7) / 8; ++k) {
+    const uint8_t* L = base(g, pc.src_loc);
+    for (int64_t k = pc.src >> 3; k <= (pc.src + pc.n - 1) >> 3; ++k) {
       uint32_t f0, f1;
       std::memcpy(&f0, L + 16 * k + 4, 4);
       std::memcpy(&f1, L + 16 * k + 12, 4);
@@ -771,7 +873,7 @@ static int emulate(Plan& P, int nC, uint8_t* const* send, uint8_t* const* recv, 
             ok = flag[g][P.sync.wait_idx[g][i]];
         }
         const Piece& pc = work[g][c][t][pos[g][c]];
-        if (ok && pc.kind == kLLRecv) ok = lines_ready(g, pc);
+        if (ok && (pc.kind & kLLSrc)) ok = lines_ready(g, pc);
         if (ok) ready.emplace_back(g, c);
       }
     if (!left) break;
@@ -779,21 +881,25 @@ static int emulate(Plan& P, int nC, uint8_t* const* send, uint8_t* const* recv, 
     auto [g, c] = ready[rnd() % ready.size()];
     const int t = next[g][c];
     const Piece& pc = work[g][c][t][pos[g][c]];
-    uint8_t* d = base(g, pc.dst_loc) + pc.dst;
-    const uint8_t* sp = base(g, pc.src_loc) + pc.src;
-    if (pc.kind == kLLSend) {
+    std::vector<uint8_t> buf((size_t)pc.n);
+    const uint8_t* sb = base(g, pc.src_loc);
+    if (pc.kind & kLLSrc) {
+      for (int64_t j = 0; j < pc.n; ++j) buf[j] = sb[ll_byte(pc.src + j)];
+    } else {
+      std::memcpy(buf.data(), sb + pc.src, (size_t)pc.n);
+    }
+    uint8_t* db = base(g, pc.dst_loc);
+    if (pc.kind & kLLDst) {   // whole lines (dst payload address is a multiple of 8)
       for (int64_t k = 0; k < (pc.n + 7) / 8; ++k) {
         uint8_t line[16] = {0};
         const int64_t w = std::min<int64_t>(8, pc.n - 8 * k);
-        for (int64_t j = 0; j < w; ++j) line[(j < 4 ? 0 : 4) + j] = sp[8 * k + j];
+        for (int64_t j = 0; j < w; ++j) line[(j < 4 ? 0 : 4) + j] = buf[8 * k + j];
         std::memcpy(line + 4, &kEpoch, 4);
         std::memcpy(line + 12, &kEpoch, 4);
-        std::memcpy(d + 16 * k, line, 16);
+        std::memcpy(db + 16 * ((pc.dst >> 3) + k), line, 16);
       }
-    } else if (pc.kind == kLLRecv) {
-      for (int64_t j = 0; j < pc.n; ++j) d[j] = sp[16 * (j / 8) + ((j & 7) < 4 ? 0 : 4) + (j & 7)];
     } else {
-      std::memmove(d, sp, (size_t)pc.n);
+      std::memcpy(db + pc.dst, buf.data(), (size_t)pc.n);
     }
     if (++pos[g][c] < (int)work[g][c][t].size()) continue;
     uint32_t mask = P.sync.dst_mask[g][(size_t)t * nC + c];
@@ -1284,17 +1390,17 @@ int a2a_plan_check_bounds(a2a_plan* plan, int32_t num_ctas) {
     if (loc == loc_send()) return P.info[g].send_bytes;
     if (loc >= 1 && loc < 1 + G) return P.info[loc - 1].recv_bytes;
     if (loc >= 1 + G && loc < 1 + 2 * G) return P.info[loc - 1 - G].scratch_bytes;
-    if (P.ll && loc >= 1 + 2 * G && loc < 1 + 3 * G) return P.ll_half[loc - 1 - 2 * G];
+    // LL landing region: payload capacity (lines are 16 bytes per 8 payload bytes)
+    if (P.ll && loc >= 1 + 2 * G && loc < 1 + 3 * G) return P.ll_half[loc - 1 - 2 * G] / 2;
     return -1;
   };
-  // LL lines: 16 bytes per 8 payload bytes on the landing-region side
   auto check = [&](int g, int sl, int64_t so, int dl, int64_t dof, int64_t n, int kind = kCopy) -> bool {
-    const int64_t ss = size_of(g, sl), ds = size_of(g, dl), nl = 2 * ((n + 7) & ~(int64_t)7);
-    const int64_t ns = kind == kLLRecv ? nl : n, nd = kind == kLLSend ? nl : n;
-    if (kind == kLLSend && (dl < loc_ll(0, G) || dl >= loc_ll(G, G) || dl == loc_ll(g, G))) return false;
-    if (kind == kLLRecv && sl != loc_ll(g, G)) return false;
-    if (kind == kCopy && dl >= 1 + 2 * G) return false;
-    return n > 0 && ss >= 0 && ds >= 0 && so >= 0 && dof >= 0 && so + ns <= ss && dof + nd <= ds;
+    const bool sll = sl >= loc_ll(0, G) && sl < loc_ll(G, G), dll = dl >= loc_ll(0, G) && dl < loc_ll(G, G);
+    if (sll != ((kind & kLLSrc) != 0) || dll != ((kind & kLLDst) != 0)) return false;
+    if (dll && (dof & 7)) return false;                         // stores whole lines
+    const int64_t ss = size_of(g, sl), ds = size_of(g, dl);
+    const int64_t nd = dll ? ((n + 7) & ~(int64_t)7) : n;
+    return n > 0 && ss >= 0 && ds >= 0 && so >= 0 && dof >= 0 && so + n <= ss && dof + nd <= ds;
   };
   char buf[200];
   for (int g = 0; g < G; ++g) {
@@ -1310,8 +1416,8 @@ int a2a_plan_check_bounds(a2a_plan* plan, int32_t num_ctas) {
       for (const DevPiece& q : P.sync.pieces[g])
         if (!check(g, q.src_loc, q.src_off, q.dst_loc, q.dst_off, q.nbytes, q.kind) ||
             !(q.src_loc == loc_send() || q.src_loc == loc_recv(g) || q.src_loc == loc_scratch(g, G) ||
-              (q.kind == kLLRecv && q.src_loc == loc_ll(g, G))) ||
-            (q.kind == kLLRecv && !(q.dst_loc == loc_recv(g) || q.dst_loc == loc_scratch(g, G)))) {
+              q.src_loc == loc_ll(g, G)) ||
+            (P.ll && !(q.kind & kLLDst) && q.dst_loc != loc_recv(g))) {   // LL: plain stores stay local
           snprintf(buf, sizeof buf, "gpu %d: piece out of bounds (src %d+%lld, dst %d+%lld, %d B)", g,
                    q.src_loc, (long long)q.src_off, q.dst_loc, (long long)q.dst_off, q.nbytes);
           return fail(A2A_ERR_INVALID, buf);

@@ -254,7 +254,7 @@ def test_call_order_errors(artifacts):
 
 
 @pytest.mark.parametrize("name", ["gk8_2", "torus2x4_h2", "ts_hypercube3"])
-@pytest.mark.parametrize("sched", ["static", "cp", "mix"])
+@pytest.mark.parametrize("sched", ["static", "cp", "mix", "ll"])
 @pytest.mark.parametrize("engine", ["tma", "lsu"])
 def test_cuda_graph_capture_and_replay(name, sched, engine, artifacts):
     """Executes captured into a CUDA graph replay as fresh all-to-alls: the
@@ -264,9 +264,9 @@ def test_cuda_graph_capture_and_replay(name, sched, engine, artifacts):
     from paper_2309_13541_b200.executor import Plan
     a = artifacts(name)
     m = 4096 + 64
-    with Plan(a.g, a.sched, m=m) as p:
+    with Plan(a.g, a.sched, m=m, protocol="ll" if sched == "ll" else "simple") as p:
         p.set_engine(engine)
-        if sched != "static":
+        if sched not in ("static", "ll"):
             p.set_schedule(sched, 4096)
         p.bind(0)
         s = torch.empty((a.g.n, a.g.n, m), dtype=torch.uint8, device="cuda")
@@ -287,3 +287,28 @@ def test_cuda_graph_capture_and_replay(name, sched, engine, artifacts):
         p.execute(s, r1)
         p.sync()
         assert torch.equal(r1, s.transpose(0, 1).contiguous())
+
+
+@pytest.mark.parametrize("name", SMALL)
+@pytest.mark.parametrize("m", [7, 1000, 4096 + 5, 65536])
+@pytest.mark.parametrize("engine", ["tma", "lsu"])
+def test_ll_protocol_bit_exact(name, m, engine, artifacts):
+    """A2A_PROTO_LL on one GPU: every hop through polled landing lines (no
+    flags); bit-exact vs the oracle over repeated executes (both landing
+    parities), device link counters equal the schedule."""
+    from paper_2309_13541_b200.executor import Plan
+    from replay_bytes import replay_bytes
+    a = artifacts(name)
+    with Plan(a.g, a.sched, m=m, protocol="ll") as p:
+        p.set_engine(engine)
+        p.bind(0)
+        p.set_timeout(10.0)
+        for rep in range(3):
+            send = _send(a.g.n, m, seed=rep + 11)
+            _, want, _ = replay_bytes(a.g, a.sched, send, m)
+            s = torch.from_numpy(send).cuda()
+            r = torch.zeros_like(s)
+            p.execute(s, r, count_links=True)
+            p.sync()
+            assert np.array_equal(r.cpu().numpy(), want), rep
+        assert np.array_equal(p.read_link_counters(), 3 * p.link_bytes())

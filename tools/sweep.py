@@ -35,7 +35,8 @@ PRESETS = {
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--preset", default=None)
-    ap.add_argument("--cases", default="", help="config:m,config:m,...")
+    ap.add_argument("--cases", default="",
+                    help="config:m[@schedule],... (a per-case schedule overrides --schedule)")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--out", default=None)
@@ -46,10 +47,11 @@ def main(argv=None):
     ap.add_argument("--schedule", default=None,
                     help="static | dynamic[:bytes] | auto; default: $A2A_SCHED or static")
     a = ap.parse_args(argv)
-    cases = list(PRESETS.get(a.preset, [])) if a.preset else []
+    cases = [(name, m, None) for name, m in PRESETS.get(a.preset, [])] if a.preset else []
     for c in filter(None, a.cases.split(",")):
+        c, _, case_sched = c.partition("@")
         name, m = c.split(":")
-        cases.append((name, int(m)))
+        cases.append((name, int(m), case_sched or None))
 
     import bench
     from paper_2309_13541_b200.artifacts import list_artifacts, load_artifact
@@ -57,7 +59,7 @@ def main(argv=None):
 
     ctx = bench.Ctx()
     have = set(list_artifacts())
-    for name, m in cases:
+    for name, m, case_sched in cases:
         rec = {"config": name, "m_bytes": m, "n_gpus": ctx.world}
         if name not in have:
             rec["skipped"] = "artifact not generated"
@@ -70,13 +72,13 @@ def main(argv=None):
                 rec["skipped"] = f"needs {mem / 2**30:.1f} GiB per GPU"
             else:
                 t0 = time.time()
-                sched = a.schedule or os.environ.get("A2A_SCHED") or "static"
+                sched = case_sched or a.schedule or os.environ.get("A2A_SCHED") or "static"
                 tune = None
                 if sched == "auto":
                     sched, tune = bench.autotune_schedule(ctx, art, m, placement=a.placement,
                                                           num_ctas=a.num_ctas)
                 r = bench.measure(ctx, art, m, a.steps, a.warmup, nccl=not a.no_nccl,
-                                  e2e=False, clocks=True, placement=a.placement, schedule=sched,
+                                  e2e=False, clocks=os.environ.get("A2A_NO_CLOCKS") != "1", placement=a.placement, schedule=sched,
                                   num_ctas=a.num_ctas)
                 rec["schedule"] = sched
                 rec["schedule_autotune_ms"] = tune
@@ -90,6 +92,8 @@ def main(argv=None):
                     "roofline": r["roofline"], "nccl": r["nccl"], "recv_ok": r["recv_ok"],
                     "clocks": r["clocks"], "sync_flags": r["sync"],
                     "host_enqueue_us_per_step": r["host_enqueue_us_per_step"],
+                    "flush_ms_p50_by_rank": r["flush_ms_p50_by_rank"],
+                    "step_period_ms_p50_by_rank": r["step_period_ms_p50_by_rank"],
                     "kernel_timeline": r["kernel_timeline"],
                     "egress_max_bytes": r["egress_max"], "scratch_bytes": r["scratch_bytes"],
                     "placement": a.placement, "l2": r["l2"], "num_ctas": r["num_ctas"],
