@@ -187,6 +187,10 @@ __device__ __forceinline__ void ll_store(uint4* dst, uint64_t v, uint32_t epoch)
                "r"(epoch), "r"((uint32_t)(v >> 32)), "r"(epoch)
                : "memory");
 }
+#ifndef A2A_LL_SPIN
+#define A2A_LL_SPIN 32
+#endif
+constexpr uint32_t kLLSpin = A2A_LL_SPIN;
 // Poll one line until both halves carry `epoch`.  Polls back off (up to
 // ~0.5 us) so that CTAs waiting on large landing regions do not flood L2 with
 // requests while the NVLink writes are arriving.  False on timeout / error.
@@ -203,8 +207,8 @@ __device__ __forceinline__ bool ll_poll(const uint4* line, uint32_t epoch, int64
       *out = (uint64_t)a | ((uint64_t)b << 32);
       return true;
     }
-    if (++spins > 4) {
-      nap = nap ? min(2 * nap, 512u) : 32u;
+    if (++spins > kLLSpin) {   // hot polling first (small shards), then back off
+      nap = nap ? min(2 * nap, 1024u) : 64u;
       __nanosleep(nap);
     }
     if ((spins & 255) == 0) {

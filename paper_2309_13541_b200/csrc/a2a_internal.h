@@ -146,7 +146,7 @@ struct Plan {
   // ---- device binding (a2a_exec.cu)
   bool bound = false, imported = false;
   int32_t rank = -1, device = -1, nC = 0, nT = 1024;
-  int32_t engine = 1, tma_chunk = 32768, tma_stages = 6;   // copy engine (a2a_plan_set_engine)
+  int32_t engine = 1, tma_chunk = 32768, tma_stages = 6;   // copy engine (a2a_plan_set_engine; LSU for LL)
   int32_t n_recv = 1;                           // arena recv buffers (multi-buffering)
   int32_t sync_mode = 2;                        // a2a_plan_set_sync_mode (2: bar.sync + st.release)
   bool coop = true;                             // cooperative launch (A2A_NONCOOP=1: plain, experiments)

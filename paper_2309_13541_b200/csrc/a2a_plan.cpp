@@ -108,6 +108,7 @@ static int build_plan(Plan& P, const a2a_schedule_desc* D) {
   const int64_t Q = D->q, m = D->m_bytes;
   P.n = n; P.T = T; P.Q = (int32_t)Q; P.E = E; P.G = G; P.m = m; P.flags = D->flags;
   P.ll = (D->flags & A2A_PROTO_LL) != 0;
+  if (P.ll) P.engine = 0;   // LL pieces are thread work: the 1024-thread kernel (measured)
   P.T_exec = std::max(T, 1);
   P.edge_uv.assign(D->edge_uv, D->edge_uv + 2 * (size_t)E);
   P.cap.resize(E, 1.0);

@@ -31,10 +31,15 @@ def main():
     art = load_artifact(a.config)
     n, m = art.g.n, a.m
     G_max = min(2, torch.cuda.device_count())
+    variants = [("simple", None), ("ll", None), ("ll", ("tma", 4096, 1)), ("ll", ("lsu", 0, 0))]
     for G in sorted({1, G_max}):
-        for proto in (["simple"] if G == 1 else ["simple", "ll"]):
-            plans = [Plan(art.g, art.sched, m=m, n_gpus=G, protocol=proto).bind(r, device=r)
-                     for r in range(G)]
+        for proto, eng in variants:
+            plans = []
+            for r in range(G):
+                p = Plan(art.g, art.sched, m=m, n_gpus=G, protocol=proto)
+                if eng:
+                    p.set_engine(*eng)
+                plans.append(p.bind(r, device=r))
             if G > 1:
                 ptrs = [p.arena_ptr() for p in plans]
                 for p in plans:
@@ -97,7 +102,7 @@ def main():
             t_graph = e0.elapsed_time(e1) * 1e3 / a.iters
             ok = all(torch.equal(recvs[r].cpu(), torch.cat([sends[q].cpu() for q in range(G)])
                                  .transpose(0, 1)[local_nodes(plans[r], r)]) for r in range(G))
-            print(json.dumps({"config": a.config, "m": m, "G": G, "proto": proto,
+            print(json.dumps({"config": a.config, "m": m, "G": G, "proto": proto, "engine": eng,
                               "noncoop": os.environ.get("A2A_NONCOOP", "0"),
                               "b2b_us": round(t_b2b, 2), "graph_us": round(t_graph, 2),
                               "single_us_p50": round(sorted(singles)[len(singles) // 2], 2),
