@@ -1,6 +1,7 @@
 """Host bounds audit of every device copy range (compute-sanitizer is closed on
 this GPU pool; this is its address-math half): all artifacts, 1/2/4/8 GPUs,
-static and dynamic schedules, scratch reuse on/off, odd shard sizes."""
+static and dynamic schedules, scratch reuse on/off, the LL protocol, odd shard
+sizes."""
 from __future__ import annotations
 
 import pytest
@@ -22,6 +23,19 @@ def test_every_copy_range_in_bounds(name, G, sched, reuse, artifacts):
     for m in (1, 1000 + 7, 65536):
         with Plan(a.g, a.sched, m=m, n_gpus=G, reuse_scratch=reuse, placement="optimized") as p:
             p.set_schedule(sched, 0 if sched == "static" else 4096)
+            assert p.check_bounds(37)
+
+
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_ll_ranges_in_bounds(name, G, artifacts):
+    """A2A_PROTO_LL pieces: LL sources/destinations inside the landing regions
+    (payload addresses, whole destination lines), plain stores GPU-local."""
+    a = artifacts(name)
+    if G > a.g.n:
+        pytest.skip("more GPUs than nodes")
+    for m in (1, 1000 + 7, 65536):
+        with Plan(a.g, a.sched, m=m, n_gpus=G, placement="optimized", protocol="ll") as p:
             assert p.check_bounds(37)
 
 
