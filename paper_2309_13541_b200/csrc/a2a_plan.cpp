@@ -1171,7 +1171,10 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
   D.units.assign(G, {});
   for (int g = 0; g < G; ++g) {
     double rb = 0, lb = 0;
-    if (P.sched_mode == 4) {  // one queue in key order; n_remote = 0, no CTA on queue 0
+    // one queue in key order (n_remote = 0, no CTA on queue 0): the mix order,
+    // and any order with a single CTA -- two queues need a CTA each, or a CTA
+    // stuck on one queue could wait for a unit only the other queue holds
+    if (P.sched_mode == 4 || nC < 2) {
       std::vector<int> q;
       for (int t = 0; t < TE; ++t)
         for (int id : per[g][t]) q.push_back(id);

@@ -31,15 +31,17 @@ def main():
     art = load_artifact(a.config)
     n, m = art.g.n, a.m
     G_max = min(2, torch.cuda.device_count())
-    variants = [("simple", None), ("ll", None), ("ll", ("tma", 4096, 1)), ("ll", ("lsu", 0, 0))]
+    ap_ctas = [int(x) for x in os.environ.get("PROBE_CTAS", "0").split(",")]
+    variants = [(proto, eng, c) for proto, eng in
+                [("simple", None), ("ll", None), ("ll", ("tma", 4096, 1))] for c in ap_ctas]
     for G in sorted({1, G_max}):
-        for proto, eng in variants:
+        for proto, eng, nctas in variants:
             plans = []
             for r in range(G):
                 p = Plan(art.g, art.sched, m=m, n_gpus=G, protocol=proto)
                 if eng:
                     p.set_engine(*eng)
-                plans.append(p.bind(r, device=r))
+                plans.append(p.bind(r, device=r, num_ctas=nctas))
             if G > 1:
                 ptrs = [p.arena_ptr() for p in plans]
                 for p in plans:
@@ -103,6 +105,7 @@ def main():
             ok = all(torch.equal(recvs[r].cpu(), torch.cat([sends[q].cpu() for q in range(G)])
                                  .transpose(0, 1)[local_nodes(plans[r], r)]) for r in range(G))
             print(json.dumps({"config": a.config, "m": m, "G": G, "proto": proto, "engine": eng,
+                              "num_ctas": nctas,
                               "noncoop": os.environ.get("A2A_NONCOOP", "0"),
                               "b2b_us": round(t_b2b, 2), "graph_us": round(t_graph, 2),
                               "single_us_p50": round(sorted(singles)[len(singles) // 2], 2),
