@@ -621,6 +621,26 @@ __device__ __forceinline__ void exec_body(const KParams& p, const uint32_t epoch
       tl[2 + t] = globaltimer();
     }
   }
+  // ---- LL exit: every peer's entry flag for this epoch has landed here, so
+  //      once the kernel completes no peer store into this arena is in flight
+  //      (the lines were all polled; the flags are stored at peer kernel start)
+  if (c == 0 && p.G > 1 && p.ll && warp == 0) {
+    const int lane = tid & 31;
+    bool ok = true;
+    if (lane < p.G && lane != p.rank) {
+      const uint32_t* f = p.entry_flags[p.rank] + lane;
+      const uint64_t t0 = globaltimer();
+      uint32_t spins = 0;
+      while ((int32_t)(ld_relaxed(f, true) - epoch) < 0) {
+        if ((++spins & 255) == 0 && ((int64_t)(globaltimer() - t0) > p.timeout_ns ||
+                                     *(volatile int32_t*)p.err != 0)) {
+          ok = false;
+          break;
+        }
+      }
+    }
+    if (!__all_sync(0xffffffffu, ok) && lane == 0) atomicCAS(p.err, 0, (int32_t)A2A_ERR_TIMEOUT);
+  }
   // ---- exit: all incoming stores of every step have landed (multi-GPU)
   if (c == 0 && p.G > 1 && !p.ll) {
     bool ok = true;
