@@ -420,16 +420,10 @@ __device__ __forceinline__ void exec_body(const KParams& p, const uint32_t epoch
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
   }
-  // stage this CTA's step program (one parallel load instead of per-step chains)
-  for (int i = tid; i < p.T; i += kThreads) s_prog[i] = p.prog[(int64_t)c * p.T + i];
-  __syncthreads();
-  const uint32_t* my_flags = p.step_flags[p.rank];
-  // one GPU (or LL: every step flag is GPU-local) -> .gpu scope suffices
-  const bool sys = (p.G > 1 && !p.ll) || (p.sync_mode & 4);
-
   // ---- LL entry: announce the epoch; a peer's landing region of this parity
   //      was last read two all-to-alls ago, so it is free once that peer has
-  //      started the previous one (its entry flag >= epoch - 1)
+  //      started the previous one (its entry flag >= epoch - 1).  Overlaps the
+  //      program staging below (one barrier for both).
   if (p.G > 1 && p.ll) {
     if (c == 0 && tid < p.G && tid != p.rank) st_relaxed(p.entry_flags[tid] + p.rank, epoch, true);
     if (warp == 0) {
@@ -450,9 +444,23 @@ __device__ __forceinline__ void exec_body(const KParams& p, const uint32_t epoch
       ok = __all_sync(0xffffffffu, ok);
       if (!ok && lane == 0) { atomicCAS(p.err, 0, (int32_t)A2A_ERR_TIMEOUT); s_abort = 1; }
     }
-    __syncthreads();
-    if (s_abort) return;
   }
+  // stage this CTA's step program (one parallel load instead of per-step
+  // chains); with the LL entry poll in warp 0, the other warps stage
+  const int st = (p.G > 1 && p.ll) ? (tid + kThreads - 32) % kThreads : tid;
+  for (int i = st; i < p.T; i += kThreads) s_prog[i] = p.prog[(int64_t)c * p.T + i];
+  // if all of this CTA's pieces (every step) fit the batch buffer, stage them
+  // now too: no per-step piece load on the latency path (small shards)
+  const int32_t pb0 = p.prog[(int64_t)c * p.T].pb, pe1 = p.prog[(int64_t)c * p.T + p.T - 1].pe;
+  const bool all_staged = pe1 - pb0 <= p.batch;
+  if (all_staged)
+    for (int i = st; i < pe1 - pb0; i += kThreads) s_pc[i] = p.pieces[pb0 + i];
+  __syncthreads();
+  if (s_abort) return;
+  const uint32_t* my_flags = p.step_flags[p.rank];
+  // one GPU (or LL: every step flag is GPU-local) -> .gpu scope suffices
+  const bool sys = (p.G > 1 && !p.ll) || (p.sync_mode & 4);
+
   // ---- entry barrier: announce epoch to every peer, then wait for theirs
   if (p.G > 1 && !p.ll) {
     if (c == 0 && tid < p.G && tid != p.rank) st_release_sys(p.entry_flags[tid] + p.rank, epoch);
@@ -491,8 +499,12 @@ __device__ __forceinline__ void exec_body(const KParams& p, const uint32_t epoch
     bool waited = cs.we <= cs.wb;
     for (int32_t base = cs.pb; base < cs.pe; base += p.batch) {
       const int n = min(p.batch, cs.pe - base);
-      // stage the batch first: independent of the flags, so it overlaps the wait
-      for (int i = tid; i < n; i += kThreads) s_pc[i] = p.pieces[base + i];
+      DevPiece* pcs = s_pc;
+      if (all_staged) {
+        pcs = s_pc + (base - pb0);
+      } else {  // stage the batch first: independent of the flags, so it overlaps the wait
+        for (int i = tid; i < n; i += kThreads) s_pc[i] = p.pieces[base + i];
+      }
       if (!waited) {
         if (warp == 0) {
           bool ok = warp_wait_flags(my_flags, p.wait_idx, cs.wb, cs.we, epoch, p.timeout_ns,
@@ -507,7 +519,7 @@ __device__ __forceinline__ void exec_body(const KParams& p, const uint32_t epoch
       // LL pieces (any size) and small copies: all threads, in program order
       // (same-step decodes are last in every CTA's step)
       for (int i = 0; i < n; ++i) {
-        const DevPiece& q = s_pc[i];
+        const DevPiece& q = pcs[i];
         if (q.kind != kCopy) {  // LL regions: this epoch's parity
           const char* sb = p.base[q.src_loc];
           char* db = p.base[q.dst_loc];
@@ -523,13 +535,13 @@ __device__ __forceinline__ void exec_body(const KParams& p, const uint32_t epoch
       }
       if (kEngine == 1) {
         bool any_big = false;
-        for (int i = 0; i < n && !any_big; ++i) any_big = s_pc[i].nbytes > kSmallPiece && s_pc[i].kind == kCopy;
+        for (int i = 0; i < n && !any_big; ++i) any_big = pcs[i].nbytes > kSmallPiece && pcs[i].kind == kCopy;
         if (!any_big) {
           // nothing for the TMA ring in this batch
         } else if (tid != 0) {  // threads 1..: heads, tails, misaligned big pieces
           const int nt = kThreads - 1, me = tid - 1;
           for (int i = 0; i < n; ++i) {
-            const DevPiece& q = s_pc[i];
+            const DevPiece& q = pcs[i];
             if (q.nbytes <= kSmallPiece || q.kind != kCopy) continue;
             const char* s0 = p.base[q.src_loc] + q.src_off;
             char* d0 = p.base[q.dst_loc] + q.dst_off;
@@ -547,7 +559,7 @@ __device__ __forceinline__ void exec_body(const KParams& p, const uint32_t epoch
         } else {  // thread 0: TMA pipeline over the batch's bodies
           fence_proxy_async();
           const uint32_t CH = (uint32_t)p.tma_chunk;
-          BodyCursor cur{s_pc, 0, n, 0};
+          BodyCursor cur{pcs, 0, n, 0};
           const uint32_t g0 = gi;
           uint32_t nl = 0, ns = 0;
           bool more = true;
@@ -587,8 +599,8 @@ __device__ __forceinline__ void exec_body(const KParams& p, const uint32_t epoch
       }
       if (p.count_links && tid == 0)
         for (int i = 0; i < n; ++i)
-          if (s_pc[i].edge >= 0)
-            atomicAdd(p.counters + (int64_t)t * p.E + s_pc[i].edge, (unsigned long long)s_pc[i].nbytes);
+          if (pcs[i].edge >= 0)
+            atomicAdd(p.counters + (int64_t)t * p.E + pcs[i].edge, (unsigned long long)pcs[i].nbytes);
       __syncthreads();
     }
     if (s_abort) return;
