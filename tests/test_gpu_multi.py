@@ -26,6 +26,17 @@ def _ngpu():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
+def _reap(ps):
+    """Join the rank processes; kill any that linger (so no child keeps a GPU
+    context alive after the test)."""
+    for p in ps:
+        p.join(timeout=60)
+    for p in ps:
+        if p.is_alive():
+            p.kill()
+            p.join(timeout=10)
+
+
 def _port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -130,8 +141,7 @@ def test_multiprocess_ipc(world, name, m, engine):
     for p in ps:
         p.start()
     res = [q.get(timeout=300) for _ in ps]
-    for p in ps:
-        p.join(timeout=60)
+    _reap(ps)
     for r in sorted(res, key=lambda x: x[0]):
         assert len(r) == 3, r
         assert r[1], f"rank {r[0]}: recv mismatch"
@@ -158,8 +168,7 @@ def test_multiprocess_ll(world, name, m, engine):
     for p in ps:
         p.start()
     res = [q.get(timeout=300) for _ in ps]
-    for p in ps:
-        p.join(timeout=60)
+    _reap(ps)
     for r in sorted(res, key=lambda x: x[0]):
         assert len(r) == 3, r
         assert r[1], f"rank {r[0]}: recv mismatch"
@@ -182,8 +191,7 @@ def test_multiprocess_cuda_graph(world, proto, sched):
     for p in ps:
         p.start()
     res = [q.get(timeout=300) for _ in ps]
-    for p in ps:
-        p.join(timeout=60)
+    _reap(ps)
     for r in sorted(res, key=lambda x: x[0]):
         assert len(r) == 3, r
         assert r[1], f"rank {r[0]}: recv mismatch"
@@ -281,8 +289,7 @@ def test_multiprocess_dynamic(world, engine, reuse, name, m, mode):
     for p in ps:
         p.start()
     res = [q.get(timeout=300) for _ in ps]
-    for p in ps:
-        p.join(timeout=60)
+    _reap(ps)
     for r in sorted(res, key=lambda x: x[0]):
         assert len(r) == 3, r
         assert r[1], f"rank {r[0]}: recv mismatch"
@@ -300,8 +307,7 @@ def test_alternating_recv_buffers():
     for p in ps:
         p.start()
     res = [q.get(timeout=300) for _ in ps]
-    for p in ps:
-        p.join(timeout=60)
+    _reap(ps)
     for r in res:
         assert r[1] is True, r
 
@@ -365,9 +371,66 @@ def test_gk256_four_gpus(name, sched):
     for p in ps:
         p.start()
     res = [q.get(timeout=600) for _ in ps]
-    for p in ps:
-        p.join(timeout=60)
+    _reap(ps)
     for r in sorted(res, key=lambda x: x[0]):
         assert len(r) == 3, r
         assert r[1], f"rank {r[0]}: recv mismatch"
         assert r[2], f"rank {r[0]}: link counters differ from schedule"
+
+
+@pytest.mark.parametrize("name,m", [("gk8_2", 65536), ("hypercube3", 4096 + 7), ("gk64_4", 2048)])
+@pytest.mark.parametrize("proto,sched", [("simple", "static"), ("simple", "cp"), ("ll", "static")])
+def test_eight_ranks_single_process(name, m, proto, sched):
+    """The 8-GPU code paths (8 peers, 8-bit destination masks, per-GPU exit
+    lists) on real hardware with fewer devices: 8 plans of an 8-GPU placement
+    in one process, rank r on device r % ndev, each with a reduced CTA count so
+    the ranks sharing a device are co-resident, launched on their own streams."""
+    ndev = _ngpu()
+    if ndev < 2:
+        pytest.skip("needs 2 GPUs")
+    from replay_bytes import make_send
+
+    from paper_2309_13541_b200.artifacts import load_artifact
+    from paper_2309_13541_b200.dist import local_nodes
+    from paper_2309_13541_b200.executor import Plan
+    a = load_artifact(name)
+    R = 8
+    per_dev = -(-R // ndev)
+    nc = max(8, 144 // per_dev)
+    plans = []
+    # plain (non-cooperative) launches: kernels of ranks sharing a device must
+    # run concurrently from different streams
+    old_env = os.environ.get("A2A_NONCOOP")
+    os.environ["A2A_NONCOOP"] = "1"
+    try:
+        for r in range(R):
+            p = Plan(a.g, a.sched, m=m, n_gpus=R, placement="optimized", protocol=proto)
+            if sched != "static":
+                p.set_schedule(sched, 4096)
+            plans.append(p.bind(r, device=r % ndev, num_ctas=nc))
+    finally:
+        if old_env is None:
+            os.environ.pop("A2A_NONCOOP", None)
+        else:
+            os.environ["A2A_NONCOOP"] = old_env
+    ptrs = [p.arena_ptr() for p in plans]
+    for p in plans:
+        p.import_pointers(ptrs)
+        p.set_timeout(20.0)
+    send_all = make_send(a.g.n, m, seed=8)
+    want = np.swapaxes(send_all, 0, 1)
+    nodes = [local_nodes(p, r) for r, p in enumerate(plans)]
+    streams = [torch.cuda.Stream(r % ndev) for r in range(R)]
+    sends = [torch.from_numpy(np.ascontiguousarray(send_all[nodes[r]])).cuda(r % ndev) for r in range(R)]
+    recvs = [p.recv_buffer() for p in plans]
+    for rep in range(2):
+        for r, p in enumerate(plans):
+            p.execute(sends[r], recvs[r], stream=streams[r], count_links=True)
+        for p in plans:
+            p.sync()
+        for r in range(R):
+            assert np.array_equal(recvs[r].cpu().numpy(), want[nodes[r]]), (rep, r)
+    total = sum(p.read_link_counters() for p in plans)
+    assert np.array_equal(total, 2 * plans[0].link_bytes())
+    for p in plans:
+        p.close()

@@ -77,6 +77,10 @@ def test_two_rank_host_logic(name, m):
     res = [q.get(timeout=120) for _ in ps]
     for p in ps:
         p.join(timeout=60)
+    for p in ps:
+        if p.is_alive():
+            p.kill()
+            p.join(timeout=10)
     for r in res:
         assert len(r) == 5, r
         assert all(r[1:]), r
