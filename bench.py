@@ -392,7 +392,8 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     # whose stream lags shows up here, not in its kernel span)
     fl = sorted(a.elapsed_time(b) for a, b in zip(ef, e0))
     gap = sorted(a.elapsed_time(b) for a, b in zip(ef[:-1], ef[1:])) or [0.0]
-    diag = [fl[len(fl) // 2], gap[len(gap) // 2]]
+    diag = [fl[len(fl) // 2], gap[len(gap) // 2],
+            [round(a.elapsed_time(b), 4) for a, b in zip(e0, e1)] if os.environ.get("A2A_DIAG") else None]
     if ctx.pg:
         alld = [None] * G
         ctx.pg.all_gather_object(alld, diag)
@@ -539,6 +540,7 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
            "host_enqueue_us_per_step": round(ctx.allmax([host_us])[0], 2),
            "flush_ms_p50_by_rank": [round(x[0], 4) for x in alld],
            "step_period_ms_p50_by_rank": [round(x[1], 4) for x in alld],
+           "step_ms_by_rank": [x[2] for x in alld] if os.environ.get("A2A_DIAG") else None,
            "sync": (plan.dyn_stats(rank, plan_ctas(plan, num_ctas)) if plan.schedule in ("dynamic", "list", "cp", "mix")
                     else plan.sync_stats(rank)),
            "kernel_timeline": tls,

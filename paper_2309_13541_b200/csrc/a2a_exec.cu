@@ -21,9 +21,10 @@
 //       work split: interval overlap of source ranges with earlier writes),
 //       then fence + bar.sync.  Steps therefore overlap: a CTA starts step t+1
 //       as soon as its own inputs exist, not when the whole GPU finished step t.
-//   entry barrier (multi-GPU): every GPU announces the epoch to all peers and
-//       waits for theirs before storing into peer memory, so a peer's buffers
-//       are never overwritten while its previous all-to-all is still live.
+//   entry barrier (multi-GPU): every GPU announces the epoch to all peers
+//       (relaxed store) and acquires theirs before storing into peer memory, so
+//       a peer's buffers are never overwritten while its previous all-to-all is
+//       still live.
 //   exit (multi-GPU): CTA 0 polls every producer flag of this GPU, so kernel
 //       completion implies this GPU's recv buffer is final.
 // Every spin is bounded by a %globaltimer timeout and reports A2A_ERR_TIMEOUT.
@@ -463,7 +464,9 @@ __device__ __forceinline__ void exec_body(const KParams& p, const uint32_t epoch
 
   // ---- entry barrier: announce epoch to every peer, then wait for theirs
   if (p.G > 1 && !p.ll) {
-    if (c == 0 && tid < p.G && tid != p.rank) st_release_sys(p.entry_flags[tid] + p.rank, epoch);
+    // relaxed: the flag orders nothing of this kernel -- the reads it vouches for
+    // (the previous all-to-all's) completed at the kernel boundary
+    if (c == 0 && tid < p.G && tid != p.rank) st_relaxed(p.entry_flags[tid] + p.rank, epoch, true);
     if (warp == 0) {
       const int lane = tid & 31;
       bool ok = true;
@@ -709,7 +712,9 @@ __device__ __forceinline__ void dyn_body(const KParams& p, const uint32_t epoch)
   const uint32_t* my_flags = p.step_flags[p.rank];
   const bool sys = p.G > 1 || (p.sync_mode & 4);
   if (p.G > 1) {  // entry barrier (same protocol as the static kernel)
-    if (c == 0 && tid < p.G && tid != p.rank) st_release_sys(p.entry_flags[tid] + p.rank, epoch);
+    // relaxed: the flag orders nothing of this kernel -- the reads it vouches for
+    // (the previous all-to-all's) completed at the kernel boundary
+    if (c == 0 && tid < p.G && tid != p.rank) st_relaxed(p.entry_flags[tid] + p.rank, epoch, true);
     if (warp == 0) {
       const int lane = tid & 31;
       bool ok = true;

@@ -94,6 +94,7 @@ def main(argv=None):
                     "host_enqueue_us_per_step": r["host_enqueue_us_per_step"],
                     "flush_ms_p50_by_rank": r["flush_ms_p50_by_rank"],
                     "step_period_ms_p50_by_rank": r["step_period_ms_p50_by_rank"],
+                    "step_ms_by_rank": r["step_ms_by_rank"],
                     "kernel_timeline": r["kernel_timeline"],
                     "egress_max_bytes": r["egress_max"], "scratch_bytes": r["scratch_bytes"],
                     "placement": a.placement, "l2": r["l2"], "num_ctas": r["num_ctas"],
