@@ -337,7 +337,9 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     # than L2 and back-to-back all-to-alls avoid per-rank flush skew
     if flush is None:
         flush = min(i["send_bytes"] for i in infos) < L2_BYTES
-    l2_policy = ("flushed between timed steps (512 MiB memset, outside events)" if flush else
+    l2_policy = ("flushed between timed steps (512 MiB memset, outside events"
+                 + (", then ranks re-aligned by an NCCL all-reduce, outside events)" if G > 1 else ")")
+                 if flush else
                  f"inputs larger than L2 ({min(i['send_bytes'] for i in infos) >> 20} MiB send per GPU "
                  f"> 126 MB), no flush")
     flush_buf = torch.empty(flush_bytes if flush else 1, dtype=torch.uint8, device=dev)
@@ -368,11 +370,18 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     # it absorbs the ranks' host launch skew in its entry barrier, so the
     # first timed step measures the pipeline and not process start-up skew
     plan.execute(send, recv, stream=stream)
+    # with a flush between all-to-alls (G > 1) the ranks are re-aligned on the
+    # device after it (an async NCCL all-reduce the stream waits on, outside the
+    # events): otherwise a rank whose flush overlaps its peers' all-to-all locks
+    # the job into a staggered steady state and the events time the stagger
+    align = torch.zeros(1, device=dev) if (flush and G > 1) else None
     h0 = time.perf_counter()
     for k in range(steps):
         ef[k].record(stream)
         if flush:
             flush_buf.zero_()
+        if align is not None:
+            ctx.pg.all_reduce(align, async_op=True).wait()
         e0[k].record(stream)
         plan.execute(send, recv, stream=stream)
         e1[k].record(stream)
@@ -443,6 +452,8 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
         for _ in range(steps):
             if flush:
                 flush_buf.zero_()
+            if align is not None:   # same re-alignment as for our kernel
+                ctx.pg.all_reduce(align, async_op=True).wait()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             ctx.pg.all_to_all_single(out, inp)
