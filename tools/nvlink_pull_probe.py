@@ -4,7 +4,7 @@ from peer memory), one direction and both directions at once, TMA bulk copies
 
   python tools/nvlink_pull_probe.py        # prints one JSON line
 
-Each variant launches one kernel per GPU (148 CTAs) that moves `bytes` through
+Each variant launches one kernel per GPU (148 CTAs unless noted) that moves `bytes` through
 a per-CTA slice; push: src local, dst peer; pull: src peer, dst local.
 """
 from __future__ import annotations
@@ -73,21 +73,21 @@ void enable_peer(int64_t dev, int64_t peer) {
   if (cudaDeviceEnablePeerAccess((int)peer, 0) != cudaSuccess) cudaGetLastError();
 }
 
-void launch(torch::Tensor dst, torch::Tensor src, int64_t dev, int64_t engine, int64_t stream) {
+void launch(torch::Tensor dst, torch::Tensor src, int64_t dev, int64_t engine, int64_t stream, int64_t ctas) {
   cudaSetDevice((int)dev);
   cudaStream_t s = (cudaStream_t)stream;
   const long long n = src.numel();
   if (engine == 1) {
     constexpr int S = 6, CH = 32768;
     cudaFuncSetAttribute(tma_copy<S, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, S * CH);
-    tma_copy<S, CH><<<148, 32, S * CH, s>>>((char*)dst.data_ptr(), (const char*)src.data_ptr(), n);
+    tma_copy<S, CH><<<(int)ctas, 32, S * CH, s>>>((char*)dst.data_ptr(), (const char*)src.data_ptr(), n);
   } else {
-    lsu_copy<<<148, 1024, 0, s>>>((int4*)dst.data_ptr(), (const int4*)src.data_ptr(), n / 16);
+    lsu_copy<<<(int)ctas, 1024, 0, s>>>((int4*)dst.data_ptr(), (const int4*)src.data_ptr(), n / 16);
   }
 }
 """
 
-CPP = ("void launch(torch::Tensor dst, torch::Tensor src, int64_t dev, int64_t engine, int64_t stream);\n"
+CPP = ("void launch(torch::Tensor dst, torch::Tensor src, int64_t dev, int64_t engine, int64_t stream, int64_t ctas);\n"
        "void enable_peer(int64_t dev, int64_t peer);")
 
 
@@ -103,7 +103,7 @@ def main():
     streams = {d: torch.cuda.Stream(d) for d in (0, 1)}
     out = {}
 
-    def run(kind, engine, both):
+    def run(kind, engine, both, ctas=148):
         # kind push: GPU d copies its own src -> peer dst; pull: peer src -> own dst
         def once():
             for d in ((0, 1) if both else (0,)):
@@ -112,7 +112,7 @@ def main():
                     dst, src = buf[q][1], buf[d][0]
                 else:
                     dst, src = buf[d][1], buf[q][0]
-                mod.launch(dst, src, d, engine, streams[d].cuda_stream)
+                mod.launch(dst, src, d, engine, streams[d].cuda_stream, ctas)
         once()
         for d in (0, 1):
             torch.cuda.synchronize(d)
@@ -135,6 +135,8 @@ def main():
         for kind in ("push", "pull"):
             out[f"{en}_{kind}_oneway_gbs"] = run(kind, engine, False)
             out[f"{en}_{kind}_bidir_gbs_per_direction"] = run(kind, engine, True)
+    for ctas in (16, 32, 48, 74, 111):   # how many pushing SMs saturate NVLink
+        out[f"tma_push_bidir_{ctas}ctas_gbs_per_direction"] = run("push", 1, True, ctas)
     print(json.dumps(out), flush=True)
 
 
