@@ -190,7 +190,7 @@ def run_reference(args, art, m):
         "n_gpus": args.gpus, "steps": len(timed), "warmup": args.warmup,
         "ms_per_step": round(T * 1e3, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": f"{args.config} (frozen decomposed-MCF schedule, hop-indexed)",
+        "config": {"workload": workload_name(args.config, n, m),
                    "m_bytes": m_cpu, "nodes": n, "hop_ops": len(art.sched.instructions),
                    "nsteps": art.sched.nsteps},
         "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": nthreads,
@@ -234,6 +234,12 @@ class Ctx:
         if self.pg:
             self.pg.barrier()
             self.pg.destroy_process_group()
+
+
+def workload_name(config, n, m):
+    """config.workload, identical in both arms (ours and --impl reference)."""
+    return (f"{config}: frozen decomposed-MCF schedule (hop i of every route at step i), "
+            f"N={n} virtual nodes, m={m} B per pair")
 
 
 LL_MAX_SHARD = 1 << 20   # autotune tries the LL transport up to this shard size
@@ -623,10 +629,8 @@ def main(argv=None):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["T"] * 1e3, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u8", "data": "synthetic",
-            "config": {"workload": f"{args.config}: frozen decomposed-MCF schedule "
-                                   f"(hop i of every route at step i), N={n} virtual nodes, "
-                                   f"m={m} B per pair, placement {args.placement} "
-                                   f"{r['placement'] if G > 1 else ''}",
+            "config": {"workload": workload_name(args.config, n, m),
+                       "placement": f"{args.placement} {r['placement'] if G > 1 else '(all nodes on GPU 0)'}",
                        "m_bytes": m, "nodes": n, "hop_ops": len(art.sched.instructions),
                        "nsteps": art.sched.nsteps, "Q": art.sched.Q,
                        "l2": r["l2"],

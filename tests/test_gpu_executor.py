@@ -312,3 +312,20 @@ def test_ll_protocol_bit_exact(name, m, engine, artifacts):
             p.sync()
             assert np.array_equal(r.cpu().numpy(), want), rep
         assert np.array_equal(p.read_link_counters(), 3 * p.link_bytes())
+
+
+@pytest.mark.parametrize("name,m", [("torus4x4x4", 4096 + 8), ("gk64_4", 2048 + 5), ("gk64_4_h2", 1000)])
+def test_ll_protocol_n64(name, m, artifacts):
+    """LL on the N=64 schedules (13 943 / 27k hop-ops, forwards split across
+    several arrivals): transpose on one GPU, twice (both landing parities)."""
+    from paper_2309_13541_b200.executor import Plan
+    a = artifacts(name)
+    g = torch.Generator(device="cuda").manual_seed(9)
+    s = torch.randint(0, 256, (64, 64, m), dtype=torch.uint8, device="cuda", generator=g)
+    with Plan(a.g, a.sched, m=m, protocol="ll") as p:
+        p.bind(0)
+        for _ in range(2):
+            r = torch.zeros_like(s)
+            p.execute(s, r)
+            p.sync()
+            assert torch.equal(r, s.transpose(0, 1).contiguous())
