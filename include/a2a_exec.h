@@ -196,7 +196,11 @@ int a2a_plan_recv_buffer_at(const a2a_plan* plan, int32_t index, void** out_ptr)
 
 /* Launch one all-to-all on `stream` (cudaStream_t; NULL = legacy default).
  * send: this rank's [V_g][N][m] buffer; recv: [V_g][N][m] (NULL = arena recv).
- * Asynchronous; call a2a_plan_sync to wait and collect device errors. */
+ * Asynchronous; call a2a_plan_sync to wait and collect device errors.
+ * Stream-capturable: the epoch of each all-to-all lives in device memory, so a
+ * captured execute (one cooperative kernel node) replays as a fresh all-to-all.
+ * Executes of one plan must be stream-ordered on every rank, and every rank
+ * must run the same number of them. */
 int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
                      int32_t options);
 /* wait for the plan's last execute; returns A2A_ERR_TIMEOUT if a device wait timed out */

@@ -326,8 +326,10 @@ def _gk256_main(rank, world, port, name, sched, q):
                                 rank=rank, world_size=world)
         a = load_artifact(name, native=True)
         m = 8192 + 64
-        plan = Plan(a.g, a.sched, m=m, n_gpus=world, placement="optimized")
-        plan.set_schedule(sched)
+        plan = Plan(a.g, a.sched, m=m, n_gpus=world, placement="optimized",
+                    protocol="ll" if sched == "ll" else "simple")
+        if sched != "ll":
+            plan.set_schedule(sched)
         plan.bind(rank, device=rank)
         plan.set_timeout(30.0)
         connect(plan)
@@ -357,7 +359,7 @@ def _gk256_main(rank, world, port, name, sched, q):
 
 
 @pytest.mark.parametrize("name", ["gk256_4", "gk256_4_h2"])
-@pytest.mark.parametrize("sched", ["static", "dynamic"])
+@pytest.mark.parametrize("sched", ["static", "dynamic", "ll"])
 def test_gk256_four_gpus(name, sched):
     """Config 4 (GenKautz N=256, with / without extra NIC forwarding) on 4 GPUs:
     transpose of device-generated shards, device link counters == schedule."""
