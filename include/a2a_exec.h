@@ -160,7 +160,9 @@ int a2a_plan_set_split(a2a_plan* plan, int32_t remote_weight);
  * an event-driven list schedule (start times) instead of step-major, so routes
  * pipeline hop by hop at unit granularity; 3 = dynamic units, step-major with
  * critical-path (bottom-level) priority within a step; 4 = one queue per GPU,
- * step-major, NVLink and HBM units merged in proportion to their time.
+ * step-major, NVLink and HBM units merged in proportion to their time; 5 = a
+ * per-GPU ready queue: units are enqueued when their last producer finishes
+ * (completion counters counted down with system-scope atomics).
  * a2a_plan_emulate follows the
  * selected mode.  Stats: units and dependency entries of `gpu`, model makespan. */
 int a2a_plan_set_schedule(a2a_plan* plan, int32_t mode, int64_t unit_bytes);

@@ -69,6 +69,13 @@ struct KParams {
   int32_t n_units, unit_base;              // this GPU's units; global id of its first
   int32_t n_remote, remote_ctas;           // remote queue = units [0, n_remote); CTAs starting on it
   unsigned long long* grab;                // per-GPU grab counters [2] (remote, local queue)
+  // ready-queue mode (sched_mode 5): per GPU its queue control words (head,
+  // tail, arrived), per-unit completion counters and queue slots (arena, peer-visible)
+  unsigned long long* qctl[A2A_MAX_GPUS];
+  unsigned long long* qdone[A2A_MAX_GPUS];
+  unsigned long long* qslot[A2A_MAX_GPUS];
+  int32_t ubase[A2A_MAX_GPUS + 1];         // global unit id range of every GPU
+  int32_t n_init, n_into;                  // own units ready at start; units writing into this GPU
 };
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -111,6 +118,27 @@ __device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v, bool sys) {
     asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
   else
     asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long atom_add_acq_rel_sys(unsigned long long* p, unsigned long long v) {
+  unsigned long long r;
+  asm volatile("atom.acq_rel.sys.global.add.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(v) : "memory");
+  return r;
+}
+__device__ __forceinline__ unsigned long long atom_add_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  unsigned long long r;
+  asm volatile("atom.relaxed.sys.global.add.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(v) : "memory");
+  return r;
+}
+__device__ __forceinline__ void red_add_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 __device__ __forceinline__ void fence_acq_rel(bool sys) {
   if (sys)
@@ -685,7 +713,20 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_exec_kernel(const KParams p) 
 }
 
 // ---- dynamic mode: CTAs grab units from a per-GPU counter ----
-template <int kEngine, int kThreads>
+// Ready-queue mode (kReady): units are enqueued on their GPU's queue when
+// their last producer finishes (per-unit completion counters, counted down
+// with acq_rel system-scope atomics over NVLink); a CTA claims the next queue
+// position while it copies its current unit and waits for that position only
+// after publishing, so CTAs never wait on a unit whose inputs are missing
+// while ready work exists (csrc/a2a_plan.cpp build_dyn, emulate_ready).
+__device__ __forceinline__ void ready_push(const KParams& p, int h, int32_t li, uint32_t epoch) {
+  const int32_t nu = p.ubase[h + 1] - p.ubase[h];
+  const unsigned long long pos =
+      atom_add_relaxed_sys(p.qctl[h] + 1, 1ull) - (unsigned long long)(epoch - 1) * (unsigned long long)nu;
+  st_release_sys_u64(p.qslot[h] + pos, ((unsigned long long)epoch << 32) | (uint32_t)li);
+}
+
+template <int kEngine, int kThreads, bool kReady>
 __device__ __forceinline__ void dyn_body(const KParams& p, const uint32_t epoch) {
   __shared__ int s_abort;
   __shared__ long long s_idx[2];
@@ -737,10 +778,20 @@ __device__ __forceinline__ void dyn_body(const KParams& p, const uint32_t epoch)
     if (s_abort) return;
   }
   if (tid == 0) tl[1] = globaltimer();
+  if (kReady && c == 0)  // seed this GPU's queue with its dependency-free units
+    for (int32_t i = tid; i < p.n_init; i += kThreads) ready_push(p, p.rank, i, epoch);
   unsigned long long waited_ns = 0, done = 0;
   int q = c < p.remote_ctas ? 0 : 1, visited = 0;  // queue state, owned by the fetching thread
   // fetch (grab + descriptor) of the next unit into slot `sl`; thread `fetcher`
+  // (ready mode: claim the next queue position only -- it is waited for in acquire)
   auto fetch = [&](int sl) {
+    if (kReady) {
+      const long long n = p.n_units;
+      const long long j = (long long)(atomicAdd(p.grab, 1ull) -
+                                      (unsigned long long)(epoch - 1) * (unsigned long long)(n + p.nC));
+      s_idx[sl] = j < n ? j : -1;
+      return;
+    }
     long long idx = -1;
     for (;;) {  // own queue first, then the other; one failing grab per queue
       const long long qn = q == 0 ? p.n_remote : (long long)p.n_units - p.n_remote;
@@ -757,8 +808,37 @@ __device__ __forceinline__ void dyn_body(const KParams& p, const uint32_t epoch)
       s_pc[sl] = DevPiece{u.src_off, u.dst_off, u.nbytes, u.edge, u.src_loc, u.dst_loc, 0};
     }
   };
-  // acquire the producers of the unit in slot `sl` (one warp)
+  // acquire the producers of the unit in slot `sl` (one warp); ready mode:
+  // wait until the claimed queue position is filled, then load the unit
   auto acquire = [&](int sl) -> bool {
+    if (kReady) {
+      if (s_idx[sl] < 0) return true;
+      bool ok = true;
+      if ((tid & 31) == 0) {
+        const unsigned long long* slot = p.qslot[p.rank] + s_idx[sl];
+        const uint64_t w0 = globaltimer();
+        uint32_t spins = 0;
+        unsigned long long v;
+        while ((uint32_t)((v = ld_acquire_sys_u64(slot)) >> 32) != epoch) {
+          if ((++spins & 255) == 0 && ((int64_t)(globaltimer() - w0) > p.timeout_ns ||
+                                       *(volatile int32_t*)p.err != 0)) {
+            ok = false;
+            break;
+          }
+        }
+        waited_ns += globaltimer() - w0;
+        if (ok) {
+          const long long li = (long long)(uint32_t)v;
+          const DevUnit u = p.units[li];
+          s_idx[sl] = li;
+          s_u[sl] = u;
+          s_pc[sl] = DevPiece{u.src_off, u.dst_off, u.nbytes, u.edge, u.src_loc, u.dst_loc, 0};
+        } else {
+          atomicCAS(p.err, 0, (int32_t)A2A_ERR_TIMEOUT);
+        }
+      }
+      return __shfl_sync(0xffffffffu, ok, 0);
+    }
     const DevUnit& u = s_u[sl];
     if (s_idx[sl] < 0 || u.we <= u.wb) return true;
     const uint64_t w0 = globaltimer();
@@ -849,7 +929,27 @@ __device__ __forceinline__ void dyn_body(const KParams& p, const uint32_t epoch)
     if (p.count_links && tid == 0 && u.edge >= 0)
       atomicAdd(p.counters + (int64_t)u.step * p.E + u.edge, (unsigned long long)u.nbytes);
     __syncthreads();
-    if (tid == 0) {
+    if (kReady && warp == 0) {
+      // count down the dependents, one lane each (acq_rel at system scope:
+      // releases this CTA's stores, which bar.sync made cumulative, and chains
+      // the earlier producers' releases); the lane that completes a dependent
+      // enqueues it on its GPU; lane 31 counts the unit into its destination
+      const int lane = tid & 31;
+      for (int32_t k = u.wb + lane; k < u.we; k += 31) {
+        if (lane == 31) break;
+        const int32_t gid = p.unit_wait[2 * k], deg = p.unit_wait[2 * k + 1];
+        int h = 0;
+        while (gid >= p.ubase[h + 1]) ++h;
+        const int32_t lj = gid - p.ubase[h];
+        const unsigned long long old = atom_add_acq_rel_sys(p.qdone[h] + lj, 1ull);
+        if (old + 1 == (unsigned long long)epoch * (unsigned long long)deg) ready_push(p, h, lj, epoch);
+      }
+      if (lane == 31) {
+        const int hd = u.dst_loc >= 1 && u.dst_loc < 1 + p.G ? u.dst_loc - 1 : u.dst_loc - 1 - p.G;
+        red_add_release_sys(p.qctl[hd] + 2, 1ull);
+      }
+      if (lane == 0) ++done;
+    } else if (!kReady && tid == 0) {
       const int64_t slot = (int64_t)p.unit_base + idx;
       uint32_t mask = u.mask;
       while (mask) {
@@ -864,7 +964,19 @@ __device__ __forceinline__ void dyn_body(const KParams& p, const uint32_t epoch)
     if (s_abort) return;
     cur ^= 1;
   }
-  if (c == 0 && p.G > 1) {  // exit: every unit flagged into this GPU has landed
+  if (kReady && c == 0 && tid == 0) {  // exit: every unit writing into this GPU has finished
+    const uint64_t t0 = globaltimer();
+    uint32_t spins = 0;
+    const unsigned long long want = (unsigned long long)epoch * (unsigned long long)p.n_into;
+    while (ld_acquire_sys_u64(p.qctl[p.rank] + 2) < want) {
+      if ((++spins & 255) == 0 && ((int64_t)(globaltimer() - t0) > p.timeout_ns ||
+                                   *(volatile int32_t*)p.err != 0)) {
+        atomicCAS(p.err, 0, (int32_t)A2A_ERR_TIMEOUT);
+        break;
+      }
+    }
+  }
+  if (!kReady && c == 0 && p.G > 1) {  // exit: every unit flagged into this GPU has landed
     bool ok = true;
     for (int32_t i = tid; i < p.n_exit && ok; i += kThreads) {
       const uint32_t* f = my_flags + p.exit_idx[i];
@@ -891,7 +1003,14 @@ __device__ __forceinline__ void dyn_body(const KParams& p, const uint32_t epoch)
 template <int kEngine, int kThreads>
 __global__ void __launch_bounds__(kThreads, 1) a2a_dyn_kernel(const KParams p) {
   const uint32_t epoch = begin_epoch(p);
-  dyn_body<kEngine, kThreads>(p, epoch);
+  dyn_body<kEngine, kThreads, false>(p, epoch);
+  end_epoch(p, epoch);
+}
+
+template <int kEngine, int kThreads>
+__global__ void __launch_bounds__(kThreads, 1) a2a_ready_kernel(const KParams p) {
+  const uint32_t epoch = begin_epoch(p);
+  dyn_body<kEngine, kThreads, true>(p, epoch);
   end_epoch(p, epoch);
 }
 
@@ -930,13 +1049,16 @@ struct EngineCfg {
 static EngineCfg engine_cfg(const Plan& P) {
   const int TE = P.T_exec;
   if (P.sched_mode >= 1) {
+    const bool rq = P.sched_mode == 5;
     if (P.engine == 1) {
       int S = P.tma_stages;
       while (S > 1 && ((20 * (size_t)S + 127) & ~(size_t)127) + (size_t)S * P.tma_chunk > 220 * 1024) --S;
       const size_t ring = ((20 * (size_t)S + 127) & ~(size_t)127) + (size_t)S * P.tma_chunk;
-      return {(const void*)a2a_dyn_kernel<1, 256>, 256, ring, S, 0, 0, 0};
+      return {rq ? (const void*)a2a_ready_kernel<1, 256> : (const void*)a2a_dyn_kernel<1, 256>, 256, ring,
+              S, 0, 0, 0};
     }
-    return {(const void*)a2a_dyn_kernel<0, 1024>, 1024, 0, 0, 0, 0, 0};
+    return {rq ? (const void*)a2a_ready_kernel<0, 1024> : (const void*)a2a_dyn_kernel<0, 1024>, 1024, 0,
+            0, 0, 0, 0};
   }
   const size_t prog = ((size_t)TE * sizeof(CtaStep) + 127) & ~(size_t)127;
   if (P.engine == 1) {
@@ -1034,8 +1156,10 @@ static int bind_plan(Plan& P, int gpu, int dev, int nC) {
   const DynTables& Dy = P.dyn;
 
   // ---- arena layout, identical on every rank: flags | recv | scratch
-  P.flags_bytes = flag_region_bytes(P.sched_mode >= 1 ? (int64_t)Dy.unit_base[G]
-                                                      : (int64_t)TE * G * nC);
+  // ready mode: per-unit u64 completion counters + u64 queue slots (4 u32 each)
+  P.flags_bytes = flag_region_bytes(P.sched_mode == 5  ? 4 * (int64_t)Dy.max_units
+                                    : P.sched_mode >= 1 ? (int64_t)Dy.unit_base[G]
+                                                        : (int64_t)TE * G * nC);
   P.recv_off.assign(G, 0);
   P.scratch_off.assign(G, 0);
   P.arena_bytes.assign(G, 0);
@@ -1057,7 +1181,8 @@ static int bind_plan(Plan& P, int gpu, int dev, int nC) {
     CK(cudaMemset((char*)P.arena + P.scratch_off[gpu] + P.ll_off[gpu], 0, (size_t)(2 * P.ll_half[gpu])));
   if (P.sched_mode >= 1) {
     if ((rc = upload(&P.d_items, Dy.units[gpu])) != A2A_OK) return rc;
-    if ((rc = upload(&P.d_wait_idx, Dy.wait_idx[gpu])) != A2A_OK) return rc;
+    if ((rc = upload(&P.d_wait_idx, P.sched_mode == 5 ? Dy.deps_out[gpu] : Dy.wait_idx[gpu])) != A2A_OK)
+      return rc;
     if ((rc = upload(&P.d_exit_idx, Dy.exit_idx[gpu])) != A2A_OK) return rc;
   } else {
     if ((rc = upload(&P.d_items, S.pieces[gpu])) != A2A_OK) return rc;
@@ -1267,6 +1392,17 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
     kp.n_units = (int32_t)Dy.units[P.rank].size();
     kp.unit_base = Dy.unit_base[P.rank];
     kp.grab = (unsigned long long*)((char*)P.arena + grab_off());
+    if (P.sched_mode == 5) {
+      for (int g = 0; g < P.G; ++g) {
+        char* ar = (char*)P.peer_arena[g];
+        kp.qctl[g] = (unsigned long long*)(ar + grab_off());
+        kp.qdone[g] = (unsigned long long*)(ar + step_flags_off());
+        kp.qslot[g] = (unsigned long long*)(ar + step_flags_off() + 8 * (int64_t)Dy.max_units);
+      }
+      for (int g = 0; g <= P.G; ++g) kp.ubase[g] = Dy.unit_base[g];
+      kp.n_init = Dy.n_init[P.rank];
+      kp.n_into = Dy.n_into[P.rank];
+    }
     kp.n_remote = Dy.n_remote[P.rank];
     kp.remote_ctas = Dy.remote_ctas[P.rank];
   } else {

@@ -111,6 +111,11 @@ struct DynTables {
   std::vector<std::vector<int32_t>> wait_idx;   // [g] global unit ids to acquire
   std::vector<std::vector<int32_t>> exit_idx;   // [g] global unit ids flagged into g
   double est_makespan = 0;                      // host model estimate (s)
+  // ready-queue mode (sched_mode 5): per unit its dependents as {global id,
+  // in-degree} pairs (DevUnit.wb/we index pairs, DevUnit.mask = own in-degree)
+  std::vector<std::vector<int32_t>> deps_out;   // [g] flattened pairs
+  std::vector<int32_t> n_init, n_into;          // [g] units ready at start; units writing into g
+  int32_t max_units = 0;                        // max units on one GPU (queue array size)
 };
 
 struct Interval {

@@ -1174,11 +1174,16 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
     // one queue in key order (n_remote = 0, no CTA on queue 0): the mix order,
     // and any order with a single CTA -- two queues need a CTA each, or a CTA
     // stuck on one queue could wait for a unit only the other queue holds
-    if (P.sched_mode == 4 || nC < 2) {
+    // (ready-queue mode: one array, units without dependencies first -- they
+    // seed the queue -- each part in key order)
+    if (P.sched_mode == 4 || P.sched_mode == 5 || nC < 2) {
       std::vector<int> q;
       for (int t = 0; t < TE; ++t)
         for (int id : per[g][t]) q.push_back(id);
-      std::stable_sort(q.begin(), q.end(), [&](int a, int b) { return key[a] < key[b]; });
+      std::stable_sort(q.begin(), q.end(), [&](int a, int b) {
+        if (P.sched_mode == 5 && all[a].deps.empty() != all[b].deps.empty()) return all[a].deps.empty();
+        return key[a] < key[b];
+      });
       qorder[g] = q;
       int k = 0;
       for (int id : qorder[g]) gid[id] = D.unit_base[g] + k++;
@@ -1226,8 +1231,116 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
           if (u.mask & (1u << h)) D.exit_idx[h].push_back(gid[id]);
       }
     }
+  if (P.sched_mode == 5) {
+    // dependents of every unit with the dependent's in-degree: a finished unit
+    // counts down its dependents on their GPUs and enqueues the ones it completes
+    const int total = D.unit_base[G];
+    std::vector<std::vector<int32_t>> dependents(total);
+    std::vector<int32_t> indeg(total, 0);
+    for (int g = 0; g < G; ++g)
+      for (size_t i = 0; i < D.units[g].size(); ++i) {
+        const DevUnit& u = D.units[g][i];
+        const int32_t me = D.unit_base[g] + (int32_t)i;
+        indeg[me] = u.we - u.wb;
+        for (int32_t k = u.wb; k < u.we; ++k) dependents[D.wait_idx[g][k]].push_back(me);
+      }
+    D.deps_out.assign(G, {});
+    D.n_init.assign(G, 0);
+    D.n_into.assign(G, 0);
+    D.max_units = 0;
+    for (int g = 0; g < G; ++g) {
+      D.max_units = std::max<int32_t>(D.max_units, (int32_t)D.units[g].size());
+      for (size_t i = 0; i < D.units[g].size(); ++i) {
+        DevUnit& u = D.units[g][i];
+        const int32_t me = D.unit_base[g] + (int32_t)i;
+        if (indeg[me] == 0) D.n_init[g]++;
+        u.mask = (uint32_t)indeg[me];
+        u.wb = (int32_t)(D.deps_out[g].size() / 2);
+        for (int32_t d : dependents[me]) {
+          D.deps_out[g].push_back(d);
+          D.deps_out[g].push_back(indeg[d]);
+        }
+        u.we = (int32_t)(D.deps_out[g].size() / 2);
+      }
+    }
+    for (int g = 0; g < G; ++g)
+      for (size_t i = 0; i < D.units[g].size(); ++i) {
+        const DevUnit& u = D.units[g][i];
+        const int h = u.dst_loc >= 1 && u.dst_loc < 1 + G ? u.dst_loc - 1 : u.dst_loc - 1 - G;
+        D.n_into[h]++;
+      }
+  }
   D.nC = nC;
   D.unit_bytes = unit_bytes;
+  return A2A_OK;
+}
+
+// Host emulation of the ready-queue protocol (sched_mode 5): per-GPU FIFO
+// queues seeded with the dependency-free units; a CTA claims the next queue
+// position, runs the unit once the position is filled, then counts down its
+// dependents (on any GPU) and enqueues the ones it completes.  Claims, runs and
+// releases interleave randomly across all CTAs of all GPUs; a stuck state is
+// an error.
+static int emulate_ready(Plan& P, int nC, uint8_t* const* send, uint8_t* const* recv,
+                         uint64_t seed, int64_t unit_bytes) {
+  int rc = build_dyn(P, nC, unit_bytes);
+  if (rc) return rc;
+  const DynTables& D = P.dyn;
+  const int G = P.G;
+  std::vector<std::vector<uint8_t>> scratch(G);
+  for (int g = 0; g < G; ++g) scratch[g].assign((size_t)P.info[g].scratch_bytes + 64, 0);
+  auto base = [&](int g, int loc) -> uint8_t* {
+    if (loc == loc_send()) return send[g];
+    if (loc >= 1 && loc < 1 + G) return recv[loc - 1];
+    return scratch[loc - 1 - G].data();
+  };
+  std::vector<std::vector<int32_t>> queue(G), done(G);
+  std::vector<int32_t> head(G, 0);
+  for (int g = 0; g < G; ++g) {
+    done[g].assign(D.units[g].size(), 0);
+    for (int32_t i = 0; i < D.n_init[g]; ++i) queue[g].push_back(i);
+  }
+  std::vector<std::vector<int32_t>> pos(G, std::vector<int32_t>(nC, -1));   // claimed position
+  uint64_t x = seed * 0x9E3779B97F4A7C15ULL + 5;
+  auto rnd = [&]() { x ^= x << 13; x ^= x >> 7; x ^= x << 17; return x; };
+  for (;;) {
+    std::vector<std::pair<int, int>> act;
+    bool pending = false;
+    for (int g = 0; g < G; ++g)
+      for (int c = 0; c < nC; ++c) {
+        const int32_t k = pos[g][c];
+        if (k < 0) {
+          if (head[g] < (int32_t)D.units[g].size()) act.emplace_back(g, c);   // claim
+        } else if (k < (int32_t)queue[g].size()) {
+          act.emplace_back(g, c);                                             // run
+        } else {
+          pending = true;                                                     // waits for its slot
+        }
+      }
+    if (act.empty()) {
+      if (pending) return fail(A2A_ERR_INVALID, "ready-queue emulation deadlock");
+      break;
+    }
+    auto [g, c] = act[rnd() % act.size()];
+    if (pos[g][c] < 0) {
+      pos[g][c] = head[g]++;
+      continue;
+    }
+    const int32_t li = queue[g][pos[g][c]];
+    pos[g][c] = -1;
+    const DevUnit& u = D.units[g][li];
+    std::memmove(base(g, u.dst_loc) + u.dst_off, base(g, u.src_loc) + u.src_off, (size_t)u.nbytes);
+    for (int32_t k = u.wb; k < u.we; ++k) {
+      const int32_t gid = D.deps_out[g][2 * k], deg = D.deps_out[g][2 * k + 1];
+      int h = 0;
+      while (gid >= D.unit_base[h + 1]) ++h;
+      const int32_t lj = gid - D.unit_base[h];
+      if (++done[h][lj] == deg) queue[h].push_back(lj);
+    }
+  }
+  for (int g = 0; g < G; ++g)
+    if ((int32_t)queue[g].size() != (int32_t)D.units[g].size())
+      return fail(A2A_ERR_INVALID, "ready-queue emulation: units never became ready");
   return A2A_OK;
 }
 
@@ -1439,7 +1552,7 @@ int a2a_plan_set_split(a2a_plan* plan, int32_t remote_weight) {
 }
 
 int a2a_plan_set_schedule(a2a_plan* plan, int32_t mode, int64_t unit_bytes) {
-  if (!plan || mode < 0 || mode > 4 || unit_bytes < 0) return fail(A2A_ERR_INVALID, "bad schedule mode");
+  if (!plan || mode < 0 || mode > 5 || unit_bytes < 0) return fail(A2A_ERR_INVALID, "bad schedule mode");
   if (plan->p.bound) return fail(A2A_ERR_STATE, "set the schedule mode before a2a_plan_bind");
   if (plan->p.ll && mode != 0)
     return fail(A2A_ERR_INVALID, "A2A_PROTO_LL plans run the static schedule only");
@@ -1475,6 +1588,9 @@ int a2a_plan_emulate(a2a_plan* plan, int32_t num_ctas, void* const* send, void* 
                      uint64_t seed) {
   if (!plan || !send || !recv) return fail(A2A_ERR_INVALID, "null argument");
   try {
+    if (plan->p.sched_mode == 5)
+      return emulate_ready(plan->p, num_ctas, (uint8_t* const*)send, (uint8_t* const*)recv, seed,
+                           plan->p.dyn_unit_bytes);
     if (plan->p.sched_mode >= 1)
       return emulate_dyn(plan->p, num_ctas, (uint8_t* const*)send, (uint8_t* const*)recv, seed,
                          plan->p.dyn_unit_bytes);

@@ -28,6 +28,7 @@ def test_random_schedule_emulation(seed):
     for proto, mode, reuse in (("simple", "static", False), ("simple", "static", True),
                                ("simple", "dynamic", False), ("simple", "list", True),
                                ("simple", "cp", False), ("simple", "mix", True),
+                               ("simple", "ready", False), ("simple", "ready", True),
                                ("ll", "static", False)):
         with Plan(g, sched, m=m, n_gpus=G, placement=placement, protocol=proto,
                   reuse_scratch=reuse) as p:
@@ -54,7 +55,8 @@ def test_random_schedule_gpu(seed):
     s = torch.from_numpy(send).cuda()
     for proto, mode, engine, nc in (("simple", "static", "tma", 0), ("simple", "static", "lsu", 5),
                                     ("simple", "cp", "tma", 0), ("simple", "dynamic", "lsu", 1),
-                                    ("simple", "list", "tma", 2), ("ll", "static", "lsu", 0),
+                                    ("simple", "list", "tma", 2), ("simple", "ready", "tma", 0),
+                                    ("simple", "ready", "lsu", 3), ("ll", "static", "lsu", 0),
                                     ("ll", "static", "tma", 3)):
         with Plan(g, sched, m=m, protocol=proto) as p:
             p.set_engine(engine)
@@ -85,7 +87,7 @@ def test_random_schedule_two_gpus(seed):
     placement[0], placement[-1] = 0, 1
     send = make_send(g.n, m, seed=seed)
     _, want, _ = replay_bytes(g, sched, send, m)
-    for proto, mode in (("simple", "static"), ("simple", "cp"), ("ll", "static")):
+    for proto, mode in (("simple", "static"), ("simple", "cp"), ("simple", "ready"), ("ll", "static")):
         plans = []
         for r in range(2):
             p = Plan(g, sched, m=m, n_gpus=2, placement=placement, protocol=proto)

@@ -274,7 +274,7 @@ def _alt_main(rank, world, port, q):
     (2, "tma", False, "gk8_2", 65536 + 64), (4, "tma", True, "torus4x4x4", 8192),
     (2, "lsu", True, "torus2x4_h2", 4099), (4, "lsu", False, "gk8_2", 65536 + 64),
     (4, "tma", False, "torus2x4_h2", 4099)])
-@pytest.mark.parametrize("mode", ["dynamic", "list", "cp", "mix"])
+@pytest.mark.parametrize("mode", ["dynamic", "list", "cp", "mix", "ready"])
 def test_multiprocess_dynamic(world, engine, reuse, name, m, mode):
     """Dynamic unit queues across GPUs (+ scratch reuse, optimized placement)."""
     if _ngpu() < world:
@@ -381,7 +381,8 @@ def test_gk256_four_gpus(name, sched):
 
 
 @pytest.mark.parametrize("name,m", [("gk8_2", 65536), ("hypercube3", 4096 + 7), ("gk64_4", 2048)])
-@pytest.mark.parametrize("proto,sched", [("simple", "static"), ("simple", "cp"), ("ll", "static")])
+@pytest.mark.parametrize("proto,sched", [("simple", "static"), ("simple", "cp"), ("simple", "mix"),
+                                         ("simple", "ready"), ("ll", "static")])
 def test_eight_ranks_single_process(name, m, proto, sched):
     """The 8-GPU code paths (8 peers, 8-bit destination masks, per-GPU exit
     lists) on real hardware with fewer devices: 8 plans of an 8-GPU placement
