@@ -723,6 +723,10 @@ __device__ __forceinline__ void ready_push(const KParams& p, int h, int32_t li, 
   const int32_t nu = p.ubase[h + 1] - p.ubase[h];
   const unsigned long long pos =
       atom_add_relaxed_sys(p.qctl[h] + 1, 1ull) - (unsigned long long)(epoch - 1) * (unsigned long long)nu;
+  if (pos >= (unsigned long long)nu) {  // more pushes than units: a broken epoch; never write past the queue
+    atomicCAS(p.err, 0, (int32_t)A2A_ERR_TIMEOUT);
+    return;
+  }
   st_release_sys_u64(p.qslot[h] + pos, ((unsigned long long)epoch << 32) | (uint32_t)li);
 }
 
