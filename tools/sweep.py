@@ -42,11 +42,14 @@ def main(argv=None):
     ap.add_argument("--out", default=None)
     ap.add_argument("--mem-limit-gib", type=float, default=150.0)
     ap.add_argument("--no-nccl", action="store_true")
-    ap.add_argument("--placement", default="optimized", choices=["optimized", "contiguous"])
+    ap.add_argument("--placement", default="optimized",
+                    help="optimized | contiguous | explicit node->GPU list '0,1,0,...'")
     ap.add_argument("--num-ctas", type=int, default=0)
     ap.add_argument("--schedule", default=None,
                     help="static | dynamic[:bytes] | auto; default: $A2A_SCHED or static")
     a = ap.parse_args(argv)
+    if a.placement not in ("optimized", "contiguous"):
+        a.placement = [int(x) for x in a.placement.split(",")]
     cases = [(name, m, None) for name, m in PRESETS.get(a.preset, [])] if a.preset else []
     for c in filter(None, a.cases.split(",")):
         c, _, case_sched = c.partition("@")
