@@ -224,8 +224,11 @@ class Plan:
         return self
 
     def set_schedule(self, mode: str = "static", unit_bytes: int = 0):
-        """Before bind: "static" per-CTA step programs or "dynamic" units
-        grabbed from a per-GPU queue."""
+        """Before bind: "static" per-CTA step programs, or unit queues (SURVEY
+        §8f f2) of ~unit_bytes units (0 = auto): "dynamic" (step-major,
+        readiness model), "list" (event-driven order), "cp" (critical-path
+        priority), "mix" (one queue, NVLink/HBM merged), "ready" (units enqueued
+        by their last producer).  LL plans run "static" only."""
         code = {"static": 0, "dynamic": 1, "list": 2, "cp": 3, "mix": 4, "ready": 5}[mode]
         self._ck(N.lib.a2a_plan_set_schedule(self._h, code, int(unit_bytes)), "a2a_plan_set_schedule")
         self.schedule = mode
