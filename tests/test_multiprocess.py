@@ -1,6 +1,6 @@
-"""World-size-2 gloo tests of the multi-GPU host logic (CPU only).
+"""Gloo tests of the multi-GPU host logic (CPU only), world sizes 2, 4 and 8.
 
-Two processes each build the plan for G=2 (as bench.py ranks do), prove they
+The processes each build the plan for G=world (as bench.py ranks do), prove they
 built identical layouts (plan digest), exchange fixed-size handles through the
 same all_gather_object path bench.py uses, and check that the per-rank pieces
 compose: each rank's recv rows from the oracle equal the transpose rows of its
@@ -66,12 +66,14 @@ def _worker(rank, world, port, name, m, q):
         q.put((rank, repr(ex)))
 
 
-@pytest.mark.parametrize("name,m", [("torus2x4", 96), ("gk8_2", 4096 + 1)])
-def test_two_rank_host_logic(name, m):
+@pytest.mark.parametrize("name,m,world", [("torus2x4", 96, 2), ("gk8_2", 4096 + 1, 2),
+                                          ("hypercube3", 4096, 4), ("gk8_2", 4096 + 1, 8)])
+def test_multi_rank_host_logic(name, m, world):
+    """world=8 is the driver's 8-GPU bench shape: one virtual node per rank."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, name, m, q)) for r in range(2)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, name, m, q)) for r in range(world)]
     for p in ps:
         p.start()
     res = [q.get(timeout=120) for _ in ps]
