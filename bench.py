@@ -246,15 +246,18 @@ LL_MAX_SHARD = 1 << 20   # autotune tries the LL transport up to this shard size
 
 
 def make_plan(art, m, G, placement, schedule):
-    """Plan for an execution-schedule spec: "static", "<dyn mode>:<unit bytes>",
-    or "ll" (static programs + the LL cross-GPU transport)."""
+    """Plan for an execution-schedule spec: "static", "<dyn mode>:<unit bytes>"
+    (optionally ":<R>": R CTAs pinned to the NVLink queue, the rest to the HBM
+    queue), or "ll" (static programs + the LL cross-GPU transport)."""
     from paper_2309_13541_b200.executor import Plan
     if schedule == "ll":
         return Plan(art.g, art.sched, m=m, n_gpus=G, placement=placement, protocol="ll")
     plan = Plan(art.g, art.sched, m=m, n_gpus=G, placement=placement)
     if schedule:
         mode, *ub = schedule.split(":")
-        plan.set_schedule(mode, *(int(x) for x in ub))
+        plan.set_schedule(mode, int(ub[0]) if ub else 0)
+        if len(ub) > 1:
+            plan.set_queue_split(int(ub[1]))
     return plan
 
 
@@ -268,7 +271,7 @@ def autotune_schedule(ctx, art, m, placement="optimized", num_ctas=0, trials=5,
     G, dev = ctx.world, ctx.dev
     if candidates is None:
         candidates = ("static", "mix:1048576", "cp:1048576", "ready:1048576") + (
-            ("ll",) if m <= LL_MAX_SHARD else ())
+            ("cp:1048576:64",) if G > 1 else ()) + (("ll",) if m <= LL_MAX_SHARD else ())
     times = {}
     for cand in candidates:
         plan = make_plan(art, m, G, placement, cand)

@@ -166,6 +166,11 @@ int a2a_plan_set_split(a2a_plan* plan, int32_t remote_weight);
  * a2a_plan_emulate follows the
  * selected mode.  Stats: units and dependency entries of `gpu`, model makespan. */
 int a2a_plan_set_schedule(a2a_plan* plan, int32_t mode, int64_t unit_bytes);
+/* Queue split of the two-queue dynamic orders (1-3), before bind: `remote_ctas`
+ * CTAs are pinned to the NVLink queue and the others to the HBM queue, and no
+ * CTA switches queues (0 = automatic split, CTAs switch when their queue
+ * drains).  Clamped so that every non-empty queue keeps at least one CTA. */
+int a2a_plan_set_queue_split(a2a_plan* plan, int32_t remote_ctas);
 int a2a_plan_dyn_stats(a2a_plan* plan, int32_t gpu, int32_t num_ctas, int64_t* n_units,
                        int64_t* n_wait, double* est_makespan_s);
 

@@ -95,6 +95,7 @@ def _load():
         "a2a_plan_check_bounds": ([P, C.c_int32], C.c_int),
         "a2a_plan_set_split": ([P, C.c_int32], C.c_int),
         "a2a_plan_set_schedule": ([P, C.c_int32, C.c_int64], C.c_int),
+        "a2a_plan_set_queue_split": ([P, C.c_int32], C.c_int),
         "a2a_plan_dyn_stats": ([P, C.c_int32, C.c_int32, C.POINTER(C.c_int64),
                                 C.POINTER(C.c_int64), C.POINTER(C.c_double)], C.c_int),
         "a2a_plan_set_engine": ([P, C.c_int32, C.c_int32, C.c_int32], C.c_int),

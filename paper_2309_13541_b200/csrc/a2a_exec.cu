@@ -68,6 +68,7 @@ struct KParams {
   const int32_t* unit_wait;                // global unit ids to acquire
   int32_t n_units, unit_base;              // this GPU's units; global id of its first
   int32_t n_remote, remote_ctas;           // remote queue = units [0, n_remote); CTAs starting on it
+  int32_t pin_queues;                      // CTAs never switch queues
   unsigned long long* grab;                // per-GPU grab counters [2] (remote, local queue)
   // ready-queue mode (sched_mode 5): per GPU its queue control words (head,
   // tail, arrived), per-unit completion counters and queue slots (arena, peer-visible)
@@ -798,11 +799,14 @@ __device__ __forceinline__ void dyn_body(const KParams& p, const uint32_t epoch)
     }
     long long idx = -1;
     for (;;) {  // own queue first, then the other; one failing grab per queue
+      // per execute a queue's counter advances by its units plus one failing
+      // grab per CTA that visits it: every CTA, or (pinned) the CTAs on it
       const long long qn = q == 0 ? p.n_remote : (long long)p.n_units - p.n_remote;
+      const long long visitors = !p.pin_queues ? p.nC : q == 0 ? p.remote_ctas : p.nC - p.remote_ctas;
       const long long j = (long long)(atomicAdd(p.grab + q, 1ull) -
-                                      (unsigned long long)(epoch - 1) * (unsigned long long)(qn + p.nC));
+                                      (unsigned long long)(epoch - 1) * (unsigned long long)(qn + visitors));
       if (j < qn) { idx = (q == 0 ? 0 : p.n_remote) + j; break; }
-      if (++visited == 2) break;
+      if (++visited == 2 || p.pin_queues) break;
       q ^= 1;
     }
     s_idx[sl] = idx;
@@ -1409,6 +1413,7 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
     }
     kp.n_remote = Dy.n_remote[P.rank];
     kp.remote_ctas = Dy.remote_ctas[P.rank];
+    kp.pin_queues = Dy.pin;
   } else {
     kp.n_exit = (int32_t)P.sync.exit_idx[P.rank].size();
   }

@@ -108,6 +108,7 @@ struct DynTables {
   std::vector<std::vector<DevUnit>> units;      // [g] grab order: remote queue, then local queue
   std::vector<int32_t> n_remote;                // [g] units in the remote (NVLink) queue
   std::vector<int32_t> remote_ctas;             // [g] CTAs that start on the remote queue
+  int32_t pin = 0;                              // CTAs never switch queues (a2a_plan_set_queue_split)
   std::vector<std::vector<int32_t>> wait_idx;   // [g] global unit ids to acquire
   std::vector<std::vector<int32_t>> exit_idx;   // [g] global unit ids flagged into g
   double est_makespan = 0;                      // host model estimate (s)
@@ -147,6 +148,7 @@ struct Plan {
   int32_t remote_weight = 1;                    // CTA split cost of an NVLink byte vs a local byte
   int32_t sched_mode = 0;                       // 0 static programs, 1 dynamic step-major, 2 dynamic list-scheduled
   int64_t dyn_unit_bytes = 0;                   // dynamic unit size (0 = auto)
+  int32_t dyn_remote_ctas = 0;                  // CTAs pinned to the NVLink queue (0 = auto split)
 
   // ---- device binding (a2a_exec.cu)
   bool bound = false, imported = false;

@@ -1214,7 +1214,17 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
     if (D.n_remote[g] > 0) nr = std::max(nr, std::max(1, nC / 4));
     if (D.n_remote[g] < (int)qorder[g].size()) nr = std::min(nr, nC - std::max(1, nC / 8));
     D.remote_ctas[g] = std::max(0, std::min(nr, nC));
+    if (P.dyn_remote_ctas > 0) {
+      // pinned split: a fixed number of CTAs on the NVLink queue, the rest on
+      // the HBM queue, and no CTA switches queues.  Fewer concurrent NVLink
+      // units each finish sooner, so their dependents are ready by the time
+      // they are grabbed (step overlap).  Deadlock-free as long as every
+      // non-empty queue keeps >= 1 CTA (same induction as above).
+      const bool has_r = D.n_remote[g] > 0, has_l = D.n_remote[g] < (int)qorder[g].size();
+      D.remote_ctas[g] = !has_r ? 0 : has_l ? std::min(P.dyn_remote_ctas, nC - 1) : nC;
+    }
   }
+  D.pin = (P.dyn_remote_ctas > 0 && nC >= 2 && P.sched_mode != 4 && P.sched_mode != 5) ? 1 : 0;
   D.wait_idx.assign(G, {});
   D.exit_idx.assign(G, {});
   for (int g = 0; g < G; ++g)
@@ -1373,7 +1383,7 @@ static int emulate_dyn(Plan& P, int nC, uint8_t* const* send, uint8_t* const* re
   auto pick_queue = [&](int g, int c) -> int {  // queue a CTA grabs from, -1 if both drained
     const int own = c < D.remote_ctas[g] ? 0 : 1;
     if (next[g][own] < qend[g][own]) return own;
-    if (next[g][1 - own] < qend[g][1 - own]) return 1 - own;
+    if (!D.pin && next[g][1 - own] < qend[g][1 - own]) return 1 - own;
     return -1;
   };
   uint64_t x = seed * 0x9E3779B97F4A7C15ULL + 3;
@@ -1558,6 +1568,14 @@ int a2a_plan_set_schedule(a2a_plan* plan, int32_t mode, int64_t unit_bytes) {
     return fail(A2A_ERR_INVALID, "A2A_PROTO_LL plans run the static schedule only");
   plan->p.sched_mode = mode;
   plan->p.dyn_unit_bytes = unit_bytes;
+  plan->p.dyn = DynTables{};
+  return A2A_OK;
+}
+
+int a2a_plan_set_queue_split(a2a_plan* plan, int32_t remote_ctas) {
+  if (!plan || remote_ctas < 0) return fail(A2A_ERR_INVALID, "bad remote CTA count");
+  if (plan->p.bound) return fail(A2A_ERR_STATE, "set the queue split before a2a_plan_bind");
+  plan->p.dyn_remote_ctas = remote_ctas;
   plan->p.dyn = DynTables{};
   return A2A_OK;
 }

@@ -234,6 +234,15 @@ class Plan:
         self.schedule = mode
         return self
 
+    def set_queue_split(self, remote_ctas: int = 0):
+        """Before bind (two-queue orders "dynamic" / "list" / "cp"): pin
+        `remote_ctas` CTAs to the NVLink queue and the rest to the HBM queue, no
+        queue switching (0 = automatic split)."""
+        self._ck(N.lib.a2a_plan_set_queue_split(self._h, int(remote_ctas)),
+                 "a2a_plan_set_queue_split")
+        self.remote_ctas = int(remote_ctas)
+        return self
+
     def dyn_stats(self, gpu: int, num_ctas: int) -> dict:
         nu, nw, est = C.c_int64(), C.c_int64(), C.c_double()
         self._ck(N.lib.a2a_plan_dyn_stats(self._h, int(gpu), int(num_ctas), C.byref(nu),

@@ -172,6 +172,35 @@ def test_dynamic_schedule_interleavings(name, G, unit, reuse, mode, artifacts):
         assert st["units"] > 0
 
 
+@pytest.mark.parametrize("name,G", [("gk8_2", 1), ("gk8_2", 2), ("gk8_2", 8), ("hypercube3", 4),
+                                    ("torus4x4x4", 4), ("torus2x4_h2", 4), ("ts_torus2x4", 2)])
+@pytest.mark.parametrize("mode", ["dynamic", "list", "cp"])
+@pytest.mark.parametrize("remote_ctas,nC", [(1, 11), (3, 11), (10, 11), (40, 11), (1, 2), (32, 148)])
+def test_pinned_queue_split_interleavings(name, G, mode, remote_ctas, nC, artifacts):
+    """Pinned two-queue split (a2a_plan_set_queue_split): CTAs never switch
+    queues; every non-empty queue keeps a CTA, so random interleavings still
+    deliver the transpose and never deadlock (emulator mirrors the kernel)."""
+    a = artifacts(name)
+    m = 5000 if a.g.n <= 9 else 640
+    send = make_send(a.g.n, m, seed=12)
+    with Plan(a.g, a.sched, m=m, n_gpus=G, placement="optimized") as p:
+        p.set_schedule(mode, 1024).set_queue_split(remote_ctas)
+        p.check_bounds(nC)
+        nodes = [local_nodes(p, g) for g in range(G)]
+        for seed in range(2):
+            recvs = p.emulate([send[ns] for ns in nodes], num_ctas=nC, seed=seed)
+            want = np.swapaxes(send, 0, 1)
+            for g in range(G):
+                assert np.array_equal(recvs[g], want[nodes[g]]), (seed, g)
+
+
+def test_queue_split_rejects(artifacts):
+    a = artifacts("gk8_2")
+    with Plan(a.g, a.sched, m=4096, n_gpus=2) as p:
+        with pytest.raises(ValueError):
+            p.set_queue_split(-1)
+
+
 @pytest.mark.parametrize("name,G", [("gk8_2", 2), ("gk8_2", 4), ("torus4x4x4", 4), ("hypercube3", 8),
                                     ("torus2x4_h2", 4), ("ts_hypercube3", 2)])
 @pytest.mark.parametrize("w", [1, 3, 8])

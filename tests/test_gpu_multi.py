@@ -64,7 +64,10 @@ def _rank_main(rank, world, port, name, m, reps, q, engine="lsu", sched="static"
         plan = Plan(a.g, a.sched, m=m, n_gpus=world, reuse_scratch=reuse, placement="optimized",
                     protocol=proto)
         plan.set_engine(engine)
-        plan.set_schedule(sched)
+        mode, *rest = sched.split(":")      # "<mode>[:<unit bytes>[:<pinned NVLink CTAs>]]"
+        plan.set_schedule(mode, int(rest[0]) if rest else 0)
+        if len(rest) > 1:
+            plan.set_queue_split(int(rest[1]))
         plan.bind(rank, device=rank)
         plan.set_timeout(20.0)
         connect(plan)
@@ -274,7 +277,7 @@ def _alt_main(rank, world, port, q):
     (2, "tma", False, "gk8_2", 65536 + 64), (4, "tma", True, "torus4x4x4", 8192),
     (2, "lsu", True, "torus2x4_h2", 4099), (4, "lsu", False, "gk8_2", 65536 + 64),
     (4, "tma", False, "torus2x4_h2", 4099)])
-@pytest.mark.parametrize("mode", ["dynamic", "list", "cp", "mix", "ready"])
+@pytest.mark.parametrize("mode", ["dynamic", "list", "cp", "mix", "ready", "cp:0:3", "dynamic:4096:40"])
 def test_multiprocess_dynamic(world, engine, reuse, name, m, mode):
     """Dynamic unit queues across GPUs (+ scratch reuse, optimized placement)."""
     if _ngpu() < world:
