@@ -1357,6 +1357,8 @@ static int emulate_ready(Plan& P, int nC, uint8_t* const* send, uint8_t* const* 
 // Host emulation of the dynamic protocol: CTAs grab units in list order and
 // execute them once their producers' flags are visible on their GPU; random
 // interleavings; a stuck state is a deadlock error.
+constexpr uint32_t kEmuEpochs = 3;  // executes per emulation (counters carry across)
+
 static int emulate_dyn(Plan& P, int nC, uint8_t* const* send, uint8_t* const* recv, uint64_t seed,
                        int64_t unit_bytes) {
   int rc = build_dyn(P, nC, unit_bytes);
@@ -1366,25 +1368,42 @@ static int emulate_dyn(Plan& P, int nC, uint8_t* const* send, uint8_t* const* re
   std::vector<std::vector<uint8_t>> scratch(G);
   for (int g = 0; g < G; ++g) scratch[g].assign((size_t)P.info[g].scratch_bytes + 64, 0);
   const int total = D.unit_base[G];
-  std::vector<std::vector<char>> flag(G, std::vector<char>((size_t)total, 0));
   // two queues per GPU: [0, n_remote) and [n_remote, n); CTA c starts on the
   // remote queue iff c < remote_ctas[g] and switches when its queue drains
-  std::vector<std::array<int, 2>> next(G), qend(G);
-  for (int g = 0; g < G; ++g) {
-    next[g] = {0, D.n_remote[g]};
-    qend[g] = {D.n_remote[g], (int)D.units[g].size()};
-  }
+  // (unless pinned).  The grab counters persist across executes exactly as on
+  // the device: a grab's queue position is counter - (epoch-1)*(units +
+  // visitors), visitors = CTAs that end with one failing grab on that queue.
+  std::vector<std::array<int, 2>> qn(G);
+  std::vector<std::array<uint64_t, 2>> ctr(G, std::array<uint64_t, 2>{0, 0});
+  for (int g = 0; g < G; ++g) qn[g] = {D.n_remote[g], (int)D.units[g].size() - D.n_remote[g]};
+  auto visitors = [&](int g, int q) -> int64_t {
+    return !D.pin ? nC : q == 0 ? D.remote_ctas[g] : nC - D.remote_ctas[g];
+  };
+  for (uint32_t epoch = 1; epoch <= kEmuEpochs; ++epoch) {
+  for (int g = 0; g < G; ++g) std::fill(scratch[g].begin(), scratch[g].end(), 0);
+  std::vector<std::vector<char>> flag(G, std::vector<char>((size_t)total, 0));
   std::vector<std::vector<int>> held(G, std::vector<int>(nC, -1));
+  std::vector<std::vector<int>> cq(G, std::vector<int>(nC)), visited(G, std::vector<int>(nC, 0));
+  std::vector<std::vector<char>> fin(G, std::vector<char>(nC, 0));
+  for (int g = 0; g < G; ++g)
+    for (int c = 0; c < nC; ++c) cq[g][c] = c < D.remote_ctas[g] ? 0 : 1;
+  int64_t ran = 0;
   auto base = [&](int g, int loc) -> uint8_t* {
     if (loc == loc_send()) return send[g];
     if (loc >= 1 && loc < 1 + G) return recv[loc - 1];
     return scratch[loc - 1 - G].data();
   };
-  auto pick_queue = [&](int g, int c) -> int {  // queue a CTA grabs from, -1 if both drained
-    const int own = c < D.remote_ctas[g] ? 0 : 1;
-    if (next[g][own] < qend[g][own]) return own;
-    if (!D.pin && next[g][1 - own] < qend[g][1 - own]) return 1 - own;
-    return -1;
+  // the kernel's fetch: own queue first, then the other; one failing grab per
+  // visited queue; returns the unit index or -1 (CTA done)
+  auto grab = [&](int g, int c) -> int {
+    for (;;) {
+      const int q = cq[g][c];
+      const int64_t j = (int64_t)(ctr[g][q]++ - (uint64_t)(epoch - 1) * (uint64_t)(qn[g][q] + visitors(g, q)));
+      if (j < 0) return -2;
+      if (j < qn[g][q]) return (q == 0 ? 0 : D.n_remote[g]) + (int)j;
+      if (++visited[g][c] == 2 || D.pin) return -1;
+      cq[g][c] ^= 1;
+    }
   };
   uint64_t x = seed * 0x9E3779B97F4A7C15ULL + 3;
   auto rnd = [&]() { x ^= x << 13; x ^= x >> 7; x ^= x << 17; return x; };
@@ -1395,7 +1414,7 @@ static int emulate_dyn(Plan& P, int nC, uint8_t* const* send, uint8_t* const* re
       for (int c = 0; c < nC; ++c) {
         int u = held[g][c];
         if (u < 0) {
-          if (pick_queue(g, c) >= 0) act.emplace_back(g, c);
+          if (!fin[g][c]) act.emplace_back(g, c);
           continue;
         }
         busy = true;
@@ -1410,8 +1429,10 @@ static int emulate_dyn(Plan& P, int nC, uint8_t* const* send, uint8_t* const* re
     }
     auto [g, c] = act[rnd() % act.size()];
     if (held[g][c] < 0) {
-      const int q = pick_queue(g, c);
-      held[g][c] = next[g][q]++;
+      const int u = grab(g, c);
+      if (u == -2) return fail(A2A_ERR_INVALID, "dynamic emulation: grab counter base mismatch across executes");
+      if (u < 0) fin[g][c] = 1;
+      else held[g][c] = u;
     } else {
       const DevUnit& du = D.units[g][held[g][c]];
       std::memmove(base(g, du.dst_loc) + du.dst_off, base(g, du.src_loc) + du.src_off, (size_t)du.nbytes);
@@ -1419,7 +1440,10 @@ static int emulate_dyn(Plan& P, int nC, uint8_t* const* send, uint8_t* const* re
       for (int h = 0; h < G; ++h)
         if (du.mask & (1u << h)) flag[h][id] = 1;
       held[g][c] = -1;
+      ++ran;
     }
+  }
+  if (ran != total) return fail(A2A_ERR_INVALID, "dynamic emulation: units skipped in an execute");
   }
   return A2A_OK;
 }
