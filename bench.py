@@ -271,7 +271,8 @@ def autotune_schedule(ctx, art, m, placement="optimized", num_ctas=0, trials=5,
     G, dev = ctx.world, ctx.dev
     if candidates is None:
         candidates = ("static", "mix:1048576", "cp:1048576", "ready:1048576") + (
-            ("cp:1048576:64",) if G > 1 else ()) + (("ll",) if m <= LL_MAX_SHARD else ())
+            ("cp:1048576:64",) if G > 1 else ()) + (
+            ("spread:1048576",) if G > 2 else ()) + (("ll",) if m <= LL_MAX_SHARD else ())
     times = {}
     for cand in candidates:
         plan = make_plan(art, m, G, placement, cand)
@@ -561,7 +562,7 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
            "flush_ms_p50_by_rank": [round(x[0], 4) for x in alld],
            "step_period_ms_p50_by_rank": [round(x[1], 4) for x in alld],
            "step_ms_by_rank": [x[2] for x in alld] if os.environ.get("A2A_DIAG") else None,
-           "sync": (plan.dyn_stats(rank, plan_ctas(plan, num_ctas)) if plan.schedule in ("dynamic", "list", "cp", "mix", "ready")
+           "sync": (plan.dyn_stats(rank, plan_ctas(plan, num_ctas)) if plan.schedule in ("dynamic", "list", "cp", "mix", "ready", "spread")
                     else plan.sync_stats(rank)),
            "kernel_timeline": tls,
            "num_ctas": plan_ctas(plan, num_ctas), "egress_max": max(i["egress_bytes"] for i in infos),

@@ -162,7 +162,9 @@ int a2a_plan_set_split(a2a_plan* plan, int32_t remote_weight);
  * critical-path (bottom-level) priority within a step; 4 = one queue per GPU,
  * step-major, NVLink and HBM units merged in proportion to their time; 5 = a
  * per-GPU ready queue: units are enqueued when their last producer finishes
- * (completion counters counted down with system-scope atomics).
+ * (completion counters counted down with system-scope atomics); 6 = as 4, with
+ * each step's NVLink units interleaved over their destination GPUs in
+ * proportion to their bytes (no incast on one peer).
  * a2a_plan_emulate follows the
  * selected mode.  Stats: units and dependency entries of `gpu`, model makespan. */
 int a2a_plan_set_schedule(a2a_plan* plan, int32_t mode, int64_t unit_bytes);

@@ -1065,11 +1065,15 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
       for (int t = 0; t < TE; ++t)
         std::stable_sort(per[g][t].begin(), per[g][t].end(),
                          [&](int a, int b) { return key[a] < key[b]; });
-  } else if (P.sched_mode == 4) {
+  } else if (P.sched_mode == 4 || P.sched_mode == 6) {
     // single queue, step-major; within a step the NVLink and HBM units are
     // merged in proportion to their estimated time (remote byte ~ hbm/nv local
     // bytes), each class ordered by critical path, so both pipes stay busy and
-    // neither class runs ahead of the other
+    // neither class runs ahead of the other.  Mode 6 ("spread") also
+    // interleaves the NVLink units over their destination GPUs in proportion
+    // to each destination's bytes, starting at g+1, so the units in flight at
+    // any moment cover every peer (no incast: a critical-path order keeps one
+    // source node's units together, i.e. a few destination GPUs at a time)
     std::vector<std::vector<int>> succ(all.size());
     for (int i = 0; i < (int)all.size(); ++i)
       for (int d : all[i].deps) succ[d].push_back(i);
@@ -1093,6 +1097,30 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
         auto bysl = [&](int a, int b) { return bl[a] > bl[b]; };
         std::stable_sort(rq.begin(), rq.end(), bysl);
         std::stable_sort(lq.begin(), lq.end(), bysl);
+        if (P.sched_mode == 6 && G > 2) {
+          std::vector<std::vector<int>> byd(G);
+          std::vector<double> tot(G, 0), done(G, 0);
+          for (int id : rq) {
+            byd[all[id].dst_gpu].push_back(id);
+            tot[all[id].dst_gpu] += all[id].u.nbytes;
+          }
+          std::vector<size_t> pos(G, 0);
+          rq.clear();
+          for (;;) {
+            int best = -1;
+            double bf = 0;
+            for (int k = 1; k < G; ++k) {
+              const int h = (g + k) % G;
+              if (pos[h] >= byd[h].size()) continue;
+              const double f = done[h] / tot[h];
+              if (best < 0 || f < bf) { best = h; bf = f; }
+            }
+            if (best < 0) break;
+            const int id = byd[best][pos[best]++];
+            done[best] += all[id].u.nbytes;
+            rq.push_back(id);
+          }
+        }
         std::vector<int> merged;
         size_t i = 0, j = 0;
         double er = 0, el = 0;
@@ -1176,7 +1204,7 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
     // stuck on one queue could wait for a unit only the other queue holds
     // (ready-queue mode: one array, units without dependencies first -- they
     // seed the queue -- each part in key order)
-    if (P.sched_mode == 4 || P.sched_mode == 5 || nC < 2) {
+    if (P.sched_mode >= 4 || nC < 2) {
       std::vector<int> q;
       for (int t = 0; t < TE; ++t)
         for (int id : per[g][t]) q.push_back(id);
@@ -1224,7 +1252,7 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
       D.remote_ctas[g] = !has_r ? 0 : has_l ? std::min(P.dyn_remote_ctas, nC - 1) : nC;
     }
   }
-  D.pin = (P.dyn_remote_ctas > 0 && nC >= 2 && P.sched_mode != 4 && P.sched_mode != 5) ? 1 : 0;
+  D.pin = (P.dyn_remote_ctas > 0 && nC >= 2 && P.sched_mode < 4) ? 1 : 0;
   D.wait_idx.assign(G, {});
   D.exit_idx.assign(G, {});
   for (int g = 0; g < G; ++g)
@@ -1586,7 +1614,7 @@ int a2a_plan_set_split(a2a_plan* plan, int32_t remote_weight) {
 }
 
 int a2a_plan_set_schedule(a2a_plan* plan, int32_t mode, int64_t unit_bytes) {
-  if (!plan || mode < 0 || mode > 5 || unit_bytes < 0) return fail(A2A_ERR_INVALID, "bad schedule mode");
+  if (!plan || mode < 0 || mode > 6 || unit_bytes < 0) return fail(A2A_ERR_INVALID, "bad schedule mode");
   if (plan->p.bound) return fail(A2A_ERR_STATE, "set the schedule mode before a2a_plan_bind");
   if (plan->p.ll && mode != 0)
     return fail(A2A_ERR_INVALID, "A2A_PROTO_LL plans run the static schedule only");

@@ -152,7 +152,7 @@ def test_scratch_reuse_saves_memory(artifacts):
                                     ("ts_torus3x3", 1), ("torus2x4_h2", 4)])
 @pytest.mark.parametrize("unit", [0, 256, 1000 * 64])
 @pytest.mark.parametrize("reuse", [False, True])
-@pytest.mark.parametrize("mode", ["dynamic", "list", "cp", "mix", "ready"])
+@pytest.mark.parametrize("mode", ["dynamic", "list", "cp", "mix", "ready", "spread"])
 def test_dynamic_schedule_interleavings(name, G, unit, reuse, mode, artifacts):
     """Dynamic unit queues (f2): in-order grabbing + per-unit producer flags
     deliver the transpose under random interleavings, with and without

@@ -29,6 +29,7 @@ def test_random_schedule_emulation(seed):
                                ("simple", "dynamic", False), ("simple", "list", True),
                                ("simple", "cp", False), ("simple", "mix", True),
                                ("simple", "ready", False), ("simple", "ready", True),
+                               ("simple", "spread", False),
                                ("ll", "static", False)):
         with Plan(g, sched, m=m, n_gpus=G, placement=placement, protocol=proto,
                   reuse_scratch=reuse) as p:

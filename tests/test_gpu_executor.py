@@ -177,7 +177,7 @@ def test_tma_engine_n64(artifacts):
 @pytest.mark.parametrize("engine", ["tma", "lsu"])
 @pytest.mark.parametrize("m,unit", [(7, 0), (4096 + 5, 0), (65536, 4096), ((1 << 20) + 48, 0)])
 @pytest.mark.parametrize("reuse", [False, True])
-@pytest.mark.parametrize("mode", ["dynamic", "list", "cp", "mix", "ready"])
+@pytest.mark.parametrize("mode", ["dynamic", "list", "cp", "mix", "ready", "spread"])
 def test_dynamic_schedule_bit_exact(name, engine, m, unit, reuse, mode, artifacts):
     """Dynamic unit queues (f2) on the device: exact over repeated executes
     (the grab counter carries across epochs), with and without scratch reuse."""

@@ -277,7 +277,7 @@ def _alt_main(rank, world, port, q):
     (2, "tma", False, "gk8_2", 65536 + 64), (4, "tma", True, "torus4x4x4", 8192),
     (2, "lsu", True, "torus2x4_h2", 4099), (4, "lsu", False, "gk8_2", 65536 + 64),
     (4, "tma", False, "torus2x4_h2", 4099)])
-@pytest.mark.parametrize("mode", ["dynamic", "list", "cp", "mix", "ready", "cp:0:3", "dynamic:4096:40"])
+@pytest.mark.parametrize("mode", ["dynamic", "list", "cp", "mix", "ready", "spread", "cp:0:3", "dynamic:4096:40"])
 def test_multiprocess_dynamic(world, engine, reuse, name, m, mode):
     """Dynamic unit queues across GPUs (+ scratch reuse, optimized placement)."""
     if _ngpu() < world:
