@@ -1221,278 +1221,310 @@ using namespace a2a;
 extern "C" {
 
 int a2a_plan_destroy(a2a_plan* plan) {
-  if (!plan) return A2A_OK;
-  if (plan->p.launched && plan->p.device >= 0) {
-    DeviceGuard dg(plan->p.device);
-    cudaDeviceSynchronize();
-  }
-  free_device(plan->p);
-  delete plan;
-  return A2A_OK;
+  return guard([&]() -> int {
+    if (!plan) return A2A_OK;
+    if (plan->p.launched && plan->p.device >= 0) {
+      DeviceGuard dg(plan->p.device);
+      cudaDeviceSynchronize();
+    }
+    free_device(plan->p);
+    delete plan;
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_bind(a2a_plan* plan, int32_t gpu, int32_t device_ordinal, int32_t num_ctas) {
-  if (!plan) return fail(A2A_ERR_INVALID, "null plan");
-  if (plan->p.bound) return fail(A2A_ERR_STATE, "plan already bound");
-  int rc = bind_plan(plan->p, gpu, device_ordinal, num_ctas);
-  if (rc != A2A_OK) {
-    std::string msg = a2a_last_error();
-    free_device(plan->p);
-    set_error(msg);
-  }
-  return rc;
+  return guard([&]() -> int {
+    if (!plan) return fail(A2A_ERR_INVALID, "null plan");
+    if (plan->p.bound) return fail(A2A_ERR_STATE, "plan already bound");
+    int rc = bind_plan(plan->p, gpu, device_ordinal, num_ctas);
+    if (rc != A2A_OK) {
+      std::string msg = a2a_last_error();
+      free_device(plan->p);
+      set_error(msg);
+    }
+    return rc;
+  });
 }
 
 int a2a_plan_export_handle(const a2a_plan* plan, void* out_handle64) {
-  if (!plan || !out_handle64) return fail(A2A_ERR_INVALID, "null argument");
-  if (!plan->p.bound) return fail(A2A_ERR_STATE, "plan not bound");
-  DeviceGuard dg(plan->p.device);
-  cudaIpcMemHandle_t h;
-  CK(cudaIpcGetMemHandle(&h, plan->p.arena));
-  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
-  std::memcpy(out_handle64, &h, 64);
-  return A2A_OK;
+  return guard([&]() -> int {
+    if (!plan || !out_handle64) return fail(A2A_ERR_INVALID, "null argument");
+    if (!plan->p.bound) return fail(A2A_ERR_STATE, "plan not bound");
+    DeviceGuard dg(plan->p.device);
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, plan->p.arena));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
+    std::memcpy(out_handle64, &h, 64);
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_import_handles(a2a_plan* plan, const void* handles) {
-  if (!plan || !handles) return fail(A2A_ERR_INVALID, "null argument");
-  Plan& P = plan->p;
-  if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound");
-  if (P.imported && P.G > 1) return fail(A2A_ERR_STATE, "peer handles already imported");
-  DeviceGuard dg(P.device);
-  for (int g = 0; g < P.G; ++g) {
-    if (g == P.rank) continue;
-    cudaIpcMemHandle_t h;
-    std::memcpy(&h, (const char*)handles + 64 * g, 64);
-    void* ptr = nullptr;
-    CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
-    P.peer_arena[g] = ptr;
-    P.peer_opened[g] = true;
-  }
-  P.imported = true;
-  return A2A_OK;
+  return guard([&]() -> int {
+    if (!plan || !handles) return fail(A2A_ERR_INVALID, "null argument");
+    Plan& P = plan->p;
+    if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound");
+    if (P.imported && P.G > 1) return fail(A2A_ERR_STATE, "peer handles already imported");
+    DeviceGuard dg(P.device);
+    for (int g = 0; g < P.G; ++g) {
+      if (g == P.rank) continue;
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, (const char*)handles + 64 * g, 64);
+      void* ptr = nullptr;
+      CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+      P.peer_arena[g] = ptr;
+      P.peer_opened[g] = true;
+    }
+    P.imported = true;
+    return A2A_OK;
+  });
 }
 
 // single-process multi-GPU: peers' arenas given directly (peer access is enabled here)
 int a2a_plan_import_pointers(a2a_plan* plan, void* const* arenas) {
-  if (!plan || !arenas) return fail(A2A_ERR_INVALID, "null argument");
-  Plan& P = plan->p;
-  if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound");
-  DeviceGuard dg(P.device);
-  for (int g = 0; g < P.G; ++g) {
-    if (g == P.rank) continue;
-    cudaPointerAttributes attr;
-    CK(cudaPointerGetAttributes(&attr, arenas[g]));
-    if (attr.device != P.device) {
-      cudaError_t e = cudaDeviceEnablePeerAccess(attr.device, 0);
-      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
-      else if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+  return guard([&]() -> int {
+    if (!plan || !arenas) return fail(A2A_ERR_INVALID, "null argument");
+    Plan& P = plan->p;
+    if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound");
+    DeviceGuard dg(P.device);
+    for (int g = 0; g < P.G; ++g) {
+      if (g == P.rank) continue;
+      cudaPointerAttributes attr;
+      CK(cudaPointerGetAttributes(&attr, arenas[g]));
+      if (attr.device != P.device) {
+        cudaError_t e = cudaDeviceEnablePeerAccess(attr.device, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+      }
+      P.peer_arena[g] = arenas[g];
+      P.peer_opened[g] = false;
     }
-    P.peer_arena[g] = arenas[g];
-    P.peer_opened[g] = false;
-  }
-  P.imported = true;
-  return A2A_OK;
+    P.imported = true;
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_arena(const a2a_plan* plan, void** out_ptr) {
-  if (!plan || !out_ptr) return fail(A2A_ERR_INVALID, "null argument");
-  if (!plan->p.bound) return fail(A2A_ERR_STATE, "plan not bound");
-  *out_ptr = plan->p.arena;
-  return A2A_OK;
+  return guard([&]() -> int {
+    if (!plan || !out_ptr) return fail(A2A_ERR_INVALID, "null argument");
+    if (!plan->p.bound) return fail(A2A_ERR_STATE, "plan not bound");
+    *out_ptr = plan->p.arena;
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_recv_buffer(const a2a_plan* plan, void** out_ptr) {
-  if (!plan || !out_ptr) return fail(A2A_ERR_INVALID, "null argument");
-  if (!plan->p.bound) return fail(A2A_ERR_STATE, "plan not bound");
-  *out_ptr = (char*)plan->p.arena + plan->p.recv_off[plan->p.rank];
-  return A2A_OK;
+  return guard([&]() -> int {
+    if (!plan || !out_ptr) return fail(A2A_ERR_INVALID, "null argument");
+    if (!plan->p.bound) return fail(A2A_ERR_STATE, "plan not bound");
+    *out_ptr = (char*)plan->p.arena + plan->p.recv_off[plan->p.rank];
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_recv_buffer_at(const a2a_plan* plan, int32_t index, void** out_ptr) {
-  if (!plan || !out_ptr) return fail(A2A_ERR_INVALID, "null argument");
-  const Plan& P = plan->p;
-  if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound");
-  if (index < 0 || index >= P.n_recv) return fail(A2A_ERR_INVALID, "recv buffer index out of range");
-  *out_ptr = (char*)P.arena + P.recv_off[P.rank] + (int64_t)index * recv_stride(P, P.rank);
-  return A2A_OK;
+  return guard([&]() -> int {
+    if (!plan || !out_ptr) return fail(A2A_ERR_INVALID, "null argument");
+    const Plan& P = plan->p;
+    if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound");
+    if (index < 0 || index >= P.n_recv) return fail(A2A_ERR_INVALID, "recv buffer index out of range");
+    *out_ptr = (char*)P.arena + P.recv_off[P.rank] + (int64_t)index * recv_stride(P, P.rank);
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_set_engine(a2a_plan* plan, int32_t engine, int32_t tma_chunk, int32_t tma_stages) {
-  if (!plan) return fail(A2A_ERR_INVALID, "null plan");
-  if (plan->p.bound) return fail(A2A_ERR_STATE, "set the copy engine before a2a_plan_bind");
-  if (engine != 0 && engine != 1) return fail(A2A_ERR_INVALID, "engine must be 0 (LSU) or 1 (TMA)");
-  if (engine == 1) {
-    if (tma_chunk <= 0) tma_chunk = 32768;
-    if (tma_stages <= 0) tma_stages = 6;
-    if (tma_chunk % 16 || tma_chunk > (1 << 19) || tma_stages > 32 ||
-        (size_t)tma_chunk * tma_stages > 220 * 1024)
-      return fail(A2A_ERR_INVALID, "bad TMA ring (chunk % 16, chunk*stages <= 220 KiB)");
-    plan->p.tma_chunk = tma_chunk;
-    plan->p.tma_stages = tma_stages;
-  }
-  plan->p.engine = engine;
-  return A2A_OK;
+  return guard([&]() -> int {
+    if (!plan) return fail(A2A_ERR_INVALID, "null plan");
+    if (plan->p.bound) return fail(A2A_ERR_STATE, "set the copy engine before a2a_plan_bind");
+    if (engine != 0 && engine != 1) return fail(A2A_ERR_INVALID, "engine must be 0 (LSU) or 1 (TMA)");
+    if (engine == 1) {
+      if (tma_chunk <= 0) tma_chunk = 32768;
+      if (tma_stages <= 0) tma_stages = 6;
+      if (tma_chunk % 16 || tma_chunk > (1 << 19) || tma_stages > 32 ||
+          (size_t)tma_chunk * tma_stages > 220 * 1024)
+        return fail(A2A_ERR_INVALID, "bad TMA ring (chunk % 16, chunk*stages <= 220 KiB)");
+      plan->p.tma_chunk = tma_chunk;
+      plan->p.tma_stages = tma_stages;
+    }
+    plan->p.engine = engine;
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_set_recv_buffers(a2a_plan* plan, int32_t count) {
-  if (!plan) return fail(A2A_ERR_INVALID, "null plan");
-  if (plan->p.bound) return fail(A2A_ERR_STATE, "set the recv buffer count before a2a_plan_bind");
-  if (count < 1 || count > 4) return fail(A2A_ERR_INVALID, "recv buffer count must be 1..4");
-  plan->p.n_recv = count;
-  return A2A_OK;
+  return guard([&]() -> int {
+    if (!plan) return fail(A2A_ERR_INVALID, "null plan");
+    if (plan->p.bound) return fail(A2A_ERR_STATE, "set the recv buffer count before a2a_plan_bind");
+    if (count < 1 || count > 4) return fail(A2A_ERR_INVALID, "recv buffer count must be 1..4");
+    plan->p.n_recv = count;
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_set_sync_mode(a2a_plan* plan, int32_t mode) {
-  if (!plan || mode < 0 || mode > 63) return fail(A2A_ERR_INVALID, "bad sync mode");
-  plan->p.sync_mode = mode;
-  return A2A_OK;
+  return guard([&]() -> int {
+    if (!plan || mode < 0 || mode > 63) return fail(A2A_ERR_INVALID, "bad sync mode");
+    plan->p.sync_mode = mode;
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_set_timeout(a2a_plan* plan, int64_t timeout_ns) {
-  if (!plan || timeout_ns <= 0) return fail(A2A_ERR_INVALID, "bad argument");
-  plan->p.timeout_ns = timeout_ns;
-  return A2A_OK;
+  return guard([&]() -> int {
+    if (!plan || timeout_ns <= 0) return fail(A2A_ERR_INVALID, "bad argument");
+    plan->p.timeout_ns = timeout_ns;
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream, int32_t options) {
-  if (!plan) return fail(A2A_ERR_INVALID, "null plan");
-  Plan& P = plan->p;
-  if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound to a device");
-  if (!P.imported) return fail(A2A_ERR_STATE, "peer arenas not imported");
-  if (*P.h_err != 0) return fail(*P.h_err, "a previous execute failed on the device (timeout)");
-  char* own_recv = (char*)P.arena + P.recv_off[P.rank];
-  if (!recv) recv = own_recv;
-  int32_t ridx = 0;
-  if (P.G > 1 && !P.ll) {
-    const int64_t st = recv_stride(P, P.rank);
-    ridx = -1;
-    for (int i = 0; i < P.n_recv; ++i)
-      if ((char*)recv == own_recv + i * st) ridx = i;
-    if (ridx < 0)
-      return fail(A2A_ERR_INVALID, "multi-GPU plans must receive into an arena recv buffer");
-  }
-  if (!send && P.info[P.rank].send_bytes > 0) return fail(A2A_ERR_INVALID, "null send buffer");
-  DeviceGuard dg(P.device);
-  KParams kp;
-  std::memset(&kp, 0, sizeof kp);
-  kp.base[loc_send()] = (char*)send;
-  for (int g = 0; g < P.G; ++g) {
-    char* ar = (char*)P.peer_arena[g];
-    kp.base[loc_recv(g)] =
-        (g == P.rank) ? (char*)recv : ar + P.recv_off[g] + (int64_t)ridx * recv_stride(P, g);
-    kp.base[loc_scratch(g, P.G)] = ar + P.scratch_off[g];
-    if (P.ll) {  // parity 0; the kernel adds (epoch & 1) * ll_half
-      kp.base[loc_ll(g, P.G)] = ar + P.scratch_off[g] + P.ll_off[g];
-      kp.ll_half[g] = P.ll_half[g];
+  return guard([&]() -> int {
+    if (!plan) return fail(A2A_ERR_INVALID, "null plan");
+    Plan& P = plan->p;
+    if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound to a device");
+    if (!P.imported) return fail(A2A_ERR_STATE, "peer arenas not imported");
+    if (*P.h_err != 0) return fail(*P.h_err, "a previous execute failed on the device (timeout)");
+    char* own_recv = (char*)P.arena + P.recv_off[P.rank];
+    if (!recv) recv = own_recv;
+    int32_t ridx = 0;
+    if (P.G > 1 && !P.ll) {
+      const int64_t st = recv_stride(P, P.rank);
+      ridx = -1;
+      for (int i = 0; i < P.n_recv; ++i)
+        if ((char*)recv == own_recv + i * st) ridx = i;
+      if (ridx < 0)
+        return fail(A2A_ERR_INVALID, "multi-GPU plans must receive into an arena recv buffer");
     }
-    kp.entry_flags[g] = (uint32_t*)(ar + entry_flags_off());
-    kp.step_flags[g] = (uint32_t*)(ar + step_flags_off());
-  }
-  kp.pieces = (const DevPiece*)P.d_items;
-  kp.prog = (const CtaStep*)P.d_step_begin;
-  kp.exit_idx = (const int32_t*)P.d_exit_idx;
-  if (P.sched_mode >= 1) {
-    const DynTables& Dy = P.dyn;
-    kp.n_exit = (int32_t)Dy.exit_idx[P.rank].size();
-    kp.units = (const DevUnit*)P.d_items;
-    kp.unit_wait = (const int32_t*)P.d_wait_idx;
-    kp.n_units = (int32_t)Dy.units[P.rank].size();
-    kp.unit_base = Dy.unit_base[P.rank];
-    kp.grab = (unsigned long long*)((char*)P.arena + grab_off());
-    if (P.sched_mode == 5) {
-      for (int g = 0; g < P.G; ++g) {
-        char* ar = (char*)P.peer_arena[g];
-        kp.qctl[g] = (unsigned long long*)(ar + grab_off());
-        kp.qdone[g] = (unsigned long long*)(ar + step_flags_off());
-        kp.qslot[g] = (unsigned long long*)(ar + step_flags_off() + 8 * (int64_t)Dy.max_units);
+    if (!send && P.info[P.rank].send_bytes > 0) return fail(A2A_ERR_INVALID, "null send buffer");
+    DeviceGuard dg(P.device);
+    KParams kp;
+    std::memset(&kp, 0, sizeof kp);
+    kp.base[loc_send()] = (char*)send;
+    for (int g = 0; g < P.G; ++g) {
+      char* ar = (char*)P.peer_arena[g];
+      kp.base[loc_recv(g)] =
+          (g == P.rank) ? (char*)recv : ar + P.recv_off[g] + (int64_t)ridx * recv_stride(P, g);
+      kp.base[loc_scratch(g, P.G)] = ar + P.scratch_off[g];
+      if (P.ll) {  // parity 0; the kernel adds (epoch & 1) * ll_half
+        kp.base[loc_ll(g, P.G)] = ar + P.scratch_off[g] + P.ll_off[g];
+        kp.ll_half[g] = P.ll_half[g];
       }
-      for (int g = 0; g <= P.G; ++g) kp.ubase[g] = Dy.unit_base[g];
-      kp.n_init = Dy.n_init[P.rank];
-      kp.n_into = Dy.n_into[P.rank];
+      kp.entry_flags[g] = (uint32_t*)(ar + entry_flags_off());
+      kp.step_flags[g] = (uint32_t*)(ar + step_flags_off());
     }
-    kp.n_remote = Dy.n_remote[P.rank];
-    kp.remote_ctas = Dy.remote_ctas[P.rank];
-    kp.pin_queues = Dy.pin;
-  } else {
-    kp.n_exit = (int32_t)P.sync.exit_idx[P.rank].size();
-  }
-  kp.wait_idx = (const int32_t*)P.d_wait_idx;
-  kp.counters = (unsigned long long*)P.d_counters;
-  kp.err = P.d_err;
-  kp.timeout_ns = P.timeout_ns;
-  kp.ctl = (uint32_t*)P.d_ctl;
-  kp.ll = P.ll ? 1 : 0;
-  kp.G = P.G;
-  kp.rank = P.rank;
-  kp.nC = P.nC;
-  kp.T = P.T_exec;
-  kp.E = P.E;
-  kp.count_links = (options & A2A_EXEC_COUNT_LINKS) ? 1 : 0;
-  void* args[] = {&kp};
-  kp.timeline = (unsigned long long*)P.d_timeline;
-  kp.sync_mode = P.sync_mode;
-  const EngineCfg ec = engine_cfg(P);
-  kp.tma_chunk = P.tma_chunk;
-  kp.tma_stages = ec.stages;
-  kp.smem_prog = ec.prog_off;
-  kp.smem_batch = ec.batch_off;
-  kp.batch = ec.batch;
-  // cooperative launch (all CTAs co-resident: CTAs spin on each other's flags);
-  // cudaLaunchKernelExC with the cooperative attribute is stream-capturable
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(P.nC);
-  cfg.blockDim = dim3(ec.threads);
-  cfg.dynamicSmemBytes = ec.smem;
-  cfg.stream = (cudaStream_t)stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = P.coop ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelExC(&cfg, ec.fn, args);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernelExC (cooperative)");
-  P.last_stream = stream;
-  P.launched = true;
-  return A2A_OK;
+    kp.pieces = (const DevPiece*)P.d_items;
+    kp.prog = (const CtaStep*)P.d_step_begin;
+    kp.exit_idx = (const int32_t*)P.d_exit_idx;
+    if (P.sched_mode >= 1) {
+      const DynTables& Dy = P.dyn;
+      kp.n_exit = (int32_t)Dy.exit_idx[P.rank].size();
+      kp.units = (const DevUnit*)P.d_items;
+      kp.unit_wait = (const int32_t*)P.d_wait_idx;
+      kp.n_units = (int32_t)Dy.units[P.rank].size();
+      kp.unit_base = Dy.unit_base[P.rank];
+      kp.grab = (unsigned long long*)((char*)P.arena + grab_off());
+      if (P.sched_mode == 5) {
+        for (int g = 0; g < P.G; ++g) {
+          char* ar = (char*)P.peer_arena[g];
+          kp.qctl[g] = (unsigned long long*)(ar + grab_off());
+          kp.qdone[g] = (unsigned long long*)(ar + step_flags_off());
+          kp.qslot[g] = (unsigned long long*)(ar + step_flags_off() + 8 * (int64_t)Dy.max_units);
+        }
+        for (int g = 0; g <= P.G; ++g) kp.ubase[g] = Dy.unit_base[g];
+        kp.n_init = Dy.n_init[P.rank];
+        kp.n_into = Dy.n_into[P.rank];
+      }
+      kp.n_remote = Dy.n_remote[P.rank];
+      kp.remote_ctas = Dy.remote_ctas[P.rank];
+      kp.pin_queues = Dy.pin;
+    } else {
+      kp.n_exit = (int32_t)P.sync.exit_idx[P.rank].size();
+    }
+    kp.wait_idx = (const int32_t*)P.d_wait_idx;
+    kp.counters = (unsigned long long*)P.d_counters;
+    kp.err = P.d_err;
+    kp.timeout_ns = P.timeout_ns;
+    kp.ctl = (uint32_t*)P.d_ctl;
+    kp.ll = P.ll ? 1 : 0;
+    kp.G = P.G;
+    kp.rank = P.rank;
+    kp.nC = P.nC;
+    kp.T = P.T_exec;
+    kp.E = P.E;
+    kp.count_links = (options & A2A_EXEC_COUNT_LINKS) ? 1 : 0;
+    void* args[] = {&kp};
+    kp.timeline = (unsigned long long*)P.d_timeline;
+    kp.sync_mode = P.sync_mode;
+    const EngineCfg ec = engine_cfg(P);
+    kp.tma_chunk = P.tma_chunk;
+    kp.tma_stages = ec.stages;
+    kp.smem_prog = ec.prog_off;
+    kp.smem_batch = ec.batch_off;
+    kp.batch = ec.batch;
+    // cooperative launch (all CTAs co-resident: CTAs spin on each other's flags);
+    // cudaLaunchKernelExC with the cooperative attribute is stream-capturable
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(P.nC);
+    cfg.blockDim = dim3(ec.threads);
+    cfg.dynamicSmemBytes = ec.smem;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = P.coop ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelExC(&cfg, ec.fn, args);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernelExC (cooperative)");
+    P.last_stream = stream;
+    P.launched = true;
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_sync(a2a_plan* plan) {
-  if (!plan) return fail(A2A_ERR_INVALID, "null plan");
-  Plan& P = plan->p;
-  if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound");
-  DeviceGuard dg(P.device);
-  CK(cudaStreamSynchronize((cudaStream_t)P.last_stream));
-  if (*P.h_err != 0) {
-    return fail(*P.h_err, "device-side flag wait timed out (a peer did not arrive)");
-  }
-  return A2A_OK;
+  return guard([&]() -> int {
+    if (!plan) return fail(A2A_ERR_INVALID, "null plan");
+    Plan& P = plan->p;
+    if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound");
+    DeviceGuard dg(P.device);
+    CK(cudaStreamSynchronize((cudaStream_t)P.last_stream));
+    if (*P.h_err != 0) {
+      return fail(*P.h_err, "device-side flag wait timed out (a peer did not arrive)");
+    }
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_read_timeline(a2a_plan* plan, uint64_t* out, int32_t* out_cols) {
-  if (!plan || !out_cols) return fail(A2A_ERR_INVALID, "null argument");
-  Plan& P = plan->p;
-  if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound");
-  *out_cols = 2 * P.T_exec + 3;
-  if (!out) return A2A_OK;
-  DeviceGuard dg(P.device);
-  CK(cudaStreamSynchronize((cudaStream_t)P.last_stream));
-  CK(cudaMemcpy(out, P.d_timeline, (size_t)P.nC * (2 * P.T_exec + 3) * 8, cudaMemcpyDeviceToHost));
-  return A2A_OK;
+  return guard([&]() -> int {
+    if (!plan || !out_cols) return fail(A2A_ERR_INVALID, "null argument");
+    Plan& P = plan->p;
+    if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound");
+    *out_cols = 2 * P.T_exec + 3;
+    if (!out) return A2A_OK;
+    DeviceGuard dg(P.device);
+    CK(cudaStreamSynchronize((cudaStream_t)P.last_stream));
+    CK(cudaMemcpy(out, P.d_timeline, (size_t)P.nC * (2 * P.T_exec + 3) * 8, cudaMemcpyDeviceToHost));
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_read_link_counters(a2a_plan* plan, int64_t* out) {
-  if (!plan || !out) return fail(A2A_ERR_INVALID, "null argument");
-  Plan& P = plan->p;
-  if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound");
-  DeviceGuard dg(P.device);
-  CK(cudaDeviceSynchronize());
-  size_t cnt = (size_t)P.T * P.E;
-  if (cnt) {
-    CK(cudaMemcpy(out, P.d_counters, cnt * 8, cudaMemcpyDeviceToHost));
-    CK(cudaMemset(P.d_counters, 0, cnt * 8));
-  }
-  return A2A_OK;
+  return guard([&]() -> int {
+    if (!plan || !out) return fail(A2A_ERR_INVALID, "null argument");
+    Plan& P = plan->p;
+    if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound");
+    DeviceGuard dg(P.device);
+    CK(cudaDeviceSynchronize());
+    size_t cnt = (size_t)P.T * P.E;
+    if (cnt) {
+      CK(cudaMemcpy(out, P.d_counters, cnt * 8, cudaMemcpyDeviceToHost));
+      CK(cudaMemset(P.d_counters, 0, cnt * 8));
+    }
+    return A2A_OK;
+  });
 }
 
 }  // extern "C"

@@ -3,6 +3,8 @@
 #pragma once
 
 #include <cstdint>
+#include <exception>
+#include <new>
 #include <string>
 #include <vector>
 
@@ -189,6 +191,22 @@ void set_error(const std::string& msg);
 int build_sync(Plan& P, int nC);
 int build_dyn(Plan& P, int nC, int64_t unit_bytes);
 int fail(int code, const std::string& msg);
+
+// Every extern "C" entry point runs its body through guard(): no C++
+// exception crosses the C ABI (allocation failure -> A2A_ERR_NOMEM, anything
+// else -> A2A_ERR_INVALID with the exception text).
+template <class F>
+int guard(F&& body) noexcept {
+  try {
+    return body();
+  } catch (const std::bad_alloc&) {
+    return fail(A2A_ERR_NOMEM, "out of host memory");
+  } catch (const std::exception& e) {
+    return fail(A2A_ERR_INVALID, std::string("internal error: ") + e.what());
+  } catch (...) {
+    return fail(A2A_ERR_INVALID, "internal error");
+  }
+}
 
 // CTA work split shared by host (flag lists) and device (copy ranges)
 A2A_HD int64_t cta_lo(int64_t B, int c, int nC) {

@@ -359,92 +359,96 @@ using namespace a2a;
 extern "C" {
 
 int a2a_load_schedule_xml(const char* path, a2a_sched_header* hdr, a2a_op** ops, int64_t* n_ops) {
-  if (!path || !hdr || !ops || !n_ops) return fail(A2A_ERR_INVALID, "null argument");
-  try {
-    Loaded L;
-    int rc = load_xml(path, &L);
-    if (rc) return rc;
-    return fill(L, hdr, ops, n_ops);
-  } catch (const std::bad_alloc&) {
-    return fail(A2A_ERR_NOMEM, "out of host memory");
-  }
+  return guard([&]() -> int {
+    if (!path || !hdr || !ops || !n_ops) return fail(A2A_ERR_INVALID, "null argument");
+    try {
+      Loaded L;
+      int rc = load_xml(path, &L);
+      if (rc) return rc;
+      return fill(L, hdr, ops, n_ops);
+    } catch (const std::bad_alloc&) {
+      return fail(A2A_ERR_NOMEM, "out of host memory");
+    }
+  });
 }
 
 int a2a_lower_path_files(const char* xml_path, const char* routes_path, const int32_t* node_map,
                          int32_t map_len, int32_t n_phys, a2a_sched_header* hdr, a2a_op** ops,
                          int64_t* n_ops) {
-  if (!xml_path || !routes_path || !hdr || !ops || !n_ops) return fail(A2A_ERR_INVALID, "null argument");
-  try {
-    Loaded L;
-    int rc = load_xml(xml_path, &L);
-    if (rc) return rc;
-    if (L.mode != 1) return fail(A2A_ERR_EVAL, "expected a path-mode schedule, got 'ts'");
-    std::string text, err;
-    if (!read_file(routes_path, &text, &err)) return fail(A2A_ERR_INVALID, err);
-    std::vector<Route> routes;
-    JsonRoutes jr(text);
-    if (!jr.doc(&routes)) return fail(A2A_ERR_INVALID, "malformed routes JSON");
-    auto phys = [&](int64_t x) -> int64_t {
-      if (!node_map) return x;
-      return (x >= 0 && x < map_len) ? node_map[x] : -1;
-    };
-    // collapse (map ids, drop consecutive repeats) -- lowering.collapse_aug_routes
-    for (auto& r : routes) {
-      r.s = phys(r.s);
-      r.d = phys(r.d);
-      if (node_map) {
-        std::vector<int32_t> seq;
-        for (int32_t x : r.nodes) {
-          int32_t v = (int32_t)phys(x);
-          if (seq.empty() || seq.back() != v) seq.push_back(v);
+  return guard([&]() -> int {
+    if (!xml_path || !routes_path || !hdr || !ops || !n_ops) return fail(A2A_ERR_INVALID, "null argument");
+    try {
+      Loaded L;
+      int rc = load_xml(xml_path, &L);
+      if (rc) return rc;
+      if (L.mode != 1) return fail(A2A_ERR_EVAL, "expected a path-mode schedule, got 'ts'");
+      std::string text, err;
+      if (!read_file(routes_path, &text, &err)) return fail(A2A_ERR_INVALID, err);
+      std::vector<Route> routes;
+      JsonRoutes jr(text);
+      if (!jr.doc(&routes)) return fail(A2A_ERR_INVALID, "malformed routes JSON");
+      auto phys = [&](int64_t x) -> int64_t {
+        if (!node_map) return x;
+        return (x >= 0 && x < map_len) ? node_map[x] : -1;
+      };
+      // collapse (map ids, drop consecutive repeats) -- lowering.collapse_aug_routes
+      for (auto& r : routes) {
+        r.s = phys(r.s);
+        r.d = phys(r.d);
+        if (node_map) {
+          std::vector<int32_t> seq;
+          for (int32_t x : r.nodes) {
+            int32_t v = (int32_t)phys(x);
+            if (seq.empty() || seq.back() != v) seq.push_back(v);
+          }
+          std::vector<int32_t> chk = seq;
+          std::sort(chk.begin(), chk.end());
+          if (std::adjacent_find(chk.begin(), chk.end()) != chk.end())
+            return fail(A2A_ERR_EVAL, "collapsed route is not simple");
+          r.nodes.swap(seq);
         }
-        std::vector<int32_t> chk = seq;
-        std::sort(chk.begin(), chk.end());
-        if (std::adjacent_find(chk.begin(), chk.end()) != chk.end())
-          return fail(A2A_ERR_EVAL, "collapsed route is not simple");
-        r.nodes.swap(seq);
       }
+      Loaded T;
+      T.n = node_map ? n_phys : L.n;
+      T.q = L.q;
+      T.mode = 0;
+      T.chunk_bytes = L.chunk_bytes;
+      int32_t nsteps = 0;
+      for (const a2a_op& o : L.ops) {
+        const int32_t rid = o.dst;
+        if (rid < 0 || rid >= (int32_t)routes.size()) {
+          char b[64];
+          snprintf(b, sizeof b, "route id %d out of range", rid);
+          return fail(A2A_ERR_EVAL, b);
+        }
+        const Route& r = routes[rid];
+        const int64_t s = phys(o.s), d = phys(o.d);
+        if (r.s != s || r.d != d || r.nodes.size() < 2 || r.nodes.front() != s || r.nodes.back() != d) {
+          char b[96];
+          snprintf(b, sizeof b, "route %d does not join shard (%lld,%lld)", rid, (long long)s,
+                   (long long)d);
+          return fail(A2A_ERR_EVAL, b);
+        }
+        for (size_t h = 0; h + 1 < r.nodes.size(); ++h)
+          T.ops.push_back(a2a_op{(int32_t)h, r.nodes[h], r.nodes[h + 1], (int32_t)s, (int32_t)d,
+                                 o.c0, o.c1});
+        nsteps = std::max<int32_t>(nsteps, (int32_t)r.nodes.size() - 1);
+      }
+      // ts sort key (t, src, dst, s, d, c0) of reference src/schedule.py:237 (stable)
+      std::stable_sort(T.ops.begin(), T.ops.end(), [](const a2a_op& a, const a2a_op& b) {
+        if (a.t != b.t) return a.t < b.t;
+        if (a.src != b.src) return a.src < b.src;
+        if (a.dst != b.dst) return a.dst < b.dst;
+        if (a.s != b.s) return a.s < b.s;
+        if (a.d != b.d) return a.d < b.d;
+        return a.c0 < b.c0;
+      });
+      T.nsteps = nsteps;
+      return fill(T, hdr, ops, n_ops);
+    } catch (const std::bad_alloc&) {
+      return fail(A2A_ERR_NOMEM, "out of host memory");
     }
-    Loaded T;
-    T.n = node_map ? n_phys : L.n;
-    T.q = L.q;
-    T.mode = 0;
-    T.chunk_bytes = L.chunk_bytes;
-    int32_t nsteps = 0;
-    for (const a2a_op& o : L.ops) {
-      const int32_t rid = o.dst;
-      if (rid < 0 || rid >= (int32_t)routes.size()) {
-        char b[64];
-        snprintf(b, sizeof b, "route id %d out of range", rid);
-        return fail(A2A_ERR_EVAL, b);
-      }
-      const Route& r = routes[rid];
-      const int64_t s = phys(o.s), d = phys(o.d);
-      if (r.s != s || r.d != d || r.nodes.size() < 2 || r.nodes.front() != s || r.nodes.back() != d) {
-        char b[96];
-        snprintf(b, sizeof b, "route %d does not join shard (%lld,%lld)", rid, (long long)s,
-                 (long long)d);
-        return fail(A2A_ERR_EVAL, b);
-      }
-      for (size_t h = 0; h + 1 < r.nodes.size(); ++h)
-        T.ops.push_back(a2a_op{(int32_t)h, r.nodes[h], r.nodes[h + 1], (int32_t)s, (int32_t)d,
-                               o.c0, o.c1});
-      nsteps = std::max<int32_t>(nsteps, (int32_t)r.nodes.size() - 1);
-    }
-    // ts sort key (t, src, dst, s, d, c0) of reference src/schedule.py:237 (stable)
-    std::stable_sort(T.ops.begin(), T.ops.end(), [](const a2a_op& a, const a2a_op& b) {
-      if (a.t != b.t) return a.t < b.t;
-      if (a.src != b.src) return a.src < b.src;
-      if (a.dst != b.dst) return a.dst < b.dst;
-      if (a.s != b.s) return a.s < b.s;
-      if (a.d != b.d) return a.d < b.d;
-      return a.c0 < b.c0;
-    });
-    T.nsteps = nsteps;
-    return fill(T, hdr, ops, n_ops);
-  } catch (const std::bad_alloc&) {
-    return fail(A2A_ERR_NOMEM, "out of host memory");
-  }
+  });
 }
 
 void a2a_free(void* p) { free(p); }

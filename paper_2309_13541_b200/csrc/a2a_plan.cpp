@@ -1486,188 +1486,210 @@ const char* a2a_last_error(void) { return g_last_error.c_str(); }
 const char* a2a_version(void) { return "b200-a2a 0.1.0 (sm_100a)"; }
 
 int a2a_plan_create(const a2a_schedule_desc* desc, a2a_plan** out) {
-  if (!out) return fail(A2A_ERR_INVALID, "null output pointer");
-  *out = nullptr;
-  a2a_plan* plan = new (std::nothrow) a2a_plan();
-  if (!plan) return fail(A2A_ERR_NOMEM, "out of host memory");
-  int rc;
-  try {
-    rc = build_plan(plan->p, desc);
-  } catch (const std::bad_alloc&) {
-    rc = fail(A2A_ERR_NOMEM, "out of host memory building the plan");
-  } catch (...) {
-    rc = fail(A2A_ERR_INVALID, "internal error building the plan");
-  }
-  if (rc != A2A_OK) {
-    delete plan;
-    return rc;
-  }
-  g_last_error.clear();
-  *out = plan;
-  return A2A_OK;
+  return guard([&]() -> int {
+    if (!out) return fail(A2A_ERR_INVALID, "null output pointer");
+    *out = nullptr;
+    a2a_plan* plan = new (std::nothrow) a2a_plan();
+    if (!plan) return fail(A2A_ERR_NOMEM, "out of host memory");
+    int rc;
+    try {
+      rc = build_plan(plan->p, desc);
+    } catch (const std::bad_alloc&) {
+      rc = fail(A2A_ERR_NOMEM, "out of host memory building the plan");
+    } catch (...) {
+      rc = fail(A2A_ERR_INVALID, "internal error building the plan");
+    }
+    if (rc != A2A_OK) {
+      delete plan;
+      return rc;
+    }
+    g_last_error.clear();
+    *out = plan;
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_model_time(const a2a_plan* plan, double m, double b, double sync_latency,
                         double* out_T) {
-  if (!plan || !out_T) return fail(A2A_ERR_INVALID, "null argument");
-  const Plan& P = plan->p;
-  // evaluate.py:74, :88-107 — same float operations in the same order
-  const double chunk_bytes = m / (double)P.Q;
-  std::vector<double> lb(P.E, 0.0);
-  std::vector<char> used(P.E, 0);
-  std::unordered_map<uint64_t, int32_t> eidx;
-  for (int e = 0; e < P.E; ++e)
-    eidx[((uint64_t)(uint32_t)P.edge_uv[2 * e] << 32) | (uint32_t)P.edge_uv[2 * e + 1]] = e;
-  double T = 0.0;
-  for (int t = 0; t < P.T; ++t) {
-    std::vector<int32_t> touched;
-    for (int64_t i : P.step_ops[t]) {
-      const a2a_op& o = P.ops[i];
-      int e = eidx[((uint64_t)(uint32_t)o.src << 32) | (uint32_t)o.dst];
-      if (!used[e]) { used[e] = 1; lb[e] = 0.0; touched.push_back(e); }
-      lb[e] += (double)(o.c1 - o.c0) * chunk_bytes;
+  return guard([&]() -> int {
+    if (!plan || !out_T) return fail(A2A_ERR_INVALID, "null argument");
+    const Plan& P = plan->p;
+    // evaluate.py:74, :88-107 — same float operations in the same order
+    const double chunk_bytes = m / (double)P.Q;
+    std::vector<double> lb(P.E, 0.0);
+    std::vector<char> used(P.E, 0);
+    std::unordered_map<uint64_t, int32_t> eidx;
+    for (int e = 0; e < P.E; ++e)
+      eidx[((uint64_t)(uint32_t)P.edge_uv[2 * e] << 32) | (uint32_t)P.edge_uv[2 * e + 1]] = e;
+    double T = 0.0;
+    for (int t = 0; t < P.T; ++t) {
+      std::vector<int32_t> touched;
+      for (int64_t i : P.step_ops[t]) {
+        const a2a_op& o = P.ops[i];
+        int e = eidx[((uint64_t)(uint32_t)o.src << 32) | (uint32_t)o.dst];
+        if (!used[e]) { used[e] = 1; lb[e] = 0.0; touched.push_back(e); }
+        lb[e] += (double)(o.c1 - o.c0) * chunk_bytes;
+      }
+      double step = 0.0;
+      for (int e : touched) {
+        double x = lb[e] / (P.cap[e] * b);
+        if (x > step) step = x;
+        used[e] = 0;
+      }
+      T += step + sync_latency;
     }
-    double step = 0.0;
-    for (int e : touched) {
-      double x = lb[e] / (P.cap[e] * b);
-      if (x > step) step = x;
-      used[e] = 0;
-    }
-    T += step + sync_latency;
-  }
-  *out_T = T;
-  return A2A_OK;
+    *out_T = T;
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_link_bytes(const a2a_plan* plan, int64_t* out) {
-  if (!plan || !out) return fail(A2A_ERR_INVALID, "null argument");
-  std::memcpy(out, plan->p.link_bytes.data(), plan->p.link_bytes.size() * sizeof(int64_t));
-  return A2A_OK;
+  return guard([&]() -> int {
+    if (!plan || !out) return fail(A2A_ERR_INVALID, "null argument");
+    std::memcpy(out, plan->p.link_bytes.data(), plan->p.link_bytes.size() * sizeof(int64_t));
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_prepare(a2a_plan* plan, int32_t num_ctas) {
-  if (!plan) return fail(A2A_ERR_INVALID, "null plan");
-  if (plan->p.bound && plan->p.sync.nC != num_ctas)
-    return fail(A2A_ERR_STATE, "plan already bound with another CTA count");
-  try {
-    return build_sync(plan->p, num_ctas);
-  } catch (const std::bad_alloc&) {
-    return fail(A2A_ERR_NOMEM, "out of host memory building the CTA tables");
-  }
+  return guard([&]() -> int {
+    if (!plan) return fail(A2A_ERR_INVALID, "null plan");
+    if (plan->p.bound && plan->p.sync.nC != num_ctas)
+      return fail(A2A_ERR_STATE, "plan already bound with another CTA count");
+    try {
+      return build_sync(plan->p, num_ctas);
+    } catch (const std::bad_alloc&) {
+      return fail(A2A_ERR_NOMEM, "out of host memory building the CTA tables");
+    }
+  });
 }
 
 // Host audit of every device copy range (what memcheck would catch in the
 // address math): each piece / unit reads inside its source buffer and writes
 // inside its destination buffer on the owning GPU.
 int a2a_plan_check_bounds(a2a_plan* plan, int32_t num_ctas) {
-  if (!plan) return fail(A2A_ERR_INVALID, "null plan");
-  Plan& P = plan->p;
-  const int G = P.G;
-  int rc = P.sched_mode >= 1 ? build_dyn(P, num_ctas, P.dyn_unit_bytes) : build_sync(P, num_ctas);
-  if (rc) return rc;
-  auto size_of = [&](int g, int loc) -> int64_t {
-    if (loc == loc_send()) return P.info[g].send_bytes;
-    if (loc >= 1 && loc < 1 + G) return P.info[loc - 1].recv_bytes;
-    if (loc >= 1 + G && loc < 1 + 2 * G) return P.info[loc - 1 - G].scratch_bytes;
-    // LL landing region: payload capacity (lines are 16 bytes per 8 payload bytes)
-    if (P.ll && loc >= 1 + 2 * G && loc < 1 + 3 * G) return P.ll_half[loc - 1 - 2 * G] / 2;
-    return -1;
-  };
-  auto check = [&](int g, int sl, int64_t so, int dl, int64_t dof, int64_t n, int kind = kCopy) -> bool {
-    const bool sll = sl >= loc_ll(0, G) && sl < loc_ll(G, G), dll = dl >= loc_ll(0, G) && dl < loc_ll(G, G);
-    if (sll != ((kind & kLLSrc) != 0) || dll != ((kind & kLLDst) != 0)) return false;
-    if (dll && (dof & 7)) return false;                         // stores whole lines
-    const int64_t ss = size_of(g, sl), ds = size_of(g, dl);
-    const int64_t nd = dll ? ((n + 7) & ~(int64_t)7) : n;
-    return n > 0 && ss >= 0 && ds >= 0 && so >= 0 && dof >= 0 && so + n <= ss && dof + nd <= ds;
-  };
-  char buf[200];
-  for (int g = 0; g < G; ++g) {
-    if (P.sched_mode >= 1) {
-      for (const DevUnit& u : P.dyn.units[g])
-        if (!check(g, u.src_loc, u.src_off, u.dst_loc, u.dst_off, u.nbytes) ||
-            !(u.src_loc == loc_send() || u.src_loc == loc_recv(g) || u.src_loc == loc_scratch(g, G))) {
-          snprintf(buf, sizeof buf, "gpu %d: unit out of bounds (src %d+%lld, dst %d+%lld, %d B)", g,
-                   u.src_loc, (long long)u.src_off, u.dst_loc, (long long)u.dst_off, u.nbytes);
-          return fail(A2A_ERR_INVALID, buf);
-        }
-    } else {
-      for (const DevPiece& q : P.sync.pieces[g])
-        if (!check(g, q.src_loc, q.src_off, q.dst_loc, q.dst_off, q.nbytes, q.kind) ||
-            !(q.src_loc == loc_send() || q.src_loc == loc_recv(g) || q.src_loc == loc_scratch(g, G) ||
-              q.src_loc == loc_ll(g, G)) ||
-            (P.ll && !(q.kind & kLLDst) && q.dst_loc != loc_recv(g))) {   // LL: plain stores stay local
-          snprintf(buf, sizeof buf, "gpu %d: piece out of bounds (src %d+%lld, dst %d+%lld, %d B)", g,
-                   q.src_loc, (long long)q.src_off, q.dst_loc, (long long)q.dst_off, q.nbytes);
-          return fail(A2A_ERR_INVALID, buf);
-        }
+  return guard([&]() -> int {
+    if (!plan) return fail(A2A_ERR_INVALID, "null plan");
+    Plan& P = plan->p;
+    const int G = P.G;
+    int rc = P.sched_mode >= 1 ? build_dyn(P, num_ctas, P.dyn_unit_bytes) : build_sync(P, num_ctas);
+    if (rc) return rc;
+    auto size_of = [&](int g, int loc) -> int64_t {
+      if (loc == loc_send()) return P.info[g].send_bytes;
+      if (loc >= 1 && loc < 1 + G) return P.info[loc - 1].recv_bytes;
+      if (loc >= 1 + G && loc < 1 + 2 * G) return P.info[loc - 1 - G].scratch_bytes;
+      // LL landing region: payload capacity (lines are 16 bytes per 8 payload bytes)
+      if (P.ll && loc >= 1 + 2 * G && loc < 1 + 3 * G) return P.ll_half[loc - 1 - 2 * G] / 2;
+      return -1;
+    };
+    auto check = [&](int g, int sl, int64_t so, int dl, int64_t dof, int64_t n, int kind = kCopy) -> bool {
+      const bool sll = sl >= loc_ll(0, G) && sl < loc_ll(G, G), dll = dl >= loc_ll(0, G) && dl < loc_ll(G, G);
+      if (sll != ((kind & kLLSrc) != 0) || dll != ((kind & kLLDst) != 0)) return false;
+      if (dll && (dof & 7)) return false;                         // stores whole lines
+      const int64_t ss = size_of(g, sl), ds = size_of(g, dl);
+      const int64_t nd = dll ? ((n + 7) & ~(int64_t)7) : n;
+      return n > 0 && ss >= 0 && ds >= 0 && so >= 0 && dof >= 0 && so + n <= ss && dof + nd <= ds;
+    };
+    char buf[200];
+    for (int g = 0; g < G; ++g) {
+      if (P.sched_mode >= 1) {
+        for (const DevUnit& u : P.dyn.units[g])
+          if (!check(g, u.src_loc, u.src_off, u.dst_loc, u.dst_off, u.nbytes) ||
+              !(u.src_loc == loc_send() || u.src_loc == loc_recv(g) || u.src_loc == loc_scratch(g, G))) {
+            snprintf(buf, sizeof buf, "gpu %d: unit out of bounds (src %d+%lld, dst %d+%lld, %d B)", g,
+                     u.src_loc, (long long)u.src_off, u.dst_loc, (long long)u.dst_off, u.nbytes);
+            return fail(A2A_ERR_INVALID, buf);
+          }
+      } else {
+        for (const DevPiece& q : P.sync.pieces[g])
+          if (!check(g, q.src_loc, q.src_off, q.dst_loc, q.dst_off, q.nbytes, q.kind) ||
+              !(q.src_loc == loc_send() || q.src_loc == loc_recv(g) || q.src_loc == loc_scratch(g, G) ||
+                q.src_loc == loc_ll(g, G)) ||
+              (P.ll && !(q.kind & kLLDst) && q.dst_loc != loc_recv(g))) {   // LL: plain stores stay local
+            snprintf(buf, sizeof buf, "gpu %d: piece out of bounds (src %d+%lld, dst %d+%lld, %d B)", g,
+                     q.src_loc, (long long)q.src_off, q.dst_loc, (long long)q.dst_off, q.nbytes);
+            return fail(A2A_ERR_INVALID, buf);
+          }
+      }
     }
-  }
-  return A2A_OK;
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_set_split(a2a_plan* plan, int32_t remote_weight) {
-  if (!plan || remote_weight < 1 || remote_weight > 64) return fail(A2A_ERR_INVALID, "bad remote weight");
-  if (plan->p.bound) return fail(A2A_ERR_STATE, "set the CTA split before a2a_plan_bind");
-  plan->p.remote_weight = remote_weight;
-  return A2A_OK;
+  return guard([&]() -> int {
+    if (!plan || remote_weight < 1 || remote_weight > 64) return fail(A2A_ERR_INVALID, "bad remote weight");
+    if (plan->p.bound) return fail(A2A_ERR_STATE, "set the CTA split before a2a_plan_bind");
+    plan->p.remote_weight = remote_weight;
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_set_schedule(a2a_plan* plan, int32_t mode, int64_t unit_bytes) {
-  if (!plan || mode < 0 || mode > 6 || unit_bytes < 0) return fail(A2A_ERR_INVALID, "bad schedule mode");
-  if (plan->p.bound) return fail(A2A_ERR_STATE, "set the schedule mode before a2a_plan_bind");
-  if (plan->p.ll && mode != 0)
-    return fail(A2A_ERR_INVALID, "A2A_PROTO_LL plans run the static schedule only");
-  plan->p.sched_mode = mode;
-  plan->p.dyn_unit_bytes = unit_bytes;
-  plan->p.dyn = DynTables{};
-  return A2A_OK;
+  return guard([&]() -> int {
+    if (!plan || mode < 0 || mode > 6 || unit_bytes < 0) return fail(A2A_ERR_INVALID, "bad schedule mode");
+    if (plan->p.bound) return fail(A2A_ERR_STATE, "set the schedule mode before a2a_plan_bind");
+    if (plan->p.ll && mode != 0)
+      return fail(A2A_ERR_INVALID, "A2A_PROTO_LL plans run the static schedule only");
+    plan->p.sched_mode = mode;
+    plan->p.dyn_unit_bytes = unit_bytes;
+    plan->p.dyn = DynTables{};
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_set_queue_split(a2a_plan* plan, int32_t remote_ctas) {
-  if (!plan || remote_ctas < 0) return fail(A2A_ERR_INVALID, "bad remote CTA count");
-  if (plan->p.bound) return fail(A2A_ERR_STATE, "set the queue split before a2a_plan_bind");
-  plan->p.dyn_remote_ctas = remote_ctas;
-  plan->p.dyn = DynTables{};
-  return A2A_OK;
+  return guard([&]() -> int {
+    if (!plan || remote_ctas < 0) return fail(A2A_ERR_INVALID, "bad remote CTA count");
+    if (plan->p.bound) return fail(A2A_ERR_STATE, "set the queue split before a2a_plan_bind");
+    plan->p.dyn_remote_ctas = remote_ctas;
+    plan->p.dyn = DynTables{};
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_dyn_stats(a2a_plan* plan, int32_t gpu, int32_t num_ctas, int64_t* n_units,
                        int64_t* n_wait, double* est_makespan_s) {
-  if (!plan || !n_units || !n_wait || !est_makespan_s) return fail(A2A_ERR_INVALID, "null argument");
-  if (gpu < 0 || gpu >= plan->p.G) return fail(A2A_ERR_INVALID, "gpu out of range");
-  int rc = build_dyn(plan->p, num_ctas, plan->p.dyn_unit_bytes);
-  if (rc) return rc;
-  *n_units = (int64_t)plan->p.dyn.units[gpu].size();
-  *n_wait = (int64_t)plan->p.dyn.wait_idx[gpu].size();
-  *est_makespan_s = plan->p.dyn.est_makespan;
-  return A2A_OK;
+  return guard([&]() -> int {
+    if (!plan || !n_units || !n_wait || !est_makespan_s) return fail(A2A_ERR_INVALID, "null argument");
+    if (gpu < 0 || gpu >= plan->p.G) return fail(A2A_ERR_INVALID, "gpu out of range");
+    int rc = build_dyn(plan->p, num_ctas, plan->p.dyn_unit_bytes);
+    if (rc) return rc;
+    *n_units = (int64_t)plan->p.dyn.units[gpu].size();
+    *n_wait = (int64_t)plan->p.dyn.wait_idx[gpu].size();
+    *est_makespan_s = plan->p.dyn.est_makespan;
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_sync_stats(const a2a_plan* plan, int32_t gpu, int64_t* n_wait, int64_t* n_exit) {
-  if (!plan || !n_wait || !n_exit) return fail(A2A_ERR_INVALID, "null argument");
-  const SyncTables& S = plan->p.sync;
-  if (S.nC == 0) return fail(A2A_ERR_STATE, "call a2a_plan_prepare first");
-  if (gpu < 0 || gpu >= plan->p.G) return fail(A2A_ERR_INVALID, "gpu out of range");
-  *n_wait = (int64_t)S.wait_idx[gpu].size();
-  *n_exit = (int64_t)S.exit_idx[gpu].size();
-  return A2A_OK;
+  return guard([&]() -> int {
+    if (!plan || !n_wait || !n_exit) return fail(A2A_ERR_INVALID, "null argument");
+    const SyncTables& S = plan->p.sync;
+    if (S.nC == 0) return fail(A2A_ERR_STATE, "call a2a_plan_prepare first");
+    if (gpu < 0 || gpu >= plan->p.G) return fail(A2A_ERR_INVALID, "gpu out of range");
+    *n_wait = (int64_t)S.wait_idx[gpu].size();
+    *n_exit = (int64_t)S.exit_idx[gpu].size();
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_emulate(a2a_plan* plan, int32_t num_ctas, void* const* send, void* const* recv,
                      uint64_t seed) {
-  if (!plan || !send || !recv) return fail(A2A_ERR_INVALID, "null argument");
-  try {
-    if (plan->p.sched_mode == 5)
-      return emulate_ready(plan->p, num_ctas, (uint8_t* const*)send, (uint8_t* const*)recv, seed,
+  return guard([&]() -> int {
+    if (!plan || !send || !recv) return fail(A2A_ERR_INVALID, "null argument");
+    try {
+      if (plan->p.sched_mode == 5)
+        return emulate_ready(plan->p, num_ctas, (uint8_t* const*)send, (uint8_t* const*)recv, seed,
+                             plan->p.dyn_unit_bytes);
+      if (plan->p.sched_mode >= 1)
+        return emulate_dyn(plan->p, num_ctas, (uint8_t* const*)send, (uint8_t* const*)recv, seed,
                            plan->p.dyn_unit_bytes);
-    if (plan->p.sched_mode >= 1)
-      return emulate_dyn(plan->p, num_ctas, (uint8_t* const*)send, (uint8_t* const*)recv, seed,
-                         plan->p.dyn_unit_bytes);
-    return emulate(plan->p, num_ctas, (uint8_t* const*)send, (uint8_t* const*)recv, seed);
-  } catch (const std::bad_alloc&) {
-    return fail(A2A_ERR_NOMEM, "out of host memory in emulation");
-  }
+      return emulate(plan->p, num_ctas, (uint8_t* const*)send, (uint8_t* const*)recv, seed);
+    } catch (const std::bad_alloc&) {
+      return fail(A2A_ERR_NOMEM, "out of host memory in emulation");
+    }
+  });
 }
 
 // ---- placement optimiser ---------------------------
@@ -1713,82 +1735,86 @@ struct PlaceEval {
 int a2a_optimize_placement(int32_t n, int32_t n_edges, const int32_t* edge_uv,
                            const int64_t* edge_bytes, int32_t n_gpus, int32_t iters,
                            uint64_t seed, int32_t* placement) {
-  if (n < 1 || n_edges < 0 || !edge_uv || !edge_bytes || !placement || n_gpus < 1 ||
-      n_gpus > A2A_MAX_GPUS)
-    return fail(A2A_ERR_INVALID, "bad placement arguments");
-  PlaceEval ev{n, n_edges, n_gpus, edge_uv, edge_bytes, {}, {}};
-  ev.init();
-  std::vector<int> P(placement, placement + n);
-  for (int v = 0; v < n; ++v)
-    if (P[v] < 0 || P[v] >= n_gpus) return fail(A2A_ERR_INVALID, "placement entry out of range");
-  auto best = ev.cost(P);
-  std::vector<int> bestP = P;
-  if (n <= 12 && n_gpus > 1) {
-    // exhaustive over balanced assignments with the same per-GPU counts,
-    // canonical (GPU labels are interchangeable only if counts match: keep labels)
-    std::vector<int> cnt(n_gpus, 0), cap(n_gpus, 0);
-    for (int v = 0; v < n; ++v) cap[P[v]]++;
-    std::vector<int> cur(n, 0);
-    std::function<void(int)> rec = [&](int v) {
-      if (v == n) {
-        auto c = ev.cost(cur);
-        if (c < best) { best = c; bestP = cur; }
-        return;
+  return guard([&]() -> int {
+    if (n < 1 || n_edges < 0 || !edge_uv || !edge_bytes || !placement || n_gpus < 1 ||
+        n_gpus > A2A_MAX_GPUS)
+      return fail(A2A_ERR_INVALID, "bad placement arguments");
+    PlaceEval ev{n, n_edges, n_gpus, edge_uv, edge_bytes, {}, {}};
+    ev.init();
+    std::vector<int> P(placement, placement + n);
+    for (int v = 0; v < n; ++v)
+      if (P[v] < 0 || P[v] >= n_gpus) return fail(A2A_ERR_INVALID, "placement entry out of range");
+    auto best = ev.cost(P);
+    std::vector<int> bestP = P;
+    if (n <= 12 && n_gpus > 1) {
+      // exhaustive over balanced assignments with the same per-GPU counts,
+      // canonical (GPU labels are interchangeable only if counts match: keep labels)
+      std::vector<int> cnt(n_gpus, 0), cap(n_gpus, 0);
+      for (int v = 0; v < n; ++v) cap[P[v]]++;
+      std::vector<int> cur(n, 0);
+      std::function<void(int)> rec = [&](int v) {
+        if (v == n) {
+          auto c = ev.cost(cur);
+          if (c < best) { best = c; bestP = cur; }
+          return;
+        }
+        for (int g = 0; g < n_gpus; ++g) {
+          if (cnt[g] >= cap[g]) continue;
+          // symmetry: the first node of each empty equal-capacity GPU goes to the lowest one
+          bool skip = false;
+          if (cnt[g] == 0)
+            for (int h = 0; h < g; ++h)
+              if (cnt[h] == 0 && cap[h] == cap[g]) { skip = true; break; }
+          if (skip) continue;
+          cnt[g]++;
+          cur[v] = g;
+          rec(v + 1);
+          cnt[g]--;
+        }
+      };
+      rec(0);
+    } else if (n_gpus > 1) {
+      // local search: best-improvement swaps touching the bottleneck GPU, random restarts of ties
+      uint64_t x = seed * 0x9E3779B97F4A7C15ULL + 7;
+      auto rnd = [&]() { x ^= x << 13; x ^= x >> 7; x ^= x << 17; return x; };
+      std::vector<int64_t> eg, ing;
+      int64_t cross;
+      for (int it = 0; it < std::max(1, iters); ++it) {
+        ev.loads(P, eg, ing, cross);
+        int gw = 0;
+        int64_t mx = -1;
+        for (int g = 0; g < n_gpus; ++g)
+          if (std::max(eg[g], ing[g]) > mx) { mx = std::max(eg[g], ing[g]); gw = g; }
+        std::pair<int64_t, int64_t> cbest = ev.cost(P);
+        int bu = -1, bv = -1;
+        // sample candidate pairs (u on the bottleneck GPU, v elsewhere)
+        std::vector<int> on, off;
+        for (int v = 0; v < n; ++v) (P[v] == gw ? on : off).push_back(v);
+        const int samples = std::min<int64_t>((int64_t)on.size() * off.size(), 4096);
+        for (int k = 0; k < samples; ++k) {
+          int u = on[rnd() % on.size()], v = off[rnd() % off.size()];
+          std::swap(P[u], P[v]);
+          auto c = ev.cost(P);
+          std::swap(P[u], P[v]);
+          if (c < cbest) { cbest = c; bu = u; bv = v; }
+        }
+        if (bu < 0) break;
+        std::swap(P[bu], P[bv]);
+        if (cbest < best) { best = cbest; bestP = P; }
       }
-      for (int g = 0; g < n_gpus; ++g) {
-        if (cnt[g] >= cap[g]) continue;
-        // symmetry: the first node of each empty equal-capacity GPU goes to the lowest one
-        bool skip = false;
-        if (cnt[g] == 0)
-          for (int h = 0; h < g; ++h)
-            if (cnt[h] == 0 && cap[h] == cap[g]) { skip = true; break; }
-        if (skip) continue;
-        cnt[g]++;
-        cur[v] = g;
-        rec(v + 1);
-        cnt[g]--;
-      }
-    };
-    rec(0);
-  } else if (n_gpus > 1) {
-    // local search: best-improvement swaps touching the bottleneck GPU, random restarts of ties
-    uint64_t x = seed * 0x9E3779B97F4A7C15ULL + 7;
-    auto rnd = [&]() { x ^= x << 13; x ^= x >> 7; x ^= x << 17; return x; };
-    std::vector<int64_t> eg, ing;
-    int64_t cross;
-    for (int it = 0; it < std::max(1, iters); ++it) {
-      ev.loads(P, eg, ing, cross);
-      int gw = 0;
-      int64_t mx = -1;
-      for (int g = 0; g < n_gpus; ++g)
-        if (std::max(eg[g], ing[g]) > mx) { mx = std::max(eg[g], ing[g]); gw = g; }
-      std::pair<int64_t, int64_t> cbest = ev.cost(P);
-      int bu = -1, bv = -1;
-      // sample candidate pairs (u on the bottleneck GPU, v elsewhere)
-      std::vector<int> on, off;
-      for (int v = 0; v < n; ++v) (P[v] == gw ? on : off).push_back(v);
-      const int samples = std::min<int64_t>((int64_t)on.size() * off.size(), 4096);
-      for (int k = 0; k < samples; ++k) {
-        int u = on[rnd() % on.size()], v = off[rnd() % off.size()];
-        std::swap(P[u], P[v]);
-        auto c = ev.cost(P);
-        std::swap(P[u], P[v]);
-        if (c < cbest) { cbest = c; bu = u; bv = v; }
-      }
-      if (bu < 0) break;
-      std::swap(P[bu], P[bv]);
-      if (cbest < best) { best = cbest; bestP = P; }
     }
-  }
-  std::copy(bestP.begin(), bestP.end(), placement);
-  return A2A_OK;
+    std::copy(bestP.begin(), bestP.end(), placement);
+    return A2A_OK;
+  });
 }
 
 int a2a_plan_gpu_info(const a2a_plan* plan, int32_t gpu, a2a_gpu_info* out) {
-  if (!plan || !out) return fail(A2A_ERR_INVALID, "null argument");
-  if (gpu < 0 || gpu >= plan->p.G) return fail(A2A_ERR_INVALID, "gpu out of range");
-  *out = plan->p.info[gpu];
-  return A2A_OK;
+  return guard([&]() -> int {
+    if (!plan || !out) return fail(A2A_ERR_INVALID, "null argument");
+    if (gpu < 0 || gpu >= plan->p.G) return fail(A2A_ERR_INVALID, "gpu out of range");
+    *out = plan->p.info[gpu];
+    return A2A_OK;
+  });
 }
 
 }  // extern "C"
