@@ -254,10 +254,7 @@ def make_plan(art, m, G, placement, schedule):
         return Plan(art.g, art.sched, m=m, n_gpus=G, placement=placement, protocol="ll")
     plan = Plan(art.g, art.sched, m=m, n_gpus=G, placement=placement)
     if schedule:
-        mode, *ub = schedule.split(":")
-        plan.set_schedule(mode, int(ub[0]) if ub else 0)
-        if len(ub) > 1:
-            plan.set_queue_split(int(ub[1]))
+        plan.set_schedule_spec(schedule)
     return plan
 
 

@@ -236,6 +236,17 @@ class Plan:
         self.schedule = mode
         return self
 
+    def set_schedule_spec(self, spec: str):
+        """Before bind: "<mode>[:<unit bytes>[:<pinned NVLink CTAs>]]", e.g.
+        "static", "cp:1048576", "cp:1048576:64" (set_schedule + set_queue_split)."""
+        mode, *rest = spec.strip().split(":")
+        if len(rest) > 2:
+            raise ValueError(f"bad schedule spec {spec!r}")
+        self.set_schedule(mode, int(rest[0]) if rest else 0)
+        if len(rest) > 1:
+            self.set_queue_split(int(rest[1]))
+        return self
+
     def set_queue_split(self, remote_ctas: int = 0):
         """Before bind (two-queue orders "dynamic" / "list" / "cp"): pin
         `remote_ctas` CTAs to the NVLink queue and the rest to the HBM queue, no
@@ -293,8 +304,7 @@ class Plan:
                 parts = env.split(":")      # tma[:chunk[:stages]]
                 self.set_engine(parts[0], *(int(x) for x in parts[1:]))
         if self.schedule is None and os.environ.get("A2A_SCHED"):
-            parts = os.environ["A2A_SCHED"].split(":")   # dynamic[:unit_bytes]
-            self.set_schedule(parts[0], *(int(x) for x in parts[1:]))
+            self.set_schedule_spec(os.environ["A2A_SCHED"])
         if os.environ.get("A2A_SPLIT_W") and getattr(self, "remote_weight", None) is None:
             self.set_split(int(os.environ["A2A_SPLIT_W"]))
         if os.environ.get("A2A_SYNC_MODE"):

@@ -199,6 +199,14 @@ def test_queue_split_rejects(artifacts):
     with Plan(a.g, a.sched, m=4096, n_gpus=2) as p:
         with pytest.raises(ValueError):
             p.set_queue_split(-1)
+        with pytest.raises(ValueError):
+            p.set_schedule_spec("cp:1:2:3")
+        with pytest.raises(KeyError):
+            p.set_schedule_spec("nope")
+        p.set_schedule_spec("spread:65536")
+        assert p.schedule == "spread"
+        p.set_schedule_spec("cp:1048576:64")
+        assert (p.schedule, p.remote_ctas) == ("cp", 64)
 
 
 @pytest.mark.parametrize("name,G", [("gk8_2", 2), ("gk8_2", 4), ("torus4x4x4", 4), ("hypercube3", 8),

@@ -64,10 +64,7 @@ def _rank_main(rank, world, port, name, m, reps, q, engine="lsu", sched="static"
         plan = Plan(a.g, a.sched, m=m, n_gpus=world, reuse_scratch=reuse, placement="optimized",
                     protocol=proto)
         plan.set_engine(engine)
-        mode, *rest = sched.split(":")      # "<mode>[:<unit bytes>[:<pinned NVLink CTAs>]]"
-        plan.set_schedule(mode, int(rest[0]) if rest else 0)
-        if len(rest) > 1:
-            plan.set_queue_split(int(rest[1]))
+        plan.set_schedule_spec(sched)      # "<mode>[:<unit bytes>[:<pinned NVLink CTAs>]]"
         plan.bind(rank, device=rank)
         plan.set_timeout(20.0)
         connect(plan)
