@@ -307,6 +307,32 @@ def autotune_schedule(ctx, art, m, placement="optimized", num_ctas=0, trials=5,
 L2_BYTES = 126 << 20
 
 
+def bound_terms(infos, n, m, sum_dist, hbm_gbs):
+    """Lower-bound terms of one all-to-all from the plan's per-GPU bytes.
+
+    t_lb: the north-star bound -- G=1: 2*m*sum(dist)/HBM; G>1:
+    max_g max(egress_g, ingress_g) / 900 GB/s.  t_hbm: max_g HBM bytes of GPU g
+    under the schedule / HBM (reads of its hops and self shards, writes of its
+    local hops, incoming peer stores and self shards).  t_both = max(t_lb,
+    t_hbm): both resources are needed, so neither term alone is a bound on a
+    multi-GPU run where local hops dominate (torus 4x4x4 at 2 GPUs)."""
+    G = len(infos)
+    # local_bytes = local hops + self shards; hop_bytes = every hop sourced on g
+    self_b = [i["local_bytes"] - (i["hop_bytes"] - i["egress_bytes"]) for i in infos]
+    hbm_b = [i["hop_bytes"] + s + i["local_bytes"] + i["ingress_bytes"]
+             for i, s in zip(infos, self_b)]
+    hb = max(hbm_b)
+    t_hbm = hb / (hbm_gbs * 1e9)
+    if G == 1:
+        t_lb = 2 * m * sum_dist / (hbm_gbs * 1e9)
+        nv = 0
+    else:
+        nv = max(max(i["egress_bytes"], i["ingress_bytes"]) for i in infos)
+        t_lb = nv / (NVLINK_NOMINAL * 1e9)
+    return {"t_lb": t_lb, "t_hbm": t_hbm, "t_both": max(t_lb, t_hbm), "hbm_bytes": hb,
+            "nvlink_bytes": nv}
+
+
 def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=True,
             flush_bytes=512 << 20, placement="optimized", schedule="static", flush=None):
     """Time K all-to-alls of `art` at shard size m on ctx.world GPUs.
@@ -421,22 +447,24 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
 
     # ---- roofline of the (only) kernel, a2a_exec_kernel
     hbm, hbm_kind = _peaks()
+    bt = bound_terms(infos, n, m, distance_sum(art.g), hbm)
     if G == 1:
-        algo = 2 * (info["hop_bytes"] + n * m)        # read + write per hop, + self shards
+        algo = bt["hbm_bytes"]                        # read + write per hop, + self shards
         achieved = algo / T / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
                 "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,
                 "peak_kind": f"{hbm_kind} copy bandwidth (MEASURED_PEAKS.json)",
                 "algorithmic_bytes_per_launch": algo}
-        t_lb = 2 * m * distance_sum(art.g) / (hbm * 1e9)
     else:
-        xfer = max(max(i["egress_bytes"], i["ingress_bytes"]) for i in infos)
+        xfer = bt["nvlink_bytes"]
         achieved = xfer / T / 1e9
         roof = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_MEASURED,
                 "unit": "GB/s", "frac": round(achieved / NVLINK_MEASURED, 4), "traffic": None,
                 "peak_kind": "measured peer-copy GB/s per direction (B200_PROFILING.md)",
-                "algorithmic_bytes_per_launch": xfer}
-        t_lb = xfer / (NVLINK_NOMINAL * 1e9)
+                "algorithmic_bytes_per_launch": xfer,
+                "hbm_term": {"bytes": bt["hbm_bytes"], "achieved": round(bt["hbm_bytes"] / T / 1e9, 1),
+                             "peak": hbm, "frac": round(bt["hbm_bytes"] / T / 1e9 / hbm, 4)}}
+    t_lb = bt["t_lb"]
     traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(traffic_file):
         with open(traffic_file) as fh:
@@ -553,7 +581,8 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     dist = {"p50": round(sp[len(sp) // 2], 4), "p90": round(sp[min(len(sp) - 1, int(0.9 * len(sp)))], 4),
             "max": round(sp[-1], 4), "min": round(sp[0], 4)}
     res = {"T": T, "per_step_ms": per, "step_ms_dist": dist, "value": value, "per_gpu": value / G,
-           "t_lb": t_lb, "bound_frac": t_lb / T, "roofline": roof, "nccl": nres, "e2e": eres,
+           "t_lb": t_lb, "bound_frac": t_lb / T, "roofline": roof,
+           "t_hbm": bt["t_hbm"], "t_both": bt["t_both"], "nccl": nres, "e2e": eres,
            "recv_ok": bool(ok), "clocks": clock_rec,
            "host_enqueue_us_per_step": round(ctx.allmax([host_us])[0], 2),
            "flush_ms_p50_by_rank": [round(x[0], 4) for x in alld],
@@ -640,7 +669,12 @@ def main(argv=None):
             "per_gpu": round(r["per_gpu"], 3),
             "step_ms_dist": r["step_ms_dist"],
             "bound": {"t_lb_ms": round(r["t_lb"] * 1e3, 4), "frac": round(r["bound_frac"], 4),
-                      "def": "G=1: 2*m*sum(dist)/HBM; G>1: max_g max(egress,ingress)/900 GB/s"},
+                      "def": "G=1: 2*m*sum(dist)/HBM; G>1: max_g max(egress,ingress)/900 GB/s",
+                      "t_hbm_ms": round(r["t_hbm"] * 1e3, 4),
+                      "t_both_ms": round(r["t_both"] * 1e3, 4),
+                      "frac_both": round(r["t_both"] / r["T"], 4),
+                      "def_both": "max(t_lb, max_g schedule HBM bytes of g / HBM): at G>1 the "
+                                  "local hops and incoming stores also need HBM time"},
             "recv_ok": r["recv_ok"],
             "roofline": r["roofline"],
             "cpu_baseline": cpu,

@@ -40,3 +40,29 @@ def test_report_tool(tmp_path):
     out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "report.py"), src],
                          capture_output=True, text=True, timeout=60)
     assert out.returncode == 0 and "| gk8_2 |" in out.stdout
+
+
+def test_bound_terms():
+    """bench.bound_terms: the north-star bound and the HBM term of a multi-GPU
+    run, from the plan's per-GPU bytes (no GPU needed)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2309_13541_b200.artifacts import load_artifact
+    from paper_2309_13541_b200.executor import Plan
+    from paper_2309_13541_b200.graphs import distance_sum
+    hbm = 6538.9
+    a = load_artifact("gk8_2")
+    m = 16 << 20
+    with Plan(a.g, a.sched, m=m, n_gpus=1) as p:
+        bt = bench.bound_terms([p.gpu_info(0)], 8, m, distance_sum(a.g), hbm)
+    # one GPU: Sigma dist = 118 (BFS) vs 122 chunk-hops of the schedule + self shards
+    assert abs(bt["t_lb"] - 2 * m * 118 / (hbm * 1e9)) < 1e-12
+    assert bt["hbm_bytes"] == 4362010624 and bt["t_both"] == bt["t_hbm"]   # = the ncu-checked bytes
+    a = load_artifact("torus4x4x4")
+    m = 4 << 20
+    with Plan(a.g, a.sched, m=m, n_gpus=2) as p:
+        infos = [p.gpu_info(g) for g in range(2)]
+    bt = bench.bound_terms(infos, 64, m, distance_sum(a.g), hbm)
+    # 2 GPUs: 32 nodes each; local hops dominate, the HBM term exceeds the NVLink term
+    assert bt["nvlink_bytes"] == max(max(i["egress_bytes"], i["ingress_bytes"]) for i in infos)
+    assert bt["t_hbm"] > bt["t_lb"] and bt["t_both"] == bt["t_hbm"]

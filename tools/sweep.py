@@ -92,6 +92,8 @@ def main(argv=None):
                     "algbw_gbs": round(r["value"], 2),
                     "algbw_per_gpu_gbs": round(r["per_gpu"], 2),
                     "t_lb_ms": round(r["t_lb"] * 1e3, 4), "bound_frac": round(r["bound_frac"], 4),
+                    "t_hbm_ms": round(r["t_hbm"] * 1e3, 4),
+                    "bound_frac_both": round(r["t_both"] / r["T"], 4),
                     "roofline": r["roofline"], "nccl": r["nccl"], "recv_ok": r["recv_ok"],
                     "clocks": r["clocks"], "sync_flags": r["sync"],
                     "host_enqueue_us_per_step": r["host_enqueue_us_per_step"],
