@@ -173,6 +173,19 @@ int a2a_plan_set_schedule(a2a_plan* plan, int32_t mode, int64_t unit_bytes);
  * CTA switches queues (0 = automatic split, CTAs switch when their queue
  * drains).  Clamped so that every non-empty queue keeps at least one CTA. */
 int a2a_plan_set_queue_split(a2a_plan* plan, int32_t remote_ctas);
+/* Fluid performance model of one execute of the selected execution schedule
+ * (static programs or dynamic orders 1-4 / 6; simple protocol) for `num_ctas`
+ * CTAs per GPU: per-GPU NVLink egress and ingress (GB/s per direction), HBM
+ * (read + write GB/s), a per-CTA copy-rate cap, a fixed cost per unit /
+ * CTA-step, the flag latency and a launch cost.  Host only; for comparing
+ * orders offline (e.g. at 8 GPUs). */
+typedef struct {
+  double nvlink_gbs, hbm_gbs, cta_gbs;
+  double flag_us, unit_us, launch_us;
+  double jitter;   /* per-CTA speed factor spread, e.g. 0.2 = +-20% */
+} a2a_sim_params;
+int a2a_plan_simulate(a2a_plan* plan, int32_t num_ctas, const a2a_sim_params* params,
+                      double* makespan_s);
 int a2a_plan_dyn_stats(a2a_plan* plan, int32_t gpu, int32_t num_ctas, int64_t* n_units,
                        int64_t* n_wait, double* est_makespan_s);
 

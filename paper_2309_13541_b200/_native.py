@@ -51,6 +51,12 @@ class GpuInfo(C.Structure):
     ]
 
 
+class SimParams(C.Structure):
+    _fields_ = [(f, C.c_double) for f in ("nvlink_gbs", "hbm_gbs", "cta_gbs",
+                                          "flag_us", "unit_us", "launch_us",
+                                          "jitter")]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -96,6 +102,7 @@ def _load():
         "a2a_plan_set_split": ([P, C.c_int32], C.c_int),
         "a2a_plan_set_schedule": ([P, C.c_int32, C.c_int64], C.c_int),
         "a2a_plan_set_queue_split": ([P, C.c_int32], C.c_int),
+        "a2a_plan_simulate": ([P, C.c_int32, C.POINTER(SimParams), C.POINTER(C.c_double)], C.c_int),
         "a2a_plan_dyn_stats": ([P, C.c_int32, C.c_int32, C.POINTER(C.c_int64),
                                 C.POINTER(C.c_int64), C.POINTER(C.c_double)], C.c_int),
         "a2a_plan_set_engine": ([P, C.c_int32, C.c_int32, C.c_int32], C.c_int),

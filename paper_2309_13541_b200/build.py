@@ -45,7 +45,7 @@ def _run(cmd, verbose):
 
 
 def build_native(force: bool = False, verbose: bool = True) -> str:
-    srcs = [os.path.join(CSRC, f) for f in ("a2a_plan.cpp", "a2a_io.cpp", "a2a_exec.cu")]
+    srcs = [os.path.join(CSRC, f) for f in ("a2a_plan.cpp", "a2a_io.cpp", "a2a_sim.cpp", "a2a_exec.cu")]
     deps = srcs + [os.path.join(CSRC, "a2a_internal.h"), os.path.join(INCLUDE, "a2a_exec.h")]
     if force or _stale(LIB, deps):
         tmp = LIB + ".tmp"

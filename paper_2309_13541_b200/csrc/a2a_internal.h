@@ -190,6 +190,7 @@ inline int64_t chunk_off(int64_t c, int64_t m, int64_t Q) {
 void set_error(const std::string& msg);
 int build_sync(Plan& P, int nC);
 int build_dyn(Plan& P, int nC, int64_t unit_bytes);
+int simulate(Plan& P, int nC, const a2a_sim_params& prm, double* makespan_s);
 int fail(int code, const std::string& msg);
 
 // Every extern "C" entry point runs its body through guard(): no C++

@@ -256,6 +256,20 @@ class Plan:
         self.remote_ctas = int(remote_ctas)
         return self
 
+    # fluid-model defaults, calibrated on measured 1/2/4-GPU runs (tools/sim_calibrate.py)
+    SIM_DEFAULTS = {"nvlink_gbs": 705.0, "hbm_gbs": 6538.9, "cta_gbs": 40.0,
+                    "flag_us": 2.0, "unit_us": 1.0, "launch_us": 8.0, "jitter": 0.1}
+
+    def simulate(self, num_ctas: int = 148, **params) -> float:
+        """Modelled seconds of one execute of the selected execution schedule
+        (a2a_plan_simulate; host only, any G -- e.g. 8 GPUs from a CPU box)."""
+        p = dict(self.SIM_DEFAULTS, **params)
+        sp = N.SimParams(**p)
+        out = C.c_double()
+        self._ck(N.lib.a2a_plan_simulate(self._h, int(num_ctas), C.byref(sp), C.byref(out)),
+                 "a2a_plan_simulate")
+        return out.value
+
     def dyn_stats(self, gpu: int, num_ctas: int) -> dict:
         nu, nw, est = C.c_int64(), C.c_int64(), C.c_double()
         self._ck(N.lib.a2a_plan_dyn_stats(self._h, int(gpu), int(num_ctas), C.byref(nu),
