@@ -183,6 +183,8 @@ typedef struct {
   double nvlink_gbs, hbm_gbs, cta_gbs;
   double flag_us, unit_us, launch_us;
   double jitter;   /* per-CTA speed factor spread, e.g. 0.2 = +-20% */
+  double unit_us_sys;  /* fixed cost per unit / CTA-step when G > 1 (system-scope
+                          publication); unit_us applies at G = 1 */
 } a2a_sim_params;
 int a2a_plan_simulate(a2a_plan* plan, int32_t num_ctas, const a2a_sim_params* params,
                       double* makespan_s);

@@ -153,7 +153,7 @@ int simulate(Plan& P, int nC, const a2a_sim_params& prm, double* out) {
   double now = 0;
   int64_t done = 0;
   const int64_t total = (int64_t)tasks.size();
-  const double unit_s = prm.unit_us * 1e-6, flag_s = prm.flag_us * 1e-6, cta = prm.cta_gbs * 1e9;
+  const double unit_s = (G > 1 ? prm.unit_us_sys : prm.unit_us) * 1e-6, flag_s = prm.flag_us * 1e-6, cta = prm.cta_gbs * 1e9;
   for (int w = 0; w < W; ++w) pq.emplace(0.0, w);
   // per-CTA speed factor in [1 - jitter, 1 + jitter] (deterministic hash): a
   // weighted share, so CTAs do not all finish their units at the same instant

@@ -24,7 +24,7 @@ def test_simulate_respects_bounds(name, m, G, sched, artifacts):
     a = artifacts(name)
     if a.g.n % G:
         pytest.skip("placement needs G | N")
-    prm = dict(Plan.SIM_DEFAULTS, jitter=0.0, launch_us=0.0, flag_us=0.0, unit_us=0.0)
+    prm = dict(Plan.SIM_DEFAULTS, jitter=0.0, launch_us=0.0, flag_us=0.0, unit_us=0.0, unit_us_sys=0.0)
     with bench.make_plan(a, m, G, "optimized", sched) as p:
         t = p.simulate(37, **prm)
         bt = bench.bound_terms([p.gpu_info(g) for g in range(G)], a.g.n, m, 1, prm["hbm_gbs"])

@@ -45,6 +45,15 @@ MEASURED = {
     ("torus4x4x4", 4 << 20, 4, "mix:1048576"): 8.0595,
     ("torus4x4x4", 4 << 20, 4, "spread:1048576"): 6.6821,
     ("torus4x4x4", 4 << 20, 4, "cp:1048576"): 12.5188,
+    # unit-size A/B (profiles/r01_unit_size_ab_G{2,4}.jsonl)
+    ("gk8_2", 16 << 20, 2, "cp:262144"): 0.7338,
+    ("gk8_2", 16 << 20, 2, "mix:262144"): 0.5673,
+    ("gk8_2", 16 << 20, 2, "list:1048576"): 0.4485,
+    ("gk8_2", 16 << 20, 2, "cp:4194304"): 0.4996,
+    ("gk8_2", 16 << 20, 4, "cp:262144"): 0.902,
+    ("gk8_2", 16 << 20, 4, "mix:262144"): 0.8016,
+    ("gk8_2", 16 << 20, 4, "list:1048576"): 0.7454,
+    ("gk8_2", 16 << 20, 4, "cp:4194304"): 0.7484,
     ("gk256_4", 1 << 20, 4, "static"): 34.0651,
     ("gk256_4", 1 << 20, 4, "mix:1048576"): 49.3659,
     ("gk256_4", 1 << 20, 4, "spread:1048576"): 34.1506,
