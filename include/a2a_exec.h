@@ -108,6 +108,17 @@ int a2a_load_schedule_xml(const char* path, a2a_sched_header* hdr, a2a_op** ops,
 int a2a_lower_path_files(const char* xml_path, const char* routes_path, const int32_t* node_map,
                          int32_t map_len, int32_t n_phys, a2a_sched_header* hdr, a2a_op** ops,
                          int64_t* n_ops);
+/* binary op table (format in csrc/a2a_io.cpp): the
+ * parsed schedule plus a SHA-256 trailer.  save rejects ops load_schedule_xml
+ * would reject (A2A_ERR_EVAL, same texts) and writes atomically (tmp + rename);
+ * load checks magic, size and digest (A2A_ERR_INVALID) and then the same op
+ * rejects.  *ops from load is malloc'd: a2a_free. */
+int a2a_save_schedule_table(const char* path, const a2a_sched_header* hdr, const a2a_op* ops,
+                            int64_t n_ops);
+int a2a_load_schedule_table(const char* path, a2a_sched_header* hdr, a2a_op** ops, int64_t* n_ops);
+/* hex SHA-256 of a file (65 bytes incl. NUL), as the reference manifest's
+ * _sha256 (reference src/cli.py:30-35) */
+int a2a_sha256_file(const char* path, char* hex_out);
 void a2a_free(void* p);
 
 /* ---- plan construction: validation exactly like the reference replay ---- */

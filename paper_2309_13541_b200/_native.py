@@ -70,6 +70,10 @@ def _load():
         "a2a_lower_path_files": ([C.c_char_p, C.c_char_p, P, C.c_int32, C.c_int32,
                                   C.POINTER(SchedHeader), C.POINTER(P), C.POINTER(C.c_int64)],
                                  C.c_int),
+        "a2a_save_schedule_table": ([C.c_char_p, C.POINTER(SchedHeader), P, C.c_int64], C.c_int),
+        "a2a_load_schedule_table": ([C.c_char_p, C.POINTER(SchedHeader), C.POINTER(P),
+                                     C.POINTER(C.c_int64)], C.c_int),
+        "a2a_sha256_file": ([C.c_char_p, C.c_char_p], C.c_int),
         "a2a_free": ([P], None),
         "a2a_plan_create": ([C.POINTER(ScheduleDesc), C.POINTER(P)], C.c_int),
         "a2a_plan_destroy": ([P], C.c_int),

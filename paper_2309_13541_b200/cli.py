@@ -18,12 +18,21 @@ Additions of this package (flags the reference does not have):
   transpose of send and print the device time.  Multi-GPU runs go through
   ``bench.py`` / ``tools/sweep.py`` (one process per GPU).
 
+* ``--sched`` may also be a binary op table written by ``pack``.
+* ``pack --sched X [--routes R --graph G] -o OUT``: parse (and, with
+  ``--routes``, lower) a schedule once and write it as a binary op table
+   plus ``OUT.manifest.json`` in the shape of the
+  reference's run manifest (command, argv, seed, version, sha256 of inputs and
+  outputs, wall_clock_s; reference cli.py:38-55).
+
 Usage: ``python -m paper_2309_13541_b200.cli eval --graph g.json --sched s.xml``.
 """
 from __future__ import annotations
 
 import argparse
+import json
 import sys
+import time
 
 
 def build_parser() -> argparse.ArgumentParser:
@@ -40,17 +49,22 @@ def build_parser() -> argparse.ArgumentParser:
     e.add_argument("--device", type=int, default=0)
     e.add_argument("--schedule", default="static",
                    help="execution schedule for --execute: static | <mode>[:unit[:R]]")
+    k = sub.add_parser("pack", help="write a schedule as a binary op table")
+    k.add_argument("--sched", required=True, help="XML schedule or op table (ts, or path with --routes)")
+    k.add_argument("--routes", default=None, help="route sidecar: lower the path schedule hop i -> step i")
+    k.add_argument("--graph", default=None, help="graph JSON (node count for --routes; checked with replay)")
+    k.add_argument("-o", "--out", required=True)
     return p
 
 
 def _load(args):
     from .graphs import load_graph
-    from .native_io import load_schedule_xml, lower_path_files
+    from .native_io import load_schedule, lower_path_files
     g = load_graph(args.graph)
     if args.routes:
         sched = lower_path_files(args.sched, args.routes, n_phys=g.n)
     else:
-        sched = load_schedule_xml(args.sched)
+        sched = load_schedule(args.sched)
     return g, sched
 
 
@@ -98,10 +112,42 @@ def _cmd_eval(args) -> None:
         print(_execute(g, sched, args))
 
 
+def _cmd_pack(args, argv) -> None:
+    from . import __version__
+    from .native_io import load_schedule, lower_path_files, save_schedule_table, sha256_file
+    started = time.time()
+    inputs = [args.sched] + [x for x in (args.routes, args.graph) if x]
+    g = None
+    if args.graph:
+        from .graphs import load_graph
+        g = load_graph(args.graph)
+    if args.routes:
+        sched = lower_path_files(args.sched, args.routes, n_phys=g.n if g is not None else 0)
+    else:
+        sched = load_schedule(args.sched)
+    if g is not None and sched.mode == "ts":
+        from .executor import replay_timestep_schedule
+        replay_timestep_schedule(g, sched)        # same rejects as eval, before writing
+    save_schedule_table(sched, args.out)
+    manifest = {"command": "pack", "argv": list(argv), "seed": None, "version": __version__,
+                "inputs": {p: sha256_file(p) for p in inputs},
+                "outputs": {args.out: sha256_file(args.out)},
+                "wall_clock_s": time.time() - started}
+    with open(args.out + ".manifest.json", "w") as fh:
+        json.dump(manifest, fh, indent=1)
+        fh.write("\n")
+    print(f"wrote {args.out}: mode {sched.mode}, n={sched.n}, nsteps={sched.nsteps}, "
+          f"Q={sched.Q}, {len(sched.ops_array)} ops")
+
+
 def main(argv: list[str] | None = None) -> int:
+    argv = sys.argv[1:] if argv is None else list(argv)
     args = build_parser().parse_args(argv)
     try:
-        {"eval": _cmd_eval}[args.command](args)
+        if args.command == "pack":
+            _cmd_pack(args, argv)
+        else:
+            _cmd_eval(args)
     except Exception as ex:   # noqa: BLE001 - CLI boundary, as the reference's main
         print(f"error: {ex}", file=sys.stderr)
         return 1

@@ -9,6 +9,11 @@
 //   * the route sidecar `<out>.routes.json` written by `a2a compile --mode path`
 //     (reference src/cli.py:289-292), lowered hop i -> step i exactly like
 //     lowering.lower_path_to_steps (optionally collapsing host-augmented ids).
+// and writes / reads this package's binary op table (A2ATBL1: header, int32
+// op rows, SHA-256 trailer), the form a lowered schedule is kept in once it
+// has been parsed -- GK(256,4)'s 255 890 hop-ops load without XML parsing.
+// a2a_sha256_file gives the digests of the reference's run manifest
+// (reference src/cli.py:30-55).
 #include <zlib.h>
 
 #include <algorithm>
@@ -338,6 +343,168 @@ struct JsonRoutes {
   }
 };
 
+// ---- SHA-256 (FIPS 180-4), for the op-table digest and run manifests ----
+struct Sha256 {
+  uint32_t h[8] = {0x6a09e667u, 0xbb67ae85u, 0x3c6ef372u, 0xa54ff53au,
+                   0x510e527fu, 0x9b05688cu, 0x1f83d9abu, 0x5be0cd19u};
+  uint8_t buf[64];
+  size_t fill = 0;
+  uint64_t total = 0;
+
+  static uint32_t rotr(uint32_t x, int n) { return (x >> n) | (x << (32 - n)); }
+  void block(const uint8_t* p) {
+    static const uint32_t K[64] = {
+        0x428a2f98u, 0x71374491u, 0xb5c0fbcfu, 0xe9b5dba5u, 0x3956c25bu, 0x59f111f1u, 0x923f82a4u,
+        0xab1c5ed5u, 0xd807aa98u, 0x12835b01u, 0x243185beu, 0x550c7dc3u, 0x72be5d74u, 0x80deb1feu,
+        0x9bdc06a7u, 0xc19bf174u, 0xe49b69c1u, 0xefbe4786u, 0x0fc19dc6u, 0x240ca1ccu, 0x2de92c6fu,
+        0x4a7484aau, 0x5cb0a9dcu, 0x76f988dau, 0x983e5152u, 0xa831c66du, 0xb00327c8u, 0xbf597fc7u,
+        0xc6e00bf3u, 0xd5a79147u, 0x06ca6351u, 0x14292967u, 0x27b70a85u, 0x2e1b2138u, 0x4d2c6dfcu,
+        0x53380d13u, 0x650a7354u, 0x766a0abbu, 0x81c2c92eu, 0x92722c85u, 0xa2bfe8a1u, 0xa81a664bu,
+        0xc24b8b70u, 0xc76c51a3u, 0xd192e819u, 0xd6990624u, 0xf40e3585u, 0x106aa070u, 0x19a4c116u,
+        0x1e376c08u, 0x2748774cu, 0x34b0bcb5u, 0x391c0cb3u, 0x4ed8aa4au, 0x5b9cca4fu, 0x682e6ff3u,
+        0x748f82eeu, 0x78a5636fu, 0x84c87814u, 0x8cc70208u, 0x90befffau, 0xa4506cebu, 0xbef9a3f7u,
+        0xc67178f2u};
+    uint32_t w[64];
+    for (int i = 0; i < 16; ++i)
+      w[i] = (uint32_t)p[4 * i] << 24 | (uint32_t)p[4 * i + 1] << 16 | (uint32_t)p[4 * i + 2] << 8 |
+             (uint32_t)p[4 * i + 3];
+    for (int i = 16; i < 64; ++i) {
+      uint32_t s0 = rotr(w[i - 15], 7) ^ rotr(w[i - 15], 18) ^ (w[i - 15] >> 3);
+      uint32_t s1 = rotr(w[i - 2], 17) ^ rotr(w[i - 2], 19) ^ (w[i - 2] >> 10);
+      w[i] = w[i - 16] + s0 + w[i - 7] + s1;
+    }
+    uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], k = h[7];
+    for (int i = 0; i < 64; ++i) {
+      uint32_t t1 = k + (rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25)) + ((e & f) ^ (~e & g)) + K[i] + w[i];
+      uint32_t t2 = (rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22)) + ((a & b) ^ (a & c) ^ (b & c));
+      k = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + t2;
+    }
+    h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += k;
+  }
+  void update(const void* data, size_t n) {
+    const uint8_t* p = (const uint8_t*)data;
+    total += n;
+    if (fill) {
+      size_t k = std::min(n, 64 - fill);
+      memcpy(buf + fill, p, k);
+      fill += k; p += k; n -= k;
+      if (fill < 64) return;
+      block(buf);
+      fill = 0;
+    }
+    for (; n >= 64; p += 64, n -= 64) block(p);
+    memcpy(buf, p, n);
+    fill = n;
+  }
+  void final(uint8_t out[32]) {
+    const uint64_t bits = total * 8;
+    const uint8_t pad = 0x80, zero = 0;
+    update(&pad, 1);
+    while (fill != 56) update(&zero, 1);
+    uint8_t len[8];
+    for (int i = 0; i < 8; ++i) len[i] = (uint8_t)(bits >> (56 - 8 * i));
+    update(len, 8);
+    for (int i = 0; i < 8; ++i)
+      for (int j = 0; j < 4; ++j) out[4 * i + j] = (uint8_t)(h[i] >> (24 - 8 * j));
+  }
+};
+
+// ---- binary op table: a validated ts/path schedule
+//      as it is handed to a2a_plan_create, loadable without XML parsing.
+//   [0, 48)       header: magic "A2ATBL1\n", u32 header bytes (48), i32 n,
+//                 nsteps, q, mode, i32 0, f64 chunk_bytes, i64 n_ops
+//   [48, 48+28K)  K ops, int32 (t, src, dst, s, d, c0, c1) each
+//   last 32 B     SHA-256 of everything before it
+//   All fields little-endian (the only byte order of the hosts this runs on).
+constexpr char kTblMagic[8] = {'A', '2', 'A', 'T', 'B', 'L', '1', '\n'};
+constexpr uint32_t kTblHeader = 48;
+static_assert(sizeof(a2a_op) == 28, "a2a_op must be 7 packed int32");
+
+// the per-op rejects of load_xml (schedule.py:370-378) on an already-parsed table
+int check_ops(int32_t nsteps, int32_t q, const a2a_op* ops, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) {
+    const a2a_op& o = ops[i];
+    if (!(0 <= o.t && o.t < nsteps)) {
+      char b[96];
+      snprintf(b, sizeof b, "step t=%d outside [0, %d)", o.t, nsteps);
+      return fail(A2A_ERR_EVAL, b);
+    }
+    if (!(0 <= o.c0 && o.c0 < o.c1 && o.c1 <= q)) {
+      char b[96];
+      snprintf(b, sizeof b, "bad chunk range [%d,%d)", o.c0, o.c1);
+      return fail(A2A_ERR_EVAL, b);
+    }
+  }
+  return A2A_OK;
+}
+
+int save_table(const char* path, const a2a_sched_header* hdr, const a2a_op* ops, int64_t n) {
+  if (hdr->mode != 0 && hdr->mode != 1) return fail(A2A_ERR_INVALID, "mode must be 0 (ts) or 1 (path)");
+  if (hdr->n < 0 || hdr->nsteps < 0 || hdr->q < 1 || n < 0)
+    return fail(A2A_ERR_INVALID, "bad schedule header");
+  if (int rc = check_ops(hdr->nsteps, hdr->q, ops, n)) return rc;
+  uint8_t h[kTblHeader] = {};
+  memcpy(h, kTblMagic, 8);
+  const int32_t f[6] = {hdr->n, hdr->nsteps, hdr->q, hdr->mode, 0, 0};
+  memcpy(h + 8, &kTblHeader, 4);
+  memcpy(h + 12, f, 20);
+  memcpy(h + 32, &hdr->chunk_bytes, 8);
+  memcpy(h + 40, &n, 8);
+  Sha256 sh;
+  sh.update(h, sizeof h);
+  sh.update(ops, (size_t)n * sizeof(a2a_op));
+  uint8_t dig[32];
+  sh.final(dig);
+  const std::string tmp = std::string(path) + ".tmp";
+  FILE* fp = fopen(tmp.c_str(), "wb");
+  if (!fp) return fail(A2A_ERR_INVALID, std::string("cannot open ") + tmp);
+  bool ok = fwrite(h, 1, sizeof h, fp) == sizeof h &&
+            (n == 0 || fwrite(ops, sizeof(a2a_op), (size_t)n, fp) == (size_t)n) &&
+            fwrite(dig, 1, 32, fp) == 32;
+  ok = (fclose(fp) == 0) && ok;
+  if (!ok || rename(tmp.c_str(), path) != 0) {
+    remove(tmp.c_str());
+    return fail(A2A_ERR_INVALID, std::string("write error on ") + path);
+  }
+  return A2A_OK;
+}
+
+int load_table(const char* path, Loaded* L) {
+  std::string text, err;
+  if (!read_file(path, &text, &err)) return fail(A2A_ERR_INVALID, err);
+  auto bad = [&](const char* why) {
+    return fail(A2A_ERR_INVALID, std::string("schedule table ") + path + ": " + why);
+  };
+  if (text.size() < 8 || memcmp(text.data(), kTblMagic, 8) != 0) return bad("not an A2ATBL1 file");
+  if (text.size() < kTblHeader + 32) return bad("truncated or oversized op table");
+  const uint8_t* p = (const uint8_t*)text.data();
+  uint32_t hb;
+  int32_t f[6];
+  int64_t n;
+  memcpy(&hb, p + 8, 4);
+  memcpy(f, p + 12, 20);
+  memcpy(&L->chunk_bytes, p + 32, 8);
+  memcpy(&n, p + 40, 8);
+  if (hb != kTblHeader) return bad("unsupported header size");
+  if (n < 0 || (uint64_t)n > (text.size() - kTblHeader - 32) / sizeof(a2a_op) ||
+      text.size() != kTblHeader + (size_t)n * sizeof(a2a_op) + 32)
+    return bad("truncated or oversized op table");
+  Sha256 sh;
+  sh.update(p, text.size() - 32);
+  uint8_t dig[32];
+  sh.final(dig);
+  if (memcmp(dig, p + text.size() - 32, 32) != 0) return bad("sha256 mismatch");
+  if (f[3] != 0 && f[3] != 1) return bad("unknown mode");
+  if (f[0] < 0 || f[1] < 0 || f[2] < 1) return bad("bad header values");
+  L->n = f[0];
+  L->nsteps = f[1];
+  L->q = f[2];
+  L->mode = f[3];
+  L->ops.resize((size_t)n);
+  if (n) memcpy(L->ops.data(), p + kTblHeader, (size_t)n * sizeof(a2a_op));
+  return check_ops(L->nsteps, L->q, L->ops.data(), n);
+}
+
 int fill(const Loaded& L, a2a_sched_header* hdr, a2a_op** ops, int64_t* n_ops) {
   hdr->n = L.n;
   hdr->nsteps = L.nsteps;
@@ -448,6 +615,48 @@ int a2a_lower_path_files(const char* xml_path, const char* routes_path, const in
     } catch (const std::bad_alloc&) {
       return fail(A2A_ERR_NOMEM, "out of host memory");
     }
+  });
+}
+
+int a2a_save_schedule_table(const char* path, const a2a_sched_header* hdr, const a2a_op* ops,
+                            int64_t n_ops) {
+  return guard([&]() -> int {
+    if (!path || !hdr || (!ops && n_ops > 0)) return fail(A2A_ERR_INVALID, "null argument");
+    return save_table(path, hdr, ops, n_ops);
+  });
+}
+
+int a2a_load_schedule_table(const char* path, a2a_sched_header* hdr, a2a_op** ops, int64_t* n_ops) {
+  return guard([&]() -> int {
+    if (!path || !hdr || !ops || !n_ops) return fail(A2A_ERR_INVALID, "null argument");
+    Loaded L;
+    int rc = load_table(path, &L);
+    if (rc) return rc;
+    return fill(L, hdr, ops, n_ops);
+  });
+}
+
+int a2a_sha256_file(const char* path, char* hex_out) {
+  return guard([&]() -> int {
+    if (!path || !hex_out) return fail(A2A_ERR_INVALID, "null argument");
+    FILE* fp = fopen(path, "rb");
+    if (!fp) return fail(A2A_ERR_INVALID, std::string("cannot open ") + path);
+    Sha256 sh;
+    std::vector<char> buf(1 << 16);
+    size_t k;
+    while ((k = fread(buf.data(), 1, buf.size(), fp)) > 0) sh.update(buf.data(), k);
+    const bool err = ferror(fp) != 0;
+    fclose(fp);
+    if (err) return fail(A2A_ERR_INVALID, std::string("read error on ") + path);
+    uint8_t dig[32];
+    sh.final(dig);
+    static const char* hx = "0123456789abcdef";
+    for (int i = 0; i < 32; ++i) {
+      hex_out[2 * i] = hx[dig[i] >> 4];
+      hex_out[2 * i + 1] = hx[dig[i] & 15];
+    }
+    hex_out[64] = 0;
+    return A2A_OK;
   });
 }
 

@@ -1,6 +1,11 @@
 """Native loader front-end: reference XML / route sidecar
 files -> ChunkedSchedule backed by an int32 op table, parsed in C++
-(csrc/a2a_io.cpp).  Same rejects and messages as schedule.parse_schedule_xml."""
+(csrc/a2a_io.cpp).  Same rejects and messages as schedule.parse_schedule_xml.
+
+Also the binary op table (``save_schedule_table`` / ``load_schedule_table``,
+format in csrc/a2a_io.cpp): a parsed or lowered schedule with a SHA-256
+trailer, reloaded without XML parsing, and ``sha256_file`` for the reference's
+run-manifest digests (reference src/cli.py:30-55)."""
 from __future__ import annotations
 
 import ctypes as C
@@ -10,7 +15,10 @@ import numpy as np
 from . import _native as N
 from .schedule import ChunkedSchedule, Instruction, ScheduleError
 
-__all__ = ["load_schedule_xml", "lower_path_files", "OpTableSchedule"]
+__all__ = ["load_schedule_xml", "lower_path_files", "OpTableSchedule", "save_schedule_table",
+           "load_schedule_table", "load_schedule", "is_schedule_table", "sha256_file"]
+
+TABLE_MAGIC = b"A2ATBL1\n"
 
 
 class OpTableSchedule(ChunkedSchedule):
@@ -69,3 +77,58 @@ def lower_path_files(xml_path, routes_path, node_map=None, n_phys: int = 0) -> O
     if rc:
         _err(rc)
     return _take(hdr, ptr, cnt)
+
+
+def _ops_of(sched) -> np.ndarray:
+    arr = getattr(sched, "ops_array", None)
+    if arr is None:
+        arr = np.array([(i.t, i.src, i.dst, i.s, i.d, i.c0, i.c1) for i in sched.instructions],
+                       dtype=np.int64).reshape(-1, 7)
+        if arr.size and (arr.min() < -2**31 or arr.max() >= 2**31):
+            raise ValueError("instruction field does not fit int32")
+    return np.ascontiguousarray(arr, dtype=np.int32).reshape(-1, 7)
+
+
+def save_schedule_table(sched, path) -> None:
+    """Write ``sched`` (this package's or the reference's ChunkedSchedule) as a
+    binary op table; rejects what load_schedule_xml would reject."""
+    if sched.mode not in ("ts", "path"):
+        raise ScheduleError(f"unknown mode '{sched.mode}'")
+    hdr = N.SchedHeader(int(sched.n), int(sched.nsteps), int(sched.Q),
+                        0 if sched.mode == "ts" else 1, float(sched.chunk_bytes))
+    ops = _ops_of(sched)
+    rc = N.lib.a2a_save_schedule_table(str(path).encode(), C.byref(hdr),
+                                       ops.ctypes.data if ops.size else None, ops.shape[0])
+    if rc:
+        _err(rc)
+
+
+def load_schedule_table(path) -> OpTableSchedule:
+    hdr, ptr, cnt = N.SchedHeader(), C.c_void_p(), C.c_int64()
+    rc = N.lib.a2a_load_schedule_table(str(path).encode(), C.byref(hdr), C.byref(ptr), C.byref(cnt))
+    if rc:
+        _err(rc)
+    return _take(hdr, ptr, cnt)
+
+
+def is_schedule_table(path) -> bool:
+    import gzip
+    with open(path, "rb") as fh:
+        head = fh.read(len(TABLE_MAGIC))
+    if head[:2] == b"\x1f\x8b":                      # gzip: the loader reads it transparently
+        with gzip.open(path, "rb") as fh:
+            head = fh.read(len(TABLE_MAGIC))
+    return head == TABLE_MAGIC
+
+
+def load_schedule(path) -> OpTableSchedule:
+    """A schedule file of either form: binary op table or reference XML (+gz)."""
+    return load_schedule_table(path) if is_schedule_table(path) else load_schedule_xml(path)
+
+
+def sha256_file(path) -> str:
+    out = C.create_string_buffer(65)
+    rc = N.lib.a2a_sha256_file(str(path).encode(), out)
+    if rc:
+        _err(rc)
+    return out.value.decode()
