@@ -652,6 +652,12 @@ def main(argv=None):
                "sample": f"{len(times)} full all-to-alls of {args.config} at m={m_cpu} B "
                          f"(median) with oracle/replay_bytes.c on {nthreads} threads",
                "recv_ok": cok}
+        # SURVEY §8d baseline 2: the same restatement on one core
+        t1, ok1 = _cpu_oracle_run(art, m_cpu, min(3.0, args.cpu_budget_s), 1)
+        t1m = sorted(t1)[len(t1) // 2]
+        cpu["single_core"] = {"value": round(n * (n - 1) * m_cpu / t1m / 1e9, 4), "cores": 1,
+                              "sample": f"{len(t1)} full all-to-alls (median), 1 thread",
+                              "recv_ok": ok1}
 
     if ctx.rank == 0:
         line = {
