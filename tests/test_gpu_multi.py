@@ -296,7 +296,6 @@ def test_multiprocess_dynamic(world, engine, reuse, name, m, mode):
         assert r[2], f"rank {r[0]}: link counters differ from schedule"
 
 
-
 @pytest.mark.parametrize("world,engine,name,m", [(2, "tma", "gk8_2", 65536 + 64),
                                                  (4, "lsu", "torus2x4_h2", 4099)])
 @pytest.mark.parametrize("mode", ["cp:0:3", "dynamic:4096:40"])
@@ -304,6 +303,7 @@ def test_multiprocess_pinned_split(world, engine, name, m, mode):
     """Pinned NVLink/HBM queue split (a2a_plan_set_queue_split) across GPUs,
     repeated executes (the per-epoch grab-counter base of pinned queues)."""
     test_multiprocess_dynamic(world, engine, False, name, m, mode)
+
 
 def test_alternating_recv_buffers():
     if _ngpu() < 2:
