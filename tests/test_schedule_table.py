@@ -233,3 +233,21 @@ def test_pack_rejects_bad_schedule(tmp_path, capsys):
     assert main(["pack", "--graph", os.path.join(d, "graph.json"), "--sched", str(bad), "-o", str(out)]) == 1
     assert capsys.readouterr().err.startswith("error: ")
     assert not out.exists()
+
+
+@pytest.mark.parametrize("seed", range(0, 200, 5))
+def test_random_schedules_round_trip(seed, tmp_path):
+    """Random valid schedules (tests/fuzz_schedules.py): the table reloads the
+    same ops, and the plan built from it has the oracle's modelled T."""
+    from fuzz_schedules import random_case
+    from replay_bytes import make_send, replay_bytes
+
+    from paper_2309_13541_b200.executor import Plan
+    g, sched, m, _, _ = random_case(seed)
+    p = tmp_path / "f.a2at"
+    save_schedule_table(sched, p)
+    t = load_schedule_table(p)
+    assert [_row(i) for i in t.instructions] == [_row(i) for i in sched.instructions]
+    T, _, _ = replay_bytes(g, sched, make_send(g.n, m, seed=seed), m)
+    with Plan(g, t, m=m) as plan:
+        assert plan.model_time(m) == T
