@@ -196,6 +196,9 @@ typedef struct {
   double jitter;   /* per-CTA speed factor spread, e.g. 0.2 = +-20% */
   double unit_us_sys;  /* fixed cost per unit / CTA-step when G > 1 (system-scope
                           publication); unit_us applies at G = 1 */
+  double incast;       /* NVLink ingress of a GPU that w CTAs (over all peers) write
+                          into at once runs at nvlink_gbs / (1 + incast * max(0,
+                          w / num_ctas - 1)); 0 = no penalty */
 } a2a_sim_params;
 int a2a_plan_simulate(a2a_plan* plan, int32_t num_ctas, const a2a_sim_params* params,
                       double* makespan_s);

@@ -54,7 +54,7 @@ class GpuInfo(C.Structure):
 class SimParams(C.Structure):
     _fields_ = [(f, C.c_double) for f in ("nvlink_gbs", "hbm_gbs", "cta_gbs",
                                           "flag_us", "unit_us", "launch_us",
-                                          "jitter", "unit_us_sys")]
+                                          "jitter", "unit_us_sys", "incast")]
 
 
 def _load():

@@ -2,7 +2,9 @@
 // per-CTA programs (static) or unit queues (dynamic orders 1-4, 6) the device
 // runs, on a machine of per-GPU resources -- NVLink egress, NVLink ingress
 // (both per direction) and HBM (read + write bytes) -- with a per-CTA copy-rate
-// cap, a fixed cost per unit / CTA-step and a flag latency.  Concurrent copies
+// cap, a fixed cost per unit / CTA-step, a flag latency and an optional incast
+// penalty (a GPU's NVLink ingress shrinks when more CTAs than one GPU's worth
+// write into it at once).  Concurrent copies
 // share each resource equally per byte of demand; a copy runs at the smallest
 // share over the resources it uses (or its CTA cap).  Used offline to compare
 // execution orders (e.g. at 8 GPUs, which the build container cannot reach);
@@ -179,6 +181,7 @@ int simulate(Plan& P, int nC, const a2a_sim_params& prm, double* out) {
     running.push_back(w);
   };
   std::vector<double> load(R);
+  std::vector<int> writers(G);
   std::vector<int> still;
   for (;;) {
     while (!pq.empty() && pq.top().first <= now) {
@@ -208,10 +211,19 @@ int simulate(Plan& P, int nC, const a2a_sim_params& prm, double* out) {
     if (running.empty() && pq.empty()) break;
     // rates: equal share per byte of demand on every resource
     std::fill(load.begin(), load.end(), 0.0);
+    std::fill(writers.begin(), writers.end(), 0);
     for (int w : running) {
       const SimTask& k = tasks[cur[w]];
-      for (int i = 0; i < k.nres; ++i) load[k.res[i]] += kw[w] * k.w[i];
+      for (int i = 0; i < k.nres; ++i) {
+        load[k.res[i]] += kw[w] * k.w[i];
+        if (k.res[i] >= G && k.res[i] < 2 * G) ++writers[k.res[i] - G];
+      }
     }
+    if (prm.incast > 0)   // more concurrent writer CTAs than one GPU's worth
+      for (int h = 0; h < G; ++h) {
+        const double over = std::max(0.0, (double)writers[h] / nC - 1.0);
+        cap[G + h] = prm.nvlink_gbs * 1e9 / (1.0 + prm.incast * over);
+      }
     double dt = pq.empty() ? kInf : pq.top().first - now;
     for (int w : running) {
       const SimTask& k = tasks[cur[w]];

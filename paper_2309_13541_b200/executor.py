@@ -259,7 +259,7 @@ class Plan:
     # fluid-model defaults, calibrated on measured 1/2/4-GPU runs (tools/sim_calibrate.py)
     SIM_DEFAULTS = {"nvlink_gbs": 705.0, "hbm_gbs": 6538.9, "cta_gbs": 40.0,
                     "flag_us": 2.0, "unit_us": 1.0, "launch_us": 8.0, "jitter": 0.1,
-                    "unit_us_sys": 10.0}
+                    "unit_us_sys": 10.0, "incast": 0.0}
 
     def simulate(self, num_ctas: int = 148, **params) -> float:
         """Modelled seconds of one execute of the selected execution schedule

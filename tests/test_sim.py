@@ -56,3 +56,17 @@ def test_simulate_rejects(artifacts):
     with Plan(a.g, a.sched, m=4096, n_gpus=2) as p:
         with pytest.raises(ValueError):
             p.simulate(8, nvlink_gbs=0.0)
+
+
+@pytest.mark.parametrize("sched", ["static", "cp:1048576", "mix:1048576"])
+def test_simulate_incast_penalty_only_slows(sched, artifacts):
+    """The optional ingress-oversubscription penalty never speeds an execute
+    up, and is a no-op on one GPU (no NVLink ingress)."""
+    import bench
+    a = artifacts("gk8_2")
+    for G in (1, 4):
+        with bench.make_plan(a, 16 << 20, G, "optimized", sched) as p:
+            t0, t1 = p.simulate(148), p.simulate(148, incast=0.5)
+            assert t1 >= t0 * (1 - 1e-9)
+            if G == 1:
+                assert t1 == t0
