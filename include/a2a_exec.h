@@ -185,7 +185,7 @@ int a2a_plan_set_schedule(a2a_plan* plan, int32_t mode, int64_t unit_bytes);
  * drains).  Clamped so that every non-empty queue keeps at least one CTA. */
 int a2a_plan_set_queue_split(a2a_plan* plan, int32_t remote_ctas);
 /* Fluid performance model of one execute of the selected execution schedule
- * (static programs or dynamic orders 1-4 / 6; simple protocol) for `num_ctas`
+ * (static programs or dynamic orders 1-6; simple protocol) for `num_ctas`
  * CTAs per GPU: per-GPU NVLink egress and ingress (GB/s per direction), HBM
  * (read + write GB/s), a per-CTA copy-rate cap, a fixed cost per unit /
  * CTA-step, the flag latency and a launch cost.  Host only; for comparing

@@ -1,5 +1,5 @@
 // Fluid performance model of one execute (a2a_plan_simulate): the exact
-// per-CTA programs (static) or unit queues (dynamic orders 1-4, 6) the device
+// per-CTA programs (static) or unit queues (dynamic orders 1-6) the device
 // runs, on a machine of per-GPU resources -- NVLink egress, NVLink ingress
 // (both per direction) and HBM (read + write bytes) -- with a per-CTA copy-rate
 // cap, a fixed cost per unit / CTA-step, a flag latency and an optional incast
@@ -67,11 +67,10 @@ int dst_gpu_of(int loc, int G) {
 
 int simulate(Plan& P, int nC, const a2a_sim_params& prm, double* out) {
   if (P.ll) return fail(A2A_ERR_INVALID, "simulate: LL plans are not modelled");
-  if (P.sched_mode == 5) return fail(A2A_ERR_INVALID, "simulate: the ready queue is not modelled");
   if (!(prm.nvlink_gbs > 0 && prm.hbm_gbs > 0 && prm.cta_gbs > 0))
     return fail(A2A_ERR_INVALID, "simulate: bandwidths must be positive");
   const int G = P.G, TE = P.T_exec, R = 3 * G;
-  const bool dyn = P.sched_mode >= 1;
+  const bool dyn = P.sched_mode >= 1, ready = P.sched_mode == 5;
   int rc = dyn ? build_dyn(P, nC, P.dyn_unit_bytes) : build_sync(P, nC);
   if (rc) return rc;
   std::vector<double> cap(R);
@@ -113,7 +112,9 @@ int simulate(Plan& P, int nC, const a2a_sim_params& prm, double* out) {
         std::fill(acc.begin(), acc.end(), 0.0);
         add_bytes(k, acc, G, g, dst_gpu_of(u.dst_loc, G), (double)u.nbytes);
         finish_task(k, acc);
-        k.deps.assign(D.wait_idx[g].begin() + u.wb, D.wait_idx[g].begin() + u.we);
+        // ready queue: a unit is enqueued only once its producers finished,
+        // so it carries no waits (u.wb/we index its dependents instead)
+        if (!ready) k.deps.assign(D.wait_idx[g].begin() + u.wb, D.wait_idx[g].begin() + u.we);
         k.flag = D.unit_base[g] + (int32_t)i;
       }
   }
@@ -144,6 +145,25 @@ int simulate(Plan& P, int nC, const a2a_sim_params& prm, double* out) {
       cq[w] ^= 1;
     }
   };
+  // ---- ready queue (mode 5): per-GPU FIFO of enqueued units; the k-th CTA
+  //      to claim a position on GPU g runs the k-th unit enqueued there
+  std::vector<int> ugpu, rem;
+  std::vector<int64_t> claim(G, 0);
+  std::vector<std::vector<int32_t>> pushed(G);
+  std::vector<std::vector<int>> slot_waiter(G);
+  if (ready) {
+    const DynTables& D = P.dyn;
+    ugpu.resize(tasks.size());
+    rem.resize(tasks.size());
+    for (int g = 0; g < G; ++g) {
+      slot_waiter[g].assign(D.units[g].size(), -1);
+      for (size_t i = 0; i < D.units[g].size(); ++i) {
+        ugpu[D.unit_base[g] + i] = g;
+        rem[D.unit_base[g] + i] = (int)D.units[g][i].mask;     // in-degree
+      }
+      for (int32_t i = 0; i < D.n_init[g]; ++i) pushed[g].push_back(D.unit_base[g] + i);
+    }
+  }
   // ---- event loop
   std::vector<double> flag_at((size_t)n_flags, kInf);          // visible from
   std::vector<std::vector<int>> waiters((size_t)n_flags);
@@ -166,6 +186,13 @@ int simulate(Plan& P, int nC, const a2a_sim_params& prm, double* out) {
     kw[w] = 1.0 + prm.jitter * (2.0 * (double)(x >> 11) / 9007199254740992.0 - 1.0);
   }
   auto try_start = [&](int w) {
+    if (cur[w] < 0 && ready) {
+      const int g = w / nC;
+      const int64_t pos = claim[g]++;
+      if (pos >= (int64_t)slot_waiter[g].size()) return;      // past the last unit: exit
+      if (pos >= (int64_t)pushed[g].size()) { slot_waiter[g][pos] = w; return; }
+      cur[w] = pushed[g][pos];
+    }
     if (cur[w] < 0) {
       cur[w] = next_task(w);
       if (cur[w] < 0) return;
@@ -187,6 +214,18 @@ int simulate(Plan& P, int nC, const a2a_sim_params& prm, double* out) {
     while (!pq.empty() && pq.top().first <= now) {
       const int w = pq.top().second;
       pq.pop();
+      if (w >= W) {                      // ready queue: unit w - W enqueued now
+        const int32_t d = w - W;
+        const int h = ugpu[d];
+        const size_t pos = pushed[h].size();
+        pushed[h].push_back(d);
+        const int x = slot_waiter[h][pos];
+        if (x >= 0) {
+          cur[x] = d;
+          pq.emplace(now, x);
+        }
+        continue;
+      }
       try_start(w);
     }
     // zero-byte tasks complete at once
@@ -198,6 +237,15 @@ int simulate(Plan& P, int nC, const a2a_sim_params& prm, double* out) {
         flag_at[k.flag] = now + flag_s;
         for (int x : waiters[k.flag]) pq.emplace(now + flag_s, x);
         waiters[k.flag].clear();
+        if (ready) {                     // count down dependents, enqueue completed ones
+          const DynTables& D = P.dyn;
+          const int g = ugpu[cur[w]];
+          const DevUnit& u = D.units[g][cur[w] - D.unit_base[g]];
+          for (int32_t j = u.wb; j < u.we; ++j) {
+            const int32_t d = D.deps_out[g][2 * (size_t)j];
+            if (--rem[d] == 0) pq.emplace(now + flag_s, W + d);
+          }
+        }
         cur[w] = -1;
         ++done;
         pq.emplace(now + unit_s, w);

@@ -18,7 +18,8 @@ sys.path.insert(0, ROOT)
 @pytest.mark.parametrize("name,m", [("gk8_2", 16 << 20), ("hypercube3", 1 << 20), ("torus2x4_h2", 65536)])
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
 @pytest.mark.parametrize("sched", ["static", "dynamic:1048576", "list:262144", "cp:1048576",
-                                   "mix:1048576", "spread:1048576", "cp:1048576:24"])
+                                   "mix:1048576", "spread:1048576", "cp:1048576:24",
+                                   "ready:1048576", "ready:262144"])
 def test_simulate_respects_bounds(name, m, G, sched, artifacts):
     import bench
     a = artifacts(name)
@@ -50,10 +51,6 @@ def test_simulate_rejects(artifacts):
         with pytest.raises(ValueError, match="LL"):
             p.simulate(8)
     with Plan(a.g, a.sched, m=4096, n_gpus=2) as p:
-        p.set_schedule("ready", 1024)
-        with pytest.raises(ValueError, match="ready"):
-            p.simulate(8)
-    with Plan(a.g, a.sched, m=4096, n_gpus=2) as p:
         with pytest.raises(ValueError):
             p.simulate(8, nvlink_gbs=0.0)
 
@@ -70,3 +67,21 @@ def test_simulate_incast_penalty_only_slows(sched, artifacts):
             assert t1 >= t0 * (1 - 1e-9)
             if G == 1:
                 assert t1 == t0
+
+
+@pytest.mark.parametrize("name", ["gk8_2", "torus2x4_h2", "hypercube3"])
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+@pytest.mark.parametrize("nc", [1, 2, 148])
+def test_simulate_ready_queue_completes(name, G, nc, artifacts):
+    """Ready queue (mode 5) in the model: the k-th CTA to claim a position
+    runs the k-th unit enqueued on its GPU; every unit runs, even with one CTA,
+    and the time grows as CTAs are taken away."""
+    import bench
+    a = artifacts(name)
+    if a.g.n % G:
+        pytest.skip("placement needs G | N")
+    with bench.make_plan(a, 1 << 20, G, "optimized", "ready:262144") as p:
+        t = p.simulate(nc)
+        assert t > 0
+        if nc == 1:
+            assert t >= p.simulate(148)

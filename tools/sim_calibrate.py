@@ -6,7 +6,8 @@ the model ranks the schedules in the measured order.  With --predict, prints the
 model's times for GPU counts that were not measured (8 GPUs).
 
 Measured numbers: profiles/r01_queue_split_ab_G{2,4}.jsonl,
-r01_spread_ab_G4.jsonl, r01_schedule_ab_G{12,4}.jsonl, r01_bench_final6_b1.log.
+r01_spread_ab_G4.jsonl, r01_schedule_ab_G{12,4}.jsonl, r01_bench_final6_b1.log,
+r01_ready_queue_ab_G{2,4}.jsonl.
 """
 from __future__ import annotations
 
@@ -54,6 +55,14 @@ MEASURED = {
     ("gk8_2", 16 << 20, 4, "mix:262144"): 0.8016,
     ("gk8_2", 16 << 20, 4, "list:1048576"): 0.7454,
     ("gk8_2", 16 << 20, 4, "cp:4194304"): 0.7484,
+    # ready queue (profiles/r01_ready_queue_ab_G{2,4}.jsonl; G=1: bench autotune, r01_bench_final6_b1.log)
+    ("gk8_2", 16 << 20, 1, "ready:1048576"): 0.6764,
+    ("gk8_2", 16 << 20, 2, "ready:1048576"): 0.4813,
+    ("gk8_2", 16 << 20, 2, "ready:2097152"): 0.5313,
+    ("gk8_2", 16 << 20, 4, "ready:1048576"): 0.6861,
+    ("gk8_2", 16 << 20, 4, "ready:2097152"): 0.7321,
+    ("hypercube3", 4 << 20, 2, "ready:1048576"): 0.1545,
+    ("hypercube3", 4 << 20, 4, "ready:1048576"): 0.164,
     ("gk256_4", 1 << 20, 4, "static"): 34.0651,
     ("gk256_4", 1 << 20, 4, "mix:1048576"): 49.3659,
     ("gk256_4", 1 << 20, 4, "spread:1048576"): 34.1506,
@@ -102,7 +111,8 @@ def main(argv=None):
           f"range {min(ratios):.2f}-{max(ratios):.2f}")
     if a.predict:
         for name, m in (("gk8_2", 16 << 20), ("hypercube3", 16 << 20), ("torus4x4x4", 4 << 20)):
-            for sched in ("static", "mix:1048576", "cp:1048576", "spread:1048576", "cp:1048576:64"):
+            for sched in ("static", "mix:1048576", "cp:1048576", "spread:1048576", "cp:1048576:64",
+                          "ready:1048576"):
                 print(f"predict {name} G=8 {sched:16s} {model(name, m, 8, sched, **params):8.4f} ms",
                       flush=True)
 
