@@ -14,7 +14,12 @@
  *   - evaluate.py:108-113 apply arrivals after the checks
  *   - evaluate.py:114-126 final transpose scan
  * Copies of one step run on `nthreads` OpenMP threads (the step's ops are
- * independent: each reads data held at the start of the step).
+ * independent: each reads data held at the start of the step), cut into
+ * pieces of at most 1 MiB so a step with few large ops still uses every
+ * thread.  oracle_replay_ws takes a caller-owned scratch workspace (one m-byte
+ * slot per distinct (holder, s, d) forwarding location, carved in first-use
+ * order) so repeated replays do not page-fault fresh scratch every call, as
+ * the device plan keeps its scratch between executes.
  * Chunk c = bytes [floor(c*m/Q), floor((c+1)*m/Q)); send/recv are [N][N][m].
  */
 #include <omp.h>
@@ -59,12 +64,18 @@ static void setbit(uint8_t* b, int64_t c) { b[c >> 3] |= (uint8_t)(1u << (c & 7)
 
 #define FAIL(...) do { snprintf(err, errlen, __VA_ARGS__); rc = 2; goto done; } while (0)
 
-int oracle_replay(int n, int T, int Q, int64_t m, int E, const int32_t* edge_uv,
-                  const double* cap, const int32_t* ops, int64_t n_ops,
-                  const uint8_t* send, uint8_t* recv, int nthreads, int copy_self,
-                  double m_model, double b, double sync, double* T_out,
-                  int64_t* link_bytes, char* err, int errlen) {
+#define PIECE_BYTES ((int64_t)1 << 20)
+
+int oracle_replay_ws(int n, int T, int Q, int64_t m, int E, const int32_t* edge_uv,
+                     const double* cap, const int32_t* ops, int64_t n_ops,
+                     const uint8_t* send, uint8_t* recv, int nthreads, int copy_self,
+                     double m_model, double b, double sync, double* T_out,
+                     int64_t* link_bytes, char* err, int errlen,
+                     uint8_t* ws, int64_t ws_bytes) {
   int rc = 0;
+  int64_t ws_used = 0;
+  int64_t* pieces = NULL;         /* [k, lo, hi] copy pieces of one step */
+  int64_t pcap = 0;
   const int64_t qbytes = (Q + 7) / 8;
   int64_t* eidx = NULL;           /* dense u*n+v -> edge (n <= 4096) */
   int64_t* order = NULL;          /* ops grouped by step, list order */
@@ -151,16 +162,44 @@ int oracle_replay(int n, int T, int Q, int64_t m, int E, const int32_t* edge_uv,
       if (o[5] >= o[6]) continue;
       if (dst != d) {
         slot_t* sl = map_get(&M, ((uint64_t)dst * n + s) * n + d, 1, qbytes);
-        if (!sl->data) sl->data = (uint8_t*)calloc((size_t)(m > 0 ? m : 1), 1);
+        if (!sl->data) {
+          if (ws) {
+            if (ws_used + m > ws_bytes) {
+              snprintf(err, errlen, "workspace too small (%lld bytes)", (long long)ws_bytes);
+              rc = 1;
+              goto done;
+            }
+            sl->data = ws + ws_used;
+            ws_used += m;
+          } else {
+            sl->data = (uint8_t*)calloc((size_t)(m > 0 ? m : 1), 1);
+          }
+        }
+      }
+    }
+    /* pieces of at most PIECE_BYTES */
+    int64_t np_ = 0;
+    for (int64_t k = a; k < z; ++k) {
+      const int32_t* o = ops + 7 * order[k];
+      if (o[5] >= o[6]) continue;
+      const int64_t lo = (int64_t)(((__int128)o[5] * m) / Q), hi = (int64_t)(((__int128)o[6] * m) / Q);
+      for (int64_t x = lo; x < hi; x += PIECE_BYTES) {
+        if (np_ == pcap) {
+          pcap = pcap ? 2 * pcap : 1024;
+          pieces = (int64_t*)realloc(pieces, sizeof(int64_t) * 3 * (size_t)pcap);
+        }
+        pieces[3 * np_] = k;
+        pieces[3 * np_ + 1] = x;
+        pieces[3 * np_ + 2] = (hi - x < PIECE_BYTES) ? hi : x + PIECE_BYTES;
+        ++np_;
       }
     }
     /* byte movement: every op reads a location it held at the start of the step */
 #pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads)
-    for (int64_t k = a; k < z; ++k) {
-      const int32_t* o = ops + 7 * order[k];
-      int src = o[1], dst = o[2], s = o[3], d = o[4], c0 = o[5], c1 = o[6];
-      if (c0 >= c1) continue;
-      int64_t lo = (int64_t)(((__int128)c0 * m) / Q), hi = (int64_t)(((__int128)c1 * m) / Q);
+    for (int64_t j = 0; j < np_; ++j) {
+      const int32_t* o = ops + 7 * order[pieces[3 * j]];
+      int src = o[1], dst = o[2], s = o[3], d = o[4];
+      const int64_t lo = pieces[3 * j + 1], hi = pieces[3 * j + 2];
       const uint8_t* from;
       if (src == s) from = send + ((int64_t)s * n + d) * m;
       else if (src == d) from = recv + ((int64_t)d * n + s) * m;
@@ -200,9 +239,18 @@ int oracle_replay(int n, int T, int Q, int64_t m, int E, const int32_t* edge_uv,
 done:
   if (M.tab) {
     for (uint64_t i = 0; i < M.cap; ++i)
-      if (M.tab[i].key) { free(M.tab[i].held); free(M.tab[i].data); }
+      if (M.tab[i].key) { free(M.tab[i].held); if (!ws) free(M.tab[i].data); }
     free(M.tab);
   }
-  free(eidx); free(order); free(step_off); free(arrivals); free(lb); free(mark);
+  free(eidx); free(order); free(step_off); free(arrivals); free(lb); free(mark); free(pieces);
   return rc;
+}
+
+int oracle_replay(int n, int T, int Q, int64_t m, int E, const int32_t* edge_uv,
+                  const double* cap, const int32_t* ops, int64_t n_ops,
+                  const uint8_t* send, uint8_t* recv, int nthreads, int copy_self,
+                  double m_model, double b, double sync, double* T_out,
+                  int64_t* link_bytes, char* err, int errlen) {
+  return oracle_replay_ws(n, T, Q, m, E, edge_uv, cap, ops, n_ops, send, recv, nthreads,
+                          copy_self, m_model, b, sync, T_out, link_bytes, err, errlen, NULL, 0);
 }

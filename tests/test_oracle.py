@@ -98,9 +98,37 @@ def test_c_oracle_equals_python_oracle(name, m, artifacts, golden):
     for (t, e), x in lb.items():
         want[t, e] = x
     assert np.array_equal(lbc, want)
+    # reused scratch workspace (the bench's CPU-baseline form), twice into one recv
+    from c_oracle import workspace
+    ws = workspace(a.sched, a.g.n, m)
+    out = np.zeros_like(send)
+    for k in range(2):
+        Tw, _, lbw = replay_bytes_c(a.g, a.sched, make_send(a.g.n, m, seed=6 + k), m,
+                                    nthreads=3, recv=out, ws=ws)
+        assert repr(Tw) == repr(T) and np.array_equal(lbw, want)
+        assert np.array_equal(out, np.swapaxes(make_send(a.g.n, m, seed=6 + k), 0, 1))
     for case in golden["configs"][name].get("corruptions", []):
         s = apply_edit(a.sched, case["edit"])
         if "error" in case["replay"]:
             with pytest.raises(CErr) as ei:
                 replay_bytes_c(a.g, s, send, m, nthreads=2)
             assert str(ei.value) == case["replay"]["error"]
+
+
+def test_c_oracle_workspace_too_small(artifacts):
+    from c_oracle import replay_bytes_c, workspace
+    a = artifacts("gk8_2")
+    m = 64
+    ws = workspace(a.sched, a.g.n, m)
+    with pytest.raises(RuntimeError, match="workspace too small"):
+        replay_bytes_c(a.g, a.sched, make_send(a.g.n, m), m, ws=ws[:len(ws) - m])
+
+
+@pytest.mark.parametrize("m", [(1 << 20) + 3, (3 << 20) + 1])
+def test_c_oracle_multi_piece_ops(m, artifacts):
+    """Ops longer than the 1 MiB copy piece are cut and reassembled exactly."""
+    from c_oracle import replay_bytes_c, workspace
+    a = artifacts("hypercube3")
+    send = make_send(a.g.n, m, seed=9)
+    _, recv, _ = replay_bytes_c(a.g, a.sched, send, m, nthreads=5, ws=workspace(a.sched, a.g.n, m))
+    assert np.array_equal(recv, np.swapaxes(send, 0, 1))
