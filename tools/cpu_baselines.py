@@ -8,8 +8,9 @@ Per frozen config, one core each:
   2. this package's ``executor.replay_timestep_schedule`` (same signature and
      result; validation + modelled T in csrc/a2a_plan.cpp), plan creation
      included;
-  3. the byte-moving restatement (oracle/replay_bytes.c, 1 thread) at m = 1 MiB
-     per pair (N <= 64; GK(256,4) needs 128 GiB of host buffers at 1 MiB).
+  3. the byte-moving restatement (oracle/replay_bytes.c, 1 thread, reused
+     scratch workspace) at m = 1 MiB per pair (N <= 64; GK(256,4) needs 128 GiB
+     of host buffers at 1 MiB).
 Writes a JSON object per config to stdout (and to --out).
 
 Usage: python tools/cpu_baselines.py [--out profiles/r01_cpu_baselines_container.json] [CONFIG ...]
@@ -50,7 +51,7 @@ def main(argv=None):
     import numpy as np
     from make_golden import RE, RG, _find, plain, ref_sched   # imports the read-only reference
 
-    from c_oracle import ops_array, replay_bytes_c
+    from c_oracle import ops_array, replay_bytes_c, workspace
     from paper_2309_13541_b200.artifacts import ARTIFACT_DIR, load_artifact
     from paper_2309_13541_b200.executor import replay_timestep_schedule
 
@@ -82,8 +83,9 @@ def main(argv=None):
             send = np.random.default_rng(0).integers(0, 256, size=(n, n, m), dtype=np.uint8)
             recv = np.zeros_like(send)
             ops = ops_array(art.sched)
+            ws = workspace(art.sched, n, m, ops)
             t_b, k_b, _ = _best(lambda: replay_bytes_c(art.g, art.sched, send, m, nthreads=1,
-                                                       recv=recv, ops=ops), budget_s=3.0)
+                                                       recv=recv, ops=ops, ws=ws), budget_s=3.0)
             rec["bytes_1core"] = {"m": m, "s": t_b, "runs": k_b,
                                   "algbw_gbs": round(n * (n - 1) * m / t_b / 1e9, 3),
                                   "recv_ok": bool(np.array_equal(recv, np.swapaxes(send, 0, 1)))}
