@@ -186,7 +186,13 @@ int oracle_replay_ws(int n, int T, int Q, int64_t m, int E, const int32_t* edge_
       for (int64_t x = lo; x < hi; x += PIECE_BYTES) {
         if (np_ == pcap) {
           pcap = pcap ? 2 * pcap : 1024;
-          pieces = (int64_t*)realloc(pieces, sizeof(int64_t) * 3 * (size_t)pcap);
+          int64_t* grown = (int64_t*)realloc(pieces, sizeof(int64_t) * 3 * (size_t)pcap);
+          if (!grown) {
+            snprintf(err, errlen, "out of host memory");
+            rc = 1;
+            goto done;
+          }
+          pieces = grown;
         }
         pieces[3 * np_] = k;
         pieces[3 * np_ + 1] = x;
