@@ -51,8 +51,9 @@ static slot_t* map_get(map_t* M, uint64_t key, int create, int64_t qbytes) {
     if (s->key == k) return s;
     if (s->key == 0) {
       if (!create) return NULL;
-      s->key = k;
       s->held = (uint8_t*)calloc((size_t)qbytes, 1);
+      if (!s->held) return NULL;   /* out of memory: slot stays empty */
+      s->key = k;
       return s;
     }
     i = (i + 1) & (M->cap - 1);
@@ -63,6 +64,7 @@ static int bit(const uint8_t* b, int64_t c) { return (b[c >> 3] >> (c & 7)) & 1;
 static void setbit(uint8_t* b, int64_t c) { b[c >> 3] |= (uint8_t)(1u << (c & 7)); }
 
 #define FAIL(...) do { snprintf(err, errlen, __VA_ARGS__); rc = 2; goto done; } while (0)
+#define OOM() do { snprintf(err, errlen, "out of host memory"); rc = 1; goto done; } while (0)
 
 #define PIECE_BYTES ((int64_t)1 << 20)
 
@@ -86,10 +88,25 @@ int oracle_replay_ws(int n, int T, int Q, int64_t m, int E, const int32_t* edge_
   map_t M = {0};
   if (n < 1 || n > 4096 || Q < 1) { snprintf(err, errlen, "bad sizes"); return 1; }
   eidx = (int64_t*)malloc(sizeof(int64_t) * (size_t)n * n);
-  for (int64_t i = 0; i < (int64_t)n * n; ++i) eidx[i] = -1;
-  for (int e = 0; e < E; ++e) eidx[(int64_t)edge_uv[2 * e] * n + edge_uv[2 * e + 1]] = e;
   step_off = (int64_t*)calloc((size_t)T + 2, sizeof(int64_t));
   order = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_ops + 1));
+  M.cap = 1024;
+  while (M.cap < (uint64_t)(4 * n_ops + 16)) M.cap <<= 1;
+  M.tab = (slot_t*)calloc((size_t)M.cap, sizeof(slot_t));
+  arrivals = (uint8_t*)calloc((size_t)n * n * Q, 1);
+  lb = (double*)calloc((size_t)(E > 0 ? E : 1), sizeof(double));
+  mark = (uint8_t*)calloc((size_t)(E > 0 ? E : 1), 1);
+  if (!eidx || !step_off || !order || !M.tab || !arrivals || !lb || !mark) OOM();
+  for (int64_t i = 0; i < (int64_t)n * n; ++i) eidx[i] = -1;
+  for (int e = 0; e < E; ++e) {
+    const int32_t u = edge_uv[2 * e], v = edge_uv[2 * e + 1];
+    if (u < 0 || u >= n || v < 0 || v >= n) {
+      snprintf(err, errlen, "edge %d (%d,%d) outside [0, %d)", e, u, v, n);
+      rc = 1;
+      goto done;
+    }
+    eidx[(int64_t)u * n + v] = e;
+  }
   for (int64_t i = 0; i < n_ops; ++i) {
     int t = ops[7 * i];
     if (t >= 0 && t < T) step_off[t + 1]++;
@@ -97,18 +114,13 @@ int oracle_replay_ws(int n, int T, int Q, int64_t m, int E, const int32_t* edge_
   for (int t = 0; t < T; ++t) step_off[t + 1] += step_off[t];
   {
     int64_t* fill = (int64_t*)calloc((size_t)T + 1, sizeof(int64_t));
+    if (!fill) OOM();
     for (int64_t i = 0; i < n_ops; ++i) {
       int t = ops[7 * i];
       if (t >= 0 && t < T) order[step_off[t] + fill[t]++] = i;
     }
     free(fill);
   }
-  M.cap = 1024;
-  while (M.cap < (uint64_t)(4 * n_ops + 16)) M.cap <<= 1;
-  M.tab = (slot_t*)calloc((size_t)M.cap, sizeof(slot_t));
-  arrivals = (uint8_t*)calloc((size_t)n * n * Q, 1);
-  lb = (double*)calloc((size_t)(E > 0 ? E : 1), sizeof(double));
-  mark = (uint8_t*)calloc((size_t)(E > 0 ? E : 1), 1);
   if (link_bytes) memset(link_bytes, 0, sizeof(int64_t) * (size_t)T * E);
   if (copy_self)
     for (int v = 0; v < n; ++v)
@@ -139,6 +151,7 @@ int oracle_replay_ws(int n, int T, int Q, int64_t m, int E, const int32_t* edge_
     double step = 0.0;
     {
       int64_t* touched = (int64_t*)malloc(sizeof(int64_t) * (size_t)(z - a + 1));
+      if (!touched) OOM();
       int64_t nt = 0;
       for (int64_t k = a; k < z; ++k) {
         const int32_t* o = ops + 7 * order[k];
@@ -162,6 +175,7 @@ int oracle_replay_ws(int n, int T, int Q, int64_t m, int E, const int32_t* edge_
       if (o[5] >= o[6]) continue;
       if (dst != d) {
         slot_t* sl = map_get(&M, ((uint64_t)dst * n + s) * n + d, 1, qbytes);
+        if (!sl) OOM();
         if (!sl->data) {
           if (ws) {
             if (ws_used + m > ws_bytes) {
@@ -173,6 +187,7 @@ int oracle_replay_ws(int n, int T, int Q, int64_t m, int E, const int32_t* edge_
             ws_used += m;
           } else {
             sl->data = (uint8_t*)calloc((size_t)(m > 0 ? m : 1), 1);
+            if (!sl->data) OOM();
           }
         }
       }
@@ -223,6 +238,7 @@ int oracle_replay_ws(int n, int T, int Q, int64_t m, int E, const int32_t* edge_
         link_bytes[(int64_t)t * E + eidx[(int64_t)src * n + dst]] +=
             (int64_t)(((__int128)c1 * m) / Q) - (int64_t)(((__int128)c0 * m) / Q);
       slot_t* sl = (dst != s) ? map_get(&M, ((uint64_t)dst * n + s) * n + d, 1, qbytes) : NULL;
+      if (dst != s && !sl) OOM();
       for (int64_t c = c0; c < c1; ++c) {
         if (sl) setbit(sl->held, c);
         if (dst == d) {
