@@ -204,7 +204,7 @@ def run_reference(args, art, m):
         "n_gpus": args.gpus, "steps": len(timed), "warmup": args.warmup,
         "ms_per_step": round(T * 1e3, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": workload_name(args.config, n, m),
+        "config": {"workload": workload_name(args.config, n, m, args.lowering),
                    "m_bytes": m_cpu, "nodes": n, "hop_ops": len(art.sched.instructions),
                    "nsteps": art.sched.nsteps},
         "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": nthreads,
@@ -251,10 +251,31 @@ class Ctx:
             self.pg.destroy_process_group()
 
 
-def workload_name(config, n, m):
+LOWERINGS = {"hop": "hop i of every route at step i",
+             "balanced": "routes delayed to balance each step's cross-GPU egress "
+                         "(lowering.balanced_offsets)"}
+
+
+def workload_name(config, n, m, lowering="hop"):
     """config.workload, identical in both arms (ours and --impl reference)."""
-    return (f"{config}: frozen decomposed-MCF schedule (hop i of every route at step i), "
+    return (f"{config}: frozen decomposed-MCF schedule ({LOWERINGS[lowering]}), "
             f"N={n} virtual nodes, m={m} B per pair")
+
+
+def balanced_artifact(art, m, G, placement):
+    """(artifact lowered with balanced_offsets for this placement, placement
+    list): same routes, links and bytes per link, different steps."""
+    from paper_2309_13541_b200.artifacts import Artifact
+    from paper_2309_13541_b200.executor import Plan
+    from paper_2309_13541_b200.lowering import balanced_offsets, lower_path_to_steps
+    if art.routes is None:
+        raise SystemExit(f"--lowering balanced needs a path-mode artifact; {art.name} is ts")
+    with Plan(art.g, art.sched, m=m, n_gpus=G, placement=placement) as p:
+        gpu = p.placement.tolist()
+    offs = balanced_offsets(art.routes, art.path_sched, gpu, m)
+    sched = lower_path_to_steps(art.routes, art.path_sched, n=art.g.n, offsets=offs)
+    return Artifact(art.name, art.g, sched, art.meta, routes=art.routes,
+                    path_sched=art.path_sched, aug_graph=art.aug_graph), gpu
 
 
 LL_MAX_SHARD = 1 << 20   # autotune tries the LL transport up to this shard size
@@ -631,12 +652,17 @@ def main(argv=None):
     ap.add_argument("--placement", default="optimized", choices=["optimized", "contiguous"])
     ap.add_argument("--schedule", default="auto",
                     help="static | dynamic[:unit_bytes] | auto (time both, keep the faster)")
+    ap.add_argument("--lowering", default="hop", choices=sorted(LOWERINGS),
+                    help="path -> step lowering of a path-mode artifact")
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
 
     from paper_2309_13541_b200.artifacts import load_artifact
     art = load_artifact(args.config)
     m = args.m
+    placement = args.placement
+    if args.lowering == "balanced":
+        art, placement = balanced_artifact(art, m, args.gpus, args.placement)
     if args.impl == "reference":
         return run_reference(args, art, m)
 
@@ -646,10 +672,10 @@ def main(argv=None):
     tune = None
     schedule = args.schedule
     if schedule == "auto":
-        schedule, tune = autotune_schedule(ctx, art, m, placement=args.placement,
+        schedule, tune = autotune_schedule(ctx, art, m, placement=placement,
                                            num_ctas=args.num_ctas)
     r = measure(ctx, art, m, args.steps, args.warmup, num_ctas=args.num_ctas,
-                nccl=not args.no_nccl, e2e=not args.no_e2e, placement=args.placement,
+                nccl=not args.no_nccl, e2e=not args.no_e2e, placement=placement,
                 schedule=schedule)
     G, n = ctx.world, art.g.n
 
@@ -682,7 +708,7 @@ def main(argv=None):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["T"] * 1e3, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u8", "data": "synthetic",
-            "config": {"workload": workload_name(args.config, n, m),
+            "config": {"workload": workload_name(args.config, n, m, args.lowering),
                        "placement": f"{args.placement} {r['placement'] if G > 1 else '(all nodes on GPU 0)'}",
                        "m_bytes": m, "nodes": n, "hop_ops": len(art.sched.instructions),
                        "nsteps": art.sched.nsteps, "Q": art.sched.Q,

@@ -16,8 +16,8 @@ from __future__ import annotations
 
 from .schedule import ChunkedSchedule, Instruction, ScheduleError
 
-__all__ = ["lower_path_to_steps", "collapse_aug_routes", "collapse_aug_schedule",
-           "schedule_link_chunks", "hop_histogram"]
+__all__ = ["lower_path_to_steps", "balanced_offsets", "step_sync_cost", "collapse_aug_routes",
+           "collapse_aug_schedule", "schedule_link_chunks", "hop_histogram"]
 
 
 def _ts_key(i):
@@ -25,17 +25,24 @@ def _ts_key(i):
     return (i.t, i.src, i.dst, i.s, i.d, i.c0)
 
 
-def lower_path_to_steps(routes, sched, n: int | None = None) -> ChunkedSchedule:
+def lower_path_to_steps(routes, sched, n: int | None = None, offsets=None) -> ChunkedSchedule:
     """Expand each route instruction into one hop-op per link, hop i at step i.
 
     ``routes`` is the route list returned by compile_path_schedule (or its
     ``.routes.json`` sidecar); ``sched`` the ``mode="path"`` schedule.
+    ``offsets`` (one per instruction, default 0) delays a whole route: hop i
+    at step offsets[k] + i (e.g. from ``balanced_offsets``).
     """
     if sched.mode != "path":
         raise ScheduleError(f"expected a path-mode schedule, got {sched.mode!r}")
+    if offsets is not None and len(offsets) != len(sched.instructions):
+        raise ScheduleError("one offset per path instruction")
     ops = []
     nsteps = 0
-    for ins in sched.instructions:
+    for k, ins in enumerate(sched.instructions):
+        off = 0 if offsets is None else int(offsets[k])
+        if off < 0:
+            raise ScheduleError(f"negative offset {off}")
         if not 0 <= ins.dst < len(routes):
             raise ScheduleError(f"route id {ins.dst} out of range")
         r = routes[ins.dst]
@@ -46,13 +53,67 @@ def lower_path_to_steps(routes, sched, n: int | None = None) -> ChunkedSchedule:
         if len(nodes) < 2:
             raise ScheduleError(f"route {ins.dst} has no hops")
         for i in range(len(nodes) - 1):
-            ops.append(Instruction(t=i, src=nodes[i], dst=nodes[i + 1],
+            ops.append(Instruction(t=off + i, src=nodes[i], dst=nodes[i + 1],
                                    s=ins.s, d=ins.d, c0=ins.c0, c1=ins.c1))
-        nsteps = max(nsteps, len(nodes) - 1)
+        nsteps = max(nsteps, off + len(nodes) - 1)
     ops.sort(key=_ts_key)
     return ChunkedSchedule(n=sched.n if n is None else n, nsteps=nsteps,
                            chunk_bytes=sched.chunk_bytes, Q=sched.Q, mode="ts",
                            instructions=ops)
+
+
+def _route_egress(routes, ins, node_gpu, m, Q):
+    """[(hop i, source GPU, cross-GPU bytes)] of one path instruction."""
+    nodes = routes[ins.dst]["nodes"]
+    nb = (ins.c1 * m) // Q - (ins.c0 * m) // Q
+    return [(i, node_gpu[nodes[i]], nb) for i in range(len(nodes) - 1)
+            if node_gpu[nodes[i]] != node_gpu[nodes[i + 1]]]
+
+
+def step_sync_cost(sched, node_gpu, m: int) -> int:
+    """Sum over steps of the busiest GPU's cross-GPU egress bytes in that step:
+    the time (x NVLink bandwidth) of a ts schedule executed step-synchronously."""
+    G = max(node_gpu) + 1
+    load = [[0] * G for _ in range(sched.nsteps)]
+    for i in sched.instructions:
+        if 0 <= i.t < sched.nsteps and node_gpu[i.src] != node_gpu[i.dst]:
+            load[i.t][node_gpu[i.src]] += (i.c1 * m) // sched.Q - (i.c0 * m) // sched.Q
+    return sum(max(x) for x in load)
+
+
+def balanced_offsets(routes, sched, node_gpu, m: int, extra_steps: int = 0) -> list:
+    """Per-route start steps for ``lower_path_to_steps`` that balance each
+    step's cross-GPU egress over the GPUs of a placement.
+
+    Hop-indexed lowering puts every route's first hop at step 0, so step 0 is
+    the heaviest and the last step nearly empty; a step-synchronous execution
+    pays sum_t max_g egress(t, g).  Greedy: routes by cross-GPU bytes x hops,
+    largest first, each at the offset in [0, L - hops] (L = longest route +
+    extra_steps) that minimises that sum so far (ties: earliest).  Hop order
+    within a route, the links and the bytes per link are unchanged; only steps
+    move.  The objective is step_sync_cost of the lowered schedule."""
+    if sched.mode != "path":
+        raise ScheduleError(f"expected a path-mode schedule, got {sched.mode!r}")
+    G = max(node_gpu) + 1
+    hops = [len(routes[i.dst]["nodes"]) - 1 for i in sched.instructions]
+    L = max(hops, default=0) + int(extra_steps)
+    load = [[0] * G for _ in range(L)]
+    eg = [_route_egress(routes, i, node_gpu, m, sched.Q) for i in sched.instructions]
+    order = sorted(range(len(eg)), key=lambda k: (-sum(b for *_, b in eg[k]) * hops[k], k))
+    offs = [0] * len(eg)
+    for k in order:
+        best = None
+        for o in range(L - hops[k] + 1):
+            delta = 0
+            for i, g, b in eg[k]:
+                row = load[o + i]
+                delta += max(0, row[g] + b - max(row))
+            if best is None or delta < best[0]:
+                best = (delta, o)
+        offs[k] = best[1]
+        for i, g, b in eg[k]:
+            load[offs[k] + i][g] += b
+    return offs
 
 
 def _phys_of(mapping):

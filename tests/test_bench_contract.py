@@ -66,3 +66,24 @@ def test_bound_terms():
     # 2 GPUs: 32 nodes each; local hops dominate, the HBM term exceeds the NVLink term
     assert bt["nvlink_bytes"] == max(max(i["egress_bytes"], i["ingress_bytes"]) for i in infos)
     assert bt["t_hbm"] > bt["t_lb"] and bt["t_both"] == bt["t_hbm"]
+
+
+def test_balanced_lowering_option():
+    """--lowering balanced: the artifact is re-lowered for the placement of
+    --gpus (same ops up to their steps), the workload says so, and the
+    reference arm replays that schedule bit-exact."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2309_13541_b200.artifacts import load_artifact
+    a = load_artifact("gk8_2")
+    b, gpu = bench.balanced_artifact(a, 1 << 20, 8, "optimized")
+    assert sorted(gpu) == list(range(8))
+    key = lambda i: (i.src, i.dst, i.s, i.d, i.c0, i.c1)  # noqa: E731
+    assert sorted(map(key, b.sched.instructions)) == sorted(map(key, a.sched.instructions))
+    assert [i.t for i in b.sched.instructions] != [i.t for i in a.sched.instructions]
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                          "--gpus", "8", "--lowering", "balanced", "--m", "4099", "--steps", "2"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
+    assert "balance" in d["config"]["workload"] and d["cpu_baseline"]["recv_ok"] is True
