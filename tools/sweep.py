@@ -47,6 +47,8 @@ def main(argv=None):
     ap.add_argument("--num-ctas", type=int, default=0)
     ap.add_argument("--schedule", default=None,
                     help="static | dynamic[:bytes] | auto; default: $A2A_SCHED or static")
+    ap.add_argument("--lowering", default="hop", choices=["hop", "balanced"],
+                    help="path -> step lowering (bench.balanced_artifact for 'balanced')")
     a = ap.parse_args(argv)
     if a.placement not in ("optimized", "contiguous"):
         a.placement = [int(x) for x in a.placement.split(",")]
@@ -68,7 +70,11 @@ def main(argv=None):
             rec["skipped"] = "artifact not generated"
         else:
             art = load_artifact(name)
-            with Plan(art.g, art.sched, m=m, n_gpus=ctx.world, placement=a.placement) as p:
+            placement = a.placement
+            if a.lowering == "balanced" and art.routes is not None:
+                art, placement = bench.balanced_artifact(art, m, ctx.world, a.placement)
+            rec["lowering"] = a.lowering if art.routes is not None else "ts artifact"
+            with Plan(art.g, art.sched, m=m, n_gpus=ctx.world, placement=placement) as p:
                 mem = max(p.gpu_info(g)["send_bytes"] * 2 + p.gpu_info(g)["scratch_bytes"]
                           for g in range(ctx.world))
             if mem > a.mem_limit_gib * 2 ** 30:
@@ -78,10 +84,10 @@ def main(argv=None):
                 sched = case_sched or a.schedule or os.environ.get("A2A_SCHED") or "static"
                 tune = None
                 if sched == "auto":
-                    sched, tune = bench.autotune_schedule(ctx, art, m, placement=a.placement,
+                    sched, tune = bench.autotune_schedule(ctx, art, m, placement=placement,
                                                           num_ctas=a.num_ctas)
                 r = bench.measure(ctx, art, m, a.steps, a.warmup, nccl=not a.no_nccl,
-                                  e2e=False, clocks=os.environ.get("A2A_NO_CLOCKS") != "1", placement=a.placement, schedule=sched,
+                                  e2e=False, clocks=os.environ.get("A2A_NO_CLOCKS") != "1", placement=placement, schedule=sched,
                                   num_ctas=a.num_ctas)
                 rec["schedule"] = sched
                 rec["schedule_autotune_ms"] = tune
