@@ -69,11 +69,13 @@ MEASURED = {
 }
 
 
-def model(name, m, G, sched, num_ctas=148, **params):
+def model(name, m, G, sched, num_ctas=148, lowering="hop", **params):
     import bench
     from paper_2309_13541_b200.artifacts import load_artifact
-    art = load_artifact(name)
-    with bench.make_plan(art, m, G, "optimized", sched) as p:
+    art, placement = load_artifact(name), "optimized"
+    if lowering == "balanced":
+        art, placement = bench.balanced_artifact(art, m, G, placement)
+    with bench.make_plan(art, m, G, placement, sched) as p:
         return p.simulate(num_ctas, **params) * 1e3
 
 
@@ -113,7 +115,8 @@ def main(argv=None):
         for name, m in (("gk8_2", 16 << 20), ("hypercube3", 16 << 20), ("torus4x4x4", 4 << 20)):
             for sched in ("static", "mix:1048576", "cp:1048576", "spread:1048576", "cp:1048576:64",
                           "ready:1048576"):
-                print(f"predict {name} G=8 {sched:16s} {model(name, m, 8, sched, **params):8.4f} ms",
+                print(f"predict {name} G=8 {sched:16s} {model(name, m, 8, sched, **params):8.4f} ms"
+                      f"   balanced lowering {model(name, m, 8, sched, lowering='balanced', **params):8.4f} ms",
                       flush=True)
 
 
