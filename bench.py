@@ -204,7 +204,8 @@ def run_reference(args, art, m):
         "n_gpus": args.gpus, "steps": len(timed), "warmup": args.warmup,
         "ms_per_step": round(T * 1e3, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": workload_name(args.config, n, m, args.lowering),
+        "config": {"workload": workload_name(args.config, n, m),
+                   "lowering": LOWERINGS["balanced" if args.lowering == "balanced" else "hop"],
                    "m_bytes": m_cpu, "nodes": n, "hop_ops": len(art.sched.instructions),
                    "nsteps": art.sched.nsteps},
         "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": nthreads,
@@ -256,10 +257,11 @@ LOWERINGS = {"hop": "hop i of every route at step i",
                          "(lowering.balanced_offsets)"}
 
 
-def workload_name(config, n, m, lowering="hop"):
-    """config.workload, identical in both arms (ours and --impl reference)."""
-    return (f"{config}: frozen decomposed-MCF schedule ({LOWERINGS[lowering]}), "
-            f"N={n} virtual nodes, m={m} B per pair")
+def workload_name(config, n, m):
+    """config.workload, identical in both arms (ours and --impl reference); the
+    path -> step lowering of the run is config.lowering."""
+    return (f"{config}: frozen decomposed-MCF schedule (routes, chunks and per-link bytes of the "
+            f"reference pipeline), N={n} virtual nodes, m={m} B per pair")
 
 
 def balanced_artifact(art, m, G, placement):
@@ -652,8 +654,9 @@ def main(argv=None):
     ap.add_argument("--placement", default="optimized", choices=["optimized", "contiguous"])
     ap.add_argument("--schedule", default="auto",
                     help="static | dynamic[:unit_bytes] | auto (time both, keep the faster)")
-    ap.add_argument("--lowering", default="hop", choices=sorted(LOWERINGS),
-                    help="path -> step lowering of a path-mode artifact")
+    ap.add_argument("--lowering", default="auto", choices=["auto"] + sorted(LOWERINGS),
+                    help="path -> step lowering of a path-mode artifact; auto = hop, and at >= 4 "
+                         "GPUs with --schedule auto the autotune also times the balanced lowering")
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
 
@@ -671,9 +674,19 @@ def main(argv=None):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ctx.world}")
     tune = None
     schedule = args.schedule
+    lowering = "balanced" if args.lowering == "balanced" else "hop"
     if schedule == "auto":
         schedule, tune = autotune_schedule(ctx, art, m, placement=placement,
                                            num_ctas=args.num_ctas)
+        if args.lowering == "auto" and ctx.world >= 4 and art.routes is not None:
+            # same routes, links and bytes, steps re-balanced over the GPUs
+            # (lowering.balanced_offsets); times are max over ranks, so every
+            # rank takes the same decision
+            bart, bpl = balanced_artifact(art, m, ctx.world, args.placement)
+            bsched, btune = autotune_schedule(ctx, bart, m, placement=bpl, num_ctas=args.num_ctas)
+            tune = {"hop": tune, "balanced": btune}
+            if btune[bsched] < tune["hop"][schedule]:
+                art, placement, schedule, lowering = bart, bpl, bsched, "balanced"
     r = measure(ctx, art, m, args.steps, args.warmup, num_ctas=args.num_ctas,
                 nccl=not args.no_nccl, e2e=not args.no_e2e, placement=placement,
                 schedule=schedule)
@@ -708,7 +721,8 @@ def main(argv=None):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["T"] * 1e3, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u8", "data": "synthetic",
-            "config": {"workload": workload_name(args.config, n, m, args.lowering),
+            "config": {"workload": workload_name(args.config, n, m),
+                       "lowering": LOWERINGS[lowering],
                        "placement": f"{args.placement} {r['placement'] if G > 1 else '(all nodes on GPU 0)'}",
                        "m_bytes": m, "nodes": n, "hop_ops": len(art.sched.instructions),
                        "nsteps": art.sched.nsteps, "Q": art.sched.Q,

@@ -63,21 +63,26 @@ def lower_path_to_steps(routes, sched, n: int | None = None, offsets=None) -> Ch
 
 
 def _route_egress(routes, ins, node_gpu, m, Q):
-    """[(hop i, source GPU, cross-GPU bytes)] of one path instruction."""
+    """[(hop i, source GPU, destination GPU, bytes)] of the cross-GPU hops of
+    one path instruction."""
     nodes = routes[ins.dst]["nodes"]
     nb = (ins.c1 * m) // Q - (ins.c0 * m) // Q
-    return [(i, node_gpu[nodes[i]], nb) for i in range(len(nodes) - 1)
+    return [(i, node_gpu[nodes[i]], node_gpu[nodes[i + 1]], nb) for i in range(len(nodes) - 1)
             if node_gpu[nodes[i]] != node_gpu[nodes[i + 1]]]
 
 
 def step_sync_cost(sched, node_gpu, m: int) -> int:
-    """Sum over steps of the busiest GPU's cross-GPU egress bytes in that step:
-    the time (x NVLink bandwidth) of a ts schedule executed step-synchronously."""
+    """Sum over steps of the busiest NVLink direction in that step (max over
+    GPUs of cross-GPU egress and ingress bytes): the time (x NVLink bandwidth
+    per direction) of a ts schedule executed step-synchronously."""
     G = max(node_gpu) + 1
-    load = [[0] * G for _ in range(sched.nsteps)]
+    load = [[0] * (2 * G) for _ in range(sched.nsteps)]
     for i in sched.instructions:
-        if 0 <= i.t < sched.nsteps and node_gpu[i.src] != node_gpu[i.dst]:
-            load[i.t][node_gpu[i.src]] += (i.c1 * m) // sched.Q - (i.c0 * m) // sched.Q
+        g, h = node_gpu[i.src], node_gpu[i.dst]
+        if 0 <= i.t < sched.nsteps and g != h:
+            nb = (i.c1 * m) // sched.Q - (i.c0 * m) // sched.Q
+            load[i.t][g] += nb
+            load[i.t][G + h] += nb
     return sum(max(x) for x in load)
 
 
@@ -89,30 +94,36 @@ def balanced_offsets(routes, sched, node_gpu, m: int, extra_steps: int = 0) -> l
     the heaviest and the last step nearly empty; a step-synchronous execution
     pays sum_t max_g egress(t, g).  Greedy: routes by cross-GPU bytes x hops,
     largest first, each at the offset in [0, L - hops] (L = longest route +
-    extra_steps) that minimises that sum so far (ties: earliest).  Hop order
-    within a route, the links and the bytes per link are unchanged; only steps
-    move.  The objective is step_sync_cost of the lowered schedule."""
+    extra_steps) that minimises that sum so far (ties: earliest).  Egress and
+    ingress both count (each step costs its busiest NVLink direction).  Hop
+    order within a route, the links and the bytes per link are unchanged; only
+    steps move.  The objective is step_sync_cost of the lowered schedule."""
     if sched.mode != "path":
         raise ScheduleError(f"expected a path-mode schedule, got {sched.mode!r}")
     G = max(node_gpu) + 1
     hops = [len(routes[i.dst]["nodes"]) - 1 for i in sched.instructions]
     L = max(hops, default=0) + int(extra_steps)
-    load = [[0] * G for _ in range(L)]
+    load = [[0] * (2 * G) for _ in range(L)]
     eg = [_route_egress(routes, i, node_gpu, m, sched.Q) for i in sched.instructions]
-    order = sorted(range(len(eg)), key=lambda k: (-sum(b for *_, b in eg[k]) * hops[k], k))
+    order = sorted(range(len(eg)), key=lambda k: (-sum(x[3] for x in eg[k]) * hops[k], k))
     offs = [0] * len(eg)
     for k in order:
         best = None
         for o in range(L - hops[k] + 1):
+            add: dict = {}
+            for i, g, h, b in eg[k]:
+                add[(o + i, g)] = add.get((o + i, g), 0) + b
+                add[(o + i, G + h)] = add.get((o + i, G + h), 0) + b
             delta = 0
-            for i, g, b in eg[k]:
-                row = load[o + i]
-                delta += max(0, row[g] + b - max(row))
+            for t in {t for t, _ in add}:
+                row = load[t]
+                delta += max(0, max(row[c] + b for (tt, c), b in add.items() if tt == t) - max(row))
             if best is None or delta < best[0]:
                 best = (delta, o)
         offs[k] = best[1]
-        for i, g, b in eg[k]:
+        for i, g, h, b in eg[k]:
             load[offs[k] + i][g] += b
+            load[offs[k] + i][G + h] += b
     return offs
 
 

@@ -86,4 +86,4 @@ def test_balanced_lowering_option():
                          capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     d = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
-    assert "balance" in d["config"]["workload"] and d["cpu_baseline"]["recv_ok"] is True
+    assert "balance" in d["config"]["lowering"] and d["cpu_baseline"]["recv_ok"] is True
