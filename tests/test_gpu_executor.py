@@ -329,3 +329,33 @@ def test_ll_protocol_n64(name, m, artifacts):
             p.execute(s, r)
             p.sync()
             assert torch.equal(r, s.transpose(0, 1).contiguous())
+
+
+@pytest.mark.parametrize("name,G", [("gk8_2", 4), ("gk8_2", 8), ("hypercube3", 8), ("torus4x4x4", 8)])
+@pytest.mark.parametrize("mode", ["static", "mix", "cp", "ready"])
+def test_balanced_lowering_one_gpu(name, G, mode, artifacts):
+    """The step-balanced lowering (bench.py autotune at >= 4 GPUs) of a
+    G-GPU placement, run with every node on one GPU: bit-exact vs the oracle
+    replaying the same lowered schedule, link counters exact."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    from paper_2309_13541_b200.executor import Plan
+    from replay_bytes import replay_bytes
+    a = artifacts(name)
+    m = 4096 + 5 if a.g.n == 8 else 1024
+    b, _ = bench.balanced_artifact(a, 16 << 20, G, "optimized")
+    with Plan(b.g, b.sched, m=m) as p:
+        if mode != "static":
+            p.set_schedule(mode, 1024)
+        p.bind(0)
+        for rep in range(2):
+            send = _send(b.g.n, m, seed=rep + G)
+            _, want, _ = replay_bytes(b.g, b.sched, send, m)
+            s = torch.from_numpy(send).cuda()
+            r = torch.zeros_like(s)
+            p.execute(s, r, count_links=True)
+            p.sync()
+            assert np.array_equal(r.cpu().numpy(), want), rep
+        assert np.array_equal(p.read_link_counters(), 2 * p.link_bytes())

@@ -46,7 +46,7 @@ def _port():
 
 
 def _rank_main(rank, world, port, name, m, reps, q, engine="lsu", sched="static", reuse=False,
-               proto="simple", graph=False):
+               proto="simple", graph=False, lowering="hop"):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     try:
@@ -61,7 +61,12 @@ def _rank_main(rank, world, port, name, m, reps, q, engine="lsu", sched="static"
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}",
                                 rank=rank, world_size=world)
         a = load_artifact(name)
-        plan = Plan(a.g, a.sched, m=m, n_gpus=world, reuse_scratch=reuse, placement="optimized",
+        placement = "optimized"
+        if lowering == "balanced":            # bench.py's step-balanced lowering
+            sys.path.insert(0, ROOT)
+            import bench
+            a, placement = bench.balanced_artifact(a, m, world, "optimized")
+        plan = Plan(a.g, a.sched, m=m, n_gpus=world, reuse_scratch=reuse, placement=placement,
                     protocol=proto)
         plan.set_engine(engine)
         plan.set_schedule_spec(sched)      # "<mode>[:<unit bytes>[:<pinned NVLink CTAs>]]"
@@ -285,6 +290,32 @@ def test_multiprocess_dynamic(world, engine, reuse, name, m, mode):
     port = _port()
     ps = [ctx.Process(target=_rank_main,
                       args=(r, world, port, name, m, 3, q, engine, mode, reuse))
+          for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=300) for _ in ps]
+    _reap(ps)
+    for r in sorted(res, key=lambda x: x[0]):
+        assert len(r) == 3, r
+        assert r[1], f"rank {r[0]}: recv mismatch"
+        assert r[2], f"rank {r[0]}: link counters differ from schedule"
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("name,m", [("gk8_2", 65536 + 64), ("hypercube3", 4099)])
+@pytest.mark.parametrize("mode", ["static", "mix:4096", "cp:4096:64", "spread:4096", "ready:4096"])
+def test_multiprocess_balanced_lowering(world, name, m, mode):
+    """The step-balanced lowering bench.py's autotune tries at >= 4 GPUs:
+    bit-exact recv and exact link counters across processes."""
+    if _ngpu() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_rank_main,
+                      args=(r, world, port, name, m, 2, q, "tma", mode, False, "simple", False,
+                            "balanced"))
           for r in range(world)]
     for p in ps:
         p.start()
