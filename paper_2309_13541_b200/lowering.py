@@ -86,7 +86,8 @@ def step_sync_cost(sched, node_gpu, m: int) -> int:
     return sum(max(x) for x in load)
 
 
-def balanced_offsets(routes, sched, node_gpu, m: int, extra_steps: int = 0) -> list:
+def balanced_offsets(routes, sched, node_gpu, m: int, extra_steps: int = 0,
+                     passes: int = 4) -> list:
     """Per-route start steps for ``lower_path_to_steps`` that balance each
     step's cross-GPU egress over the GPUs of a placement.
 
@@ -97,7 +98,8 @@ def balanced_offsets(routes, sched, node_gpu, m: int, extra_steps: int = 0) -> l
     extra_steps) that minimises that sum so far (ties: earliest).  Egress and
     ingress both count (each step costs its busiest NVLink direction).  Hop
     order within a route, the links and the bytes per link are unchanged; only
-    steps move.  The objective is step_sync_cost of the lowered schedule."""
+    steps move; ``passes`` rounds of single-route moves then lower the sum
+    further.  The objective is step_sync_cost of the lowered schedule."""
     if sched.mode != "path":
         raise ScheduleError(f"expected a path-mode schedule, got {sched.mode!r}")
     G = max(node_gpu) + 1
@@ -107,7 +109,13 @@ def balanced_offsets(routes, sched, node_gpu, m: int, extra_steps: int = 0) -> l
     eg = [_route_egress(routes, i, node_gpu, m, sched.Q) for i in sched.instructions]
     order = sorted(range(len(eg)), key=lambda k: (-sum(x[3] for x in eg[k]) * hops[k], k))
     offs = [0] * len(eg)
-    for k in order:
+
+    def place(k, o, sign):
+        for i, g, h, b in eg[k]:
+            load[o + i][g] += sign * b
+            load[o + i][G + h] += sign * b
+
+    def best_offset(k):
         best = None
         for o in range(L - hops[k] + 1):
             add: dict = {}
@@ -120,10 +128,30 @@ def balanced_offsets(routes, sched, node_gpu, m: int, extra_steps: int = 0) -> l
                 delta += max(0, max(row[c] + b for (tt, c), b in add.items() if tt == t) - max(row))
             if best is None or delta < best[0]:
                 best = (delta, o)
-        offs[k] = best[1]
-        for i, g, h, b in eg[k]:
-            load[offs[k] + i][g] += b
-            load[offs[k] + i][G + h] += b
+        return best[1]
+
+    for k in order:
+        offs[k] = best_offset(k)
+        place(k, offs[k], 1)
+    # improvement passes: take each route out and put it back at its best
+    # offset given all the others; keep a move only if the total drops
+    total = sum(max(r) for r in load)
+    for _ in range(int(passes)):
+        moved = False
+        for k in order:
+            if not eg[k]:
+                continue
+            place(k, offs[k], -1)
+            o = best_offset(k)
+            place(k, o, 1)
+            t = sum(max(r) for r in load)
+            if t < total:
+                offs[k], total, moved = o, t, True
+            else:
+                place(k, o, -1)
+                place(k, offs[k], 1)
+        if not moved:
+            break
     return offs
 
 
