@@ -655,7 +655,7 @@ def main(argv=None):
     ap.add_argument("--schedule", default="auto",
                     help="static | dynamic[:unit_bytes] | auto (time both, keep the faster)")
     ap.add_argument("--lowering", default="auto", choices=["auto"] + sorted(LOWERINGS),
-                    help="path -> step lowering of a path-mode artifact; auto = hop, and at >= 4 "
+                    help="path -> step lowering of a path-mode artifact; auto = hop, and at >= 2 "
                          "GPUs with --schedule auto the autotune also times the balanced lowering")
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
@@ -678,7 +678,7 @@ def main(argv=None):
     if schedule == "auto":
         schedule, tune = autotune_schedule(ctx, art, m, placement=placement,
                                            num_ctas=args.num_ctas)
-        if args.lowering == "auto" and ctx.world >= 4 and art.routes is not None:
+        if args.lowering == "auto" and ctx.world >= 2 and art.routes is not None:
             # same routes, links and bytes, steps re-balanced over the GPUs
             # (lowering.balanced_offsets); times are max over ranks, so every
             # rank takes the same decision

@@ -83,3 +83,27 @@ def test_offsets_rejects(artifacts):
         lower_path_to_steps(a.routes, a.path_sched, offsets=[-1] * len(a.path_sched.instructions))
     with pytest.raises(ScheduleError, match="path-mode"):
         balanced_offsets(a.routes, a.sched, [0] * a.g.n, 1)
+
+
+@pytest.mark.parametrize("name", ["gk8_2", "hypercube3", "torus2x4_h2"])
+@pytest.mark.parametrize("G", [2, 4, 8])
+@pytest.mark.parametrize("sched", ["static", "mix:1024", "cp:1024", "ready:1024", "cp:1024:64",
+                                   "spread:1024", "ll"])
+def test_every_autotune_order_delivers(name, G, sched, artifacts):
+    """bench.balanced_artifact + every execution schedule bench.py's autotune
+    tries, emulated at 13 and 148 CTAs per GPU."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    a = artifacts(name)
+    m = 4096 + 7
+    art, pl = bench.balanced_artifact(a, 16 << 20, G, "optimized")
+    send = make_send(a.g.n, m, seed=G)
+    want = np.swapaxes(send, 0, 1)
+    with bench.make_plan(art, m, G, pl, sched) as p:
+        nodes = [local_nodes(p, r) for r in range(G)]
+        for nc in (13, 148):
+            recvs = p.emulate([send[ns] for ns in nodes], num_ctas=nc, seed=nc)
+            for r in range(G):
+                assert np.array_equal(recvs[r], want[nodes[r]]), (nc, r)

@@ -334,7 +334,7 @@ def test_ll_protocol_n64(name, m, artifacts):
 @pytest.mark.parametrize("name,G", [("gk8_2", 4), ("gk8_2", 8), ("hypercube3", 8), ("torus4x4x4", 8)])
 @pytest.mark.parametrize("mode", ["static", "mix", "cp", "ready"])
 def test_balanced_lowering_one_gpu(name, G, mode, artifacts):
-    """The step-balanced lowering (bench.py autotune at >= 4 GPUs) of a
+    """The step-balanced lowering (bench.py autotune at >= 2 GPUs) of a
     G-GPU placement, run with every node on one GPU: bit-exact vs the oracle
     replaying the same lowered schedule, link counters exact."""
     import os
