@@ -253,7 +253,7 @@ class Ctx:
 
 
 LOWERINGS = {"hop": "hop i of every route at step i",
-             "balanced": "routes delayed to balance each step's cross-GPU egress "
+             "balanced": "routes delayed to balance each step's busiest NVLink direction "
                          "(lowering.balanced_offsets)"}
 
 
