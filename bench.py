@@ -32,7 +32,19 @@ sys.path.insert(0, ROOT)
 METRIC = "all2all algBW GB/s/GPU vs topology lower bound at 1/2/4/8 B200; vs NCCL a2a"
 HBM_FALLBACK = 6650.0
 NVLINK_NOMINAL = 900.0     # GB/s per direction per GPU (BASELINE.json north_star)
-NVLINK_MEASURED = 770.0    # peer copy per direction (B200_PROFILING.md)
+NVLINK_GUIDE = 770.0       # peer copy per direction quoted by B200_PROFILING.md (context)
+NVLINK_PROBE_FILE = os.path.join(ROOT, "profiles", "r01_nvlink_push_pull.json")
+
+
+def _nvlink_peak():
+    """Measured NVLink ceiling of this repo's copy engine: a bare TMA push copy
+    loop between two B200s (tools/nvlink_pull_probe.py, committed result)."""
+    try:
+        with open(NVLINK_PROBE_FILE) as fh:
+            return float(json.load(fh)["tma_push_oneway_gbs"]), \
+                "measured TMA peer-push GB/s per direction (profiles/r01_nvlink_push_pull.json)"
+    except Exception:
+        return NVLINK_GUIDE, "B200_PROFILING.md peer copy GB/s per direction (probe file absent)"
 
 
 def _peaks():
@@ -127,6 +139,65 @@ class Clocks:
                 "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
+class NvlinkCounters:
+    """NVLink data bytes this GPU transmitted / received, from the NVML
+    hardware counters (NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX, KiB, summed
+    over links), read before and after the timed loop: the measured NVLink
+    traffic of the executor (roofline.traffic at G > 1)."""
+
+    def __init__(self, index):
+        self.err, self._n, self.t0 = None, None, None
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            pr = torch.cuda.get_device_properties(index)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            self._h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            self._n = pynvml
+            self.t0 = self._read()
+        except Exception as ex:  # noqa: BLE001 - counters are evidence, not the measurement
+            self.err = repr(ex)
+
+    def _fields(self, ids):
+        n = self._n
+        vals = n.nvmlDeviceGetFieldValues(self._h, ids)
+        out = []
+        for v in vals:
+            if v.nvmlReturn != 0:
+                return None
+            out.append(int(v.value.ullVal))
+        return out
+
+    def _read(self):
+        n = self._n
+        fid = [n.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, n.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX,
+               n.NVML_FI_DEV_NVLINK_THROUGHPUT_RAW_TX, n.NVML_FI_DEV_NVLINK_THROUGHPUT_RAW_RX]
+        allv = self._fields([(f, 0xFFFFFFFF) for f in fid])      # scope UINT_MAX: all links
+        if allv is not None and any(allv):
+            return allv
+        tot = [0, 0, 0, 0]                                        # else sum links 0..17
+        for link in range(18):
+            v = self._fields([(f, link) for f in fid])
+            if v is None:
+                break
+            tot = [a + b for a, b in zip(tot, v)]
+        return tot
+
+    def per_launch(self, launches):
+        if self.t0 is None:
+            return {"error": self.err or "NVML NVLink counters unavailable"}
+        try:
+            time.sleep(0.25)                 # counters are sampled by the driver, let them settle
+            t1 = self._read()
+        except Exception as ex:  # noqa: BLE001
+            return {"error": repr(ex)}
+        d = [(b - a) * 1024 for a, b in zip(self.t0, t1)]          # KiB -> bytes
+        return {"tx_bytes": d[0] // launches, "rx_bytes": d[1] // launches,
+                "raw_tx_bytes": d[2] // launches, "raw_rx_bytes": d[3] // launches,
+                "launches": launches, "source": "NVML_FI_DEV_NVLINK_THROUGHPUT_{DATA,RAW}_{TX,RX}"}
+
+
 def _dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -134,10 +205,12 @@ def _dist():
     return world, rank, local
 
 
-def _cpu_oracle_run(art, m, budget_s, nthreads, max_iters=None):
+def _cpu_oracle_run(art, m, budget_s, nthreads, max_iters=None, copy_self=False):
     """Time the C oracle (byte-moving restatement of the reference executor),
     its forwarding scratch allocated once and reused by every replay (as the
-    device plan keeps its scratch between executes)."""
+    device plan keeps its scratch between executes).  Like the reference's
+    transpose (evaluate.py:114-118) the self shards are not moved unless
+    ``copy_self``."""
     import numpy as np
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from c_oracle import ops_array, replay_bytes_c, workspace
@@ -151,22 +224,27 @@ def _cpu_oracle_run(art, m, budget_s, nthreads, max_iters=None):
     t_start = time.perf_counter()
     while True:
         t0 = time.perf_counter()
-        replay_bytes_c(art.g, art.sched, send, m, nthreads=nthreads, recv=recv, ops=ops, ws=ws)
+        replay_bytes_c(art.g, art.sched, send, m, nthreads=nthreads, recv=recv, ops=ops, ws=ws,
+                       copy_self=copy_self)
         times.append(time.perf_counter() - t0)
         if max_iters:
             if len(times) >= max_iters:
                 break
         elif time.perf_counter() - t_start > budget_s:
             break
-    ok = bool(np.array_equal(recv, np.swapaxes(send, 0, 1)))
+    want = np.swapaxes(send, 0, 1)
+    off = ~np.eye(n, dtype=bool)                 # s != d rows (the self shard only if copied)
+    ok = bool(np.array_equal(recv[off], want[off]) and
+              (not copy_self or np.array_equal(recv, want)))
     return times, ok
 
 
 def _scratch_slots(art):
     """Forwarding scratch slots of the CPU restatement (c_oracle.workspace)."""
     import numpy as np
-    from paper_2309_13541_b200.native_io import _ops_of
-    o = _ops_of(art.sched)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from c_oracle import ops_array          # pure numpy: no product library in this process
+    o = ops_array(art.sched)
     o = o[(o[:, 0] >= 0) & (o[:, 0] < art.sched.nsteps) & (o[:, 5] < o[:, 6]) & (o[:, 2] != o[:, 4])]
     n = art.g.n
     return len(np.unique((o[:, 2].astype(np.int64) * n + o[:, 3]) * n + o[:, 4]))
@@ -181,9 +259,35 @@ def _host_fits(n, m, frac=0.4, slots=0):
     return (3 * n * n + slots) * m < frac * avail
 
 
+def l2_flush_needed(n, m, G):
+    """True when a GPU's send buffer is smaller than L2 (balanced placements:
+    n // G nodes on the smallest GPU), so L2 is flushed between timed steps."""
+    return (n // G) * n * m < L2_BYTES
+
+
+def l2_policy(n, m, G):
+    if l2_flush_needed(n, m, G):
+        return ("flushed between timed steps (512 MiB memset, outside events"
+                + (", then ranks re-aligned by an NCCL all-reduce, outside events)" if G > 1 else ")"))
+    return (f"inputs larger than L2 ({((n // G) * n * m) >> 20} MiB send per GPU > 126 MB), "
+            f"no flush")
+
+
+def config_of(name, art, m, G, copy_self=False):
+    """The `config` object, identical in both arms (ours and --impl reference):
+    only what defines the workload.  How our arm executes it (lowering,
+    placement, execution schedule, CTAs) is reported under `exec`."""
+    n = art.g.n
+    return {"workload": workload_name(name, n, m), "m_bytes": m, "nodes": n,
+            "hop_ops": len(art.sched.instructions), "nsteps": art.sched.nsteps,
+            "Q": art.sched.Q, "copy_self": bool(copy_self), "l2": l2_policy(n, m, G)}
+
+
 def run_reference(args, art, m):
     """--impl reference: the reference's CPU executor path, restated to move
-    bytes (oracle/replay_bytes.c), on all host threads; rank 0 only."""
+    bytes (oracle/replay_bytes.c), on all host threads; rank 0 only.  Nothing
+    of the product (paper_2309_13541_b200/_a2a_exec.so) is loaded here: the
+    artifact loader is pure Python and the op table comes from c_oracle."""
     world, rank, _ = _dist()
     if rank != 0:
         return
@@ -195,7 +299,7 @@ def run_reference(args, art, m):
         m_cpu //= 2
         note = f"bounded sample: m reduced to {m_cpu} B to fit host memory"
     times, ok = _cpu_oracle_run(art, m_cpu, budget_s=0, nthreads=nthreads,
-                                max_iters=args.warmup + args.steps)
+                                max_iters=args.warmup + args.steps, copy_self=False)
     timed = times[args.warmup:] or times
     T = sum(timed) / len(timed)
     val = n * (n - 1) * m_cpu / T / 1e9
@@ -204,15 +308,15 @@ def run_reference(args, art, m):
         "n_gpus": args.gpus, "steps": len(timed), "warmup": args.warmup,
         "ms_per_step": round(T * 1e3, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": workload_name(args.config, n, m),
-                   "lowering": LOWERINGS["balanced" if args.lowering == "balanced" else "hop"],
-                   "m_bytes": m_cpu, "nodes": n, "hop_ops": len(art.sched.instructions),
-                   "nsteps": art.sched.nsteps},
+        "config": config_of(args.config, art, m, args.gpus),
         "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": nthreads,
                          "kind": "port",
-                         "sample": f"{note}; oracle/replay_bytes.c, OpenMP {nthreads} threads, "
+                         "sample": f"{note}; oracle/replay_bytes.c (restated reference replay, "
+                                   f"evaluate.py:56-127, moving bytes), OpenMP {nthreads} threads, "
                                    f"1 MiB copy pieces, scratch reused across all-to-alls, "
-                                   f"{len(timed)} full all-to-alls", "recv_ok": ok},
+                                   f"{len(timed)} full all-to-alls, "
+                                   f"{LOWERINGS['balanced' if args.lowering == 'balanced' else 'hop']}",
+                         "recv_ok": ok},
         "e2e": {"value": round(val, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -283,44 +387,77 @@ def balanced_artifact(art, m, G, placement):
 LL_MAX_SHARD = 1 << 20   # autotune tries the LL transport up to this shard size
 
 
-def make_plan(art, m, G, placement, schedule):
+def make_plan(art, m, G, placement, schedule, copy_self=False):
     """Plan for an execution-schedule spec: "static", "<dyn mode>:<unit bytes>"
     (optionally ":<R>": R CTAs pinned to the NVLink queue, the rest to the HBM
     queue), or "ll" (static programs + the LL cross-GPU transport)."""
     from paper_2309_13541_b200.executor import Plan
     if schedule == "ll":
-        return Plan(art.g, art.sched, m=m, n_gpus=G, placement=placement, protocol="ll")
-    plan = Plan(art.g, art.sched, m=m, n_gpus=G, placement=placement)
+        return Plan(art.g, art.sched, m=m, n_gpus=G, placement=placement, protocol="ll",
+                    copy_self=copy_self)
+    plan = Plan(art.g, art.sched, m=m, n_gpus=G, placement=placement, copy_self=copy_self)
     if schedule:
         plan.set_schedule_spec(schedule)
     return plan
 
 
+def default_candidates(G, m):
+    """Autotune candidates (at most three execution orders, plus LL for small
+    shards): static per-CTA programs, critical-path unit queues, and the
+    single merged queue (`mix`; at G > 2 `spread`, which interleaves each
+    step's NVLink units over their destination GPUs)."""
+    return ("static", "cp:1048576", "spread:1048576" if G > 2 else "mix:1048576") + (
+        ("ll",) if m <= LL_MAX_SHARD else ())
+
+
+def _node_send(dev, s, n, m, salt=0):
+    """Deterministic synthetic shards of virtual node s: [n, m] u8 on `dev`."""
+    import torch
+    gen = torch.Generator(device=dev).manual_seed(1000003 * (s + 1) + m + salt)
+    return torch.randint(0, 256, (n, m), dtype=torch.uint8, device=dev, generator=gen)
+
+
+def _recv_ok(ctx, recv, nodes, n, m, copy_self, salt=0):
+    """recv[i, s] == send of node s, row nodes[i] (the transpose)
+    for every s != nodes[i] (and the self shard when it is copied); all ranks."""
+    import torch
+    ok = True
+    for s in range(n):
+        row = _node_send(ctx.dev, s, n, m, salt)
+        for i, v in enumerate(nodes):
+            if v != s or copy_self:
+                ok &= bool(torch.equal(recv[i, s], row[v]))
+    return ctx.allmax([0.0 if ok else 1.0])[0] == 0.0
+
+
 def autotune_schedule(ctx, art, m, placement="optimized", num_ctas=0, trials=5,
-                      candidates=None):
+                      candidates=None, copy_self=False):
     """Time a few executes of each execution schedule (same placement, same
-    buffers) and return (best, {candidate: ms}); identical on every rank."""
+    buffers) and return (best, {candidate: ms}); identical on every rank.
+    Each candidate's receive buffers are checked against the transpose of
+    synthetic shards first; a candidate whose output is wrong is reported as
+    {"recv_ok": false} and never chosen."""
     import torch
 
-    from paper_2309_13541_b200.dist import connect
+    from paper_2309_13541_b200.dist import connect, local_nodes
     G, dev = ctx.world, ctx.dev
     if candidates is None:
-        candidates = ("static", "mix:1048576", "cp:1048576", "ready:1048576") + (
-            ("cp:1048576:64",) if G > 1 else ()) + (
-            ("spread:1048576",) if G > 2 else ()) + (("ll",) if m <= LL_MAX_SHARD else ())
+        candidates = default_candidates(G, m)
     times = {}
+    n = art.g.n
     for cand in candidates:
-        plan = make_plan(art, m, G, placement, cand)
+        plan = make_plan(art, m, G, placement, cand, copy_self=copy_self)
         plan.bind(ctx.rank, device=ctx.local, num_ctas=num_ctas)
         if G > 1:
             connect(plan)
-        V = plan.gpu_info(ctx.rank)["n_local_nodes"]
-        send = torch.zeros((V, art.g.n, m), dtype=torch.uint8, device=dev)
+        nodes = local_nodes(plan, ctx.rank)
+        send = torch.stack([_node_send(dev, s, n, m, salt=7) for s in nodes])
         recv = plan.recv_buffer() if G > 1 else torch.empty_like(send)
         stream = torch.cuda.current_stream(dev)
         for _ in range(3):
             plan.execute(send, recv, stream=stream)
         plan.sync()
+        ok = _recv_ok(ctx, recv, nodes, n, m, copy_self, salt=7)
         ctx.barrier()
         plan.execute(send, recv, stream=stream)   # skew absorber (see measure)
         ev = []
@@ -333,13 +470,26 @@ def autotune_schedule(ctx, art, m, placement="optimized", num_ctas=0, trials=5,
         plan.sync()
         torch.cuda.synchronize(dev)
         t = ctx.allmax([x.elapsed_time(y) for x, y in ev])
-        times[cand] = round(sorted(t)[len(t) // 2], 4)
-        plan.close()
+        times[cand] = round(sorted(t)[len(t) // 2], 4) if ok else {"recv_ok": False}
+        plan_close(ctx, plan)
         del send, recv
         torch.cuda.empty_cache()
-        ctx.barrier()
-    best = min(times, key=lambda k: (times[k], k))
+    good = {k: v for k, v in times.items() if not isinstance(v, dict)}
+    if not good:
+        raise SystemExit(f"every execution schedule produced a wrong all-to-all: {times}")
+    best = min(good, key=lambda k: (good[k], k))
     return best, times
+
+
+def plan_close(ctx, plan):
+    """Multi-GPU teardown in two phases: close the imported peer arenas, wait
+    until every rank has done so, then free our own (a peer may still map it
+    until then: freeing an exported allocation before the importers closed it
+    is undefined, cudaIpcCloseMemHandle)."""
+    if ctx.world > 1:
+        plan.close_peers()
+        ctx.barrier()
+    plan.close()
 
 
 L2_BYTES = 126 << 20
@@ -372,11 +522,13 @@ def bound_terms(infos, n, m, sum_dist, hbm_gbs):
 
 
 def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=True,
-            flush_bytes=512 << 20, placement="optimized", schedule="static", flush=None):
+            flush_bytes=512 << 20, placement="optimized", schedule="static", flush=None,
+            copy_self=False):
     """Time K all-to-alls of `art` at shard size m on ctx.world GPUs.
 
     Returns a dict (identical on every rank) with T, algBW, bound, roofline,
-    NCCL baseline and e2e numbers."""
+    NCCL baseline and e2e numbers.  Raises SystemExit if the receive buffers
+    of the timed executes are not the transpose of the send shards."""
     import torch
 
     from paper_2309_13541_b200.dist import connect, local_nodes
@@ -384,7 +536,7 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
 
     G, rank, dev = ctx.world, ctx.rank, ctx.dev
     n = art.g.n
-    plan = make_plan(art, m, G, placement, schedule)
+    plan = make_plan(art, m, G, placement, schedule, copy_self=copy_self)
     if e2e and G > 1:
         plan.set_recv_buffers(2)          # double-buffered recv for the pipelined e2e
     plan.bind(rank, device=ctx.local, num_ctas=num_ctas)
@@ -395,24 +547,20 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     V = info["n_local_nodes"]
     nodes = local_nodes(plan, rank)
 
-    def node_send(s):  # deterministic synthetic shards of node s: [n, m]
-        gen = torch.Generator(device=dev).manual_seed(1000003 * (s + 1) + m)
-        return torch.randint(0, 256, (n, m), dtype=torch.uint8, device=dev, generator=gen)
-
     send = torch.empty((V, n, m), dtype=torch.uint8, device=dev)
     for i, s in enumerate(nodes):
-        send[i] = node_send(s)
+        send[i] = _node_send(dev, s, n, m)
     recv = plan.recv_buffer() if G > 1 else torch.empty_like(send)
     # L2 policy: flush (512 MiB memset outside the events) unless every GPU's
     # send buffer alone exceeds L2 (126 MB), in which case inputs are larger
     # than L2 and back-to-back all-to-alls avoid per-rank flush skew
     if flush is None:
         flush = min(i["send_bytes"] for i in infos) < L2_BYTES
-    l2_policy = ("flushed between timed steps (512 MiB memset, outside events"
-                 + (", then ranks re-aligned by an NCCL all-reduce, outside events)" if G > 1 else ")")
-                 if flush else
-                 f"inputs larger than L2 ({min(i['send_bytes'] for i in infos) >> 20} MiB send per GPU "
-                 f"> 126 MB), no flush")
+    l2_txt = ("flushed between timed steps (512 MiB memset, outside events"
+              + (", then ranks re-aligned by an NCCL all-reduce, outside events)" if G > 1 else ")")
+              if flush else
+              f"inputs larger than L2 ({min(i['send_bytes'] for i in infos) >> 20} MiB send per GPU "
+              f"> 126 MB), no flush")
     flush_buf = torch.empty(flush_bytes if flush else 1, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -422,12 +570,10 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
         plan.execute(send, recv, stream=stream)
     plan.sync()
     ctx.barrier()
-    ok = True
-    for s in range(n):
-        row = node_send(s)
-        for i, v in enumerate(nodes):
-            ok &= bool(torch.equal(recv[i, s], row[v]))
-    ok = ctx.allmax([0.0 if ok else 1.0])[0] == 0.0
+    ok = _recv_ok(ctx, recv, nodes, n, m, copy_self)
+    if not ok:
+        raise SystemExit(f"{art.name} m={m} {schedule}: receive buffers differ from the "
+                         f"transpose of the send shards; no number is reported")
 
     # ---- timed region: K all-to-alls, L2 flushed between them (outside the events)
     e0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
@@ -435,6 +581,7 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     ef = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]   # before the flush
     ctx.barrier()
     torch.cuda.synchronize(dev)
+    nvl = NvlinkCounters(ctx.local) if G > 1 else None
     if clk:
         clk.start()
     # one untimed all-to-all right before the timed ones (no host sync between):
@@ -460,6 +607,9 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     plan.sync()                   # the sampler thread keeps sampling while the GPU drains
     torch.cuda.synchronize(dev)
     clock_rec = clk.stop() if clk else None
+    # NVLink hardware byte counters of this GPU over the timed loop (steps + 1
+    # all-to-alls, the skew absorber included), per all-to-all
+    nvl_rec = nvl.per_launch(steps + 1) if nvl else None
     ctx.barrier()
     from paper_2309_13541_b200.executor import timeline_summary
     tls = timeline_summary(plan.read_timeline(), schedule)    # last timed launch, this rank
@@ -496,20 +646,35 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     else:
         xfer = bt["nvlink_bytes"]
         achieved = xfer / T / 1e9
-        roof = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_MEASURED,
-                "unit": "GB/s", "frac": round(achieved / NVLINK_MEASURED, 4), "traffic": None,
-                "peak_kind": "measured peer-copy GB/s per direction (B200_PROFILING.md)",
+        nvpk, nvkind = _nvlink_peak()
+        roof = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": nvpk,
+                "unit": "GB/s", "frac": round(achieved / nvpk, 4), "traffic": None,
+                "peak_kind": nvkind,
+                "frac_vs_770": round(achieved / NVLINK_GUIDE, 4),
                 "algorithmic_bytes_per_launch": xfer,
                 "hbm_term": {"bytes": bt["hbm_bytes"], "achieved": round(bt["hbm_bytes"] / T / 1e9, 1),
                              "peak": hbm, "frac": round(bt["hbm_bytes"] / T / 1e9 / hbm, 4)}}
     t_lb = bt["t_lb"]
+    if nvl_rec is not None:
+        allv = [None] * G
+        ctx.pg.all_gather_object(allv, nvl_rec)
+        roof["nvlink_counters"] = {"per_rank": allv, "source": nvl_rec.get("source")}
+        tx = [x.get("tx_bytes") for x in allv]
+        rx = [x.get("rx_bytes") for x in allv]
+        if all(v is not None for v in tx + rx):
+            # hardware NVLink bytes of the busiest GPU direction per all-to-all
+            roof["traffic"] = int(max(max(tx), max(rx)))
+            roof["traffic_source"] = ("NVML NVLink data tx/rx counters around the timed loop, "
+                                      "busiest GPU direction, per all-to-all")
     traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(traffic_file):
         with open(traffic_file) as fh:
             tr = json.load(fh).get(f"{art.name}:{m}:G{G}")
-        if tr:
+        if tr and roof["traffic"] is None:
             roof["traffic"] = tr["per_launch_bytes"]
             roof["traffic_source"] = tr["source"]
+        elif tr:
+            roof["ncu"] = tr
 
     # ---- NCCL all_to_all_single on the same bytes (baseline, not the target)
     nres = None
@@ -631,11 +796,122 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
            "kernel_timeline": tls,
            "num_ctas": plan_ctas(plan, num_ctas), "egress_max": max(i["egress_bytes"] for i in infos),
            "scratch_bytes": info["scratch_bytes"], "placement": plan.placement.tolist(),
-           "schedule": schedule, "l2": l2_policy}
-    plan.close()
+           "schedule": schedule, "l2": l2_txt, "copy_self": copy_self}
+    plan_close(ctx, plan)
     del send, recv, flush_buf
     torch.cuda.empty_cache()
     return res
+
+
+def cpu_baseline(args, art, m, name):
+    """Rank 0, N=1: the C oracle (restated reference replay) on all host cores
+    and on one core, on a bounded sample of the workload."""
+    n = art.g.n
+    nthreads = os.cpu_count() or 1
+    m_cpu = m
+    slots = _scratch_slots(art)
+    while not _host_fits(n, m_cpu, slots=slots) and m_cpu > 4096:
+        m_cpu //= 2
+    times, cok = _cpu_oracle_run(art, m_cpu, args.cpu_budget_s, nthreads)
+    tc = sorted(times)[len(times) // 2]
+    cpu = {"value": round(n * (n - 1) * m_cpu / tc / 1e9, 4), "unit": "GB/s",
+           "cores": nthreads, "kind": "port",
+           "sample": f"{len(times)} full all-to-alls of {name} at m={m_cpu} B "
+                     f"(median) with oracle/replay_bytes.c on {nthreads} threads "
+                     f"(1 MiB copy pieces, scratch reused across all-to-alls, self shards "
+                     f"not moved as in the reference transpose)",
+           "recv_ok": cok}
+    # SURVEY §8d baseline 2: the same restatement on one core
+    t1, ok1 = _cpu_oracle_run(art, m_cpu, min(3.0, args.cpu_budget_s), 1)
+    t1m = sorted(t1)[len(t1) // 2]
+    cpu["single_core"] = {"value": round(n * (n - 1) * m_cpu / t1m / 1e9, 4), "cores": 1,
+                          "sample": f"{len(t1)} full all-to-alls (median), 1 thread",
+                          "recv_ok": ok1}
+    return cpu
+
+
+def choose_execution(ctx, args, art, m, placement):
+    """(art, placement, schedule, lowering, autotune record, skip note):
+    autotune the execution order and, at >= 2 GPUs, the path -> step lowering."""
+    tune, skipped = None, None
+    schedule = args.schedule
+    lowering = "balanced" if args.lowering == "balanced" else "hop"
+    if schedule == "auto":
+        schedule, tune = autotune_schedule(ctx, art, m, placement=placement,
+                                           num_ctas=args.num_ctas)
+        if args.lowering == "auto" and ctx.world >= 2 and art.routes is not None:
+            # same routes, links and bytes, steps re-balanced over the GPUs
+            # (lowering.balanced_offsets); times are max over ranks, so every
+            # rank takes the same decision
+            from paper_2309_13541_b200.schedule import ScheduleError
+            try:                    # host-only and deterministic: same outcome on every rank
+                bart, bpl = balanced_artifact(art, m, ctx.world, args.placement)
+            except (ScheduleError, ValueError) as ex:
+                skipped = repr(ex)  # keep the measured hop lowering; say why in the line
+                bart = None
+            if bart is not None:
+                bsched, btune = autotune_schedule(ctx, bart, m, placement=bpl,
+                                                  num_ctas=args.num_ctas)
+                tune = {"hop": tune, "balanced": btune}
+                if btune[bsched] < tune["hop"][schedule]:
+                    art, placement, schedule, lowering = bart, bpl, bsched, "balanced"
+    return art, placement, schedule, lowering, tune, skipped
+
+
+def run_ours(ctx, args, name, m, steps, e2e=True, nccl=True, cpu=True, self_copy_run=True):
+    """Autotune + measure one workload; returns the JSON fields of its line."""
+    from paper_2309_13541_b200.artifacts import load_artifact
+    art0 = load_artifact(name)
+    placement = args.placement
+    art = art0
+    if args.lowering == "balanced":
+        art, placement = balanced_artifact(art0, m, ctx.world, args.placement)
+    art, placement, schedule, lowering, tune, skipped = choose_execution(ctx, args, art, m, placement)
+    G, n = ctx.world, art.g.n
+    r = measure(ctx, art, m, steps, args.warmup, num_ctas=args.num_ctas, nccl=nccl, e2e=e2e,
+                placement=placement, schedule=schedule,
+                flush=l2_flush_needed(n, m, G), copy_self=False)
+    # the same execution with the self shards copied too (all_to_all_single
+    # semantics; not part of the reference transpose, evaluate.py:114-118)
+    selfc = None
+    if self_copy_run:
+        rs = measure(ctx, art, m, max(3, min(steps, 10)), args.warmup, num_ctas=args.num_ctas,
+                     nccl=False, e2e=False, clocks=False, placement=placement, schedule=schedule,
+                     flush=l2_flush_needed(n, m, G), copy_self=True)
+        selfc = {"ms_per_step": round(rs["T"] * 1e3, 4), "value": round(rs["value"], 3),
+                 "bound_frac": round(rs["bound_frac"], 4), "roofline_frac": rs["roofline"]["frac"],
+                 "roofline_achieved": rs["roofline"]["achieved"], "recv_ok": rs["recv_ok"],
+                 "note": "copy_self=True: the N self shards are copied too (2*N*m more HBM "
+                         "bytes on their GPUs), as torch all_to_all_single does"}
+    cpu_rec = None
+    if cpu and ctx.rank == 0 and G == 1 and not args.no_cpu_baseline:
+        cpu_rec = cpu_baseline(args, art, m, name)
+    return {
+        "value": round(r["value"], 3), "ms_per_step": round(r["T"] * 1e3, 4),
+        "config": config_of(name, art0, m, G),
+        "exec": {"lowering": LOWERINGS[lowering], "lowering_skipped": skipped,
+                 "placement": f"{args.placement} {r['placement'] if G > 1 else '(all nodes on GPU 0)'}",
+                 "num_ctas": r["num_ctas"], "schedule": schedule, "schedule_autotune_ms": tune,
+                 "engine": "tma (cp.async.bulk)" if schedule != "ll" else "ll lines (st.volatile.v4)"},
+        "per_gpu": round(r["per_gpu"], 3),
+        "step_ms_dist": r["step_ms_dist"],
+        "bound": {"t_lb_ms": round(r["t_lb"] * 1e3, 4), "frac": round(r["bound_frac"], 4),
+                  "def": "G=1: 2*m*sum(dist)/HBM; G>1: max_g max(egress,ingress)/900 GB/s",
+                  "t_hbm_ms": round(r["t_hbm"] * 1e3, 4),
+                  "t_both_ms": round(r["t_both"] * 1e3, 4),
+                  "frac_both": round(r["t_both"] / r["T"], 4),
+                  "def_both": "max(t_lb, max_g schedule HBM bytes of g / HBM): at G>1 the "
+                              "local hops and incoming stores also need HBM time"},
+        "recv_ok": r["recv_ok"],
+        "roofline": r["roofline"],
+        "cpu_baseline": cpu_rec,
+        "e2e": r["e2e"],
+        "nccl": r["nccl"],
+        "with_self_copy": selfc,
+        "gpu_launches": steps,
+        "kernel_timeline_last_step": r["kernel_timeline"],
+        "clocks": r["clocks"],
+    }
 
 
 def main(argv=None):
@@ -650,109 +926,51 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--no-self-copy-run", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--placement", default="optimized", choices=["optimized", "contiguous"])
     ap.add_argument("--schedule", default="auto",
-                    help="static | dynamic[:unit_bytes] | auto (time both, keep the faster)")
+                    help="static | <mode>:<unit bytes> | ll | auto (time the candidates, keep the fastest)")
     ap.add_argument("--lowering", default="auto", choices=["auto"] + sorted(LOWERINGS),
                     help="path -> step lowering of a path-mode artifact; auto = hop, and at >= 2 "
                          "GPUs with --schedule auto the autotune also times the balanced lowering")
+    ap.add_argument("--largest", default="torus4x4x4:4194304",
+                    help="at N=1 also measure this config:m (BASELINE configs[2], the largest "
+                         "single-GPU workload) into the line's `largest_single_gpu`; '' = off")
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
 
-    from paper_2309_13541_b200.artifacts import load_artifact
-    art = load_artifact(args.config)
-    m = args.m
-    placement = args.placement
-    if args.lowering == "balanced":
-        art, placement = balanced_artifact(art, m, args.gpus, args.placement)
     if args.impl == "reference":
-        return run_reference(args, art, m)
+        from paper_2309_13541_b200.artifacts import load_artifact
+        art = load_artifact(args.config)
+        if args.lowering == "balanced":
+            art, _ = balanced_artifact(art, args.m, args.gpus, args.placement)
+        return run_reference(args, art, args.m)
 
     ctx = Ctx()
     if ctx.world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ctx.world}")
-    tune = None
-    schedule = args.schedule
-    lowering = "balanced" if args.lowering == "balanced" else "hop"
-    if schedule == "auto":
-        schedule, tune = autotune_schedule(ctx, art, m, placement=placement,
-                                           num_ctas=args.num_ctas)
-        if args.lowering == "auto" and ctx.world >= 2 and art.routes is not None:
-            # same routes, links and bytes, steps re-balanced over the GPUs
-            # (lowering.balanced_offsets); times are max over ranks, so every
-            # rank takes the same decision
-            try:                    # host-only and deterministic: same outcome on every rank
-                bart, bpl = balanced_artifact(art, m, ctx.world, args.placement)
-            except Exception as ex:  # noqa: BLE001 - keep the measured hop lowering
-                print(f"balanced lowering skipped: {ex!r}", file=sys.stderr)
-                bart = None
-            if bart is not None:
-                bsched, btune = autotune_schedule(ctx, bart, m, placement=bpl,
-                                                  num_ctas=args.num_ctas)
-                tune = {"hop": tune, "balanced": btune}
-                if btune[bsched] < tune["hop"][schedule]:
-                    art, placement, schedule, lowering = bart, bpl, bsched, "balanced"
-    r = measure(ctx, art, m, args.steps, args.warmup, num_ctas=args.num_ctas,
-                nccl=not args.no_nccl, e2e=not args.no_e2e, placement=placement,
-                schedule=schedule)
-    G, n = ctx.world, art.g.n
-
-    # ---- CPU baseline: rank 0, N=1 only, bounded sample
-    cpu = None
-    if ctx.rank == 0 and G == 1 and not args.no_cpu_baseline:
-        nthreads = os.cpu_count() or 1
-        m_cpu = m
-        slots = _scratch_slots(art)
-        while not _host_fits(n, m_cpu, slots=slots) and m_cpu > 4096:
-            m_cpu //= 2
-        times, cok = _cpu_oracle_run(art, m_cpu, args.cpu_budget_s, nthreads)
-        tc = sorted(times)[len(times) // 2]
-        cpu = {"value": round(n * (n - 1) * m_cpu / tc / 1e9, 4), "unit": "GB/s",
-               "cores": nthreads, "kind": "port",
-               "sample": f"{len(times)} full all-to-alls of {args.config} at m={m_cpu} B "
-                         f"(median) with oracle/replay_bytes.c on {nthreads} threads "
-                         f"(1 MiB copy pieces, scratch reused across all-to-alls)",
-               "recv_ok": cok}
-        # SURVEY §8d baseline 2: the same restatement on one core
-        t1, ok1 = _cpu_oracle_run(art, m_cpu, min(3.0, args.cpu_budget_s), 1)
-        t1m = sorted(t1)[len(t1) // 2]
-        cpu["single_core"] = {"value": round(n * (n - 1) * m_cpu / t1m / 1e9, 4), "cores": 1,
-                              "sample": f"{len(t1)} full all-to-alls (median), 1 thread",
-                              "recv_ok": ok1}
-
+    res = run_ours(ctx, args, args.config, args.m, args.steps, e2e=not args.no_e2e,
+                   nccl=not args.no_nccl, self_copy_run=not args.no_self_copy_run)
+    largest = None
+    if args.largest and ctx.world == 1:
+        lname, lm = args.largest.split(":")
+        lr = run_ours(ctx, args, lname, int(lm), max(3, min(args.steps, 10)),
+                      e2e=not args.no_e2e, nccl=False, self_copy_run=False)
+        largest = {k: lr[k] for k in ("value", "ms_per_step", "config", "exec", "bound",
+                                      "roofline", "cpu_baseline", "e2e", "recv_ok",
+                                      "step_ms_dist", "clocks")}
+        largest["steps"] = max(3, min(args.steps, 10))
+        largest["gpu_launches"] = largest["steps"]
     if ctx.rank == 0:
-        line = {
-            "metric": METRIC, "value": round(r["value"], 3), "unit": "GB/s", "n_gpus": G,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["T"] * 1e3, 4),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "u8", "data": "synthetic",
-            "config": {"workload": workload_name(args.config, n, m),
-                       "lowering": LOWERINGS[lowering],
-                       "placement": f"{args.placement} {r['placement'] if G > 1 else '(all nodes on GPU 0)'}",
-                       "m_bytes": m, "nodes": n, "hop_ops": len(art.sched.instructions),
-                       "nsteps": art.sched.nsteps, "Q": art.sched.Q,
-                       "l2": r["l2"],
-                       "num_ctas": r["num_ctas"], "schedule": schedule,
-                       "schedule_autotune_ms": tune},
-            "per_gpu": round(r["per_gpu"], 3),
-            "step_ms_dist": r["step_ms_dist"],
-            "bound": {"t_lb_ms": round(r["t_lb"] * 1e3, 4), "frac": round(r["bound_frac"], 4),
-                      "def": "G=1: 2*m*sum(dist)/HBM; G>1: max_g max(egress,ingress)/900 GB/s",
-                      "t_hbm_ms": round(r["t_hbm"] * 1e3, 4),
-                      "t_both_ms": round(r["t_both"] * 1e3, 4),
-                      "frac_both": round(r["t_both"] / r["T"], 4),
-                      "def_both": "max(t_lb, max_g schedule HBM bytes of g / HBM): at G>1 the "
-                                  "local hops and incoming stores also need HBM time"},
-            "recv_ok": r["recv_ok"],
-            "roofline": r["roofline"],
-            "cpu_baseline": cpu,
-            "e2e": r["e2e"],
-            "nccl": r["nccl"],
-            "gpu_launches": args.steps,
-            "kernel_timeline_last_step": r["kernel_timeline"],
-            "clocks": r["clocks"],
-        }
+        G = ctx.world
+        line = {"metric": METRIC, "value": res["value"], "unit": "GB/s", "n_gpus": G,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "u8", "data": "synthetic"}
+        line.update({k: v for k, v in res.items() if k not in ("value", "ms_per_step")})
+        if largest is not None:
+            line["largest_single_gpu"] = largest
         print(json.dumps(line), flush=True)
     ctx.close()
 

@@ -219,6 +219,16 @@ int a2a_plan_import_handles(a2a_plan* plan, const void* handles);
  * (a2a_plan_arena), peer access is enabled on this rank's device */
 int a2a_plan_arena(const a2a_plan* plan, void** out_ptr);
 int a2a_plan_import_pointers(a2a_plan* plan, void* const* arenas);
+/* multi-GPU teardown, phase 1: wait for this rank's executes, then close the
+ * imported peer arenas (the plan refuses further executes).  Every rank must
+ * reach phase 1 before any rank frees its own arena (a2a_plan_destroy): an
+ * exported allocation must outlive its importers' mappings. */
+int a2a_plan_close_peers(a2a_plan* plan);
+/* after bind: the device-layout parameters every rank must agree on, as 8
+ * int64 {num_ctas, sched_mode, dyn_unit_bytes, n_recv, flags_bytes,
+ * arena_bytes of every GPU summed, engine, protocol LL} -- a rank that
+ * computed a different layout would store to wrong offsets of its peers */
+int a2a_plan_layout(const a2a_plan* plan, int64_t* out8);
 /* pointer to this rank's arena recv buffer ([V_g][N][m]); with n_gpus > 1
  * peers store into it directly, so execute must be given this buffer (any
  * device buffer with A2A_PROTO_LL, where only local CTAs write recv) */

@@ -91,6 +91,8 @@ def _load():
         "a2a_plan_import_handles": ([P, C.c_void_p], C.c_int),
         "a2a_plan_arena": ([P, C.POINTER(P)], C.c_int),
         "a2a_plan_import_pointers": ([P, C.POINTER(P)], C.c_int),
+        "a2a_plan_close_peers": ([P], C.c_int),
+        "a2a_plan_layout": ([P, C.POINTER(C.c_int64)], C.c_int),
         "a2a_plan_recv_buffer": ([P, C.POINTER(P)], C.c_int),
         "a2a_plan_execute": ([P, P, P, P, C.c_int32], C.c_int),
         "a2a_plan_sync": ([P], C.c_int),

@@ -1305,6 +1305,38 @@ int a2a_plan_import_pointers(a2a_plan* plan, void* const* arenas) {
   });
 }
 
+int a2a_plan_close_peers(a2a_plan* plan) {
+  return guard([&]() -> int {
+    if (!plan) return fail(A2A_ERR_INVALID, "null plan");
+    Plan& P = plan->p;
+    if (!P.bound) return A2A_OK;
+    DeviceGuard dg(P.device);
+    if (P.launched) CK(cudaDeviceSynchronize());
+    for (int g = 0; g < A2A_MAX_GPUS; ++g) {
+      if (g == P.rank) continue;
+      if (P.peer_opened[g] && P.peer_arena[g]) CK(cudaIpcCloseMemHandle(P.peer_arena[g]));
+      P.peer_opened[g] = false;
+      P.peer_arena[g] = nullptr;
+    }
+    P.imported = (P.G == 1);
+    return A2A_OK;
+  });
+}
+
+int a2a_plan_layout(const a2a_plan* plan, int64_t* out8) {
+  return guard([&]() -> int {
+    if (!plan || !out8) return fail(A2A_ERR_INVALID, "null argument");
+    const Plan& P = plan->p;
+    if (!P.bound) return fail(A2A_ERR_STATE, "plan not bound");
+    int64_t arena = 0;
+    for (int64_t b : P.arena_bytes) arena += b;
+    const int64_t v[8] = {P.nC, P.sched_mode, P.dyn_unit_bytes, P.n_recv, P.flags_bytes, arena,
+                          P.engine, P.ll ? 1 : 0};
+    std::memcpy(out8, v, sizeof v);
+    return A2A_OK;
+  });
+}
+
 int a2a_plan_arena(const a2a_plan* plan, void** out_ptr) {
   return guard([&]() -> int {
     if (!plan || !out_ptr) return fail(A2A_ERR_INVALID, "null argument");

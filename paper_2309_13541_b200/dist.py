@@ -11,16 +11,22 @@ import hashlib
 
 import numpy as np
 
-__all__ = ["plan_digest", "check_same_plan", "connect", "local_nodes"]
+__all__ = ["plan_digest", "check_same_plan", "connect", "disconnect", "local_nodes"]
 
 
 def plan_digest(plan) -> str:
-    """Hash of everything that must agree across ranks (layout + schedule bytes)."""
+    """Hash of everything that must agree across ranks: per-GPU buffer sizes,
+    schedule bytes, placement and -- once bound -- the device layout (CTA
+    count, execution schedule, unit size, recv buffer count, flag region and
+    arena sizes, engine, protocol), from which every rank computes the
+    offsets it stores to in its peers' arenas."""
     h = hashlib.sha256()
     for g in range(plan.n_gpus):
         h.update(repr(sorted(plan.gpu_info(g).items())).encode())
     h.update(np.ascontiguousarray(plan.link_bytes()).tobytes())
     h.update(plan.placement.tobytes())
+    if plan.rank is not None:
+        h.update(repr(sorted(plan.layout().items())).encode())
     return h.hexdigest()
 
 
@@ -41,6 +47,15 @@ def connect(plan, group=None, check: bool = True):
     hs = [None] * plan.n_gpus
     dist.all_gather_object(hs, plan.export_handle(), group=group)
     plan.import_handles(hs)
+
+
+def disconnect(plan, group=None):
+    """Two-phase multi-GPU teardown: unmap the peers' arenas, wait until every
+    rank has, then free this rank's own arena (a peer may map it until then)."""
+    import torch.distributed as dist
+    plan.close_peers()
+    dist.barrier(group=group)
+    plan.close()
 
 
 def local_nodes(plan, rank: int) -> list:

@@ -348,6 +348,21 @@ class Plan:
         self._ck(N.lib.a2a_plan_arena(self._h, C.byref(p)), "a2a_plan_arena")
         return p.value
 
+    def close_peers(self):
+        """Multi-GPU teardown phase 1 (a2a_plan_close_peers): wait for this
+        rank's executes and unmap the peers' arenas.  Every rank must get here
+        before any rank calls ``close()`` (see dist.disconnect)."""
+        if getattr(self, "_h", None):
+            self._ck(N.lib.a2a_plan_close_peers(self._h), "a2a_plan_close_peers")
+
+    def layout(self) -> dict:
+        """Device-layout parameters every rank must agree on (after bind)."""
+        out = (C.c_int64 * 8)()
+        self._ck(N.lib.a2a_plan_layout(self._h, out), "a2a_plan_layout")
+        keys = ("num_ctas", "sched_mode", "dyn_unit_bytes", "n_recv", "flags_bytes",
+                "arena_bytes_total", "engine", "protocol_ll")
+        return dict(zip(keys, list(out)))
+
     def import_pointers(self, ptrs):
         arr = (C.c_void_p * self.n_gpus)(*ptrs)
         self._ck(N.lib.a2a_plan_import_pointers(self._h, arr), "a2a_plan_import_pointers")

@@ -101,7 +101,7 @@ def test_every_autotune_order_delivers(name, G, sched, artifacts):
     art, pl = bench.balanced_artifact(a, 16 << 20, G, "optimized")
     send = make_send(a.g.n, m, seed=G)
     want = np.swapaxes(send, 0, 1)
-    with bench.make_plan(art, m, G, pl, sched) as p:
+    with bench.make_plan(art, m, G, pl, sched, copy_self=True) as p:
         nodes = [local_nodes(p, r) for r in range(G)]
         for nc in (13, 148):
             recvs = p.emulate([send[ns] for ns in nodes], num_ctas=nc, seed=nc)

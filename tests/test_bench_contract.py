@@ -86,4 +86,36 @@ def test_balanced_lowering_option():
                          capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     d = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
-    assert "balance" in d["config"]["lowering"] and d["cpu_baseline"]["recv_ok"] is True
+    assert "balance" in d["cpu_baseline"]["sample"] and d["cpu_baseline"]["recv_ok"] is True
+
+
+def test_reference_arm_loads_no_product_library():
+    """The reference arm times only the CPU restatement: the product's
+    _a2a_exec.so must not be mapped in that process."""
+    code = ("import runpy, sys\n"
+            "sys.argv = ['bench.py', '--impl', 'reference', '--config', 'gk8_2', '--m', '4096',"
+            " '--steps', '1']\n"
+            "runpy.run_path('bench.py', run_name='__main__')\n"
+            "maps = open('/proc/self/maps').read()\n"
+            "print('PRODUCT' if '_a2a_exec' in maps else 'CLEAN')\n"
+            "print('ORACLE' if 'liboracle_replay' in maps else 'NO-ORACLE')\n")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                         timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "CLEAN" in out.stdout and "ORACLE" in out.stdout
+
+
+def test_config_identical_in_both_arms():
+    """`config` holds only the workload: the reference arm's line carries the
+    dict our arm builds with the same function for the same artifact."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2309_13541_b200.artifacts import load_artifact
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                          "--gpus", "4", "--config", "gk8_2", "--m", "65536", "--steps", "1"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT,
+                         env=dict(os.environ, RANK="0", WORLD_SIZE="4", LOCAL_RANK="0"))
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
+    assert d["config"] == bench.config_of("gk8_2", load_artifact("gk8_2"), 65536, 4)
+    assert d["config"]["copy_self"] is False and "l2" in d["config"]

@@ -284,3 +284,28 @@ def test_ll_rejects(artifacts):
             p.set_schedule("dynamic")
     with pytest.raises(ValueError):
         Plan(a.g, a.sched, m=4096, n_gpus=2, protocol="bogus")
+
+
+@pytest.mark.parametrize("name", ["gk8_2", "torus2x4_h2", "ts_hypercube3"])
+@pytest.mark.parametrize("G", [1, 2, 4])
+@pytest.mark.parametrize("sched", ["static", "cp", "spread"])
+def test_without_self_copy(name, G, sched, artifacts):
+    """copy_self=False (what bench.py times: the reference transpose skips
+    s == d, evaluate.py:114-118): every s != d shard delivered, the self
+    rows of recv untouched."""
+    a = artifacts(name)
+    m = 4096 + 24
+    send = make_send(a.g.n, m, seed=5)
+    with Plan(a.g, a.sched, m=m, n_gpus=G, copy_self=False) as p:
+        if sched != "static":
+            p.set_schedule(sched, 1024)
+        nodes = [local_nodes(p, g) for g in range(G)]
+        recvs = p.emulate([send[ns] for ns in nodes], num_ctas=7, seed=3)
+    want = np.swapaxes(send, 0, 1)
+    for g in range(G):
+        for i, v in enumerate(nodes[g]):
+            for s in range(a.g.n):
+                if s == v:
+                    assert not recvs[g][i, s].any()
+                else:
+                    assert np.array_equal(recvs[g][i, s], want[v, s]), (g, v, s)

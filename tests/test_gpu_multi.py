@@ -55,7 +55,7 @@ def _rank_main(rank, world, port, name, m, reps, q, engine="lsu", sched="static"
         from replay_bytes import make_send, replay_bytes
 
         from paper_2309_13541_b200.artifacts import load_artifact
-        from paper_2309_13541_b200.dist import connect, local_nodes
+        from paper_2309_13541_b200.dist import connect, disconnect, local_nodes
         from paper_2309_13541_b200.executor import Plan
         torch.cuda.set_device(rank)
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}",
@@ -123,7 +123,7 @@ def _rank_main(rank, world, port, name, m, reps, q, engine="lsu", sched="static"
         for (t, e), x in ob.items():
             ref[t, e] = x * reps
         q.put((rank, ok, bool(np.array_equal(summed, ref))))
-        plan.close()
+        disconnect(plan)
         dist.destroy_process_group()
     except Exception as ex:
         import traceback
@@ -244,7 +244,7 @@ def _alt_main(rank, world, port, q):
         from replay_bytes import make_send
 
         from paper_2309_13541_b200.artifacts import load_artifact
-        from paper_2309_13541_b200.dist import connect, local_nodes
+        from paper_2309_13541_b200.dist import connect, disconnect, local_nodes
         from paper_2309_13541_b200.executor import Plan
         torch.cuda.set_device(rank)
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}",
@@ -268,7 +268,7 @@ def _alt_main(rank, world, port, q):
                 ok &= bool(np.array_equal(bufs[(k - 1) & 1].cpu().numpy(), wants[k - 1]))
             ok &= bool(np.array_equal(bufs[k & 1].cpu().numpy(), wants[k]))
         q.put((rank, ok))
-        plan.close()
+        disconnect(plan)
         dist.destroy_process_group()
     except Exception as ex:
         import traceback
@@ -359,7 +359,7 @@ def _gk256_main(rank, world, port, name, sched, q):
         import torch.distributed as dist
 
         from paper_2309_13541_b200.artifacts import load_artifact
-        from paper_2309_13541_b200.dist import connect, local_nodes
+        from paper_2309_13541_b200.dist import connect, disconnect, local_nodes
         from paper_2309_13541_b200.executor import Plan
         torch.cuda.set_device(rank)
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}",
@@ -391,7 +391,7 @@ def _gk256_main(rank, world, port, name, sched, q):
         tot = [None] * world
         dist.all_gather_object(tot, counters)
         q.put((rank, ok, bool(np.array_equal(sum(tot), plan.link_bytes()))))
-        plan.close()
+        disconnect(plan)
         dist.destroy_process_group()
     except Exception as ex:
         import traceback
