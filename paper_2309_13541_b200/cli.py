@@ -1,18 +1,26 @@
 """`eval` command of the reference CLI, on the B200 executor.
 
-Mirrors ``a2a eval --graph G --sched X [--m M] [--b B] [--sync S]``
-(reference pkg/src/a2aflow/cli.py:133-139, :326-343): loads the graph JSON and
-the ts-mode XML schedule, replays it (same validation, same EvalError texts,
-bit-identical T) and prints ``T = <T:.9g>, delivered = True``; any error prints
-``error: <message>`` on stderr and exits 1, usage errors exit 2 (argparse), as
-the reference's ``main`` does (cli.py:419-431).  The reference's run manifest
-(cli.py:40-55) is not written: it records the reference's own pipeline runs.
+Mirrors ``a2a eval --graph G (--sched X | --routes R) [--m M] [--b B] [--sync S]``
+(reference pkg/src/a2aflow/cli.py:133-139, :326-343):
+
+* ``--sched X``: load the graph JSON and the ts-mode XML schedule, replay it
+  (same validation, same EvalError texts, bit-identical T) and print
+  ``T = <T:.9g>, delivered = True``;
+* ``--routes R`` (a weighted path set, the reference's route JSON): the
+  cut-through fluid time ``eval_path_alltoall`` (evaluate.py:130-139), printed
+  as ``T = <T:.9g>`` (fluid.py);
+* neither: ``error: eval needs --sched or --routes``.
+
+Any error prints ``error: <message>`` on stderr and exits 1, usage errors exit
+2 (argparse), as the reference's ``main`` does (cli.py:419-431).  The
+reference's run manifest (cli.py:40-55) is not written: it records the
+reference's own pipeline runs.
 
 Additions of this package (flags the reference does not have):
 
-* ``--routes R`` with a path-mode ``--sched``: lower the path schedule and its
-  route sidecar hop i -> step i natively (a2a_lower_path_files) and replay that
-  (the reference replay only accepts ts schedules, evaluate.py:70-71).
+* ``--path-routes R`` with a path-mode ``--sched``: lower the path schedule and
+  its route sidecar hop i -> step i natively (a2a_lower_path_files) and replay
+  that (the reference replay only accepts ts schedules, evaluate.py:70-71).
 * ``--execute``: also move real bytes on GPU ``--device`` (integer ``--m``
   bytes per shard, every virtual node on that GPU), check recv against the
   transpose of send and print the device time.  Multi-GPU runs go through
@@ -38,10 +46,13 @@ import time
 def build_parser() -> argparse.ArgumentParser:
     p = argparse.ArgumentParser(prog="b200-a2a")
     sub = p.add_subparsers(dest="command", required=True)
-    e = sub.add_parser("eval", help="replay / execute a ts schedule")
+    e = sub.add_parser("eval", help="replay / evaluate / execute a schedule")
     e.add_argument("--graph", required=True)
-    e.add_argument("--sched", required=True, help="XML schedule (ts mode, or path mode with --routes)")
-    e.add_argument("--routes", default=None, help="route sidecar of a path-mode --sched")
+    e.add_argument("--sched", default=None,
+                   help="XML schedule or op table (ts mode, or path mode with --path-routes)")
+    e.add_argument("--routes", default=None, help="route JSON (path mode): fluid eval_path_alltoall")
+    e.add_argument("--path-routes", default=None,
+                   help="route sidecar of a path-mode --sched: lower it hop i -> step i")
     e.add_argument("--m", type=float, default=1.0)
     e.add_argument("--b", type=float, default=1.0)
     e.add_argument("--sync", type=float, default=0.0)
@@ -61,8 +72,8 @@ def _load(args):
     from .graphs import load_graph
     from .native_io import load_schedule, lower_path_files
     g = load_graph(args.graph)
-    if args.routes:
-        sched = lower_path_files(args.sched, args.routes, n_phys=g.n)
+    if args.path_routes:
+        sched = lower_path_files(args.sched, args.path_routes, n_phys=g.n)
     else:
         sched = load_schedule(args.sched)
     return g, sched
@@ -104,6 +115,15 @@ def _execute(g, sched, args) -> str:
 
 
 def _cmd_eval(args) -> None:
+    if not args.sched:
+        if not args.routes:
+            from .graphs import GraphError
+            raise GraphError("eval needs --sched or --routes")
+        from .fluid import eval_path_alltoall, load_routes
+        from .graphs import load_graph
+        T = eval_path_alltoall(load_graph(args.graph), load_routes(args.routes), m=args.m, b=args.b)
+        print(f"T = {T:.9g}")
+        return
     from .executor import replay_timestep_schedule
     g, sched = _load(args)
     T, ok = replay_timestep_schedule(g, sched, m=args.m, b=args.b, sync_latency=args.sync)

@@ -24,6 +24,7 @@ import os
 import numpy as np
 
 from . import _native as N
+from .errors import EvalError
 
 __all__ = ["EvalError", "ExecutorError", "Plan", "replay_timestep_schedule",
            "execute_timestep_schedule", "contiguous_placement", "timeline_summary"]
@@ -50,11 +51,6 @@ def timeline_summary(tl: np.ndarray, schedule: str | None = "static") -> dict:
             "entry_us": us(tl[:, 1].max()),
             "step_acquired_us": [last(3 + T + t) for t in range(T)],
             "step_done_us": [last(2 + t) for t in range(T)]}
-
-
-class EvalError(RuntimeError):
-    """A schedule the reference replay would reject; same messages
-    (reference pkg/src/a2aflow/evaluate.py:30-31)."""
 
 
 class ExecutorError(RuntimeError):

@@ -43,15 +43,7 @@ def lower_path_to_steps(routes, sched, n: int | None = None, offsets=None) -> Ch
         off = 0 if offsets is None else int(offsets[k])
         if off < 0:
             raise ScheduleError(f"negative offset {off}")
-        if not 0 <= ins.dst < len(routes):
-            raise ScheduleError(f"route id {ins.dst} out of range")
-        r = routes[ins.dst]
-        nodes = list(r["nodes"])
-        if (r["s"], r["d"]) != (ins.s, ins.d) or nodes[0] != ins.s or nodes[-1] != ins.d:
-            raise ScheduleError(
-                f"route {ins.dst} {nodes} does not join shard ({ins.s},{ins.d})")
-        if len(nodes) < 2:
-            raise ScheduleError(f"route {ins.dst} has no hops")
+        nodes = _route_nodes(routes, ins)
         for i in range(len(nodes) - 1):
             ops.append(Instruction(t=off + i, src=nodes[i], dst=nodes[i + 1],
                                    s=ins.s, d=ins.d, c0=ins.c0, c1=ins.c1))
@@ -60,6 +52,22 @@ def lower_path_to_steps(routes, sched, n: int | None = None, offsets=None) -> Ch
     return ChunkedSchedule(n=sched.n if n is None else n, nsteps=nsteps,
                            chunk_bytes=sched.chunk_bytes, Q=sched.Q, mode="ts",
                            instructions=ops)
+
+
+def _route_nodes(routes, ins) -> list:
+    """Node sequence of the route a path instruction names (dst = route id),
+    checked: the id exists, the route joins the instruction's shard, it has
+    at least one hop."""
+    if not 0 <= ins.dst < len(routes):
+        raise ScheduleError(f"route id {ins.dst} out of range")
+    r = routes[ins.dst]
+    nodes = list(r["nodes"])
+    if (r["s"], r["d"]) != (ins.s, ins.d) or nodes[0] != ins.s or nodes[-1] != ins.d:
+        raise ScheduleError(
+            f"route {ins.dst} {nodes} does not join shard ({ins.s},{ins.d})")
+    if len(nodes) < 2:
+        raise ScheduleError(f"route {ins.dst} has no hops")
+    return nodes
 
 
 def _route_egress(routes, ins, node_gpu, m, Q):
@@ -102,8 +110,10 @@ def balanced_offsets(routes, sched, node_gpu, m: int, extra_steps: int = 0,
     further.  The objective is step_sync_cost of the lowered schedule."""
     if sched.mode != "path":
         raise ScheduleError(f"expected a path-mode schedule, got {sched.mode!r}")
+    if len(node_gpu) != sched.n or min(node_gpu, default=0) < 0:
+        raise ScheduleError(f"placement must list one GPU >= 0 per node ({sched.n})")
     G = max(node_gpu) + 1
-    hops = [len(routes[i.dst]["nodes"]) - 1 for i in sched.instructions]
+    hops = [len(_route_nodes(routes, i)) - 1 for i in sched.instructions]
     L = max(hops, default=0) + int(extra_steps)
     load = [[0] * (2 * G) for _ in range(L)]
     eg = [_route_egress(routes, i, node_gpu, m, sched.Q) for i in sched.instructions]

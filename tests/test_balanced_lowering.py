@@ -107,3 +107,25 @@ def test_every_autotune_order_delivers(name, G, sched, artifacts):
             recvs = p.emulate([send[ns] for ns in nodes], num_ctas=nc, seed=nc)
             for r in range(G):
                 assert np.array_equal(recvs[r], want[nodes[r]]), (nc, r)
+
+
+def test_balanced_offsets_validates_routes(artifacts):
+    """Bad routes fail with the lowering's ScheduleError texts, not IndexError."""
+    import copy
+
+    from paper_2309_13541_b200.schedule import ScheduleError
+    a = artifacts("gk8_2")
+    gpu = [v % 2 for v in range(a.g.n)]
+    bad = copy.deepcopy(a.path_sched)
+    bad.instructions[0] = bad.instructions[0]._replace(dst=len(a.routes) + 5) \
+        if hasattr(bad.instructions[0], "_replace") else type(bad.instructions[0])(
+            t=0, src=bad.instructions[0].src, dst=len(a.routes) + 5, s=bad.instructions[0].s,
+            d=bad.instructions[0].d, c0=bad.instructions[0].c0, c1=bad.instructions[0].c1)
+    with pytest.raises(ScheduleError, match="out of range"):
+        balanced_offsets(a.routes, bad, gpu, 4096)
+    routes = copy.deepcopy(a.routes)
+    routes[0]["nodes"] = list(reversed(routes[0]["nodes"]))
+    with pytest.raises(ScheduleError, match="does not join"):
+        balanced_offsets(routes, a.path_sched, gpu, 4096)
+    with pytest.raises(ScheduleError, match="one GPU"):
+        balanced_offsets(a.routes, a.path_sched, gpu[:-1], 4096)

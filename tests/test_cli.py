@@ -28,7 +28,7 @@ def _files(name):
             return ["--graph", os.path.join(d, "graph.json"), "--sched", os.path.join(d, x)]
     z = "" if os.path.exists(os.path.join(d, "path.xml")) else ".gz"
     return ["--graph", os.path.join(d, "graph.json"), "--sched", os.path.join(d, "path.xml" + z),
-            "--routes", os.path.join(d, "path.xml.routes.json" + z)]
+            "--path-routes", os.path.join(d, "path.xml.routes.json" + z)]
 
 
 # augmented (host-bottleneck) configs need the node map: covered by test_native_io
@@ -66,8 +66,31 @@ def test_eval_reject_exit_1(tmp_path, capsys):
 
 def test_eval_usage_exit_2():
     with pytest.raises(SystemExit) as ex:
-        main(["eval", "--graph", "g.json"])
+        main(["eval"])
     assert ex.value.code == 2
+
+
+def test_eval_needs_sched_or_routes(capsys):
+    """The reference raises GraphError("eval needs --sched or --routes") -> exit 1."""
+    g = os.path.join(ARTIFACT_DIR, "gk8_2", "graph.json")
+    rc = main(["eval", "--graph", g])
+    assert rc == 1 and capsys.readouterr().err.strip() == "error: eval needs --sched or --routes"
+
+
+@pytest.mark.parametrize("name", ["torus2x4", "hypercube3", "gk8_2", "torus4x4x4", "gk64_4"])
+def test_eval_routes_fluid_time(name, capsys):
+    """`eval --graph G --routes R`: the reference's cut-through fluid time
+    eval_path_alltoall (cli.py:338-342, evaluate.py:130-139), same output line
+    as the reference for its own widest-path set (golden fluid_max_load)."""
+    gold = _golden()["configs"][name]
+    d = os.path.join(ARTIFACT_DIR, name)
+    wps = [os.path.join(d, x) for x in ("wps.json", "wps.json.gz") if os.path.exists(os.path.join(d, x))][0]
+    for m, b in ((1.0, 1.0), (2.0, 1.0), (1048576.0, 3.0)):
+        rc = main(["eval", "--graph", os.path.join(d, "graph.json"), "--routes", wps,
+                   "--m", repr(m), "--b", repr(b)])
+        out = capsys.readouterr().out.strip()
+        assert rc == 0
+        assert out == f"T = {float(gold['fluid_max_load']) * m / b:.9g}"
 
 
 @pytest.mark.gpu
