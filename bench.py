@@ -445,9 +445,22 @@ def autotune_schedule(ctx, art, m, placement="optimized", num_ctas=0, trials=5,
         candidates = default_candidates(G, m)
     times = {}
     n = art.g.n
+    from paper_2309_13541_b200.executor import ExecutorError
     for cand in candidates:
         plan = make_plan(art, m, G, placement, cand, copy_self=copy_self)
-        plan.bind(ctx.rank, device=ctx.local, num_ctas=num_ctas)
+        nomem = ""
+        try:
+            plan.bind(ctx.rank, device=ctx.local, num_ctas=num_ctas)
+        except ExecutorError as ex:          # e.g. LL landing regions of a huge schedule
+            if "NOMEM" not in str(ex):
+                raise
+            nomem = str(ex)
+        if ctx.allmax([1.0 if nomem else 0.0])[0]:   # every rank skips the candidate together
+            times[cand] = {"skipped": nomem or "out of device memory on a peer"}
+            plan.close()
+            torch.cuda.empty_cache()
+            ctx.barrier()
+            continue
         if G > 1:
             connect(plan)
         nodes = local_nodes(plan, ctx.rank)
@@ -661,7 +674,7 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
         roof["nvlink_counters"] = {"per_rank": allv, "source": nvl_rec.get("source")}
         tx = [x.get("tx_bytes") for x in allv]
         rx = [x.get("rx_bytes") for x in allv]
-        if all(v is not None for v in tx + rx):
+        if all(v is not None for v in tx + rx) and max(tx + rx) > 0:
             # hardware NVLink bytes of the busiest GPU direction per all-to-all
             roof["traffic"] = int(max(max(tx), max(rx)))
             roof["traffic_source"] = ("NVML NVLink data tx/rx counters around the timed loop, "
