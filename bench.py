@@ -47,6 +47,20 @@ def _nvlink_peak():
         return NVLINK_GUIDE, "B200_PROFILING.md peer copy GB/s per direction (probe file absent)"
 
 
+def _a2a_probe(G, achieved):
+    """Context for a G-GPU NVLink roofline: the bare TMA push loop with every
+    GPU pushing to all its peers at once (tools/nvlink_a2a_probe.py), i.e. the
+    link ceiling of an all-to-all-shaped traffic pattern on this pool."""
+    f = os.path.join(ROOT, "profiles", f"r02_nvlink_a2a_probe_G{G}.json")
+    try:
+        with open(f) as fh:
+            gbs = float(json.load(fh)["uniform"]["busiest_gbs_per_direction"])
+        return {"gbs_per_direction": gbs, "frac": round(achieved / gbs, 4),
+                "source": os.path.relpath(f, ROOT)}
+    except Exception:
+        return None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -137,65 +151,6 @@ class Clocks:
                 "sm_max_mhz": max(self.mx) if self.mx else None,
                 "reasons": sorted(self.reasons), "samples": len(sm),
                 "source": "nvml" if self._nvml else "nvidia-smi"}
-
-
-class NvlinkCounters:
-    """NVLink data bytes this GPU transmitted / received, from the NVML
-    hardware counters (NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX, KiB, summed
-    over links), read before and after the timed loop: the measured NVLink
-    traffic of the executor (roofline.traffic at G > 1)."""
-
-    def __init__(self, index):
-        self.err, self._n, self.t0 = None, None, None
-        try:
-            import pynvml
-            import torch
-            pynvml.nvmlInit()
-            pr = torch.cuda.get_device_properties(index)
-            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
-            self._h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
-            self._n = pynvml
-            self.t0 = self._read()
-        except Exception as ex:  # noqa: BLE001 - counters are evidence, not the measurement
-            self.err = repr(ex)
-
-    def _fields(self, ids):
-        n = self._n
-        vals = n.nvmlDeviceGetFieldValues(self._h, ids)
-        out = []
-        for v in vals:
-            if v.nvmlReturn != 0:
-                return None
-            out.append(int(v.value.ullVal))
-        return out
-
-    def _read(self):
-        n = self._n
-        fid = [n.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, n.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX,
-               n.NVML_FI_DEV_NVLINK_THROUGHPUT_RAW_TX, n.NVML_FI_DEV_NVLINK_THROUGHPUT_RAW_RX]
-        allv = self._fields([(f, 0xFFFFFFFF) for f in fid])      # scope UINT_MAX: all links
-        if allv is not None and any(allv):
-            return allv
-        tot = [0, 0, 0, 0]                                        # else sum links 0..17
-        for link in range(18):
-            v = self._fields([(f, link) for f in fid])
-            if v is None:
-                break
-            tot = [a + b for a, b in zip(tot, v)]
-        return tot
-
-    def per_launch(self, launches):
-        if self.t0 is None:
-            return {"error": self.err or "NVML NVLink counters unavailable"}
-        try:
-            time.sleep(0.25)                 # counters are sampled by the driver, let them settle
-            t1 = self._read()
-        except Exception as ex:  # noqa: BLE001
-            return {"error": repr(ex)}
-        d = [(b - a) * 1024 for a, b in zip(self.t0, t1)]          # KiB -> bytes
-        return {"tx_bytes": d[0] // launches, "rx_bytes": d[1] // launches,
-                "raw_tx_bytes": d[2] // launches, "raw_rx_bytes": d[3] // launches,
-                "launches": launches, "source": "NVML_FI_DEV_NVLINK_THROUGHPUT_{DATA,RAW}_{TX,RX}"}
 
 
 def _dist():
@@ -594,7 +549,6 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     ef = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]   # before the flush
     ctx.barrier()
     torch.cuda.synchronize(dev)
-    nvl = NvlinkCounters(ctx.local) if G > 1 else None
     if clk:
         clk.start()
     # one untimed all-to-all right before the timed ones (no host sync between):
@@ -620,9 +574,7 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     plan.sync()                   # the sampler thread keeps sampling while the GPU drains
     torch.cuda.synchronize(dev)
     clock_rec = clk.stop() if clk else None
-    # NVLink hardware byte counters of this GPU over the timed loop (steps + 1
-    # all-to-alls, the skew absorber included), per all-to-all
-    nvl_rec = nvl.per_launch(steps + 1) if nvl else None
+
     ctx.barrier()
     from paper_2309_13541_b200.executor import timeline_summary
     tls = timeline_summary(plan.read_timeline(), schedule)    # last timed launch, this rank
@@ -664,21 +616,11 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
                 "unit": "GB/s", "frac": round(achieved / nvpk, 4), "traffic": None,
                 "peak_kind": nvkind,
                 "frac_vs_770": round(achieved / NVLINK_GUIDE, 4),
+                "a2a_probe": _a2a_probe(G, achieved),
                 "algorithmic_bytes_per_launch": xfer,
                 "hbm_term": {"bytes": bt["hbm_bytes"], "achieved": round(bt["hbm_bytes"] / T / 1e9, 1),
                              "peak": hbm, "frac": round(bt["hbm_bytes"] / T / 1e9 / hbm, 4)}}
     t_lb = bt["t_lb"]
-    if nvl_rec is not None:
-        allv = [None] * G
-        ctx.pg.all_gather_object(allv, nvl_rec)
-        roof["nvlink_counters"] = {"per_rank": allv, "source": nvl_rec.get("source")}
-        tx = [x.get("tx_bytes") for x in allv]
-        rx = [x.get("rx_bytes") for x in allv]
-        if all(v is not None for v in tx + rx) and max(tx + rx) > 0:
-            # hardware NVLink bytes of the busiest GPU direction per all-to-all
-            roof["traffic"] = int(max(max(tx), max(rx)))
-            roof["traffic_source"] = ("NVML NVLink data tx/rx counters around the timed loop, "
-                                      "busiest GPU direction, per all-to-all")
     traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(traffic_file):
         with open(traffic_file) as fh:
