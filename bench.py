@@ -347,8 +347,8 @@ def make_plan(art, m, G, placement, schedule, copy_self=False):
     (optionally ":<R>": R CTAs pinned to the NVLink queue, the rest to the HBM
     queue), or "ll" (static programs + the LL cross-GPU transport)."""
     from paper_2309_13541_b200.executor import Plan
-    if schedule == "ll":
-        return Plan(art.g, art.sched, m=m, n_gpus=G, placement=placement, protocol="ll",
+    if schedule in ("ll", "ll128"):
+        return Plan(art.g, art.sched, m=m, n_gpus=G, placement=placement, protocol=schedule,
                     copy_self=copy_self)
     plan = Plan(art.g, art.sched, m=m, n_gpus=G, placement=placement, copy_self=copy_self)
     if schedule:

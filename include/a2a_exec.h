@@ -59,6 +59,13 @@ typedef struct {
  * stay GPU-local, the entry barrier lags one all-to-all, and recv may be any
  * device buffer.  Twice the NVLink bytes: for small shards. */
 #define A2A_PROTO_LL 8
+/* LL128 variant of the low-latency transport (implies A2A_PROTO_LL): lines of
+ * 128 bytes = 120 payload bytes + an 8-byte epoch flag, each line stored and
+ * loaded as ONE warp instruction (8 lanes x 16 bytes), as NCCL's LL128 does
+ * over NVLink.  1.07x the bytes instead of 2x: small-to-medium shards.  Relies
+ * on a warp's 128-byte line store arriving as a unit (tools/ll128_stress.py
+ * validates it on the hardware). */
+#define A2A_PROTO_LL128 16
 
 typedef struct {
   int32_t n_nodes;         /* Digraph.n (must equal ChunkedSchedule.n)      */
@@ -72,7 +79,7 @@ typedef struct {
   int64_t n_ops;
   const int32_t* node_gpu; /* [n_nodes] virtual node -> GPU rank; NULL = all on 0 */
   int32_t n_gpus;          /* >= 1                                           */
-  int32_t flags;           /* A2A_COPY_SELF | A2A_INTERLEAVE | A2A_REUSE_SCRATCH | A2A_PROTO_LL */
+  int32_t flags;           /* A2A_COPY_SELF | A2A_INTERLEAVE | A2A_REUSE_SCRATCH | A2A_PROTO_LL[128] */
   int64_t split_bytes;     /* piece size for A2A_INTERLEAVE (0 = 256 KiB)    */
 } a2a_schedule_desc;
 

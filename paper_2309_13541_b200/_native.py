@@ -17,6 +17,7 @@ A2A_COPY_SELF = 1
 A2A_INTERLEAVE = 2
 A2A_REUSE_SCRATCH = 4
 A2A_PROTO_LL = 8
+A2A_PROTO_LL128 = 16
 A2A_EXEC_COUNT_LINKS = 1
 STATUS = {0: "OK", 1: "INVALID", 2: "EVAL", 3: "CUDA", 4: "TIMEOUT", 5: "STATE", 6: "NOMEM"}
 

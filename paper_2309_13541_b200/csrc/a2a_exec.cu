@@ -58,6 +58,7 @@ struct KParams {
   int64_t ll_half[A2A_MAX_GPUS];           // LL landing region bytes per epoch parity
   int32_t G, rank, nC, T, E, count_links;
   int32_t ll;                              // A2A_PROTO_LL: cross-GPU bytes as LL lines
+  int32_t ll128, smem_ll;                  // A2A_PROTO_LL128 lines; its per-warp gather smem
   int32_t tma_chunk, tma_stages;           // TMA engine: bytes per bulk copy, ring depth
   int32_t sync_mode;                       // bit0: acq_rel (not sc) publish fence; bit1: no
                                            // explicit publish fence; bit2: force .sys at G=1
@@ -298,6 +299,106 @@ __device__ __forceinline__ bool ll_piece(const char* sbase, char* dbase, const D
     }
     if (dll) ll_store(dl + k, v, epoch);
     else plain_store8(dp + b, v, nb);
+  }
+  return true;
+}
+
+// ---- LL128 transport (A2A_PROTO_LL128) ----
+// A 128-byte line = 120 payload bytes + the 8-byte epoch flag (bytes 120..127).
+// A warp moves 4 lines per instruction: lane = 8 * line + seg, seg j holds line
+// bytes [16j, 16j + 16) (seg 7: 8 payload bytes + the flag), each lane one
+// ld/st.volatile.v2.u64.  A reader trusts a line whose flag carries the epoch:
+// the whole line is one warp store (NCCL's LL128 protocol over NVLink; validated
+// on this hardware by tools/ll128_stress.py).  Offsets are payload addresses:
+// payload byte x of a landing region lives at byte 128 * (x / 120) + x % 120.
+__device__ __forceinline__ void st16v(char* p, uint64_t a, uint64_t b) {
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1,%2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void ld16v(const char* p, uint64_t& a, uint64_t& b) {
+  asm volatile("ld.volatile.global.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+// Every lane of the warp: poll its segment of `line` (when `need`) until every
+// needed line of the warp carries epoch E.  Hot polling first, then back off.
+// False (all lanes) on timeout / device error.
+__device__ __forceinline__ bool ll128_poll(const char* line, bool need, int j, uint64_t E,
+                                           uint64_t& a, uint64_t& b, int64_t timeout_ns, int32_t* err) {
+  const int lane = threadIdx.x & 31;
+  uint32_t spins = 0, nap = 0;
+  uint64_t t0 = 0;
+  for (;;) {
+    if (need) ld16v(line + 16 * j, a, b);
+    const uint64_t f = __shfl_sync(0xffffffffu, b, lane | 7);
+    if (__all_sync(0xffffffffu, !need || f == E)) return true;
+    if (++spins > kLLSpin) {
+      nap = nap ? min(2 * nap, 1024u) : 64u;
+      __nanosleep(nap);
+    }
+    if ((spins & 255) == 0) {
+      const uint64_t now = globaltimer();
+      if (t0 == 0) t0 = now;
+      const bool out = (int64_t)(now - t0) > timeout_ns || *(volatile int32_t*)err != 0;
+      if (__any_sync(0xffffffffu, out)) return false;
+    }
+  }
+}
+__device__ __forceinline__ void ld16_plain(const char* s, int nb, uint64_t& a, uint64_t& b) {
+  a = plain_load8(s, min(nb, 8));
+  b = nb > 8 ? plain_load8(s + 8, nb - 8) : 0;
+}
+// One LL128 piece, all threads of the CTA (4 output lines per warp and turn).
+// Sources: plain bytes (send), LL128 lines on a line boundary (a forwarded
+// arrival: a verbatim line copy), or LL128 lines at any payload offset (the
+// warp gathers the source window through shared memory `wsm`, 640 B per warp).
+// Destinations: LL128 lines (whole lines, flag = epoch) or plain bytes (recv).
+__device__ __forceinline__ bool ll128_piece(const char* sbase, char* dbase, const DevPiece& q,
+                                            uint32_t epoch, int64_t timeout_ns, int32_t* err,
+                                            char* wsm) {
+  const bool sll = q.kind & kLLSrc, dll = q.kind & kLLDst;
+  const int64_t n = q.nbytes, NL = (n + 119) / 120, sa = q.src_off;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int j = lane & 7, li = lane >> 3;
+  const uint64_t E = epoch;
+  const int64_t r = sll ? sa % 120 : 0;
+  char* ws = wsm + warp * 640;
+  for (int64_t L0 = (int64_t)warp * 4; L0 < NL; L0 += (int64_t)nw * 4) {
+    const int64_t L = L0 + li;
+    const bool live = L < NL;
+    const int64_t pb = 120 * L + 16 * j;
+    const int nb = live ? (int)max((int64_t)0, min((int64_t)(j == 7 ? 8 : 16), n - pb)) : 0;
+    uint64_t a = 0, b = 0;
+    if (!sll) {
+      if (nb > 0) ld16_plain(sbase + sa + pb, nb, a, b);
+    } else if (r == 0) {
+      if (!ll128_poll(sbase + 128 * (sa / 120 + L), live, j, E, a, b, timeout_ns, err)) return false;
+    } else {
+      const int64_t A = (sa + 120 * L0) / 120;
+      const int64_t Aend = (sa + min(n, 120 * (L0 + 4)) - 1) / 120;
+      uint64_t x = 0, y = 0;
+      bool need = A + li <= Aend;
+      if (!ll128_poll(sbase + 128 * (A + li), need, j, E, x, y, timeout_ns, err)) return false;
+      if (need) {
+        uint64_t* w = reinterpret_cast<uint64_t*>(ws + 120 * li + 16 * j);
+        w[0] = x;
+        if (j < 7) w[1] = y;
+      }
+      need = li == 0 && A + 4 <= Aend;
+      if (!ll128_poll(sbase + 128 * (A + 4), need, j, E, x, y, timeout_ns, err)) return false;
+      if (need) {
+        uint64_t* w = reinterpret_cast<uint64_t*>(ws + 480 + 16 * j);
+        w[0] = x;
+        if (j < 7) w[1] = y;
+      }
+      __syncwarp();
+      if (nb > 0) ld16_plain(ws + r + 120 * li + 16 * j, nb, a, b);
+      __syncwarp();
+    }
+    if (dll) {
+      if (live) st16v(dbase + 128 * (q.dst_off / 120 + L) + 16 * j, a, j == 7 ? E : b);
+    } else if (nb > 0) {
+      char* d = dbase + q.dst_off + pb;
+      plain_store8(d, a, min(nb, 8));
+      if (nb > 8) plain_store8(d + 8, b, nb - 8);
+    }
   }
   return true;
 }
@@ -557,7 +658,10 @@ __device__ __forceinline__ void exec_body(const KParams& p, const uint32_t epoch
           char* db = p.base[q.dst_loc];
           if (q.kind & kLLSrc) sb += (epoch & 1) * p.ll_half[p.rank];
           if (q.kind & kLLDst) db += (epoch & 1) * p.ll_half[q.dst_loc - (1 + 2 * p.G)];
-          if (!ll_piece(sb, db, q, epoch, p.timeout_ns, p.err)) {
+          const bool ok = p.ll128 ? ll128_piece(sb, db, q, epoch, p.timeout_ns, p.err,
+                                                reinterpret_cast<char*>(dsmem + p.smem_ll))
+                                  : ll_piece(sb, db, q, epoch, p.timeout_ns, p.err);
+          if (!ok) {
             atomicCAS(p.err, 0, (int32_t)A2A_ERR_TIMEOUT);
             s_abort = 1;
           }
@@ -1053,6 +1157,7 @@ struct EngineCfg {
   int threads;
   size_t smem;
   int stages, prog_off, batch_off, batch;
+  int ll_off = 0;   // LL128 per-warp gather buffers
 };
 static EngineCfg engine_cfg(const Plan& P) {
   const int TE = P.T_exec;
@@ -1071,19 +1176,21 @@ static EngineCfg engine_cfg(const Plan& P) {
   const size_t prog = ((size_t)TE * sizeof(CtaStep) + 127) & ~(size_t)127;
   if (P.engine == 1) {
     const int batch = 64;
-    const size_t fixed = prog + batch * sizeof(DevPiece) + 1024;
+    const size_t fixed = prog + batch * sizeof(DevPiece) + 1024 + (P.ll128 ? 8 * 640 : 0);
     int S = P.tma_stages;
     while (S > 1 && ((20 * (size_t)S + 127) & ~(size_t)127) + (size_t)S * P.tma_chunk + fixed >
                         227 * 1024)
       --S;
     const size_t ring = ((20 * (size_t)S + 127) & ~(size_t)127) + (size_t)S * P.tma_chunk;
     const size_t po = (ring + 127) & ~(size_t)127;
-    return {(const void*)a2a_exec_kernel<1, 256>, 256, po + prog + batch * sizeof(DevPiece), S,
-            (int)po, (int)(po + prog), batch};
+    const size_t ll = P.ll128 ? (256 / 32) * 640 : 0;
+    return {(const void*)a2a_exec_kernel<1, 256>, 256, po + prog + batch * sizeof(DevPiece) + ll, S,
+            (int)po, (int)(po + prog), batch, (int)(po + prog + batch * sizeof(DevPiece))};
   }
   const int batch = 128;
-  return {(const void*)a2a_exec_kernel<0, 1024>, 1024, prog + batch * sizeof(DevPiece), 0, 0,
-          (int)prog, batch};
+  const size_t ll = P.ll128 ? (1024 / 32) * 640 : 0;
+  return {(const void*)a2a_exec_kernel<0, 1024>, 1024, prog + batch * sizeof(DevPiece) + ll, 0, 0,
+          (int)prog, batch, (int)(prog + batch * sizeof(DevPiece))};
 }
 
 // arena flag region: entry[G] u32 | grab counters u64 @128 | flags @256:
@@ -1480,6 +1587,7 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
     kp.timeout_ns = P.timeout_ns;
     kp.ctl = (uint32_t*)P.d_ctl;
     kp.ll = P.ll ? 1 : 0;
+    kp.ll128 = P.ll128 ? 1 : 0;
     kp.G = P.G;
     kp.rank = P.rank;
     kp.nC = P.nC;
@@ -1495,6 +1603,7 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
     kp.smem_prog = ec.prog_off;
     kp.smem_batch = ec.batch_off;
     kp.batch = ec.batch;
+    kp.smem_ll = ec.ll_off;
     // cooperative launch (all CTAs co-resident: CTAs spin on each other's flags);
     // cudaLaunchKernelExC with the cooperative attribute is stream-capturable
     cudaLaunchConfig_t cfg = {};

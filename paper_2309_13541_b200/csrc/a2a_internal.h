@@ -138,6 +138,8 @@ struct Plan {
   int32_t T_exec = 1;                           // max(T, 1): self copies need a step
   bool reuse = false;                           // scratch liveness reuse (A2A_REUSE_SCRATCH)
   bool ll = false;                              // low-latency cross-GPU transport (A2A_PROTO_LL)
+  bool ll128 = false;                           // ... with 128-byte lines (A2A_PROTO_LL128)
+  int64_t gran = 64;                            // CTA piece boundaries: multiples of gran item bytes
   std::vector<int64_t> ll_off, ll_half;         // per gpu: landing region in scratch, bytes per parity
 
   // ---- layout / tables (host)
@@ -181,6 +183,18 @@ struct Plan {
   void* last_stream = nullptr;
   bool launched = false;
 };
+
+// LL line geometry: payload bytes per line / line bytes.  A2A_PROTO_LL: 8 / 16
+// ({4 B data, epoch, 4 B data, epoch}); A2A_PROTO_LL128: 120 / 128 (payload,
+// then the 8-byte epoch flag).  LL offsets are payload addresses.
+constexpr int64_t kLL128Payload = 120, kLL128Line = 128;
+inline int64_t ll_payload(bool ll128) { return ll128 ? kLL128Payload : 8; }
+inline int64_t ll_line(bool ll128) { return ll128 ? kLL128Line : 16; }
+// byte of the landing region holding payload address x
+inline int64_t ll_byte(bool ll128, int64_t x) {
+  if (ll128) return kLL128Line * (x / kLL128Payload) + x % kLL128Payload;
+  return 16 * (x >> 3) + ((x & 7) < 4 ? (x & 7) : (x & 7) + 4);
+}
 
 // chunk c of an m-byte shard split in Q chunks starts at floor(c*m/Q)
 inline int64_t chunk_off(int64_t c, int64_t m, int64_t Q) {

@@ -102,13 +102,16 @@ static int build_plan(Plan& P, const a2a_schedule_desc* D) {
   if (D->n_ops < 0 || (D->n_ops > 0 && !D->ops)) return fail(A2A_ERR_INVALID, "bad op list");
   if (D->n_gpus < 1 || D->n_gpus > A2A_MAX_GPUS)
     return fail(A2A_ERR_INVALID, "n_gpus must be in [1, 8]");
-  if ((D->flags & A2A_PROTO_LL) && (D->flags & (A2A_INTERLEAVE | A2A_REUSE_SCRATCH)))
+  if ((D->flags & (A2A_PROTO_LL | A2A_PROTO_LL128)) && (D->flags & (A2A_INTERLEAVE | A2A_REUSE_SCRATCH)))
     return fail(A2A_ERR_INVALID, "A2A_PROTO_LL cannot be combined with A2A_INTERLEAVE or A2A_REUSE_SCRATCH");
   const int n = D->n_nodes, T = D->n_steps, E = D->n_edges, G = D->n_gpus;
   const int64_t Q = D->q, m = D->m_bytes;
   P.n = n; P.T = T; P.Q = (int32_t)Q; P.E = E; P.G = G; P.m = m; P.flags = D->flags;
-  P.ll = (D->flags & A2A_PROTO_LL) != 0;
+  P.ll128 = (D->flags & A2A_PROTO_LL128) != 0;
+  P.ll = P.ll128 || (D->flags & A2A_PROTO_LL) != 0;
   if (P.ll) P.engine = 0;   // LL pieces are thread work: the 1024-thread kernel (measured)
+  // LL128: CTA pieces start on line boundaries (120 B) and keep 64-byte alignment
+  P.gran = P.ll128 ? 15 * 64 : 64;
   P.T_exec = std::max(T, 1);
   P.edge_uv.assign(D->edge_uv, D->edge_uv + 2 * (size_t)E);
   P.cap.resize(E, 1.0);
@@ -557,7 +560,8 @@ static int build_ll_items(Plan& P, const std::function<int32_t(int32_t, int32_t)
               dc.kind = kLLSrc | kDecode;
               per[h][t].push_back(dc);
             }
-            cursor[h] += (it.nbytes + 7) & ~(int64_t)7;
+            const int64_t pl = ll_payload(P.ll128);   // slots start on a line
+            cursor[h] += (it.nbytes + pl - 1) / pl * pl;
           }
           per[g][t].push_back(it);
           auto& Ig = P.info[g];
@@ -591,7 +595,8 @@ static int build_ll_items(Plan& P, const std::function<int32_t(int32_t, int32_t)
   P.ll_off.assign(G, 0);
   P.ll_half.assign(G, 0);
   for (int g = 0; g < G; ++g) {
-    P.ll_half[g] = (2 * cursor[g] + 4095) & ~(int64_t)4095;   // line bytes per parity
+    const int64_t lines = cursor[g] / ll_payload(P.ll128);
+    P.ll_half[g] = (lines * ll_line(P.ll128) + 4095) & ~(int64_t)4095;   // line bytes per parity
     P.info[g].scratch_bytes = 2 * P.ll_half[g];               // epoch parity 0 | 1
   }
   return order_items(P, per, 0);
@@ -619,7 +624,7 @@ struct Seg {
 inline int64_t piece_src(const DevItem& it, int64_t x) { return it.src_off + x; }
 inline int64_t piece_dst(const DevItem& it, int64_t x) { return it.dst_off + x; }
 template <typename F>
-void for_each_piece(const GpuTables& tb, int g, int t, int nC, int wr, F&& f) {
+void for_each_piece(const GpuTables& tb, int g, int t, int nC, int wr, int64_t gran, F&& f) {
   const int64_t b0 = tb.step_begin[t], b1 = tb.step_begin[t + 1];
   if (b1 <= b0) return;
   std::vector<int64_t> pw(b1 - b0 + 1, 0);  // weighted prefix
@@ -633,7 +638,7 @@ void for_each_piece(const GpuTables& tb, int g, int t, int nC, int wr, F&& f) {
     const int64_t w = it.dst_gpu != g ? wr : 1, P0 = pw[j - b0];
     if (b <= P0) return 0;
     if (b >= P0 + w * it.nbytes) return it.nbytes;
-    return std::min<int64_t>(it.nbytes, ((b - P0) / w) & ~(int64_t)63);
+    return std::min<int64_t>(it.nbytes, ((b - P0) / w) / gran * gran);
   };
   int64_t k = b0;
   for (int c = 0; c < nC; ++c) {
@@ -660,7 +665,7 @@ int build_sync(Plan& P, int nC) {
   std::vector<std::array<std::vector<Seg>, 2>> segs(G);
   for (int g = 0; g < G; ++g) {
     for (int t = 0; t < TE; ++t) {
-      for_each_piece(P.tables[g], g, t, nC, P.remote_weight, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
+      for_each_piece(P.tables[g], g, t, nC, P.remote_weight, P.gran, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
         if (P.ll) return;   // LL: no flags, consumers poll the lines
         S.dst_mask[g][(size_t)t * nC + c] |= 1u << it.dst_gpu;
         const int cls = (it.dst_loc == loc_recv(it.dst_gpu)) ? 0 : 1;
@@ -693,7 +698,7 @@ int build_sync(Plan& P, int nC) {
     std::vector<std::vector<int32_t>> rcta(G), wg(G);   // producer GPU of each segment
     for (int g = 0; g < G; ++g)
       for (int t = 0; t < TE; ++t)
-        for_each_piece(P.tables[g], g, t, nC, P.remote_weight, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
+        for_each_piece(P.tables[g], g, t, nC, P.remote_weight, P.gran, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
           const int32_t slot = (int32_t)(((int64_t)t * G + g) * nC + c);
           if (it.src_loc == loc_scratch(g, G)) {
             rseg[g].push_back(Seg{it.src_off + x0, it.src_off + x1, t, slot});
@@ -739,7 +744,7 @@ int build_sync(Plan& P, int nC) {
     off.assign((size_t)TE * nC + 1, 0);
     auto& per = per_all[h];
     for (int t = 0; t < TE; ++t) {
-      for_each_piece(P.tables[h], h, t, nC, P.remote_weight, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
+      for_each_piece(P.tables[h], h, t, nC, P.remote_weight, P.gran, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
         if (it.src_loc == loc_send() || P.ll) return;
         const int cls = (it.src_loc == loc_recv(h)) ? 0 : 1;
         const int64_t a = it.src_off + x0, b = it.src_off + x1;
@@ -776,7 +781,7 @@ int build_sync(Plan& P, int nC) {
   for (int g = 0; g < G; ++g) {
     std::vector<std::vector<std::vector<DevPiece>>> per_ct(nC, std::vector<std::vector<DevPiece>>(TE));
     for (int t = 0; t < TE; ++t)
-      for_each_piece(P.tables[g], g, t, nC, P.remote_weight, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
+      for_each_piece(P.tables[g], g, t, nC, P.remote_weight, P.gran, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
         for (int64_t x = x0; x < x1; x += (1LL << 30)) {
           DevPiece pc{};
           pc.src_off = piece_src(it, x);
@@ -832,7 +837,7 @@ static int emulate(Plan& P, int nC, uint8_t* const* send, uint8_t* const* recv, 
   std::vector<Work> work(G, Work(nC, std::vector<std::vector<Piece>>(TE)));
   for (int g = 0; g < G; ++g)
     for (int t = 0; t < TE; ++t) {
-      for_each_piece(P.tables[g], g, t, nC, P.remote_weight, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
+      for_each_piece(P.tables[g], g, t, nC, P.remote_weight, P.gran, [&](int c, const DevItem& it, int64_t x0, int64_t x1) {
         work[g][c][t].push_back(
             Piece{it.src_loc, it.dst_loc, it.kind, piece_src(it, x0), piece_dst(it, x0), x1 - x0});
       });
@@ -843,11 +848,17 @@ static int emulate(Plan& P, int nC, uint8_t* const* send, uint8_t* const* recv, 
     if (loc < 1 + 2 * G) return scratch[loc - 1 - G].data();
     return ll[loc - 1 - 2 * G].data();
   };
-  // LL payload address x -> byte of the line region
-  auto ll_byte = [](int64_t x) -> int64_t { return 16 * (x >> 3) + ((x & 7) < 4 ? (x & 7) : (x & 7) + 4); };
+  const bool l128 = P.ll128;
+  const int64_t PL = ll_payload(l128), LB = ll_line(l128);
   auto lines_ready = [&](int g, const Piece& pc) {
     const uint8_t* L = base(g, pc.src_loc);
-    for (int64_t k = pc.src >> 3; k <= (pc.src + pc.n - 1) >> 3; ++k) {
+    for (int64_t k = pc.src / PL; k <= (pc.src + pc.n - 1) / PL; ++k) {
+      if (l128) {
+        uint64_t f;
+        std::memcpy(&f, L + LB * k + kLL128Payload, 8);
+        if (f != kEpoch) return false;
+        continue;
+      }
       uint32_t f0, f1;
       std::memcpy(&f0, L + 16 * k + 4, 4);
       std::memcpy(&f1, L + 16 * k + 12, 4);
@@ -885,12 +896,21 @@ static int emulate(Plan& P, int nC, uint8_t* const* send, uint8_t* const* recv, 
     std::vector<uint8_t> buf((size_t)pc.n);
     const uint8_t* sb = base(g, pc.src_loc);
     if (pc.kind & kLLSrc) {
-      for (int64_t j = 0; j < pc.n; ++j) buf[j] = sb[ll_byte(pc.src + j)];
+      for (int64_t j = 0; j < pc.n; ++j) buf[j] = sb[ll_byte(l128, pc.src + j)];
     } else {
       std::memcpy(buf.data(), sb + pc.src, (size_t)pc.n);
     }
     uint8_t* db = base(g, pc.dst_loc);
-    if (pc.kind & kLLDst) {   // whole lines (dst payload address is a multiple of 8)
+    if ((pc.kind & kLLDst) && l128) {   // whole 128-byte lines (dst on a line boundary)
+      for (int64_t k = 0; k < (pc.n + PL - 1) / PL; ++k) {
+        uint8_t line[kLL128Line] = {0};
+        const int64_t w = std::min<int64_t>(PL, pc.n - PL * k);
+        std::memcpy(line, buf.data() + PL * k, (size_t)w);
+        const uint64_t f = kEpoch;
+        std::memcpy(line + kLL128Payload, &f, 8);
+        std::memcpy(db + LB * (pc.dst / PL + k), line, kLL128Line);
+      }
+    } else if (pc.kind & kLLDst) {   // whole lines (dst payload address is a multiple of 8)
       for (int64_t k = 0; k < (pc.n + 7) / 8; ++k) {
         uint8_t line[16] = {0};
         const int64_t w = std::min<int64_t>(8, pc.n - 8 * k);
@@ -1579,15 +1599,17 @@ int a2a_plan_check_bounds(a2a_plan* plan, int32_t num_ctas) {
       if (loc >= 1 && loc < 1 + G) return P.info[loc - 1].recv_bytes;
       if (loc >= 1 + G && loc < 1 + 2 * G) return P.info[loc - 1 - G].scratch_bytes;
       // LL landing region: payload capacity (lines are 16 bytes per 8 payload bytes)
-      if (P.ll && loc >= 1 + 2 * G && loc < 1 + 3 * G) return P.ll_half[loc - 1 - 2 * G] / 2;
+      if (P.ll && loc >= 1 + 2 * G && loc < 1 + 3 * G)
+        return P.ll_half[loc - 1 - 2 * G] / ll_line(P.ll128) * ll_payload(P.ll128);
       return -1;
     };
     auto check = [&](int g, int sl, int64_t so, int dl, int64_t dof, int64_t n, int kind = kCopy) -> bool {
       const bool sll = sl >= loc_ll(0, G) && sl < loc_ll(G, G), dll = dl >= loc_ll(0, G) && dl < loc_ll(G, G);
       if (sll != ((kind & kLLSrc) != 0) || dll != ((kind & kLLDst) != 0)) return false;
-      if (dll && (dof & 7)) return false;                         // stores whole lines
+      const int64_t PL = ll_payload(P.ll128);
+      if (dll && (dof % PL)) return false;                        // stores whole lines
       const int64_t ss = size_of(g, sl), ds = size_of(g, dl);
-      const int64_t nd = dll ? ((n + 7) & ~(int64_t)7) : n;
+      const int64_t nd = dll ? (n + PL - 1) / PL * PL : n;
       return n > 0 && ss >= 0 && ds >= 0 && so >= 0 && dof >= 0 && so + n <= ss && dof + nd <= ds;
     };
     char buf[200];

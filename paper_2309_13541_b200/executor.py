@@ -135,17 +135,19 @@ class Plan:
         if reuse_scratch is None:
             reuse_scratch = os.environ.get("A2A_REUSE_SCRATCH", "0") == "1"
         self.reuse_scratch = bool(reuse_scratch)
-        # cross-GPU transport: "simple" (peer stores + release/acquire flags) or
-        # "ll" (16-byte {data, epoch} lines polled by the receiving GPU; small shards)
+        # transport: "simple" (peer stores + release/acquire flags), "ll" (16-byte
+        # {data, epoch} lines polled by the receiving GPU; small shards) or
+        # "ll128" (128-byte lines, 120 payload bytes + epoch flag; medium shards)
         if protocol is None:
             protocol = os.environ.get("A2A_PROTO", "simple").strip().lower() or "simple"
-        if protocol not in ("simple", "ll"):
-            raise ValueError("protocol must be 'simple' or 'll'")
+        if protocol not in ("simple", "ll", "ll128"):
+            raise ValueError("protocol must be 'simple', 'll' or 'll128'")
         self.protocol = protocol
         d.flags = (N.A2A_COPY_SELF if copy_self else 0) | \
             (N.A2A_INTERLEAVE if order == "interleaved" else 0) | \
             (N.A2A_REUSE_SCRATCH if reuse_scratch else 0) | \
-            (N.A2A_PROTO_LL if protocol == "ll" else 0)
+            (N.A2A_PROTO_LL if protocol == "ll" else 0) | \
+            (N.A2A_PROTO_LL128 if protocol == "ll128" else 0)
         d.split_bytes = int(split_bytes)
         h = C.c_void_p()
         rc = N.lib.a2a_plan_create(C.byref(d), C.byref(h))

@@ -28,14 +28,15 @@ def test_every_copy_range_in_bounds(name, G, sched, reuse, artifacts):
 
 @pytest.mark.parametrize("name", NAMES)
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
-def test_ll_ranges_in_bounds(name, G, artifacts):
+@pytest.mark.parametrize("proto", ["ll", "ll128"])
+def test_ll_ranges_in_bounds(name, G, proto, artifacts):
     """A2A_PROTO_LL pieces: LL sources/destinations inside the landing regions
     (payload addresses, whole destination lines), plain stores GPU-local."""
     a = artifacts(name)
     if G > a.g.n:
         pytest.skip("more GPUs than nodes")
     for m in (1, 1000 + 7, 65536):
-        with Plan(a.g, a.sched, m=m, n_gpus=G, placement="optimized", protocol="ll") as p:
+        with Plan(a.g, a.sched, m=m, n_gpus=G, placement="optimized", protocol=proto) as p:
             assert p.check_bounds(37)
 
 

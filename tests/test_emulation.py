@@ -233,7 +233,8 @@ def test_weighted_split_interleavings(name, G, w, artifacts):
                                   "ts_torus2x4", "ts_gk8_2", "ts_torus3x3", "ts_ring3"])
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
 @pytest.mark.parametrize("nC", [1, 5, 148])
-def test_ll_interleavings_deliver_transpose(name, G, nC, artifacts):
+@pytest.mark.parametrize("proto", ["ll", "ll128"])
+def test_ll_interleavings_deliver_transpose(name, G, nC, proto, artifacts):
     """LL everywhere: every hop lands as lines, forwarders poll them, same-step
     decodes of remote final hops come last in each CTA step; lines in the
     device format; odd shard sizes exercise partial lines and unaligned
@@ -241,9 +242,9 @@ def test_ll_interleavings_deliver_transpose(name, G, nC, artifacts):
     a = artifacts(name)
     if G > a.g.n:
         pytest.skip("more GPUs than nodes")
-    for seed, m in enumerate((4096, 1000, 77)):
+    for seed, m in enumerate((4096, 1000, 77, 123457)):
         send = make_send(a.g.n, m, seed=seed)
-        with Plan(a.g, a.sched, m=m, n_gpus=G, protocol="ll") as p:
+        with Plan(a.g, a.sched, m=m, n_gpus=G, protocol=proto) as p:
             nodes = [local_nodes(p, g) for g in range(G)]
             recvs = p.emulate([send[ns] for ns in nodes], num_ctas=nC, seed=seed)
             p.check_bounds(nC)
@@ -262,15 +263,29 @@ def test_ll_interleavings_deliver_transpose(name, G, nC, artifacts):
 
 
 @pytest.mark.parametrize("name,G", [("torus4x4x4", 8), ("gk64_4", 4)])
-def test_ll_n64_interleavings(name, G, artifacts):
+@pytest.mark.parametrize("proto", ["ll", "ll128"])
+def test_ll_n64_interleavings(name, G, proto, artifacts):
     a = artifacts(name)
     send = make_send(a.g.n, 512, seed=3)
-    with Plan(a.g, a.sched, m=512, n_gpus=G, protocol="ll") as p:
+    with Plan(a.g, a.sched, m=512, n_gpus=G, protocol=proto) as p:
         nodes = [local_nodes(p, g) for g in range(G)]
         recvs = p.emulate([send[ns] for ns in nodes], num_ctas=148, seed=3)
     want = np.swapaxes(send, 0, 1)
     for g in range(G):
         assert np.array_equal(recvs[g], want[nodes[g]])
+
+
+def test_ll128_landing_region_and_lines(artifacts):
+    """LL128 slots start on 120-byte payload boundaries, the landing region is
+    128 bytes per 120 payload bytes (vs 16 per 8 for LL): ~1.07x the payload."""
+    a = artifacts("gk8_2")
+    m = 1 << 20
+    with Plan(a.g, a.sched, m=m, n_gpus=4, protocol="ll128") as p128, \
+            Plan(a.g, a.sched, m=m, n_gpus=4, protocol="ll") as p16:
+        for g in range(4):
+            s128, s16 = p128.gpu_info(g)["scratch_bytes"], p16.gpu_info(g)["scratch_bytes"]
+            assert s128 < 0.56 * s16
+        assert np.array_equal(p128.link_bytes(), p16.link_bytes())
 
 
 def test_ll_rejects(artifacts):

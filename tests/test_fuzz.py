@@ -30,7 +30,7 @@ def test_random_schedule_emulation(seed):
                                ("simple", "cp", False), ("simple", "mix", True),
                                ("simple", "ready", False), ("simple", "ready", True),
                                ("simple", "spread", False),
-                               ("ll", "static", False)):
+                               ("ll", "static", False), ("ll128", "static", False)):
         with Plan(g, sched, m=m, n_gpus=G, placement=placement, protocol=proto,
                   reuse_scratch=reuse) as p:
             if mode != "static":
@@ -58,7 +58,8 @@ def test_random_schedule_gpu(seed):
                                     ("simple", "cp", "tma", 0), ("simple", "dynamic", "lsu", 1),
                                     ("simple", "list", "tma", 2), ("simple", "ready", "tma", 0),
                                     ("simple", "ready", "lsu", 3), ("ll", "static", "lsu", 0),
-                                    ("ll", "static", "tma", 3)):
+                                    ("ll", "static", "tma", 3), ("ll128", "static", "lsu", 0),
+                                    ("ll128", "static", "tma", 2)):
         with Plan(g, sched, m=m, protocol=proto) as p:
             p.set_engine(engine)
             if mode != "static":
@@ -88,7 +89,8 @@ def test_random_schedule_two_gpus(seed):
     placement[0], placement[-1] = 0, 1
     send = make_send(g.n, m, seed=seed)
     _, want, _ = replay_bytes(g, sched, send, m)
-    for proto, mode in (("simple", "static"), ("simple", "cp"), ("simple", "ready"), ("ll", "static")):
+    for proto, mode in (("simple", "static"), ("simple", "cp"), ("simple", "ready"), ("ll", "static"),
+                        ("ll128", "static")):
         plans = []
         for r in range(2):
             p = Plan(g, sched, m=m, n_gpus=2, placement=placement, protocol=proto)

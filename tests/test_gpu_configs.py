@@ -97,10 +97,10 @@ def test_torus2x4_1mib_bit_exact(artifacts):
     ref = np.zeros((a.sched.nsteps, len(a.g.edges)), dtype=np.int64)
     for (t, e), x in ob.items():
         ref[t, e] = x
-    for sched in ("static", "cp:1048576", "ll"):
-        proto = "ll" if sched == "ll" else "simple"
+    for sched in ("static", "cp:1048576", "ll", "ll128"):
+        proto = sched if sched in ("ll", "ll128") else "simple"
         with Plan(a.g, a.sched, m=m, protocol=proto) as p:
-            if sched != "ll":
+            if proto == "simple":
                 p.set_schedule_spec(sched)
             p.bind(0)
             s = torch.from_numpy(send).cuda()
@@ -131,7 +131,7 @@ def test_torus4x4x4_4mib_transpose_and_counters(sched, artifacts):
 
 
 @pytest.mark.parametrize("name", ["gk8_2", "torus2x4_h2", "ts_hypercube3"])
-@pytest.mark.parametrize("sched", ["static", "cp:1048576", "spread:1048576", "ll"])
+@pytest.mark.parametrize("sched", ["static", "cp:1048576", "spread:1048576", "ll", "ll128"])
 def test_without_self_copy(name, sched, artifacts):
     """copy_self=False, as bench.py times it: every s != d shard bit-exact vs
     the oracle, the self rows of recv untouched (the reference transpose
@@ -144,8 +144,8 @@ def test_without_self_copy(name, sched, artifacts):
     send = make_send(a.g.n, m, seed=3)
     _, want, _ = replay_bytes(a.g, a.sched, send, m, copy_self=False)
     with Plan(a.g, a.sched, m=m, copy_self=False,
-              protocol="ll" if sched == "ll" else "simple") as p:
-        if sched != "ll":
+              protocol=sched if sched in ("ll", "ll128") else "simple") as p:
+        if sched not in ("ll", "ll128"):
             p.set_schedule_spec(sched)
         p.bind(0)
         s = torch.from_numpy(send).cuda()

@@ -254,7 +254,7 @@ def test_call_order_errors(artifacts):
 
 
 @pytest.mark.parametrize("name", ["gk8_2", "torus2x4_h2", "ts_hypercube3"])
-@pytest.mark.parametrize("sched", ["static", "cp", "mix", "ll"])
+@pytest.mark.parametrize("sched", ["static", "cp", "mix", "ll", "ll128"])
 @pytest.mark.parametrize("engine", ["tma", "lsu"])
 def test_cuda_graph_capture_and_replay(name, sched, engine, artifacts):
     """Executes captured into a CUDA graph replay as fresh all-to-alls: the
@@ -264,9 +264,9 @@ def test_cuda_graph_capture_and_replay(name, sched, engine, artifacts):
     from paper_2309_13541_b200.executor import Plan
     a = artifacts(name)
     m = 4096 + 64
-    with Plan(a.g, a.sched, m=m, protocol="ll" if sched == "ll" else "simple") as p:
+    with Plan(a.g, a.sched, m=m, protocol=sched if sched in ("ll", "ll128") else "simple") as p:
         p.set_engine(engine)
-        if sched not in ("static", "ll"):
+        if sched not in ("static", "ll", "ll128"):
             p.set_schedule(sched, 4096)
         p.bind(0)
         s = torch.empty((a.g.n, a.g.n, m), dtype=torch.uint8, device="cuda")
@@ -290,16 +290,17 @@ def test_cuda_graph_capture_and_replay(name, sched, engine, artifacts):
 
 
 @pytest.mark.parametrize("name", SMALL)
-@pytest.mark.parametrize("m", [7, 1000, 4096 + 5, 65536])
+@pytest.mark.parametrize("m", [7, 1000, 4096 + 5, 65536, 123457])
 @pytest.mark.parametrize("engine", ["tma", "lsu"])
-def test_ll_protocol_bit_exact(name, m, engine, artifacts):
+@pytest.mark.parametrize("proto", ["ll", "ll128"])
+def test_ll_protocol_bit_exact(name, m, engine, proto, artifacts):
     """A2A_PROTO_LL on one GPU: every hop through polled landing lines (no
     flags); bit-exact vs the oracle over repeated executes (both landing
     parities), device link counters equal the schedule."""
     from paper_2309_13541_b200.executor import Plan
     from replay_bytes import replay_bytes
     a = artifacts(name)
-    with Plan(a.g, a.sched, m=m, protocol="ll") as p:
+    with Plan(a.g, a.sched, m=m, protocol=proto) as p:
         p.set_engine(engine)
         p.bind(0)
         p.set_timeout(10.0)
@@ -315,14 +316,15 @@ def test_ll_protocol_bit_exact(name, m, engine, artifacts):
 
 
 @pytest.mark.parametrize("name,m", [("torus4x4x4", 4096 + 8), ("gk64_4", 2048 + 5), ("gk64_4_h2", 1000)])
-def test_ll_protocol_n64(name, m, artifacts):
+@pytest.mark.parametrize("proto", ["ll", "ll128"])
+def test_ll_protocol_n64(name, m, proto, artifacts):
     """LL on the N=64 schedules (13 943 / 27k hop-ops, forwards split across
     several arrivals): transpose on one GPU, twice (both landing parities)."""
     from paper_2309_13541_b200.executor import Plan
     a = artifacts(name)
     g = torch.Generator(device="cuda").manual_seed(9)
     s = torch.randint(0, 256, (64, 64, m), dtype=torch.uint8, device="cuda", generator=g)
-    with Plan(a.g, a.sched, m=m, protocol="ll") as p:
+    with Plan(a.g, a.sched, m=m, protocol=proto) as p:
         p.bind(0)
         for _ in range(2):
             r = torch.zeros_like(s)

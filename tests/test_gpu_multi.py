@@ -75,10 +75,10 @@ def _rank_main(rank, world, port, name, m, reps, q, engine="lsu", sched="static"
         connect(plan)
         nodes = local_nodes(plan, rank)
         # LL: only local CTAs write recv, so any device buffer works
-        recv = plan.recv_buffer() if proto != "ll" else torch.empty(
+        recv = plan.recv_buffer() if proto not in ("ll", "ll128") else torch.empty(
             (len(nodes), a.g.n, m), dtype=torch.uint8, device=f"cuda:{rank}")
         ok = True
-        if proto == "ll":
+        if proto in ("ll", "ll128"):
             # back-to-back all-to-alls, no host sync in between: exercises the
             # epoch-parity landing regions and the lagged entry flags
             K = 6
@@ -157,10 +157,11 @@ def test_multiprocess_ipc(world, name, m, engine):
 @pytest.mark.parametrize("name,m,engine", [
     ("torus2x4", 4096 + 7, "tma"), ("gk8_2", 65536, "tma"), ("hypercube3", 4096, "tma"),
     ("torus4x4x4", 2048, "tma"), ("ts_gk8_2", 1000, "tma"), ("gk8_2", 20000, "lsu"),
-    ("torus2x4", 333, "lsu")])
-def test_multiprocess_ll(world, name, m, engine):
-    """A2A_PROTO_LL across GPUs: bit-exact recv (also back-to-back without host
-    sync), device link counters equal the schedule."""
+    ("torus2x4", 333, "lsu"), ("hypercube3", 1 << 20, "lsu")])
+@pytest.mark.parametrize("proto", ["ll", "ll128"])
+def test_multiprocess_ll(world, name, m, engine, proto):
+    """A2A_PROTO_LL / LL128 across GPUs: bit-exact recv (also back-to-back
+    without host sync), device link counters equal the schedule."""
     if _ngpu() < world:
         pytest.skip(f"needs {world} GPUs")
     import torch.multiprocessing as mp
@@ -168,7 +169,7 @@ def test_multiprocess_ll(world, name, m, engine):
     q = ctx.Queue()
     port = _port()
     ps = [ctx.Process(target=_rank_main,
-                      args=(r, world, port, name, m, 3, q, engine, "static", False, "ll"))
+                      args=(r, world, port, name, m, 3, q, engine, "static", False, proto))
           for r in range(world)]
     for p in ps:
         p.start()
@@ -181,7 +182,8 @@ def test_multiprocess_ll(world, name, m, engine):
 
 
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("proto,sched", [("simple", "static"), ("ll", "static"), ("simple", "cp")])
+@pytest.mark.parametrize("proto,sched", [("simple", "static"), ("ll", "static"), ("ll128", "static"),
+                                         ("simple", "cp")])
 def test_multiprocess_cuda_graph(world, proto, sched):
     """Executes captured into CUDA graphs on every rank, replayed repeatedly."""
     if _ngpu() < world:

@@ -22,6 +22,10 @@ import json
 import os
 import time
 
+# kernels that wait on each other must be loaded before either runs (lazy
+# module loading can block a launch until the running kernel finishes)
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
 import torch
 from torch.utils.cpp_extension import load_inline
 
@@ -44,7 +48,7 @@ __device__ __forceinline__ void ld16(const uint64_t* p, uint64_t& a, uint64_t& b
 __device__ __forceinline__ uint64_t gtime() {
   uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t;
 }
-constexpr uint64_t kTimeout = 20000000000ULL;   // 20 s: a stuck spin bails out (never a hang)
+constexpr uint64_t kTimeout = 10000000000ULL;   // 10 s: a stuck spin bails out (never a hang)
 __device__ __forceinline__ unsigned long long ldv(const unsigned long long* p) {
   unsigned long long v; asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory"); return v;
 }
@@ -148,6 +152,13 @@ def main():
         mod.enable_peer(0, 1)
         mod.enable_peer(1, 0)
         cases.append(("remote", 0, 1))
+    # warm-up: load both kernels on both devices before any pair runs concurrently
+    for d in range(min(2, torch.cuda.device_count())):
+        z = torch.zeros(64, dtype=torch.int64, device=f"cuda:{d}")
+        st = torch.cuda.Stream(d)
+        mod.run_consumer(z, z[:1], z[1:2], z[2:3], 0, 0, d, 1, st.cuda_stream)
+        mod.run_producer(z, z[:1], 0, 0, 1, d, 1, st.cuda_stream)
+        torch.cuda.synchronize(d)
     for name, pdev, cdev in cases:
         nl = a.lines
         lines = torch.zeros(2 * nl * 16, dtype=torch.int64, device=f"cuda:{cdev}")
