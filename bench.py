@@ -339,7 +339,8 @@ def balanced_artifact(art, m, G, placement):
                     path_sched=art.path_sched, aug_graph=art.aug_graph), gpu
 
 
-LL_MAX_SHARD = 1 << 20   # autotune tries the LL transport up to this shard size
+LL_MAX_SHARD = 1 << 20       # autotune tries the LL transport up to this shard size
+LL128_MAX_SHARD = 16 << 20   # ... and LL128 (1.07x the bytes) up to this one
 
 
 def make_plan(art, m, G, placement, schedule, copy_self=False):
@@ -362,7 +363,7 @@ def default_candidates(G, m):
     single merged queue (`mix`; at G > 2 `spread`, which interleaves each
     step's NVLink units over their destination GPUs)."""
     return ("static", "cp:1048576", "spread:1048576" if G > 2 else "mix:1048576") + (
-        ("ll",) if m <= LL_MAX_SHARD else ())
+        ("ll",) if m <= LL_MAX_SHARD else ()) + (("ll128",) if m <= LL128_MAX_SHARD else ())
 
 
 def _node_send(dev, s, n, m, salt=0):

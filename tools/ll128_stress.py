@@ -54,7 +54,8 @@ __device__ __forceinline__ unsigned long long ldv(const unsigned long long* p) {
 }
 
 // lines: [2 parities][nl][16 u64]; done: consumer CTAs finished per epoch (cumulative)
-__global__ void producer(uint64_t* lines, const unsigned long long* done, long long nl, int epochs, int ncons) {
+__device__ void producer_body(uint64_t* lines, const unsigned long long* done, long long nl, int epochs,
+                              int ncons, int bid, int nblk) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int j = lane & 7;
   __shared__ int s_abort;
@@ -72,7 +73,7 @@ __global__ void producer(uint64_t* lines, const unsigned long long* done, long l
       if (s_abort) return;
     }
     uint64_t* buf = lines + (size_t)(e & 1) * nl * 16;
-    for (long long L0 = ((long long)blockIdx.x * nw + warp) * 4; L0 < nl; L0 += (long long)gridDim.x * nw * 4) {
+    for (long long L0 = ((long long)bid * nw + warp) * 4; L0 < nl; L0 += (long long)nblk * nw * 4) {
       const long long L = L0 + (lane >> 3);
       if (L >= nl) continue;
       const uint64_t a = word(e, L, 2 * j);
@@ -82,14 +83,15 @@ __global__ void producer(uint64_t* lines, const unsigned long long* done, long l
   }
 }
 
-__global__ void consumer(const uint64_t* lines, unsigned long long* done, unsigned long long* bad,
-                         unsigned long long* checked, long long nl, int epochs) {
+__device__ void consumer_body(const uint64_t* lines, unsigned long long* done, unsigned long long* bad,
+                              unsigned long long* checked, long long nl, int epochs, int bid, int nblk) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int j = lane & 7;
   unsigned long long nbad = 0, nchk = 0;
+  if ((long long)bid * nw * 4 >= nl) return;   // no lines: not counted in `done`
   for (int e = 1; e <= epochs; ++e) {
     const uint64_t* buf = lines + (size_t)(e & 1) * nl * 16;
-    for (long long L0 = ((long long)blockIdx.x * nw + warp) * 4; L0 < nl; L0 += (long long)gridDim.x * nw * 4) {
+    for (long long L0 = ((long long)bid * nw + warp) * 4; L0 < nl; L0 += (long long)nblk * nw * 4) {
       const long long L = L0 + (lane >> 3);
       const bool live = L < nl;
       uint64_t a = 0, b = 0;
@@ -114,6 +116,26 @@ __global__ void consumer(const uint64_t* lines, unsigned long long* done, unsign
   atomicAdd(checked, nchk);
 }
 
+__global__ void producer(uint64_t* lines, const unsigned long long* done, long long nl, int epochs, int ncons) {
+  producer_body(lines, done, nl, epochs, ncons, blockIdx.x, gridDim.x);
+}
+__global__ void consumer(const uint64_t* lines, unsigned long long* done, unsigned long long* bad,
+                         unsigned long long* checked, long long nl, int epochs) {
+  consumer_body(lines, done, bad, checked, nl, epochs, blockIdx.x, gridDim.x);
+}
+// local case: one launch, CTAs [0, np) produce, the rest consume (co-resident by construction)
+__global__ void both(uint64_t* lines, unsigned long long* done, unsigned long long* bad,
+                     unsigned long long* checked, long long nl, int epochs, int np, int ncons) {
+  if ((int)blockIdx.x < np) producer_body(lines, done, nl, epochs, ncons, blockIdx.x, np);
+  else consumer_body(lines, done, bad, checked, nl, epochs, blockIdx.x - np, gridDim.x - np);
+}
+void run_both(torch::Tensor lines, torch::Tensor done, torch::Tensor bad, torch::Tensor chk,
+              int64_t nl, int64_t epochs, int64_t np, int64_t nc, int64_t ncons, int64_t dev, int64_t stream) {
+  cudaSetDevice((int)dev);
+  both<<<(int)(np + nc), 256, 0, (cudaStream_t)stream>>>((uint64_t*)lines.data_ptr(),
+      (unsigned long long*)done.data_ptr(), (unsigned long long*)bad.data_ptr(),
+      (unsigned long long*)chk.data_ptr(), nl, (int)epochs, (int)np, (int)ncons);
+}
 void enable_peer(int64_t dev, int64_t peer) {
   cudaSetDevice((int)dev);
   if (cudaDeviceEnablePeerAccess((int)peer, 0) != cudaSuccess) cudaGetLastError();
@@ -133,6 +155,7 @@ void run_consumer(torch::Tensor lines, torch::Tensor done, torch::Tensor bad, to
 }
 """
 CPP = ("void enable_peer(int64_t dev, int64_t peer);\n"
+       "void run_both(torch::Tensor lines, torch::Tensor done, torch::Tensor bad, torch::Tensor chk, int64_t nl, int64_t epochs, int64_t np, int64_t nc, int64_t ncons, int64_t dev, int64_t stream);\n"
        "void run_producer(torch::Tensor lines, torch::Tensor done, int64_t nl, int64_t epochs, int64_t ncons, int64_t dev, int64_t ctas, int64_t stream);\n"
        "void run_consumer(torch::Tensor lines, torch::Tensor done, torch::Tensor bad, torch::Tensor chk, int64_t nl, int64_t epochs, int64_t dev, int64_t ctas, int64_t stream);")
 
@@ -143,7 +166,7 @@ def main():
     ap.add_argument("--lines", type=int, default=65536)
     a = ap.parse_args()
     mod = load_inline("ll128_stress", cpp_sources=CPP, cuda_sources=SRC,
-                      functions=["enable_peer", "run_producer", "run_consumer"],
+                      functions=["enable_peer", "run_producer", "run_consumer", "run_both"],
                       extra_cuda_cflags=["-gencode", "arch=compute_100a,code=sm_100a", "-O3"],
                       verbose=False)
     out = {"epochs": a.epochs, "lines": a.lines}
@@ -167,9 +190,13 @@ def main():
         chk = torch.zeros(1, dtype=torch.int64, device=f"cuda:{cdev}")
         sp, sc = torch.cuda.Stream(pdev), torch.cuda.Stream(cdev)
         pc, cc = (64, 64) if pdev == cdev else (132, 132)
+        cc = min(cc, (nl + 31) // 32)             # consumer CTAs that own lines (8 warps x 4)
         t0 = time.time()
-        mod.run_consumer(lines, done, bad, chk, nl, a.epochs, cdev, cc, sc.cuda_stream)
-        mod.run_producer(lines, done, nl, a.epochs, cc, pdev, pc, sp.cuda_stream)
+        if pdev == cdev:
+            mod.run_both(lines, done, bad, chk, nl, a.epochs, pc, 64, cc, cdev, sc.cuda_stream)
+        else:
+            mod.run_consumer(lines, done, bad, chk, nl, a.epochs, cdev, cc, sc.cuda_stream)
+            mod.run_producer(lines, done, nl, a.epochs, cc, pdev, pc, sp.cuda_stream)
         torch.cuda.synchronize(pdev)
         torch.cuda.synchronize(cdev)
         dt = time.time() - t0

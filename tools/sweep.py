@@ -47,8 +47,9 @@ def main(argv=None):
     ap.add_argument("--num-ctas", type=int, default=0)
     ap.add_argument("--schedule", default=None,
                     help="static | dynamic[:bytes] | auto; default: $A2A_SCHED or static")
-    ap.add_argument("--lowering", default="hop", choices=["hop", "balanced"],
-                    help="path -> step lowering (bench.balanced_artifact for 'balanced')")
+    ap.add_argument("--lowering", default="hop", choices=["hop", "balanced", "auto"],
+                    help="path -> step lowering (bench.balanced_artifact for 'balanced'; 'auto' "
+                         "with --schedule auto: time both, keep the faster, as bench.py does)")
     a = ap.parse_args(argv)
     if a.placement not in ("optimized", "contiguous"):
         a.placement = [int(x) for x in a.placement.split(",")]
@@ -71,6 +72,7 @@ def main(argv=None):
         else:
             art = load_artifact(name)
             placement = a.placement
+            auto_low = a.lowering == "auto" and (case_sched or a.schedule) == "auto"
             if a.lowering == "balanced" and art.routes is not None:
                 art, placement = bench.balanced_artifact(art, m, ctx.world, a.placement)
             rec["lowering"] = a.lowering if art.routes is not None else "ts artifact"
@@ -83,7 +85,14 @@ def main(argv=None):
                 t0 = time.time()
                 sched = case_sched or a.schedule or os.environ.get("A2A_SCHED") or "static"
                 tune = None
-                if sched == "auto":
+                if sched == "auto" and auto_low:
+                    ns = argparse.Namespace(schedule="auto", lowering="auto", num_ctas=a.num_ctas,
+                                            placement=a.placement if isinstance(a.placement, str)
+                                            else "optimized")
+                    art, placement, sched, low, tune, _ = bench.choose_execution(ctx, ns, art, m,
+                                                                                 placement)
+                    rec["lowering"] = low
+                elif sched == "auto":
                     sched, tune = bench.autotune_schedule(ctx, art, m, placement=placement,
                                                           num_ctas=a.num_ctas)
                 r = bench.measure(ctx, art, m, a.steps, a.warmup, nccl=not a.no_nccl,
