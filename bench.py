@@ -343,11 +343,23 @@ LL_MAX_SHARD = 1 << 20       # autotune tries the LL transport up to this shard 
 LL128_MAX_SHARD = 16 << 20   # ... and LL128 (1.07x the bytes) up to this one
 
 
+def spec_ctas(spec, num_ctas=0):
+    """("<spec>", CTA count) of an execution-schedule spec with an optional
+    "@<CTAs>" suffix (e.g. "ll@16": the LL transport on 16 CTAs per GPU, for
+    tiny shards where launching 148 CTAs costs more than it moves)."""
+    if spec and "@" in spec:
+        s, c = spec.split("@")
+        return s, int(c)
+    return spec, num_ctas
+
+
 def make_plan(art, m, G, placement, schedule, copy_self=False):
     """Plan for an execution-schedule spec: "static", "<dyn mode>:<unit bytes>"
     (optionally ":<R>": R CTAs pinned to the NVLink queue, the rest to the HBM
-    queue), or "ll" (static programs + the LL cross-GPU transport)."""
+    queue), or "ll" / "ll128" (static programs + the LL / LL128 cross-GPU
+    transport); an "@<CTAs>" suffix is the bind's CTA count (spec_ctas)."""
     from paper_2309_13541_b200.executor import Plan
+    schedule, _ = spec_ctas(schedule)
     if schedule in ("ll", "ll128"):
         return Plan(art.g, art.sched, m=m, n_gpus=G, placement=placement, protocol=schedule,
                     copy_self=copy_self)
@@ -363,7 +375,8 @@ def default_candidates(G, m):
     single merged queue (`mix`; at G > 2 `spread`, which interleaves each
     step's NVLink units over their destination GPUs)."""
     return ("static", "cp:1048576", "spread:1048576" if G > 2 else "mix:1048576") + (
-        ("ll",) if m <= LL_MAX_SHARD else ()) + (("ll128",) if m <= LL128_MAX_SHARD else ())
+        ("ll",) if m <= LL_MAX_SHARD else ()) + (("ll@16",) if m <= 65536 else ()) + (
+        ("ll128",) if m <= LL128_MAX_SHARD else ())
 
 
 def _node_send(dev, s, n, m, salt=0):
@@ -406,7 +419,7 @@ def autotune_schedule(ctx, art, m, placement="optimized", num_ctas=0, trials=5,
         plan = make_plan(art, m, G, placement, cand, copy_self=copy_self)
         nomem = ""
         try:
-            plan.bind(ctx.rank, device=ctx.local, num_ctas=num_ctas)
+            plan.bind(ctx.rank, device=ctx.local, num_ctas=spec_ctas(cand, num_ctas)[1])
         except ExecutorError as ex:          # e.g. LL landing regions of a huge schedule
             if "NOMEM" not in str(ex):
                 raise
@@ -423,9 +436,19 @@ def autotune_schedule(ctx, art, m, placement="optimized", num_ctas=0, trials=5,
         send = torch.stack([_node_send(dev, s, n, m, salt=7) for s in nodes])
         recv = plan.recv_buffer() if G > 1 else torch.empty_like(send)
         stream = torch.cuda.current_stream(dev)
-        for _ in range(3):
-            plan.execute(send, recv, stream=stream)
-        plan.sync()
+        err = ""
+        try:                 # a device-side failure (flag-wait timeout) drops the candidate
+            for _ in range(3):
+                plan.execute(send, recv, stream=stream)
+            plan.sync()
+        except ExecutorError as ex:
+            err = str(ex)
+        if ctx.allmax([1.0 if err else 0.0])[0]:
+            times[cand] = {"error": err or "device error on a peer"}
+            plan_close(ctx, plan)
+            del send, recv
+            torch.cuda.empty_cache()
+            continue
         ok = _recv_ok(ctx, recv, nodes, n, m, copy_self, salt=7)
         ctx.barrier()
         plan.execute(send, recv, stream=stream)   # skew absorber (see measure)
@@ -508,6 +531,7 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     plan = make_plan(art, m, G, placement, schedule, copy_self=copy_self)
     if e2e and G > 1:
         plan.set_recv_buffers(2)          # double-buffered recv for the pipelined e2e
+    num_ctas = spec_ctas(schedule, num_ctas)[1]
     plan.bind(rank, device=ctx.local, num_ctas=num_ctas)
     if G > 1:
         connect(plan)

@@ -360,17 +360,71 @@ __device__ __forceinline__ bool ll128_piece(const char* sbase, char* dbase, cons
   const uint64_t E = epoch;
   const int64_t r = sll ? sa % 120 : 0;
   char* ws = wsm + warp * 640;
+  if (!sll || r == 0) {
+    // plain source or a line-aligned LL128 source: kU line groups (16 lines)
+    // per warp and turn, all their loads in flight before the first use
+    constexpr int kU = 4;
+    for (int64_t L0 = (int64_t)warp * 4 * kU; L0 < NL; L0 += (int64_t)nw * 4 * kU) {
+      uint64_t a[kU], b[kU];
+      int nb[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t L = L0 + 4 * u + li, pb = 120 * L + 16 * j;
+        nb[u] = L < NL ? (int)max((int64_t)0, min((int64_t)(j == 7 ? 8 : 16), n - pb)) : -1;
+        a[u] = b[u] = 0;
+        if (!sll) {
+          if (nb[u] > 0) ld16_plain(sbase + sa + pb, nb[u], a[u], b[u]);
+        } else if (nb[u] >= 0) {
+          ld16v(sbase + 128 * (sa / 120 + L) + 16 * j, a[u], b[u]);
+        }
+      }
+      if (sll) {  // poll: reload the line groups whose flag is not yet the epoch
+        uint32_t spins = 0, nap = 0;
+        uint64_t t0 = 0;
+        for (;;) {
+          bool ok = true;
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const uint64_t f = __shfl_sync(0xffffffffu, b[u], lane | 7);
+            if (nb[u] >= 0 && f != E) {
+              ok = false;
+              ld16v(sbase + 128 * (sa / 120 + L0 + 4 * u + li) + 16 * j, a[u], b[u]);
+            }
+          }
+          if (__all_sync(0xffffffffu, ok)) break;
+          if (++spins > kLLSpin) {
+            nap = nap ? min(2 * nap, 1024u) : 64u;
+            __nanosleep(nap);
+          }
+          if ((spins & 255) == 0) {
+            const uint64_t now = globaltimer();
+            if (t0 == 0) t0 = now;
+            const bool out = (int64_t)(now - t0) > timeout_ns || *(volatile int32_t*)err != 0;
+            if (__any_sync(0xffffffffu, out)) return false;
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t L = L0 + 4 * u + li;
+        if (dll) {
+          if (nb[u] >= 0) st16v(dbase + 128 * (q.dst_off / 120 + L) + 16 * j, a[u], j == 7 ? E : b[u]);
+        } else if (nb[u] > 0) {
+          char* d = dbase + q.dst_off + 120 * L + 16 * j;
+          plain_store8(d, a[u], min(nb[u], 8));
+          if (nb[u] > 8) plain_store8(d + 8, b[u], nb[u] - 8);
+        }
+      }
+    }
+    return true;
+  }
   for (int64_t L0 = (int64_t)warp * 4; L0 < NL; L0 += (int64_t)nw * 4) {
     const int64_t L = L0 + li;
     const bool live = L < NL;
     const int64_t pb = 120 * L + 16 * j;
     const int nb = live ? (int)max((int64_t)0, min((int64_t)(j == 7 ? 8 : 16), n - pb)) : 0;
     uint64_t a = 0, b = 0;
-    if (!sll) {
-      if (nb > 0) ld16_plain(sbase + sa + pb, nb, a, b);
-    } else if (r == 0) {
-      if (!ll128_poll(sbase + 128 * (sa / 120 + L), live, j, E, a, b, timeout_ns, err)) return false;
-    } else {
+    {  // misaligned LL128 source: gather the window through shared memory
       const int64_t A = (sa + 120 * L0) / 120;
       const int64_t Aend = (sa + min(n, 120 * (L0 + 4)) - 1) / 120;
       uint64_t x = 0, y = 0;
