@@ -1,16 +1,20 @@
-"""One rank of a G-GPU all-to-all for per-rank ncu captures (NVLink + DRAM bytes).
+"""One rank of a G-GPU all-to-all for ncu captures of the multi-GPU kernel
+(NVLink tx/rx + DRAM bytes of one GPU).
 
-ncu serialises the kernels of the process it profiles, so a multi-GPU
-execute cannot be profiled from one process (each GPU's kernel waits on its
-peers' flags).  Here every rank is its own process, started by a shell loop
-(no torchrun), each under its own ncu with a single-pass metric set; the
-ranks exchange their CUDA-IPC arena handles through files in --dir.  The
-gpurun ncu shim first runs the command once without ncu: both runs of a rank
-rendezvous only with the same kind of run of their peers (file prefix
-"plain" / "ncu", from the ncu injection variable).
+ncu serialises the kernels it profiles (also across processes), so a
+multi-GPU execute cannot be profiled on every rank at once: each GPU's kernel
+waits on its peers' flags.  Here every rank is its own process (no torchrun;
+CUDA-IPC arena handles are exchanged through files in --dir) and only ONE rank
+runs under ncu with a single-pass metric set, its profiled launch running
+concurrently with the peers' plain launches of the same all-to-all.  The
+gpurun ncu shim first runs the profiled command once without ncu; the peers
+therefore run twice (--phase plain --optional, then --phase ncu) and rendezvous
+only with the same phase (the profiled rank's phase comes from the ncu
+injection variable).
 
-  for r in 0 1; do ncu --metrics ... -k regex:a2a -s 3 -c 1 --csv --log-file out_$r.csv \
-      python tools/ncu_rank.py --rank $r --world 2 & done; wait
+  python tools/ncu_rank.py --rank 1 --world 2 --phase plain --optional && \
+      python tools/ncu_rank.py --rank 1 --world 2 --phase ncu &
+  ncu --metrics ... -k regex:a2a -s 3 -c 1 python tools/ncu_rank.py --rank 0 --world 2
 """
 from __future__ import annotations
 
@@ -23,12 +27,15 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def _wait_files(paths, timeout=120.0):
+def _wait_files(paths, timeout=150.0, optional=False):
     t0 = time.time()
     while not all(os.path.exists(p) for p in paths):
         if time.time() - t0 > timeout:
+            if optional:
+                return False
             raise SystemExit(f"peer files missing after {timeout}s: {paths}")
         time.sleep(0.05)
+    return True
 
 
 def _put(path, data: bytes):
@@ -47,13 +54,16 @@ def main():
     ap.add_argument("--schedule", default="spread:1048576")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--dir", default="/tmp/a2a_ncu_rdv")
+    ap.add_argument("--phase", default=None, help="plain | ncu (default: from the ncu injection env)")
+    ap.add_argument("--optional", action="store_true",
+                    help="exit 0 if the peers of this phase never show up (no ncu shim pre-run)")
     a = ap.parse_args()
     import torch
 
     import bench
     from paper_2309_13541_b200.artifacts import load_artifact
-    phase = "ncu" if any(k.startswith(("CUDA_INJECTION64", "NV_NSIGHT", "NSYS_", "NV_COMPUTE_PROFILER"))
-                         for k in os.environ) else "plain"
+    phase = a.phase or ("ncu" if any(k.startswith(("CUDA_INJECTION64", "NV_NSIGHT", "NV_COMPUTE_PROFILER"))
+                                     for k in os.environ) else "plain")
     os.makedirs(a.dir, exist_ok=True)
     G, r = a.world, a.rank
     torch.cuda.set_device(r)
@@ -63,7 +73,10 @@ def main():
     plan.set_timeout(5.0)
     _put(os.path.join(a.dir, f"{phase}_h{r}"), plan.export_handle())
     hs = [os.path.join(a.dir, f"{phase}_h{g}") for g in range(G)]
-    _wait_files(hs)
+    if not _wait_files(hs, timeout=90.0 if a.optional else 150.0, optional=a.optional):
+        plan.close()
+        print(f"rank {r} ({phase}): no peers of this phase, skipped", flush=True)
+        return
     plan.import_handles([open(p, "rb").read() for p in hs])
     nodes = [v for v in range(art.g.n) if int(plan.placement[v]) == r]
     send = torch.randint(0, 256, (len(nodes), art.g.n, a.m), dtype=torch.uint8, device=f"cuda:{r}")
