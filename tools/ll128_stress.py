@@ -188,6 +188,10 @@ def main():
         done = torch.zeros(1, dtype=torch.int64, device=f"cuda:{cdev}")
         bad = torch.zeros(1, dtype=torch.int64, device=f"cuda:{cdev}")
         chk = torch.zeros(1, dtype=torch.int64, device=f"cuda:{cdev}")
+        # the zero fills above run on the default stream; the test streams do not
+        # wait for it, so finish them first (a late fill would erase epoch-1 lines)
+        torch.cuda.synchronize(pdev)
+        torch.cuda.synchronize(cdev)
         sp, sc = torch.cuda.Stream(pdev), torch.cuda.Stream(cdev)
         pc, cc = (64, 64) if pdev == cdev else (132, 132)
         cc = min(cc, (nl + 31) // 32)             # consumer CTAs that own lines (8 warps x 4)
