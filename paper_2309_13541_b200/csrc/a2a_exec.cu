@@ -362,20 +362,36 @@ __device__ __forceinline__ bool ll128_piece(const char* sbase, char* dbase, cons
   char* ws = wsm + warp * 640;
   if (!sll || r == 0) {
     // plain source or a line-aligned LL128 source: kU line groups (16 lines)
-    // per warp and turn, all their loads in flight before the first use
+    // per warp and turn, all their loads in flight before the first use.
+    // Per-lane base pointers and strides are set up once (no division in the
+    // loop); only the piece's last line can be partial.
     constexpr int kU = 4;
+    const int cap = j == 7 ? 8 : 16;
+    const int64_t NLfull = n / 120;                       // lines entirely inside the piece
+    const char* sp = sll ? sbase + 128 * (sa / 120) + 16 * j : sbase + sa + 16 * j;
+    const int64_t ss = sll ? 128 : 120;
+    const bool sal = sll || (((uintptr_t)(sbase + sa)) & 7) == 0;   // 8-byte aligned plain loads
+    char* dp = dll ? dbase + 128 * (q.dst_off / 120) + 16 * j : dbase + q.dst_off + 16 * j;
+    const int64_t ds = dll ? 128 : 120;
+    const bool dal = dll || (((uintptr_t)(dbase + q.dst_off)) & 7) == 0;
     for (int64_t L0 = (int64_t)warp * 4 * kU; L0 < NL; L0 += (int64_t)nw * 4 * kU) {
       uint64_t a[kU], b[kU];
       int nb[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        const int64_t L = L0 + 4 * u + li, pb = 120 * L + 16 * j;
-        nb[u] = L < NL ? (int)max((int64_t)0, min((int64_t)(j == 7 ? 8 : 16), n - pb)) : -1;
+        const int64_t L = L0 + 4 * u + li;
+        nb[u] = L < NLfull ? cap : L < NL ? (int)max((int64_t)0, min((int64_t)cap, n - 120 * L - 16 * j)) : -1;
         a[u] = b[u] = 0;
-        if (!sll) {
-          if (nb[u] > 0) ld16_plain(sbase + sa + pb, nb[u], a[u], b[u]);
-        } else if (nb[u] >= 0) {
-          ld16v(sbase + 128 * (sa / 120 + L) + 16 * j, a[u], b[u]);
+        const char* s = sp + L * ss;
+        if (sll) {
+          if (nb[u] >= 0) ld16v(s, a[u], b[u]);
+        } else if (nb[u] == 16 && sal) {
+          a[u] = reinterpret_cast<const uint64_t*>(s)[0];
+          b[u] = reinterpret_cast<const uint64_t*>(s)[1];
+        } else if (nb[u] == 8 && sal) {
+          a[u] = reinterpret_cast<const uint64_t*>(s)[0];
+        } else if (nb[u] > 0) {
+          ld16_plain(s, nb[u], a[u], b[u]);
         }
       }
       if (sll) {  // poll: reload the line groups whose flag is not yet the epoch
@@ -388,7 +404,7 @@ __device__ __forceinline__ bool ll128_piece(const char* sbase, char* dbase, cons
             const uint64_t f = __shfl_sync(0xffffffffu, b[u], lane | 7);
             if (nb[u] >= 0 && f != E) {
               ok = false;
-              ld16v(sbase + 128 * (sa / 120 + L0 + 4 * u + li) + 16 * j, a[u], b[u]);
+              ld16v(sp + (L0 + 4 * u + li) * ss, a[u], b[u]);
             }
           }
           if (__all_sync(0xffffffffu, ok)) break;
@@ -406,11 +422,15 @@ __device__ __forceinline__ bool ll128_piece(const char* sbase, char* dbase, cons
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        const int64_t L = L0 + 4 * u + li;
+        char* d = dp + (L0 + 4 * u + li) * ds;
         if (dll) {
-          if (nb[u] >= 0) st16v(dbase + 128 * (q.dst_off / 120 + L) + 16 * j, a[u], j == 7 ? E : b[u]);
+          if (nb[u] >= 0) st16v(d, a[u], j == 7 ? E : b[u]);
+        } else if (nb[u] == 16 && dal) {
+          reinterpret_cast<uint64_t*>(d)[0] = a[u];
+          reinterpret_cast<uint64_t*>(d)[1] = b[u];
+        } else if (nb[u] == 8 && dal) {
+          reinterpret_cast<uint64_t*>(d)[0] = a[u];
         } else if (nb[u] > 0) {
-          char* d = dbase + q.dst_off + 120 * L + 16 * j;
           plain_store8(d, a[u], min(nb[u], 8));
           if (nb[u] > 8) plain_store8(d + 8, b[u], nb[u] - 8);
         }
@@ -712,9 +732,13 @@ __device__ __forceinline__ void exec_body(const KParams& p, const uint32_t epoch
           char* db = p.base[q.dst_loc];
           if (q.kind & kLLSrc) sb += (epoch & 1) * p.ll_half[p.rank];
           if (q.kind & kLLDst) db += (epoch & 1) * p.ll_half[q.dst_loc - (1 + 2 * p.G)];
-          const bool ok = p.ll128 ? ll128_piece(sb, db, q, epoch, p.timeout_ns, p.err,
-                                                reinterpret_cast<char*>(dsmem + p.smem_ll))
-                                  : ll_piece(sb, db, q, epoch, p.timeout_ns, p.err);
+          bool ok;
+          if constexpr (kThreads <= 512)   // LL128 plans launch the 512- or 256-thread kernels
+            ok = p.ll128 ? ll128_piece(sb, db, q, epoch, p.timeout_ns, p.err,
+                                       reinterpret_cast<char*>(dsmem + p.smem_ll))
+                         : ll_piece(sb, db, q, epoch, p.timeout_ns, p.err);
+          else
+            ok = ll_piece(sb, db, q, epoch, p.timeout_ns, p.err);
           if (!ok) {
             atomicCAS(p.err, 0, (int32_t)A2A_ERR_TIMEOUT);
             s_abort = 1;
@@ -1242,9 +1266,13 @@ static EngineCfg engine_cfg(const Plan& P) {
             (int)po, (int)(po + prog), batch, (int)(po + prog + batch * sizeof(DevPiece))};
   }
   const int batch = 128;
-  const size_t ll = P.ll128 ? (1024 / 32) * 640 : 0;
-  return {(const void*)a2a_exec_kernel<0, 1024>, 1024, prog + batch * sizeof(DevPiece) + ll, 0, 0,
-          (int)prog, batch, (int)(prog + batch * sizeof(DevPiece))};
+  if (P.ll128) {  // LL128: 512 threads with 128 registers each keep 16 lines per warp in flight
+    const size_t ll = (512 / 32) * 640;
+    return {(const void*)a2a_exec_kernel<0, 512>, 512, prog + batch * sizeof(DevPiece) + ll, 0, 0,
+            (int)prog, batch, (int)(prog + batch * sizeof(DevPiece))};
+  }
+  return {(const void*)a2a_exec_kernel<0, 1024>, 1024, prog + batch * sizeof(DevPiece), 0, 0,
+          (int)prog, batch, 0};
 }
 
 // arena flag region: entry[G] u32 | grab counters u64 @128 | flags @256:
