@@ -391,11 +391,13 @@ def _recv_ok(ctx, recv, nodes, n, m, copy_self, salt=0):
     for every s != nodes[i] (and the self shard when it is copied); all ranks."""
     import torch
     ok = True
-    for s in range(n):
+    for s in range(n):          # one comparison per source node (all local rows at once)
         row = _node_send(ctx.dev, s, n, m, salt)
-        for i, v in enumerate(nodes):
-            if v != s or copy_self:
-                ok &= bool(torch.equal(recv[i, s], row[v]))
+        sel = [i for i, v in enumerate(nodes) if v != s or copy_self]
+        if sel:
+            ri = torch.tensor(sel, device=ctx.dev)
+            ci = torch.tensor([nodes[i] for i in sel], device=ctx.dev)
+            ok &= bool(torch.equal(recv[ri, s], row[ci]))
     return ctx.allmax([0.0 if ok else 1.0])[0] == 0.0
 
 

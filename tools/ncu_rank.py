@@ -70,7 +70,7 @@ def main():
     art = load_artifact(a.config)
     plan = bench.make_plan(art, a.m, G, "optimized", a.schedule)
     plan.bind(r, device=r)
-    plan.set_timeout(5.0)
+    plan.set_timeout(60.0)      # the profiled launch starts seconds late (ncu set-up)
     _put(os.path.join(a.dir, f"{phase}_h{r}"), plan.export_handle())
     hs = [os.path.join(a.dir, f"{phase}_h{g}") for g in range(G)]
     if not _wait_files(hs, timeout=90.0 if a.optional else 150.0, optional=a.optional):
