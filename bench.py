@@ -370,11 +370,12 @@ def make_plan(art, m, G, placement, schedule, copy_self=False):
 
 
 def default_candidates(G, m):
-    """Autotune candidates (at most three execution orders, plus LL for small
-    shards): static per-CTA programs, critical-path unit queues, and the
-    single merged queue (`mix`; at G > 2 `spread`, which interleaves each
-    step's NVLink units over their destination GPUs)."""
-    return ("static", "cp:1048576", "spread:1048576" if G > 2 else "mix:1048576") + (
+    """Autotune candidates: static per-CTA programs, critical-path unit
+    queues, the single merged queue (`mix`; at G > 2 `spread`, which
+    interleaves each step's NVLink units over their destination GPUs), chains
+    (each route's local hops streamed through L2 on one CTA), plus LL / LL128
+    for small and medium shards."""
+    return ("static", "cp:1048576", "spread:1048576" if G > 2 else "mix:1048576", "chain:262144") + (
         ("ll",) if m <= LL_MAX_SHARD else ()) + (("ll@16",) if m <= 65536 else ()) + (
         ("ll128",) if m <= LL128_MAX_SHARD else ())
 
@@ -794,7 +795,7 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
            "flush_ms_p50_by_rank": [round(x[0], 4) for x in alld],
            "step_period_ms_p50_by_rank": [round(x[1], 4) for x in alld],
            "step_ms_by_rank": [x[2] for x in alld] if os.environ.get("A2A_DIAG") else None,
-           "sync": (plan.dyn_stats(rank, plan_ctas(plan, num_ctas)) if plan.schedule in ("dynamic", "list", "cp", "mix", "ready", "spread")
+           "sync": (plan.dyn_stats(rank, plan_ctas(plan, num_ctas)) if plan.schedule in ("dynamic", "list", "cp", "mix", "ready", "spread", "chain")
                     else plan.sync_stats(rank)),
            "kernel_timeline": tls,
            "num_ctas": plan_ctas(plan, num_ctas), "egress_max": max(i["egress_bytes"] for i in infos),

@@ -78,6 +78,9 @@ struct KParams {
   unsigned long long* qslot[A2A_MAX_GPUS];
   int32_t ubase[A2A_MAX_GPUS + 1];         // global unit id range of every GPU
   int32_t n_init, n_into;                  // own units ready at start; units writing into this GPU
+  // chain mode (sched_mode 7): task k = units [chain_begin[k], chain_begin[k+1])
+  const int32_t* chain_begin;
+  int32_t n_tasks;
 };
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -1204,6 +1207,209 @@ __global__ void __launch_bounds__(kThreads, 1) a2a_ready_kernel(const KParams p)
   end_epoch(p, epoch);
 }
 
+
+// ---- chain mode (sched_mode 7): a route's consecutive local hops stream through L2 ----
+// A task is a chain of units (build_dyn): the head waits on its producers' flags;
+// every later unit reads exactly the bytes the previous one stored, on the same
+// CTA.  Thread 0 streams the whole chain through one TMA ring: chunk c of hop
+// u+1 is loaded K chunks after chunk c of hop u was stored (K = chunks per unit
+// >= ring depth), once `cp.async.bulk.wait_group` says that store completed, so
+// the forwarded bytes are read back while they still sit in L2 and the ring
+// never drains between hops.  Tasks whose units are not 16-byte clean at run
+// time (odd shard sizes, user buffers) copy unit by unit with all threads.
+__device__ __forceinline__ void bulk_wait_n(uint32_t n) {
+  switch (n) {
+    case 0: asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.bulk.wait_group 2;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.bulk.wait_group 3;" ::: "memory"); break;
+    case 4: asm volatile("cp.async.bulk.wait_group 4;" ::: "memory"); break;
+    case 5: asm volatile("cp.async.bulk.wait_group 5;" ::: "memory"); break;
+    case 6: asm volatile("cp.async.bulk.wait_group 6;" ::: "memory"); break;
+    default: asm volatile("cp.async.bulk.wait_group 7;" ::: "memory"); break;
+  }
+}
+
+template <int kEngine, int kThreads>
+__device__ __forceinline__ void chain_body(const KParams& p, const uint32_t epoch) {
+  __shared__ int s_abort, s_clean;
+  __shared__ long long s_task;
+  extern __shared__ __align__(128) unsigned char dsmem[];
+  const int c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5;
+  const int S = p.tma_stages;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dsmem);
+  char** ring_dst = reinterpret_cast<char**>(dsmem + 8 * S);
+  uint32_t* ring_n = reinterpret_cast<uint32_t*>(dsmem + 16 * S);
+  char* stages = reinterpret_cast<char*>(dsmem + ((20 * S + 127) & ~127));
+  uint32_t gi = 0;
+  unsigned long long* tl = p.timeline + (int64_t)c * (2 * p.T + 3);
+  if (tid == 0) {
+    tl[0] = globaltimer();
+    s_abort = 0;
+    if (kEngine == 1) {
+      for (int i = 0; i < S; ++i) mbar_init(&bars[i], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
+  __syncthreads();
+  const uint32_t* my_flags = p.step_flags[p.rank];
+  const bool sys = p.G > 1 || (p.sync_mode & 4);
+  if (p.G > 1) {  // entry barrier (same protocol as the other kernels)
+    if (c == 0 && tid < p.G && tid != p.rank) st_relaxed(p.entry_flags[tid] + p.rank, epoch, true);
+    if (warp == 0) {
+      const int lane = tid & 31;
+      bool ok = true;
+      if (lane < p.G && lane != p.rank) {
+        const uint32_t* f = p.entry_flags[p.rank] + lane;
+        uint64_t t0 = globaltimer();
+        uint32_t spins = 0;
+        while ((int32_t)(ld_acquire_sys(f) - epoch) < 0) {
+          if ((++spins & 255) == 0 && ((int64_t)(globaltimer() - t0) > p.timeout_ns ||
+                                       *(volatile int32_t*)p.err != 0)) {
+            ok = false;
+            break;
+          }
+        }
+      }
+      ok = __all_sync(0xffffffffu, ok);
+      if (!ok && lane == 0) { atomicCAS(p.err, 0, (int32_t)A2A_ERR_TIMEOUT); s_abort = 1; }
+    }
+    __syncthreads();
+    if (s_abort) return;
+  }
+  if (tid == 0) tl[1] = globaltimer();
+  unsigned long long waited_ns = 0, done = 0;
+  for (;;) {
+    if (tid == 0) {
+      const long long nt = p.n_tasks;
+      const long long j = (long long)(atomicAdd(p.grab, 1ull) -
+                                      (unsigned long long)(epoch - 1) * (unsigned long long)(nt + p.nC));
+      s_task = j < nt ? j : -1;
+    }
+    __syncthreads();
+    const long long task = s_task;
+    if (task < 0) break;
+    const int32_t ub = p.chain_begin[task], ue = p.chain_begin[task + 1];
+    const DevUnit head = p.units[ub];
+    if (warp == 0 && head.we > head.wb) {
+      const uint64_t w0 = globaltimer();
+      if (!warp_wait_flags(my_flags, p.unit_wait, head.wb, head.we, epoch, p.timeout_ns, p.err, sys,
+                           p.sync_mode) && tid == 0)
+        s_abort = 1;
+      if (tid == 0) waited_ns += globaltimer() - w0;
+    }
+    if (tid == 32) {  // TMA streaming needs every unit 16-byte clean and larger than a small piece
+      int clean = kEngine == 1;
+      for (int32_t k = ub; k < ue && clean; ++k) {
+        const DevUnit u = p.units[k];
+        const uintptr_t a = (uintptr_t)(p.base[u.src_loc] + u.src_off) | (uintptr_t)(p.base[u.dst_loc] + u.dst_off);
+        clean = ((a | (uintptr_t)u.nbytes) & 15) == 0 && u.nbytes > kSmallPiece && u.nbytes == head.nbytes;
+      }
+      // a later hop's chunk is loaded >= S chunks after its store was issued
+      if (ue - ub > 1 && (head.nbytes + p.tma_chunk - 1) / p.tma_chunk < S) clean = 0;
+      s_clean = clean;
+    }
+    __syncthreads();
+    if (s_abort) return;
+    if (kEngine == 1 && s_clean) {
+      if (tid == 0) {
+        fence_proxy_async();
+        const uint32_t CH = (uint32_t)p.tma_chunk;
+        const int64_t n = head.nbytes;
+        const uint32_t K = (uint32_t)((n + CH - 1) / CH), total = K * (uint32_t)(ue - ub);
+        const uint32_t g0 = gi;
+        uint32_t nl = 0, ns = 0;
+        auto issue = [&]() -> bool {
+          if (nl >= total) return false;
+          const int32_t k = ub + (int32_t)(nl / K);
+          const int64_t off = (int64_t)(nl % K) * CH;
+          const uint32_t len = (uint32_t)min((int64_t)CH, n - off);
+          if (nl >= K) bulk_wait_n(ns - 1 - (nl - K));   // the previous hop's store of these bytes
+          const DevUnit& u = p.units[k];
+          const uint32_t st = (g0 + nl) % S;
+          ring_dst[st] = p.base[u.dst_loc] + u.dst_off + off;
+          ring_n[st] = len;
+          mbar_expect_tx(&bars[st], len);
+          bulk_load(stages + (size_t)st * CH, p.base[u.src_loc] + u.src_off + off, len, &bars[st]);
+          ++nl;
+          return true;
+        };
+        bool more = true;
+        while (more && nl < (uint32_t)S) more = issue();
+        while (ns < nl) {
+          const uint32_t st = (g0 + ns) % S;
+          mbar_wait(&bars[st], ((g0 + ns) / S) & 1);
+          bulk_store(ring_dst[st], stages + (size_t)st * CH, ring_n[st]);
+          ++ns;
+          if (more) {
+            if (S == 1) {
+              asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+              more = issue();
+            } else if (ns >= 2 && nl - (uint32_t)S == ns - 2) {
+              bulk_wait_read1();
+              more = issue();
+            }
+          }
+        }
+        bulk_wait_all();
+        fence_proxy_async();
+        gi = g0 + nl;
+      }
+    } else {
+      for (int32_t k = ub; k < ue; ++k) {   // unit by unit, every thread
+        const DevUnit u = p.units[k];
+        cta_copy<4>(p.base[u.dst_loc] + u.dst_off, p.base[u.src_loc] + u.src_off, u.nbytes);
+        __syncthreads();                    // the next unit reads these bytes
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {   // every unit of the task: link counters, then its flag on each GPU of its mask
+      for (int32_t k = ub; k < ue; ++k) {
+        const DevUnit u = p.units[k];
+        if (p.count_links && u.edge >= 0)
+          atomicAdd(p.counters + (int64_t)u.step * p.E + u.edge, (unsigned long long)u.nbytes);
+        const int64_t slot = (int64_t)p.unit_base + k;
+        uint32_t mask = u.mask;
+        while (mask) {
+          const int h = __ffs(mask) - 1;
+          mask &= mask - 1;
+          st_release(p.step_flags[h] + slot, epoch, sys);
+        }
+        ++done;
+      }
+    }
+  }
+  if (c == 0 && p.G > 1) {  // exit: every unit flagged into this GPU has landed
+    bool ok = true;
+    for (int32_t i = tid; i < p.n_exit && ok; i += kThreads) {
+      const uint32_t* f = my_flags + p.exit_idx[i];
+      uint64_t t0 = globaltimer();
+      uint32_t spins = 0;
+      while ((int32_t)(ld_acquire_sys(f) - epoch) < 0) {
+        if ((++spins & 255) == 0 && ((int64_t)(globaltimer() - t0) > p.timeout_ns ||
+                                     *(volatile int32_t*)p.err != 0)) {
+          ok = false;
+          break;
+        }
+      }
+    }
+    if (!ok) atomicCAS(p.err, 0, (int32_t)A2A_ERR_TIMEOUT);
+    __syncthreads();
+  }
+  if (tid == 0) {
+    tl[2] = done;
+    tl[3] = waited_ns;
+    tl[2 + p.T] = globaltimer();
+  }
+}
+
+template <int kEngine, int kThreads>
+__global__ void __launch_bounds__(kThreads, 1) a2a_chain_kernel(const KParams p) {
+  const uint32_t epoch = begin_epoch(p);
+  chain_body<kEngine, kThreads>(p, epoch);
+  end_epoch(p, epoch);
+}
+
 static int cuda_fail(cudaError_t e, const char* what) {
   char buf[256];
   snprintf(buf, sizeof buf, "%s: %s", what, cudaGetErrorString(e));
@@ -1240,16 +1446,18 @@ struct EngineCfg {
 static EngineCfg engine_cfg(const Plan& P) {
   const int TE = P.T_exec;
   if (P.sched_mode >= 1) {
-    const bool rq = P.sched_mode == 5;
+    const bool rq = P.sched_mode == 5, ch = P.sched_mode == 7;
     if (P.engine == 1) {
       int S = P.tma_stages;
       while (S > 1 && ((20 * (size_t)S + 127) & ~(size_t)127) + (size_t)S * P.tma_chunk > 220 * 1024) --S;
       const size_t ring = ((20 * (size_t)S + 127) & ~(size_t)127) + (size_t)S * P.tma_chunk;
-      return {rq ? (const void*)a2a_ready_kernel<1, 256> : (const void*)a2a_dyn_kernel<1, 256>, 256, ring,
-              S, 0, 0, 0};
+      return {ch ? (const void*)a2a_chain_kernel<1, 256>
+                 : rq ? (const void*)a2a_ready_kernel<1, 256> : (const void*)a2a_dyn_kernel<1, 256>,
+              256, ring, S, 0, 0, 0};
     }
-    return {rq ? (const void*)a2a_ready_kernel<0, 1024> : (const void*)a2a_dyn_kernel<0, 1024>, 1024, 0,
-            0, 0, 0, 0};
+    return {ch ? (const void*)a2a_chain_kernel<0, 1024>
+               : rq ? (const void*)a2a_ready_kernel<0, 1024> : (const void*)a2a_dyn_kernel<0, 1024>,
+            1024, 0, 0, 0, 0, 0};
   }
   const size_t prog = ((size_t)TE * sizeof(CtaStep) + 127) & ~(size_t)127;
   if (P.engine == 1) {
@@ -1378,6 +1586,7 @@ static int bind_plan(Plan& P, int gpu, int dev, int nC) {
     CK(cudaMemset((char*)P.arena + P.scratch_off[gpu] + P.ll_off[gpu], 0, (size_t)(2 * P.ll_half[gpu])));
   if (P.sched_mode >= 1) {
     if ((rc = upload(&P.d_items, Dy.units[gpu])) != A2A_OK) return rc;
+    if (P.sched_mode == 7 && (rc = upload(&P.d_step_begin, Dy.chain_begin[gpu])) != A2A_OK) return rc;
     if ((rc = upload(&P.d_wait_idx, P.sched_mode == 5 ? Dy.deps_out[gpu] : Dy.wait_idx[gpu])) != A2A_OK)
       return rc;
     if ((rc = upload(&P.d_exit_idx, Dy.exit_idx[gpu])) != A2A_OK) return rc;
@@ -1570,6 +1779,7 @@ int a2a_plan_set_engine(a2a_plan* plan, int32_t engine, int32_t tma_chunk, int32
       plan->p.tma_stages = tma_stages;
     }
     plan->p.engine = engine;
+    plan->p.dyn = DynTables{};   // chain links depend on the TMA ring size
     return A2A_OK;
   });
 }
@@ -1656,6 +1866,10 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
         for (int g = 0; g <= P.G; ++g) kp.ubase[g] = Dy.unit_base[g];
         kp.n_init = Dy.n_init[P.rank];
         kp.n_into = Dy.n_into[P.rank];
+      }
+      if (P.sched_mode == 7) {
+        kp.chain_begin = (const int32_t*)P.d_step_begin;
+        kp.n_tasks = (int32_t)Dy.chain_begin[P.rank].size() - 1;
       }
       kp.n_remote = Dy.n_remote[P.rank];
       kp.remote_ctas = Dy.remote_ctas[P.rank];

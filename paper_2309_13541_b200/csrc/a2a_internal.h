@@ -119,6 +119,10 @@ struct DynTables {
   std::vector<std::vector<int32_t>> deps_out;   // [g] flattened pairs
   std::vector<int32_t> n_init, n_into;          // [g] units ready at start; units writing into g
   int32_t max_units = 0;                        // max units on one GPU (queue array size)
+  // chain mode (sched_mode 7): per GPU, task k = units [chain_begin[k], chain_begin[k+1])
+  // of that GPU's unit array, run in order by one CTA
+  std::vector<std::vector<int32_t>> chain_begin;
+  int32_t max_chain = 0;                        // longest task (units)
 };
 
 struct Interval {
@@ -150,7 +154,7 @@ struct Plan {
   SyncTables sync;
   DynTables dyn;
   int32_t remote_weight = 1;                    // CTA split cost of an NVLink byte vs a local byte
-  int32_t sched_mode = 0;                       // 0 static programs, 1 dynamic step-major, 2 dynamic list-scheduled
+  int32_t sched_mode = 0;                       // 0 static programs, 1..6 unit queues, 7 chains
   int64_t dyn_unit_bytes = 0;                   // dynamic unit size (0 = auto)
   int32_t dyn_remote_ctas = 0;                  // CTAs pinned to the NVLink queue (0 = auto split)
 

@@ -1035,6 +1035,33 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
     std::sort(x.deps.begin(), x.deps.end());
     x.deps.erase(std::unique(x.deps.begin(), x.deps.end()), x.deps.end());
   }
+  // chain mode (sched_mode 7): a unit v whose only producer u is the previous
+  // hop of the same route -- u wrote exactly v's source bytes into its own
+  // GPU's scratch and v is u's only consumer -- runs right after u on the same
+  // CTA: the route's hops stream through L2 (v reads what u just stored) with
+  // no flag between them.  Linked units are TMA-clean (16-byte aligned
+  // offsets, whole 16-byte words) and span at least one TMA ring of chunks,
+  // so the ring never waits on its own stores (see the kernel's chain_body).
+  std::vector<int> chain_next(all.size(), -1);
+  std::vector<char> chain_prev(all.size(), 0);
+  if (P.sched_mode == 7 && !P.reuse) {
+    std::vector<int> ndep(all.size(), 0);
+    for (const TU& x : all)
+      for (int d : x.deps) ++ndep[d];
+    const int64_t min_bytes = (int64_t)std::max(1, P.tma_stages) * std::max(16, P.tma_chunk);
+    for (int v = 0; v < (int)all.size(); ++v) {
+      const TU& y = all[v];
+      if (y.deps.size() != 1) continue;
+      const int u = y.deps[0];
+      const TU& x = all[u];
+      if (ndep[u] != 1 || chain_next[u] >= 0 || x.g != x.dst_gpu || y.g != x.g) continue;
+      if (x.u.dst_loc != loc_scratch(x.g, G) || y.u.src_loc != loc_scratch(y.g, G)) continue;
+      if (x.u.dst_off != y.u.src_off || x.u.nbytes != y.u.nbytes || x.u.nbytes < min_bytes) continue;
+      if ((x.u.dst_off | x.u.src_off | y.u.dst_off | x.u.nbytes) & 15) continue;
+      chain_next[u] = v;
+      chain_prev[v] = 1;
+    }
+  }
   // readiness model: remote bytes at ~700 GB/s per GPU direction, local copies at ~3.2 TB/s
   const double nv = 700e9, hbm = 3.2e12;
   std::vector<double> eg_free(G, 0), in_free(G, 0), hbm_free(G, 0);
@@ -1085,7 +1112,7 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
       for (int t = 0; t < TE; ++t)
         std::stable_sort(per[g][t].begin(), per[g][t].end(),
                          [&](int a, int b) { return key[a] < key[b]; });
-  } else if (P.sched_mode == 4 || P.sched_mode == 6) {
+  } else if (P.sched_mode == 4 || P.sched_mode == 6 || P.sched_mode == 7) {
     // single queue, step-major; within a step the NVLink and HBM units are
     // merged in proportion to their estimated time (remote byte ~ hbm/nv local
     // bytes), each class ordered by critical path, so both pipes stay busy and
@@ -1217,6 +1244,8 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
   std::vector<int> gid(all.size(), -1);
   std::vector<std::vector<int>> qorder(G);
   D.units.assign(G, {});
+  D.chain_begin.assign(G, {});
+  D.max_chain = 0;
   for (int g = 0; g < G; ++g) {
     double rb = 0, lb = 0;
     // one queue in key order (n_remote = 0, no CTA on queue 0): the mix order,
@@ -1232,6 +1261,23 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
         if (P.sched_mode == 5 && all[a].deps.empty() != all[b].deps.empty()) return all[a].deps.empty();
         return key[a] < key[b];
       });
+      if (P.sched_mode == 7) {
+        // tasks in the order of their first unit (step-major): each chain head
+        // followed by its linked units; a task only waits (at its head) on units
+        // of earlier steps, whose tasks precede it in every queue
+        std::vector<int> cq;
+        D.chain_begin[g].clear();
+        for (int id : q) {
+          if (chain_prev[id]) continue;
+          D.chain_begin[g].push_back((int32_t)cq.size());
+          for (int x = id; x >= 0; x = chain_next[x]) cq.push_back(x);
+        }
+        D.chain_begin[g].push_back((int32_t)cq.size());
+        D.max_chain = 1;
+        for (size_t k = 0; k + 1 < D.chain_begin[g].size(); ++k)
+          D.max_chain = std::max(D.max_chain, D.chain_begin[g][k + 1] - D.chain_begin[g][k]);
+        q = cq;
+      }
       qorder[g] = q;
       int k = 0;
       for (int id : qorder[g]) gid[id] = D.unit_base[g] + k++;
@@ -1281,7 +1327,8 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
         TU& x = all[id];
         DevUnit u = x.u;
         u.wb = (int32_t)D.wait_idx[g].size();
-        for (int d : x.deps) D.wait_idx[g].push_back(gid[d]);
+        if (!chain_prev[id])   // a linked unit's only producer ran just before it, on its CTA
+          for (int d : x.deps) D.wait_idx[g].push_back(gid[d]);
         u.we = (int32_t)D.wait_idx[g].size();
         u.mask = (1u << x.dst_gpu) | x.notify;
         D.units[g].push_back(u);
@@ -1496,6 +1543,83 @@ static int emulate_dyn(Plan& P, int nC, uint8_t* const* send, uint8_t* const* re
   return A2A_OK;
 }
 
+// Host emulation of the chain protocol (sched_mode 7): CTAs grab tasks (chains
+// of units) from one per-GPU queue; a task waits only at its head unit (its
+// dependency list), runs its units in order (one emulation event each, other
+// CTAs interleave), and publishes the flags of all its units when it ends --
+// exactly what chain_body does.  Three executes, persistent grab counters.
+static int emulate_chain(Plan& P, int nC, uint8_t* const* send, uint8_t* const* recv, uint64_t seed,
+                         int64_t unit_bytes) {
+  int rc = build_dyn(P, nC, unit_bytes);
+  if (rc) return rc;
+  const DynTables& D = P.dyn;
+  const int G = P.G;
+  std::vector<std::vector<uint8_t>> scratch(G);
+  for (int g = 0; g < G; ++g) scratch[g].assign((size_t)P.info[g].scratch_bytes + 64, 0);
+  const int total = D.unit_base[G];
+  std::vector<uint64_t> ctr(G, 0);
+  for (uint32_t epoch = 1; epoch <= kEmuEpochs; ++epoch) {
+    for (int g = 0; g < G; ++g) std::fill(scratch[g].begin(), scratch[g].end(), 0);
+    std::vector<std::vector<char>> flag(G, std::vector<char>((size_t)total, 0));
+    std::vector<std::vector<int>> task(G, std::vector<int>(nC, -1)), pos(G, std::vector<int>(nC, 0));
+    std::vector<std::vector<char>> fin(G, std::vector<char>(nC, 0));
+    int64_t ran = 0;
+    auto base = [&](int g, int loc) -> uint8_t* {
+      if (loc == loc_send()) return send[g];
+      if (loc >= 1 && loc < 1 + G) return recv[loc - 1];
+      return scratch[loc - 1 - G].data();
+    };
+    uint64_t x = seed * 0x9E3779B97F4A7C15ULL + 5;
+    auto rnd = [&]() { x ^= x << 13; x ^= x >> 7; x ^= x << 17; return x; };
+    for (;;) {
+      std::vector<std::pair<int, int>> act;
+      bool busy = false;
+      for (int g = 0; g < G; ++g)
+        for (int c = 0; c < nC; ++c) {
+          const int k = task[g][c];
+          if (k < 0) {
+            if (!fin[g][c]) act.emplace_back(g, c);
+            continue;
+          }
+          busy = true;
+          bool ok = true;
+          if (pos[g][c] == 0) {   // the head's dependencies
+            const DevUnit& du = D.units[g][D.chain_begin[g][k]];
+            for (int32_t i = du.wb; i < du.we && ok; ++i) ok = flag[g][D.wait_idx[g][i]];
+          }
+          if (ok) act.emplace_back(g, c);
+        }
+      if (act.empty()) {
+        if (busy) return fail(A2A_ERR_INVALID, "chain emulation deadlock");
+        break;
+      }
+      auto [g, c] = act[rnd() % act.size()];
+      if (task[g][c] < 0) {
+        const int64_t nt = (int64_t)D.chain_begin[g].size() - 1;
+        const int64_t j = (int64_t)(ctr[g]++ - (uint64_t)(epoch - 1) * (uint64_t)(nt + nC));
+        if (j < 0) return fail(A2A_ERR_INVALID, "chain emulation: grab counter base mismatch across executes");
+        if (j >= nt) fin[g][c] = 1;
+        else { task[g][c] = (int)j; pos[g][c] = 0; }
+        continue;
+      }
+      const int k = task[g][c];
+      const int32_t ub = D.chain_begin[g][k], ue = D.chain_begin[g][k + 1];
+      const DevUnit& du = D.units[g][ub + pos[g][c]];
+      std::memmove(base(g, du.dst_loc) + du.dst_off, base(g, du.src_loc) + du.src_off, (size_t)du.nbytes);
+      ++ran;
+      if (ub + ++pos[g][c] < ue) continue;
+      for (int32_t i = ub; i < ue; ++i) {   // task end: every unit's flag
+        const DevUnit& w = D.units[g][i];
+        for (int h = 0; h < G; ++h)
+          if (w.mask & (1u << h)) flag[h][D.unit_base[g] + i] = 1;
+      }
+      task[g][c] = -1;
+    }
+    if (ran != total) return fail(A2A_ERR_INVALID, "chain emulation: units skipped in an execute");
+  }
+  return A2A_OK;
+}
+
 }  // namespace a2a
 
 using namespace a2a;
@@ -1649,7 +1773,7 @@ int a2a_plan_set_split(a2a_plan* plan, int32_t remote_weight) {
 
 int a2a_plan_set_schedule(a2a_plan* plan, int32_t mode, int64_t unit_bytes) {
   return guard([&]() -> int {
-    if (!plan || mode < 0 || mode > 6 || unit_bytes < 0) return fail(A2A_ERR_INVALID, "bad schedule mode");
+    if (!plan || mode < 0 || mode > 7 || unit_bytes < 0) return fail(A2A_ERR_INVALID, "bad schedule mode");
     if (plan->p.bound) return fail(A2A_ERR_STATE, "set the schedule mode before a2a_plan_bind");
     if (plan->p.ll && mode != 0)
       return fail(A2A_ERR_INVALID, "A2A_PROTO_LL plans run the static schedule only");
@@ -1705,8 +1829,11 @@ int a2a_plan_emulate(a2a_plan* plan, int32_t num_ctas, void* const* send, void* 
         return emulate_ready(plan->p, num_ctas, (uint8_t* const*)send, (uint8_t* const*)recv, seed,
                              plan->p.dyn_unit_bytes);
       if (plan->p.sched_mode >= 1)
-        return emulate_dyn(plan->p, num_ctas, (uint8_t* const*)send, (uint8_t* const*)recv, seed,
-                           plan->p.dyn_unit_bytes);
+        return plan->p.sched_mode == 7
+                   ? emulate_chain(plan->p, num_ctas, (uint8_t* const*)send, (uint8_t* const*)recv, seed,
+                                   plan->p.dyn_unit_bytes)
+                   : emulate_dyn(plan->p, num_ctas, (uint8_t* const*)send, (uint8_t* const*)recv, seed,
+                                 plan->p.dyn_unit_bytes);
       return emulate(plan->p, num_ctas, (uint8_t* const*)send, (uint8_t* const*)recv, seed);
     } catch (const std::bad_alloc&) {
       return fail(A2A_ERR_NOMEM, "out of host memory in emulation");

@@ -324,3 +324,36 @@ def test_without_self_copy(name, G, sched, artifacts):
                     assert not recvs[g][i, s].any()
                 else:
                     assert np.array_equal(recvs[g][i, s], want[v, s]), (g, v, s)
+
+
+@pytest.mark.parametrize("name", ["gk8_2", "torus2x4", "hypercube3", "torus2x4_h2", "ts_gk8_2",
+                                  "ts_torus3x3"])
+@pytest.mark.parametrize("G", [1, 2, 4])
+@pytest.mark.parametrize("m,unit", [(1 << 20, 262144), (262144 + 48, 196608), (1000, 0)])
+def test_chain_interleavings_deliver_transpose(name, G, m, unit, artifacts):
+    """Chain mode (schedule "chain"): a route's consecutive local hops run on
+    one CTA with no flag between them, tasks wait only at their head, all
+    unit flags are published when the task ends; random interleavings of all
+    CTAs of all GPUs over three executes deliver the transpose."""
+    a = artifacts(name)
+    if G > a.g.n:
+        pytest.skip("more GPUs than nodes")
+    send = make_send(a.g.n, m, seed=G)
+    with Plan(a.g, a.sched, m=m, n_gpus=G) as p:
+        p.set_schedule("chain", unit)
+        nodes = [local_nodes(p, g) for g in range(G)]
+        for nc in (1, 7, 148):
+            recvs = p.emulate([send[ns] for ns in nodes], num_ctas=nc, seed=nc)
+            for g in range(G):
+                assert np.array_equal(recvs[g], np.swapaxes(send, 0, 1)[nodes[g]]), (nc, g)
+        p.check_bounds(37)
+
+
+def test_chain_links_routes(artifacts):
+    """On one GPU the path schedules' routes become single tasks: every hop
+    after the first has no wait list (GK(8,2): 4 of 7814 units keep one)."""
+    a = artifacts("gk8_2")
+    with Plan(a.g, a.sched, m=16 << 20, copy_self=False) as p:
+        p.set_schedule("chain", 262144)
+        st = p.dyn_stats(0, 148)
+    assert st["units"] > 7000 and st["wait_entries"] < 16

@@ -361,3 +361,48 @@ def test_balanced_lowering_one_gpu(name, G, mode, artifacts):
             p.sync()
             assert np.array_equal(r.cpu().numpy(), want), rep
         assert np.array_equal(p.read_link_counters(), 2 * p.link_bytes())
+
+
+@pytest.mark.parametrize("name", ["gk8_2", "torus2x4", "hypercube3", "torus2x4_h2", "ts_gk8_2"])
+@pytest.mark.parametrize("m,unit", [(1 << 20, 262144), ((1 << 20) + 48, 262144), (4096 + 5, 0),
+                                    (4 << 20, 196608)])
+@pytest.mark.parametrize("engine", ["tma", "lsu"])
+def test_chain_schedule_bit_exact(name, m, unit, engine, artifacts):
+    """Chain mode on the device (a2a_chain_kernel): the TMA ring streams each
+    route's local hops through L2 (hop u+1 loads a chunk once hop u's store of
+    it completed); odd sizes take the all-thread path.  Bit-exact vs the
+    oracle over repeated executes, link counters exact."""
+    from paper_2309_13541_b200.executor import Plan
+    from replay_bytes import replay_bytes
+    a = artifacts(name)
+    with Plan(a.g, a.sched, m=m) as p:
+        p.set_schedule("chain", unit)
+        p.set_engine(engine)
+        p.bind(0)
+        for rep in range(3):
+            send = _send(a.g.n, m, seed=rep + 21)
+            _, want, _ = replay_bytes(a.g, a.sched, send, m)
+            s = torch.from_numpy(send).cuda()
+            r = torch.zeros_like(s)
+            p.execute(s, r, count_links=True)
+            p.sync()
+            assert np.array_equal(r.cpu().numpy(), want), rep
+        assert np.array_equal(p.read_link_counters(), 3 * p.link_bytes())
+
+
+@pytest.mark.parametrize("name,m", [("torus4x4x4", 4 << 20), ("gk64_4", 1 << 20), ("gk256_4", 65536)])
+def test_chain_large_transpose(name, m, artifacts):
+    from paper_2309_13541_b200.executor import Plan
+    a = artifacts(name)
+    n = a.g.n
+    g = torch.Generator(device="cuda").manual_seed(13)
+    s = torch.randint(0, 256, (n, n, m), dtype=torch.uint8, device="cuda", generator=g)
+    r = torch.zeros_like(s)
+    with Plan(a.g, a.sched, m=m) as p:
+        p.set_schedule("chain", 262144)
+        p.bind(0)
+        for _ in range(2):
+            p.execute(s, r, count_links=True)
+            p.sync()
+        assert np.array_equal(p.read_link_counters(), 2 * p.link_bytes())
+    assert torch.equal(r, s.transpose(0, 1).contiguous())

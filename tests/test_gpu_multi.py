@@ -479,3 +479,29 @@ def test_eight_ranks_single_process(name, m, proto, sched):
     assert np.array_equal(total, 2 * plans[0].link_bytes())
     for p in plans:
         p.close()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("name,m", [("gk8_2", 1 << 20), ("torus4x4x4", 262144), ("hypercube3", (1 << 20) + 48)])
+@pytest.mark.parametrize("lowering", ["hop", "balanced"])
+def test_multiprocess_chain(world, name, m, lowering):
+    """Chain mode across GPUs: local hop chains stream on one CTA, chains break
+    at GPU boundaries (flags + exit wait as for the unit queues)."""
+    if _ngpu() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_rank_main,
+                      args=(r, world, port, name, m, 2, q, "tma", "chain:262144", False, "simple",
+                            False, lowering))
+          for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=300) for _ in ps]
+    _reap(ps)
+    for r in sorted(res, key=lambda x: x[0]):
+        assert len(r) == 3, r
+        assert r[1], f"rank {r[0]}: recv mismatch"
+        assert r[2], f"rank {r[0]}: link counters differ from schedule"
