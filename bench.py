@@ -795,7 +795,7 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
            "flush_ms_p50_by_rank": [round(x[0], 4) for x in alld],
            "step_period_ms_p50_by_rank": [round(x[1], 4) for x in alld],
            "step_ms_by_rank": [x[2] for x in alld] if os.environ.get("A2A_DIAG") else None,
-           "sync": (plan.dyn_stats(rank, plan_ctas(plan, num_ctas)) if plan.schedule in ("dynamic", "list", "cp", "mix", "ready", "spread", "chain")
+           "sync": (plan.dyn_stats(rank, plan_ctas(plan, num_ctas)) if plan.schedule in ("dynamic", "list", "cp", "mix", "ready", "spread", "chain", "chaind")
                     else plan.sync_stats(rank)),
            "kernel_timeline": tls,
            "num_ctas": plan_ctas(plan, num_ctas), "egress_max": max(i["egress_bytes"] for i in infos),

@@ -81,6 +81,7 @@ struct KParams {
   // chain mode (sched_mode 7): task k = units [chain_begin[k], chain_begin[k+1])
   const int32_t* chain_begin;
   int32_t n_tasks;
+  int32_t chain_discard;                   // sched_mode 8: discard the chain's dead scratch lines
 };
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -1363,6 +1364,20 @@ __device__ __forceinline__ void chain_body(const KParams& p, const uint32_t epoc
       }
     }
     __syncthreads();
+    if (p.chain_discard && ue - ub > 1) {
+      // every hop but the last stored into scratch that only the next hop of
+      // this task reads (build_dyn links a unit only to its sole consumer), and
+      // that read has completed: drop those dirty L2 lines instead of writing
+      // dead bytes back to HBM.  Only 128-byte lines entirely inside a unit's
+      // range are discarded (a partial line may hold a neighbour's live bytes).
+      for (int32_t k = ub; k + 1 < ue; ++k) {
+        const DevUnit u = p.units[k];
+        const uintptr_t a = (uintptr_t)(p.base[u.dst_loc] + u.dst_off);
+        const uintptr_t lo = (a + 127) & ~(uintptr_t)127, hi = (a + u.nbytes) & ~(uintptr_t)127;
+        for (uintptr_t x = lo + (uintptr_t)tid * 128; x < hi; x += (uintptr_t)kThreads * 128)
+          asm volatile("discard.global.L2 [%0], 128;" ::"l"(x) : "memory");
+      }
+    }
     if (tid == 0) {   // every unit of the task: link counters, then its flag on each GPU of its mask
       for (int32_t k = ub; k < ue; ++k) {
         const DevUnit u = p.units[k];
@@ -1446,7 +1461,7 @@ struct EngineCfg {
 static EngineCfg engine_cfg(const Plan& P) {
   const int TE = P.T_exec;
   if (P.sched_mode >= 1) {
-    const bool rq = P.sched_mode == 5, ch = P.sched_mode == 7;
+    const bool rq = P.sched_mode == 5, ch = P.sched_mode >= 7;
     if (P.engine == 1) {
       int S = P.tma_stages;
       while (S > 1 && ((20 * (size_t)S + 127) & ~(size_t)127) + (size_t)S * P.tma_chunk > 220 * 1024) --S;
@@ -1586,7 +1601,7 @@ static int bind_plan(Plan& P, int gpu, int dev, int nC) {
     CK(cudaMemset((char*)P.arena + P.scratch_off[gpu] + P.ll_off[gpu], 0, (size_t)(2 * P.ll_half[gpu])));
   if (P.sched_mode >= 1) {
     if ((rc = upload(&P.d_items, Dy.units[gpu])) != A2A_OK) return rc;
-    if (P.sched_mode == 7 && (rc = upload(&P.d_step_begin, Dy.chain_begin[gpu])) != A2A_OK) return rc;
+    if (P.sched_mode >= 7 && (rc = upload(&P.d_step_begin, Dy.chain_begin[gpu])) != A2A_OK) return rc;
     if ((rc = upload(&P.d_wait_idx, P.sched_mode == 5 ? Dy.deps_out[gpu] : Dy.wait_idx[gpu])) != A2A_OK)
       return rc;
     if ((rc = upload(&P.d_exit_idx, Dy.exit_idx[gpu])) != A2A_OK) return rc;
@@ -1867,9 +1882,10 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
         kp.n_init = Dy.n_init[P.rank];
         kp.n_into = Dy.n_into[P.rank];
       }
-      if (P.sched_mode == 7) {
+      if (P.sched_mode >= 7) {
         kp.chain_begin = (const int32_t*)P.d_step_begin;
         kp.n_tasks = (int32_t)Dy.chain_begin[P.rank].size() - 1;
+        kp.chain_discard = P.sched_mode == 8 ? 1 : 0;
       }
       kp.n_remote = Dy.n_remote[P.rank];
       kp.remote_ctas = Dy.remote_ctas[P.rank];

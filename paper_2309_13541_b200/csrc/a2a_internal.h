@@ -154,7 +154,7 @@ struct Plan {
   SyncTables sync;
   DynTables dyn;
   int32_t remote_weight = 1;                    // CTA split cost of an NVLink byte vs a local byte
-  int32_t sched_mode = 0;                       // 0 static programs, 1..6 unit queues, 7 chains
+  int32_t sched_mode = 0;                       // 0 static programs, 1..6 unit queues, 7 chains (8: + L2 discard)
   int64_t dyn_unit_bytes = 0;                   // dynamic unit size (0 = auto)
   int32_t dyn_remote_ctas = 0;                  // CTAs pinned to the NVLink queue (0 = auto split)
 

@@ -1044,7 +1044,7 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
   // so the ring never waits on its own stores (see the kernel's chain_body).
   std::vector<int> chain_next(all.size(), -1);
   std::vector<char> chain_prev(all.size(), 0);
-  if (P.sched_mode == 7 && !P.reuse) {
+  if (P.sched_mode >= 7 && !P.reuse) {
     std::vector<int> ndep(all.size(), 0);
     for (const TU& x : all)
       for (int d : x.deps) ++ndep[d];
@@ -1112,7 +1112,7 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
       for (int t = 0; t < TE; ++t)
         std::stable_sort(per[g][t].begin(), per[g][t].end(),
                          [&](int a, int b) { return key[a] < key[b]; });
-  } else if (P.sched_mode == 4 || P.sched_mode == 6 || P.sched_mode == 7) {
+  } else if (P.sched_mode == 4 || P.sched_mode == 6 || P.sched_mode >= 7) {
     // single queue, step-major; within a step the NVLink and HBM units are
     // merged in proportion to their estimated time (remote byte ~ hbm/nv local
     // bytes), each class ordered by critical path, so both pipes stay busy and
@@ -1261,7 +1261,7 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
         if (P.sched_mode == 5 && all[a].deps.empty() != all[b].deps.empty()) return all[a].deps.empty();
         return key[a] < key[b];
       });
-      if (P.sched_mode == 7) {
+      if (P.sched_mode >= 7) {
         // tasks in the order of their first unit (step-major): each chain head
         // followed by its linked units; a task only waits (at its head) on units
         // of earlier steps, whose tasks precede it in every queue
@@ -1608,6 +1608,11 @@ static int emulate_chain(Plan& P, int nC, uint8_t* const* send, uint8_t* const* 
       std::memmove(base(g, du.dst_loc) + du.dst_off, base(g, du.src_loc) + du.src_off, (size_t)du.nbytes);
       ++ran;
       if (ub + ++pos[g][c] < ue) continue;
+      if (P.sched_mode == 8)   // discarded L2 lines read back undefined: poison the dead scratch
+        for (int32_t i = ub; i + 1 < ue; ++i) {
+          const DevUnit& w = D.units[g][i];
+          std::memset(base(g, w.dst_loc) + w.dst_off, 0xCD, (size_t)w.nbytes);
+        }
       for (int32_t i = ub; i < ue; ++i) {   // task end: every unit's flag
         const DevUnit& w = D.units[g][i];
         for (int h = 0; h < G; ++h)
@@ -1773,7 +1778,7 @@ int a2a_plan_set_split(a2a_plan* plan, int32_t remote_weight) {
 
 int a2a_plan_set_schedule(a2a_plan* plan, int32_t mode, int64_t unit_bytes) {
   return guard([&]() -> int {
-    if (!plan || mode < 0 || mode > 7 || unit_bytes < 0) return fail(A2A_ERR_INVALID, "bad schedule mode");
+    if (!plan || mode < 0 || mode > 8 || unit_bytes < 0) return fail(A2A_ERR_INVALID, "bad schedule mode");
     if (plan->p.bound) return fail(A2A_ERR_STATE, "set the schedule mode before a2a_plan_bind");
     if (plan->p.ll && mode != 0)
       return fail(A2A_ERR_INVALID, "A2A_PROTO_LL plans run the static schedule only");
@@ -1829,7 +1834,7 @@ int a2a_plan_emulate(a2a_plan* plan, int32_t num_ctas, void* const* send, void* 
         return emulate_ready(plan->p, num_ctas, (uint8_t* const*)send, (uint8_t* const*)recv, seed,
                              plan->p.dyn_unit_bytes);
       if (plan->p.sched_mode >= 1)
-        return plan->p.sched_mode == 7
+        return plan->p.sched_mode >= 7
                    ? emulate_chain(plan->p, num_ctas, (uint8_t* const*)send, (uint8_t* const*)recv, seed,
                                    plan->p.dyn_unit_bytes)
                    : emulate_dyn(plan->p, num_ctas, (uint8_t* const*)send, (uint8_t* const*)recv, seed,

@@ -67,7 +67,7 @@ int dst_gpu_of(int loc, int G) {
 
 int simulate(Plan& P, int nC, const a2a_sim_params& prm, double* out) {
   if (P.ll) return fail(A2A_ERR_INVALID, "simulate: LL plans are not modelled");
-  if (P.sched_mode == 7) return fail(A2A_ERR_INVALID, "simulate: chain plans are not modelled");
+  if (P.sched_mode >= 7) return fail(A2A_ERR_INVALID, "simulate: chain plans are not modelled");
   if (!(prm.nvlink_gbs > 0 && prm.hbm_gbs > 0 && prm.cta_gbs > 0))
     return fail(A2A_ERR_INVALID, "simulate: bandwidths must be positive");
   const int G = P.G, TE = P.T_exec, R = 3 * G;

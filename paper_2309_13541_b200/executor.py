@@ -38,7 +38,7 @@ def timeline_summary(tl: np.ndarray, schedule: str | None = "static") -> dict:
     T = (tl.shape[1] - 3) // 2
     t0 = int(tl[:, 0].min())
     us = lambda x: round((int(x) - t0) / 1e3, 3)  # noqa: E731
-    if schedule and schedule.split(":")[0] in ("dynamic", "list", "cp", "mix", "ready", "spread", "chain"):
+    if schedule and schedule.split(":")[0] in ("dynamic", "list", "cp", "mix", "ready", "spread", "chain", "chaind"):
         units = tl[:, 2].astype(np.int64)
         return {"kernel_us": us(tl[:, 2 + T].max()), "start_spread_us": us(tl[:, 0].max()),
                 "entry_us": us(tl[:, 1].max()), "units_per_cta": [int(units.min()), int(units.max())],
@@ -229,9 +229,11 @@ class Plan:
         by their last producer), "spread" ("mix" with the NVLink units of a step
         interleaved over their destination GPUs), "chain" ("mix" order, but each
         route's consecutive local hops run back to back on one CTA, streaming
-        through L2 with no flag between them).  LL plans run "static" only."""
+        through L2 with no flag between them), "chaind" ("chain", and each task
+        then discards its dead intermediate scratch lines from L2 instead of
+        writing them back).  LL plans run "static" only."""
         code = {"static": 0, "dynamic": 1, "list": 2, "cp": 3, "mix": 4, "ready": 5,
-                "spread": 6, "chain": 7}[mode]
+                "spread": 6, "chain": 7, "chaind": 8}[mode]
         self._ck(N.lib.a2a_plan_set_schedule(self._h, code, int(unit_bytes)), "a2a_plan_set_schedule")
         self.schedule = mode
         return self

@@ -330,7 +330,8 @@ def test_without_self_copy(name, G, sched, artifacts):
                                   "ts_torus3x3"])
 @pytest.mark.parametrize("G", [1, 2, 4])
 @pytest.mark.parametrize("m,unit", [(1 << 20, 262144), (262144 + 48, 196608), (1000, 0)])
-def test_chain_interleavings_deliver_transpose(name, G, m, unit, artifacts):
+@pytest.mark.parametrize("mode", ["chain", "chaind"])
+def test_chain_interleavings_deliver_transpose(name, G, m, unit, mode, artifacts):
     """Chain mode (schedule "chain"): a route's consecutive local hops run on
     one CTA with no flag between them, tasks wait only at their head, all
     unit flags are published when the task ends; random interleavings of all

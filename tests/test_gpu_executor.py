@@ -367,7 +367,8 @@ def test_balanced_lowering_one_gpu(name, G, mode, artifacts):
 @pytest.mark.parametrize("m,unit", [(1 << 20, 262144), ((1 << 20) + 48, 262144), (4096 + 5, 0),
                                     (4 << 20, 196608)])
 @pytest.mark.parametrize("engine", ["tma", "lsu"])
-def test_chain_schedule_bit_exact(name, m, unit, engine, artifacts):
+@pytest.mark.parametrize("mode", ["chain", "chaind"])
+def test_chain_schedule_bit_exact(name, m, unit, engine, mode, artifacts):
     """Chain mode on the device (a2a_chain_kernel): the TMA ring streams each
     route's local hops through L2 (hop u+1 loads a chunk once hop u's store of
     it completed); odd sizes take the all-thread path.  Bit-exact vs the
@@ -376,7 +377,7 @@ def test_chain_schedule_bit_exact(name, m, unit, engine, artifacts):
     from replay_bytes import replay_bytes
     a = artifacts(name)
     with Plan(a.g, a.sched, m=m) as p:
-        p.set_schedule("chain", unit)
+        p.set_schedule(mode, unit)
         p.set_engine(engine)
         p.bind(0)
         for rep in range(3):
@@ -391,7 +392,8 @@ def test_chain_schedule_bit_exact(name, m, unit, engine, artifacts):
 
 
 @pytest.mark.parametrize("name,m", [("torus4x4x4", 4 << 20), ("gk64_4", 1 << 20), ("gk256_4", 65536)])
-def test_chain_large_transpose(name, m, artifacts):
+@pytest.mark.parametrize("mode", ["chain", "chaind"])
+def test_chain_large_transpose(name, m, mode, artifacts):
     from paper_2309_13541_b200.executor import Plan
     a = artifacts(name)
     n = a.g.n
@@ -399,7 +401,7 @@ def test_chain_large_transpose(name, m, artifacts):
     s = torch.randint(0, 256, (n, n, m), dtype=torch.uint8, device="cuda", generator=g)
     r = torch.zeros_like(s)
     with Plan(a.g, a.sched, m=m) as p:
-        p.set_schedule("chain", 262144)
+        p.set_schedule(mode, 262144)
         p.bind(0)
         for _ in range(2):
             p.execute(s, r, count_links=True)
