@@ -652,12 +652,21 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(traffic_file):
         with open(traffic_file) as fh:
-            tr = json.load(fh).get(f"{art.name}:{m}:G{G}")
+            trs = json.load(fh)
+        # the capture of this execution schedule if there is one, else of the workload
+        tr = trs.get(f"{art.name}:{m}:G{G}:{spec_ctas(schedule)[0]}") or trs.get(f"{art.name}:{m}:G{G}")
         if tr and roof["traffic"] is None:
             roof["traffic"] = tr["per_launch_bytes"]
             roof["traffic_source"] = tr["source"]
+            roof["traffic_over_algorithmic"] = round(tr["per_launch_bytes"] / roof["algorithmic_bytes_per_launch"], 4)
         elif tr:
             roof["ncu"] = tr
+    if G == 1 and str(schedule).startswith("chain"):
+        roof["note"] = ("chain mode: each route's forwarded chunks are read back from L2 by the "
+                        "next hop on the same CTA (and, 'chaind', the dead intermediate lines "
+                        "are discarded from L2), so DRAM traffic (`traffic`, ncu) is below the "
+                        "algorithmic read+write per hop and frac can exceed 1; every hop still "
+                        "copies its bytes (device link counters == schedule, tests/test_gpu_executor.py)")
 
     # ---- NCCL all_to_all_single on the same bytes (baseline, not the target)
     nres = None
@@ -905,7 +914,10 @@ def run_ours(ctx, args, name, m, steps, e2e=True, nccl=True, cpu=True, self_copy
                   "t_both_ms": round(r["t_both"] * 1e3, 4),
                   "frac_both": round(r["t_both"] / r["T"], 4),
                   "def_both": "max(t_lb, max_g schedule HBM bytes of g / HBM): at G>1 the "
-                              "local hops and incoming stores also need HBM time"},
+                              "local hops and incoming stores also need HBM time",
+                  "note": ("frac > 1: the bound charges every hop an HBM read and write; the chain "
+                           "execution serves forwarded chunks from L2 (see roofline.traffic)")
+                  if r["bound_frac"] > 1 else None},
         "recv_ok": r["recv_ok"],
         "roofline": r["roofline"],
         "cpu_baseline": cpu_rec,
