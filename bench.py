@@ -653,8 +653,11 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
     if os.path.exists(traffic_file):
         with open(traffic_file) as fh:
             trs = json.load(fh)
-        # the capture of this execution schedule if there is one, else of the workload
-        tr = trs.get(f"{art.name}:{m}:G{G}:{spec_ctas(schedule)[0]}") or trs.get(f"{art.name}:{m}:G{G}")
+        # the capture of this execution schedule; the workload's generic capture
+        # stands for the schedules whose hops all read and write DRAM (not chains)
+        sched0 = spec_ctas(schedule)[0]
+        tr = trs.get(f"{art.name}:{m}:G{G}:{sched0}") or (
+            None if str(sched0).startswith("chain") else trs.get(f"{art.name}:{m}:G{G}"))
         if tr and roof["traffic"] is None:
             roof["traffic"] = tr["per_launch_bytes"]
             roof["traffic_source"] = tr["source"]
