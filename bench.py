@@ -662,6 +662,9 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
             roof["traffic"] = tr["per_launch_bytes"]
             roof["traffic_source"] = tr["source"]
             roof["traffic_over_algorithmic"] = round(tr["per_launch_bytes"] / roof["algorithmic_bytes_per_launch"], 4)
+            if G == 1:   # the DRAM bytes the kernel really moved, over this run's time
+                roof["dram_achieved"] = round(tr["per_launch_bytes"] / T / 1e9, 1)
+                roof["dram_frac"] = round(tr["per_launch_bytes"] / T / 1e9 / hbm, 4)
         elif tr:
             roof["ncu"] = tr
     if G == 1 and str(schedule).startswith("chain"):
