@@ -119,3 +119,28 @@ def test_config_identical_in_both_arms():
     d = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
     assert d["config"] == bench.config_of("gk8_2", load_artifact("gk8_2"), 65536, 4)
     assert d["config"]["copy_self"] is False and "l2" in d["config"]
+
+
+def test_autotune_candidates():
+    """Three unit orders plus chains for every size; LL up to 1 MiB (16-CTA LL up
+    to 64 KiB), LL128 up to 4 MiB."""
+    sys.path.insert(0, ROOT)
+    import bench
+    big = bench.default_candidates(4, 16 << 20)
+    assert big == ("static", "cp:1048576", "spread:1048576", "chain:262144")
+    assert bench.default_candidates(1, 16 << 20)[2] == "mix:1048576"
+    small = bench.default_candidates(2, 4096)
+    assert "ll" in small and "ll@16" in small and "ll128" in small
+    mid = bench.default_candidates(2, 4 << 20)
+    assert "ll128" in mid and "ll" not in mid
+    assert bench.spec_ctas("ll@16") == ("ll", 16) and bench.spec_ctas("cp:1048576", 7) == ("cp:1048576", 7)
+
+
+def test_traffic_capture_matches_schedule():
+    """A chain run is never reported with the unit queues' DRAM capture."""
+    with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+        tr = json.load(fh)
+    chain = tr["gk8_2:16777216:G1:chain:262144"]
+    generic = tr["gk8_2:16777216:G1"]
+    assert chain["per_launch_bytes"] < generic["per_launch_bytes"]
+    assert chain["dram_read_bytes"] < 0.5 * generic["dram_read_bytes"]   # forwarded chunks come from L2
