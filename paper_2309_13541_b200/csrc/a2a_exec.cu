@@ -1233,8 +1233,8 @@ __device__ __forceinline__ void bulk_wait_n(uint32_t n) {
 
 template <int kEngine, int kThreads>
 __device__ __forceinline__ void chain_body(const KParams& p, const uint32_t epoch) {
-  __shared__ int s_abort, s_clean;
-  __shared__ long long s_task;
+  __shared__ int s_abort, s_cleans[2];
+  __shared__ long long s_tasks[2];
   extern __shared__ __align__(128) unsigned char dsmem[];
   const int c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5;
   const int S = p.tma_stages;
@@ -1280,15 +1280,34 @@ __device__ __forceinline__ void chain_body(const KParams& p, const uint32_t epoc
   }
   if (tid == 0) tl[1] = globaltimer();
   unsigned long long waited_ns = 0, done = 0;
-  for (;;) {
-    if (tid == 0) {
-      const long long nt = p.n_tasks;
-      const long long j = (long long)(atomicAdd(p.grab, 1ull) -
-                                      (unsigned long long)(epoch - 1) * (unsigned long long)(nt + p.nC));
-      s_task = j < nt ? j : -1;
+  // warp 1 grabs the next task and reads its head while thread 0 streams the
+  // current one; the head's dependency wait comes only after the current
+  // task has published (it may depend on it), as in dyn_body
+  auto grab = [&](int sl) {
+    const long long nt = p.n_tasks;
+    const long long j = (long long)(atomicAdd(p.grab, 1ull) -
+                                    (unsigned long long)(epoch - 1) * (unsigned long long)(nt + p.nC));
+    s_tasks[sl] = j < nt ? j : -1;
+    if (j < nt) {
+      const int32_t ub = p.chain_begin[j], ue = p.chain_begin[j + 1];
+      const DevUnit head = p.units[ub];
+      // TMA streaming needs every unit 16-byte clean, larger than a small piece,
+      // and (several hops) a later hop's chunk loaded >= S chunks after its store
+      int clean = kEngine == 1;
+      for (int32_t k = ub; k < ue && clean; ++k) {
+        const DevUnit u = p.units[k];
+        const uintptr_t a = (uintptr_t)(p.base[u.src_loc] + u.src_off) | (uintptr_t)(p.base[u.dst_loc] + u.dst_off);
+        clean = ((a | (uintptr_t)u.nbytes) & 15) == 0 && u.nbytes > kSmallPiece && u.nbytes == head.nbytes;
+      }
+      if (ue - ub > 1 && (head.nbytes + p.tma_chunk - 1) / p.tma_chunk < S) clean = 0;
+      s_cleans[sl] = clean;
     }
-    __syncthreads();
-    const long long task = s_task;
+  };
+  if (tid == 32) grab(0);
+  __syncthreads();
+  int cur = 0;
+  for (;;) {
+    const long long task = s_tasks[cur];
     if (task < 0) break;
     const int32_t ub = p.chain_begin[task], ue = p.chain_begin[task + 1];
     const DevUnit head = p.units[ub];
@@ -1299,20 +1318,11 @@ __device__ __forceinline__ void chain_body(const KParams& p, const uint32_t epoc
         s_abort = 1;
       if (tid == 0) waited_ns += globaltimer() - w0;
     }
-    if (tid == 32) {  // TMA streaming needs every unit 16-byte clean and larger than a small piece
-      int clean = kEngine == 1;
-      for (int32_t k = ub; k < ue && clean; ++k) {
-        const DevUnit u = p.units[k];
-        const uintptr_t a = (uintptr_t)(p.base[u.src_loc] + u.src_off) | (uintptr_t)(p.base[u.dst_loc] + u.dst_off);
-        clean = ((a | (uintptr_t)u.nbytes) & 15) == 0 && u.nbytes > kSmallPiece && u.nbytes == head.nbytes;
-      }
-      // a later hop's chunk is loaded >= S chunks after its store was issued
-      if (ue - ub > 1 && (head.nbytes + p.tma_chunk - 1) / p.tma_chunk < S) clean = 0;
-      s_clean = clean;
-    }
     __syncthreads();
     if (s_abort) return;
-    if (kEngine == 1 && s_clean) {
+    const int clean_now = s_cleans[cur];
+    if (tid == 32 && (kEngine == 1 && clean_now)) grab(cur ^ 1);   // overlaps thread 0's stream
+    if (kEngine == 1 && clean_now) {
       if (tid == 0) {
         fence_proxy_async();
         const uint32_t CH = (uint32_t)p.tma_chunk;
@@ -1362,6 +1372,7 @@ __device__ __forceinline__ void chain_body(const KParams& p, const uint32_t epoc
         cta_copy<4>(p.base[u.dst_loc] + u.dst_off, p.base[u.src_loc] + u.src_off, u.nbytes);
         __syncthreads();                    // the next unit reads these bytes
       }
+      if (tid == 32) grab(cur ^ 1);
     }
     __syncthreads();
     if (p.chain_discard && ue - ub > 1) {
@@ -1393,6 +1404,8 @@ __device__ __forceinline__ void chain_body(const KParams& p, const uint32_t epoc
         ++done;
       }
     }
+    __syncthreads();   // the next task's slot is filled; this task is published
+    cur ^= 1;
   }
   if (c == 0 && p.G > 1) {  // exit: every unit flagged into this GPU has landed
     bool ok = true;
