@@ -182,7 +182,13 @@ int a2a_plan_set_split(a2a_plan* plan, int32_t remote_weight);
  * per-GPU ready queue: units are enqueued when their last producer finishes
  * (completion counters counted down with system-scope atomics); 6 = as 4, with
  * each step's NVLink units interleaved over their destination GPUs in
- * proportion to their bytes (no incast on one peer).
+ * proportion to their bytes (no incast on one peer); 7 = chains: a unit whose
+ * only producer is the previous local hop of the same route (same bytes, its
+ * only consumer) runs right after it on the same CTA -- each task (a route's
+ * consecutive local hops over one unit) streams through one TMA ring, the next
+ * hop reading the previous hop's bytes back from L2, no flag between them;
+ * 8 = as 7, and each task discards its dead intermediate scratch lines from L2
+ * (discard.global.L2) instead of writing them back.
  * a2a_plan_emulate follows the
  * selected mode.  Stats: units and dependency entries of `gpu`, model makespan. */
 int a2a_plan_set_schedule(a2a_plan* plan, int32_t mode, int64_t unit_bytes);
