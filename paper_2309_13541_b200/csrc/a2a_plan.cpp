@@ -964,12 +964,15 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
       target = std::max<int64_t>(64, std::min<int64_t>(target, 1LL << 30) & ~63LL);
       for (int64_t k = tb.step_begin[t]; k < tb.step_begin[t + 1]; ++k) {
         const DevItem& it = tb.items[k];
-        for (int64_t x = 0; x < it.nbytes; x += target) {
+        // chains link local hops only; an NVLink unit pays a system-scope flag,
+        // so remote items keep >= 1 MiB units in chain mode
+        const int64_t tgt = (P.sched_mode >= 7 && it.dst_gpu != g) ? std::max<int64_t>(target, 1 << 20) : target;
+        for (int64_t x = 0; x < it.nbytes; x += tgt) {
           TU tu;
           tu.u = DevUnit{};
           tu.u.src_off = it.src_off + x;
           tu.u.dst_off = it.dst_off + x;
-          tu.u.nbytes = (int32_t)std::min(target, it.nbytes - x);
+          tu.u.nbytes = (int32_t)std::min(tgt, it.nbytes - x);
           tu.u.edge = it.edge;
           tu.u.src_loc = (int16_t)it.src_loc;
           tu.u.dst_loc = (int16_t)it.dst_loc;
