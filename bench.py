@@ -659,8 +659,12 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
         tr = trs.get(f"{art.name}:{m}:G{G}:{sched0}") or (
             None if str(sched0).startswith("chain") else trs.get(f"{art.name}:{m}:G{G}"))
         if tr and roof["traffic"] is None:
-            roof["traffic"] = tr["per_launch_bytes"]
+            roof["traffic"] = tr["per_launch_bytes"]   # G>1: NVLink tx user bytes of the busiest GPU
             roof["traffic_source"] = tr["source"]
+            if "nvl_tx_bytes" in tr:
+                roof["ncu_nvlink"] = {k: tr[k] for k in ("rank", "nvl_tx_user_bytes", "nvl_rx_user_bytes",
+                                                         "nvl_tx_bytes", "nvl_rx_bytes", "dram_read_bytes",
+                                                         "dram_write_bytes", "nvl_tx_user_gbs", "nvl_tx_raw_gbs")}
             roof["traffic_over_algorithmic"] = round(tr["per_launch_bytes"] / roof["algorithmic_bytes_per_launch"], 4)
             if G == 1:   # the DRAM bytes the kernel really moved, over this run's time
                 roof["dram_achieved"] = round(tr["per_launch_bytes"] / T / 1e9, 1)
