@@ -657,7 +657,7 @@ def measure(ctx, art, m, steps, warmup, num_ctas=0, nccl=True, e2e=True, clocks=
         # stands for the schedules whose hops all read and write DRAM (not chains)
         sched0 = spec_ctas(schedule)[0]
         tr = trs.get(f"{art.name}:{m}:G{G}:{sched0}") or (
-            None if str(sched0).startswith("chain") else trs.get(f"{art.name}:{m}:G{G}"))
+            None if (str(sched0).startswith("chain") and G == 1) else trs.get(f"{art.name}:{m}:G{G}"))
         if tr and roof["traffic"] is None:
             roof["traffic"] = tr["per_launch_bytes"]   # G>1: NVLink tx user bytes of the busiest GPU
             roof["traffic_source"] = tr["source"]
