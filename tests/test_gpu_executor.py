@@ -408,3 +408,28 @@ def test_chain_large_transpose(name, m, mode, artifacts):
             p.sync()
         assert np.array_equal(p.read_link_counters(), 2 * p.link_bytes())
     assert torch.equal(r, s.transpose(0, 1).contiguous())
+
+
+@pytest.mark.parametrize("mode", ["chain", "chaind"])
+def test_chain_with_self_copy_and_graph(mode, artifacts):
+    """Chains with the self shards copied too, and captured into a CUDA graph:
+    every replay is a fresh all-to-all (the grab counter base follows the
+    device epoch)."""
+    from paper_2309_13541_b200.executor import Plan
+    a = artifacts("gk8_2")
+    m = 1 << 20
+    with Plan(a.g, a.sched, m=m, copy_self=True) as p:
+        p.set_schedule(mode, 262144)
+        p.bind(0)
+        s = torch.empty((8, 8, m), dtype=torch.uint8, device="cuda")
+        r = torch.zeros_like(s)
+        p.execute(s.zero_(), r)
+        p.sync()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            p.execute(s, r)
+        for rep in range(3):
+            s.copy_(torch.from_numpy(_send(8, m, seed=40 + rep)).cuda())
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(r, s.transpose(0, 1).contiguous()), rep

@@ -424,7 +424,8 @@ def test_gk256_four_gpus(name, sched):
 
 @pytest.mark.parametrize("name,m", [("gk8_2", 65536), ("hypercube3", 4096 + 7), ("gk64_4", 2048)])
 @pytest.mark.parametrize("proto,sched", [("simple", "static"), ("simple", "cp"), ("simple", "mix"),
-                                         ("simple", "ready"), ("ll", "static")])
+                                         ("simple", "ready"), ("ll", "static"), ("ll128", "static"),
+                                         ("simple", "spread"), ("simple", "chain")])
 def test_eight_ranks_single_process(name, m, proto, sched):
     """The 8-GPU code paths (8 peers, 8-bit destination masks, per-GPU exit
     lists) on real hardware with fewer devices: 8 plans of an 8-GPU placement
