@@ -164,6 +164,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--epochs", type=int, default=4000)
     ap.add_argument("--lines", type=int, default=65536)
+    ap.add_argument("--local-only", action="store_true")
     a = ap.parse_args()
     mod = load_inline("ll128_stress", cpp_sources=CPP, cuda_sources=SRC,
                       functions=["enable_peer", "run_producer", "run_consumer", "run_both"],
@@ -171,7 +172,7 @@ def main():
                       verbose=False)
     out = {"epochs": a.epochs, "lines": a.lines}
     cases = [("local", 0, 0)]
-    if torch.cuda.device_count() >= 2:
+    if torch.cuda.device_count() >= 2 and not a.local_only:
         mod.enable_peer(0, 1)
         mod.enable_peer(1, 0)
         cases.append(("remote", 0, 1))
