@@ -1270,29 +1270,10 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
         // of earlier steps, whose tasks precede it in every queue
         std::vector<int> cq;
         D.chain_begin[g].clear();
-        // mode 7 packs consecutive chains into one task while every chain head
-        // after the first is dependency-free and all units have the same size:
-        // the CTA's TMA ring then streams across chain boundaries without a
-        // drain (the hop rule only adds a wait on an older store there).  Not in
-        // mode 8: a packed chain's last unit may feed another task, and the
-        // task-end discard would drop its bytes.
-        constexpr int kMaxPack = 32;   // units per packed task
-        int32_t open_units = 0, open_bytes = -1;
         for (int id : q) {
           if (chain_prev[id]) continue;
-          int len = 0;
-          for (int x = id; x >= 0; x = chain_next[x]) ++len;
-          const bool pack = P.sched_mode == 7 && open_units > 0 && all[id].deps.empty() &&
-                            all[id].u.nbytes == open_bytes && open_units + len <= kMaxPack &&
-                            len > 1;
-          if (!pack) {
-            D.chain_begin[g].push_back((int32_t)cq.size());
-            open_units = 0;
-            open_bytes = all[id].u.nbytes;
-          }
+          D.chain_begin[g].push_back((int32_t)cq.size());
           for (int x = id; x >= 0; x = chain_next[x]) cq.push_back(x);
-          open_units += len;
-          if (len == 1) open_units = kMaxPack;   // a lone unit closes its task
         }
         D.chain_begin[g].push_back((int32_t)cq.size());
         D.max_chain = 1;
