@@ -331,12 +331,30 @@ def balanced_artifact(art, m, G, placement):
     from paper_2309_13541_b200.lowering import balanced_offsets, lower_path_to_steps
     if art.routes is None:
         raise SystemExit(f"--lowering balanced needs a path-mode artifact; {art.name} is ts")
+    from paper_2309_13541_b200.lowering import split_path_schedule, step_sync_cost
     with Plan(art.g, art.sched, m=m, n_gpus=G, placement=placement) as p:
         gpu = p.placement.tolist()
-    offs = balanced_offsets(art.routes, art.path_sched, gpu, m)
-    sched = lower_path_to_steps(art.routes, art.path_sched, n=art.g.n, offsets=offs)
-    return Artifact(art.name, art.g, sched, art.meta, routes=art.routes,
-                    path_sched=art.path_sched, aug_graph=art.aug_graph), gpu
+    # whole routes, or each route's chunk range cut in 2 / 4 pieces placed
+    # independently, with 0 or 1 extra step: keep the lowest step-synchronous
+    # NVLink cost (ties: the simpler lowering); host-only and deterministic
+    best = None
+    for split, extra in BALANCE_VARIANTS:
+        ps = split_path_schedule(art.path_sched, split) if split > 1 else art.path_sched
+        offs = balanced_offsets(art.routes, ps, gpu, m, extra_steps=extra)
+        sched = lower_path_to_steps(art.routes, ps, n=art.g.n, offsets=offs)
+        cost = step_sync_cost(sched, gpu, m)
+        if best is None or cost < best[0]:
+            best = (cost, sched, ps, split, extra)
+    _, sched, ps, split, extra = best
+    meta = dict(art.meta, balanced={"split": split, "extra_steps": extra, "step_sync_bytes": best[0]})
+    return Artifact(art.name, art.g, sched, meta, routes=art.routes,
+                    path_sched=ps, aug_graph=art.aug_graph), gpu
+
+
+# (pieces per route, extra steps) tried by balanced_artifact; GK(8,2) at 8 GPUs:
+# 320 MiB step-synchronous egress with whole routes, 296 MiB with 2 pieces and one
+# extra step, against an aggregate bound of 288 MiB
+BALANCE_VARIANTS = ((1, 0), (2, 0), (2, 1), (4, 1))
 
 
 LL_MAX_SHARD = 1 << 20       # autotune tries the LL transport up to this shard size
@@ -912,7 +930,9 @@ def run_ours(ctx, args, name, m, steps, e2e=True, nccl=True, cpu=True, self_copy
     return {
         "value": round(r["value"], 3), "ms_per_step": round(r["T"] * 1e3, 4),
         "config": config_of(name, art0, m, G),
-        "exec": {"lowering": LOWERINGS[lowering], "lowering_skipped": skipped,
+        "exec": {"lowering": LOWERINGS[lowering] + (
+                     f" {art.meta['balanced']}" if lowering == "balanced" and "balanced" in art.meta else ""),
+                 "lowering_skipped": skipped,
                  "placement": f"{args.placement} {r['placement'] if G > 1 else '(all nodes on GPU 0)'}",
                  "num_ctas": r["num_ctas"], "schedule": schedule, "schedule_autotune_ms": tune,
                  "engine": "tma (cp.async.bulk)" if schedule != "ll" else "ll lines (st.volatile.v4)"},

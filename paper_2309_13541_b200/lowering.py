@@ -16,7 +16,8 @@ from __future__ import annotations
 
 from .schedule import ChunkedSchedule, Instruction, ScheduleError
 
-__all__ = ["lower_path_to_steps", "balanced_offsets", "step_sync_cost", "collapse_aug_routes",
+__all__ = ["lower_path_to_steps", "balanced_offsets", "split_path_schedule", "step_sync_cost",
+           "collapse_aug_routes",
            "collapse_aug_schedule", "schedule_link_chunks", "hop_histogram"]
 
 
@@ -52,6 +53,27 @@ def lower_path_to_steps(routes, sched, n: int | None = None, offsets=None) -> Ch
     return ChunkedSchedule(n=sched.n if n is None else n, nsteps=nsteps,
                            chunk_bytes=sched.chunk_bytes, Q=sched.Q, mode="ts",
                            instructions=ops)
+
+
+def split_path_schedule(sched, parts: int) -> ChunkedSchedule:
+    """The same path schedule with every instruction's chunk range [c0, c1)
+    cut into up to `parts` near-equal sub-ranges (one instruction each, same
+    route).  Routes, links and bytes per link are unchanged; the pieces can
+    then start at different steps (balanced_offsets), which balances the
+    per-step NVLink load at a finer grain than whole routes."""
+    if sched.mode != "path":
+        raise ScheduleError(f"expected a path-mode schedule, got {sched.mode!r}")
+    parts = max(1, int(parts))
+    ins = []
+    for i in sched.instructions:
+        n = i.c1 - i.c0
+        k = max(1, min(parts, n))
+        for j in range(k):
+            a, b = i.c0 + n * j // k, i.c0 + n * (j + 1) // k
+            if b > a:
+                ins.append(Instruction(t=i.t, src=i.src, dst=i.dst, s=i.s, d=i.d, c0=a, c1=b))
+    return ChunkedSchedule(n=sched.n, nsteps=sched.nsteps, chunk_bytes=sched.chunk_bytes,
+                           Q=sched.Q, mode="path", instructions=ins)
 
 
 def _route_nodes(routes, ins) -> list:

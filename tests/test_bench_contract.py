@@ -78,9 +78,27 @@ def test_balanced_lowering_option():
     a = load_artifact("gk8_2")
     b, gpu = bench.balanced_artifact(a, 1 << 20, 8, "optimized")
     assert sorted(gpu) == list(range(8))
-    key = lambda i: (i.src, i.dst, i.s, i.d, i.c0, i.c1)  # noqa: E731
-    assert sorted(map(key, b.sched.instructions)) == sorted(map(key, a.sched.instructions))
+    # the same hops carrying the same chunks (a route's chunk range may be cut into
+    # pieces that start at different steps), different steps
+    def hops(s):
+        cover = {}
+        for i in s.instructions:
+            cover.setdefault((i.src, i.dst, i.s, i.d), []).append((i.c0, i.c1))
+        out = {}
+        for k, iv in cover.items():
+            iv.sort()
+            merged = [list(iv[0])]
+            for c0, c1 in iv[1:]:
+                assert c0 >= merged[-1][1]                 # no chunk twice on a hop
+                if c0 == merged[-1][1]:
+                    merged[-1][1] = c1
+                else:
+                    merged.append([c0, c1])
+            out[k] = merged
+        return out
+    assert hops(b.sched) == hops(a.sched)
     assert [i.t for i in b.sched.instructions] != [i.t for i in a.sched.instructions]
+    assert b.meta["balanced"]["step_sync_bytes"] <= 320 << 20
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
                           "--gpus", "8", "--lowering", "balanced", "--m", "4099", "--steps", "2"],
                          capture_output=True, text=True, timeout=300, cwd=ROOT)
