@@ -426,7 +426,8 @@ def test_gk256_four_gpus(name, sched):
 @pytest.mark.parametrize("proto,sched", [("simple", "static"), ("simple", "cp"), ("simple", "mix"),
                                          ("simple", "ready"), ("ll", "static"), ("ll128", "static"),
                                          ("simple", "spread"), ("simple", "chain")])
-def test_eight_ranks_single_process(name, m, proto, sched):
+@pytest.mark.parametrize("lowering", ["hop", "balanced"])
+def test_eight_ranks_single_process(name, m, proto, sched, lowering):
     """The 8-GPU code paths (8 peers, 8-bit destination masks, per-GPU exit
     lists) on real hardware with fewer devices: 8 plans of an 8-GPU placement
     in one process, rank r on device r % ndev, each with a reduced CTA count so
@@ -441,6 +442,11 @@ def test_eight_ranks_single_process(name, m, proto, sched):
     from paper_2309_13541_b200.executor import Plan
     a = load_artifact(name)
     R = 8
+    placement = "optimized"
+    if lowering == "balanced":        # bench.py's 8-GPU lowering (route pieces, extra step)
+        sys.path.insert(0, ROOT)
+        import bench
+        a, placement = bench.balanced_artifact(a, 16 << 20, R, "optimized")
     per_dev = -(-R // ndev)
     nc = max(8, 144 // per_dev)
     plans = []
@@ -450,7 +456,7 @@ def test_eight_ranks_single_process(name, m, proto, sched):
     os.environ["A2A_NONCOOP"] = "1"
     try:
         for r in range(R):
-            p = Plan(a.g, a.sched, m=m, n_gpus=R, placement="optimized", protocol=proto)
+            p = Plan(a.g, a.sched, m=m, n_gpus=R, placement=placement, protocol=proto)
             if sched != "static":
                 p.set_schedule(sched, 4096)
             plans.append(p.bind(r, device=r % ndev, num_ctas=nc))
