@@ -369,7 +369,7 @@ __device__ __forceinline__ bool ll128_piece(const char* sbase, char* dbase, cons
     // per warp and turn, all their loads in flight before the first use.
     // Per-lane base pointers and strides are set up once (no division in the
     // loop); only the piece's last line can be partial.
-    constexpr int kU = 8;
+    constexpr int kU = 4;
     const int cap = j == 7 ? 8 : 16;
     const int64_t NLfull = n / 120;                       // lines entirely inside the piece
     const char* sp = sll ? sbase + 128 * (sa / 120) + 16 * j : sbase + sa + 16 * j;
