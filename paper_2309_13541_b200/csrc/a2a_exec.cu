@@ -63,7 +63,6 @@ struct KParams {
   int32_t sync_mode;                       // bit0: acq_rel (not sc) publish fence; bit1: no
                                            // explicit publish fence; bit2: force .sys at G=1
   int32_t smem_prog, smem_batch, batch;    // dynamic smem offsets, pieces per staged batch
-  int32_t piece_stride;                    // > 0: CTA c's pieces start at c * piece_stride
   unsigned long long* timeline;            // [nC][2T'+3] %globaltimer stamps (see read_timeline)
   // dynamic mode (a2a_dyn_kernel)
   const DevUnit* units;                    // this GPU's units in grab order
@@ -661,11 +660,7 @@ __device__ __forceinline__ void exec_body(const KParams& p, const uint32_t epoch
   for (int i = st; i < p.T; i += kThreads) s_prog[i] = p.prog[(int64_t)c * p.T + i];
   // if all of this CTA's pieces (every step) fit the batch buffer, stage them
   // now too: no per-step piece load on the latency path (small shards)
-  // stride layout (small plans): this CTA's pieces sit at c * stride, so they are
-  // loaded together with the program instead of after it
-  const bool strided = p.piece_stride > 0 && p.piece_stride <= p.batch;
-  const int32_t pb0 = strided ? c * p.piece_stride : p.prog[(int64_t)c * p.T].pb;
-  const int32_t pe1 = strided ? pb0 + p.piece_stride : p.prog[(int64_t)c * p.T + p.T - 1].pe;
+  const int32_t pb0 = p.prog[(int64_t)c * p.T].pb, pe1 = p.prog[(int64_t)c * p.T + p.T - 1].pe;
   const bool all_staged = pe1 - pb0 <= p.batch;
   if (all_staged)
     for (int i = st; i < pe1 - pb0; i += kThreads) s_pc[i] = p.pieces[pb0 + i];
@@ -1910,7 +1905,6 @@ int a2a_plan_execute(a2a_plan* plan, const void* send, void* recv, void* stream,
       kp.pin_queues = Dy.pin;
     } else {
       kp.n_exit = (int32_t)P.sync.exit_idx[P.rank].size();
-      kp.piece_stride = P.sync.stride.empty() ? 0 : P.sync.stride[P.rank];
     }
     kp.wait_idx = (const int32_t*)P.d_wait_idx;
     kp.counters = (unsigned long long*)P.d_counters;

@@ -88,9 +88,6 @@ struct SyncTables {
   std::vector<std::vector<int32_t>> wait_off;   // [g][t*nC + c .. +1] into wait_idx[g]
   std::vector<std::vector<int32_t>> wait_idx;   // [g] producer slots to acquire
   std::vector<std::vector<int32_t>> exit_idx;   // [g] every producer slot that writes into g
-  // [g] > 0: CTA c's pieces start at c * stride (padded with empty pieces), so a
-  // CTA stages its program and its pieces with independent loads (small plans)
-  std::vector<int32_t> stride;
 };
 
 // Dynamic mode: one unit of work = a contiguous sub-range of

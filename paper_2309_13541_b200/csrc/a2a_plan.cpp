@@ -778,7 +778,6 @@ int build_sync(Plan& P, int nC) {
   // per-CTA programs: exact piece lists (split below 1 GiB so nbytes fits int32)
   S.pieces.assign(G, {});
   S.prog.assign(G, {});
-  S.stride.assign(G, 0);
   for (int g = 0; g < G; ++g) {
     std::vector<std::vector<std::vector<DevPiece>>> per_ct(nC, std::vector<std::vector<DevPiece>>(TE));
     for (int t = 0; t < TE; ++t)
@@ -798,19 +797,7 @@ int build_sync(Plan& P, int nC) {
     auto& pcs = S.pieces[g];
     auto& prog = S.prog[g];
     prog.assign((size_t)nC * TE, CtaStep{});
-    // small plans: pad every CTA's pieces to a common stride (<= 128, the
-    // smallest staging batch is 64), so the kernel finds them at c * stride
-    // without first reading the CTA's program (one dependent load less)
-    int32_t stride = 0;
-    for (int c = 0; c < nC; ++c) {
-      int32_t k = 0;
-      for (int t = 0; t < TE; ++t) k += (int32_t)per_ct[c][t].size();
-      stride = std::max(stride, k);
-    }
-    if (stride > 64 || stride < 1) stride = 0;
-    S.stride[g] = stride;
-    for (int c = 0; c < nC; ++c) {
-      if (stride) pcs.resize((size_t)c * stride, DevPiece{});   // empty pieces (nbytes 0) pad
+    for (int c = 0; c < nC; ++c)
       for (int t = 0; t < TE; ++t) {
         CtaStep& cs = prog[(size_t)c * TE + t];
         cs.pb = (int32_t)pcs.size();
@@ -820,8 +807,6 @@ int build_sync(Plan& P, int nC) {
         cs.we = S.wait_off[g][(size_t)t * nC + c + 1];
         cs.mask = S.dst_mask[g][(size_t)t * nC + c];
       }
-    }
-    if (stride) pcs.resize((size_t)nC * stride, DevPiece{});
   }
   P.sync = std::move(S);
   return A2A_OK;
@@ -1771,8 +1756,7 @@ int a2a_plan_check_bounds(a2a_plan* plan, int32_t num_ctas) {
           }
       } else {
         for (const DevPiece& q : P.sync.pieces[g])
-          if (q.nbytes == 0 && P.sync.stride[g]) continue;   // stride padding, never in a program range
-          else if (!check(g, q.src_loc, q.src_off, q.dst_loc, q.dst_off, q.nbytes, q.kind) ||
+          if (!check(g, q.src_loc, q.src_off, q.dst_loc, q.dst_off, q.nbytes, q.kind) ||
               !(q.src_loc == loc_send() || q.src_loc == loc_recv(g) || q.src_loc == loc_scratch(g, G) ||
                 q.src_loc == loc_ll(g, G)) ||
               (P.ll && !(q.kind & kLLDst) && q.dst_loc != loc_recv(g))) {   // LL: plain stores stay local
