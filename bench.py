@@ -7,14 +7,24 @@ N=1 runs in-process; N>1 is launched by torchrun (one rank per GPU, NCCL only
 for bootstrap / barriers / the NCCL baseline, never on the executor path).
 
 Workload: BASELINE.json configs[1], GenKautz N=8 d=2, 16 MiB per pair, the
-frozen decomposed-MCF schedule (artifacts/gk8_2), hop i of every route at step
-i; the 8 virtual nodes are placed v*G//8 on G GPUs (one per GPU at G=8).
-A "step" = one complete all-to-all.  value = whole-job algBW
-N(N-1)m / T (GB/s); per_gpu = value / G.
+frozen decomposed-MCF schedule (artifacts/gk8_2), lowered hop i -> step i (at
+G >= 2 the autotune also times the step-balanced lowering); the 8 virtual nodes
+are placed by the placement optimiser on G GPUs (one per GPU at G=8).  At N=1
+the line also carries `largest_single_gpu`: torus 4x4x4 at 4 MiB (configs[2]).
+A "step" = one complete all-to-all of the s != d shards (the reference
+transpose; the self-copy variant is reported as `with_self_copy`).  value =
+whole-job algBW N(N-1)m / T (GB/s); per_gpu = value / G.
+Execution: autotuned among static per-CTA programs, unit queues (cp, mix /
+spread), chains (a route's local hops streamed through L2 on one CTA) and, for
+small shards, the LL / LL128 line protocols; every candidate's output is
+checked first.  `config` (the workload) is identical in both arms; `exec` says
+how our arm ran it.
 Timing: W warm-up steps, then K steps each bracketed by CUDA events on the
 launching stream; L2 flushed (512 MiB memset, outside the events) between steps unless
 every GPU's send buffer exceeds L2 (then inputs are larger than L2, recorded in config.l2);
 barrier + synchronize around the timed region; per-step max over ranks.
+--impl reference: the CPU restatement of the reference replay (oracle/replay_bytes.c)
+on all host threads, rank 0 only; nothing of the product library is loaded.
 """
 from __future__ import annotations
 
