@@ -1135,6 +1135,15 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
           for (int sx : succ[id]) best = std::max(best, bl[sx]);
           bl[id] = best + all[id].u.nbytes / (all[id].dst_gpu != all[id].g ? nv : hbm);
         }
+    // chains (mode >= 7): a head costs its whole chain (it is run with its
+    // linked units, which are emitted with it and cost nothing on their own step)
+    auto lcost = [&](int id) -> double {
+      if (P.sched_mode < 7) return all[id].u.nbytes / hbm;
+      if (chain_prev[id]) return 0.0;
+      double c = 0;
+      for (int x = id; x >= 0; x = chain_next[x]) c += all[x].u.nbytes / hbm;
+      return c;
+    };
     for (int g = 0; g < G; ++g) {
       double k = 0;
       for (int t = 0; t < TE; ++t) {
@@ -1142,7 +1151,7 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
         double rt = 0, lt = 0;
         for (int id : per[g][t]) {
           if (all[id].dst_gpu != g) { rq.push_back(id); rt += all[id].u.nbytes / nv; }
-          else { lq.push_back(id); lt += all[id].u.nbytes / hbm; }
+          else { lq.push_back(id); lt += lcost(id); }
         }
         auto bysl = [&](int a, int b) { return bl[a] > bl[b]; };
         std::stable_sort(rq.begin(), rq.end(), bysl);
@@ -1178,7 +1187,7 @@ int build_dyn(Plan& P, int nC, int64_t unit_bytes) {
           const bool take_r = j >= lq.size() ||
                               (i < rq.size() && (rt > 0 ? er / rt : 1.0) <= (lt > 0 ? el / lt : 1.0));
           if (take_r) { er += all[rq[i]].u.nbytes / nv; merged.push_back(rq[i++]); }
-          else { el += all[lq[j]].u.nbytes / hbm; merged.push_back(lq[j++]); }
+          else { el += lcost(lq[j]); merged.push_back(lq[j++]); }
         }
         per[g][t] = merged;
         for (int id : per[g][t]) key[id] = k++;
