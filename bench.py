@@ -403,7 +403,9 @@ def default_candidates(G, m):
     interleaves each step's NVLink units over their destination GPUs), chains
     (each route's local hops streamed through L2 on one CTA), plus LL / LL128
     for small and medium shards."""
-    return ("static", "cp:1048576", "spread:1048576" if G > 2 else "mix:1048576", "chain:262144") + (
+    q = "spread" if G > 2 else "mix"
+    return ("static", "cp:1048576", f"{q}:1048576", "chain:262144") + (
+        (f"{q}:262144",) if G > 1 and m <= LL128_MAX_SHARD else ()) + (
         ("ll",) if m <= LL_MAX_SHARD else ()) + (("ll@16",) if m <= 65536 else ()) + (
         ("ll128",) if m <= LL128_MAX_SHARD else ())
 

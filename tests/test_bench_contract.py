@@ -150,7 +150,8 @@ def test_autotune_candidates():
     small = bench.default_candidates(2, 4096)
     assert "ll" in small and "ll@16" in small and "ll128" in small
     mid = bench.default_candidates(2, 4 << 20)
-    assert "ll128" in mid and "ll" not in mid
+    assert "ll128" in mid and "ll" not in mid and "mix:262144" in mid
+    assert "spread:262144" in bench.default_candidates(4, 4 << 20)
     assert bench.spec_ctas("ll@16") == ("ll", 16) and bench.spec_ctas("cp:1048576", 7) == ("cp:1048576", 7)
 
 
