@@ -1861,7 +1861,7 @@ int a2a_plan_set_recv_buffers(a2a_plan* plan, int32_t count) {
 
 int a2a_plan_set_sync_mode(a2a_plan* plan, int32_t mode) {
   return guard([&]() -> int {
-    if (!plan || mode < 0 || mode > 127) return fail(A2A_ERR_INVALID, "bad sync mode");
+    if (!plan || mode < 0 || mode > 63) return fail(A2A_ERR_INVALID, "bad sync mode");
     plan->p.sync_mode = mode;
     return A2A_OK;
   });
