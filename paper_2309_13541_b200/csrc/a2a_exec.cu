@@ -515,32 +515,6 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uin
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
-// L2 eviction-priority variants (chains): the next hop re-reads an intermediate
-// store soon, so it is kept (evict_last); bytes read or written for the last
-// time (send, a consumed intermediate, recv) go first (evict_first)
-__device__ __forceinline__ uint64_t l2_policy(bool keep) {
-  uint64_t pol;
-  if (keep)
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  else
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void bulk_load_hint(void* smem_dst, const void* gsrc, uint32_t bytes,
-                                               uint64_t* bar, uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(smem_dst)),
-      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_store_hint(void* gdst, const void* smem_src, uint32_t bytes,
-                                                uint64_t pol) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
-               "r"(smem_u32(smem_src)), "r"(bytes), "l"(pol)
-               : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
 __device__ __forceinline__ void bulk_wait_read1() {
   asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
 }
@@ -1259,7 +1233,6 @@ __device__ __forceinline__ void bulk_wait_n(uint32_t n) {
 
 template <int kEngine, int kThreads>
 __device__ __forceinline__ void chain_body(const KParams& p, const uint32_t epoch) {
-  __shared__ bool ring_keep[32];
   __shared__ int s_abort, s_cleans[2];
   __shared__ long long s_tasks[2];
   extern __shared__ __align__(128) unsigned char dsmem[];
@@ -1352,7 +1325,6 @@ __device__ __forceinline__ void chain_body(const KParams& p, const uint32_t epoc
     if (kEngine == 1 && clean_now) {
       if (tid == 0) {
         fence_proxy_async();
-        const uint64_t pol_last = l2_policy(true), pol_first = l2_policy(false);
         const uint32_t CH = (uint32_t)p.tma_chunk;
         const int64_t n = head.nbytes;
         const uint32_t K = (uint32_t)((n + CH - 1) / CH), total = K * (uint32_t)(ue - ub);
@@ -1368,13 +1340,8 @@ __device__ __forceinline__ void chain_body(const KParams& p, const uint32_t epoc
           const uint32_t st = (g0 + nl) % S;
           ring_dst[st] = p.base[u.dst_loc] + u.dst_off + off;
           ring_n[st] = len;
-          ring_keep[st] = k + 1 < ue;   // an intermediate store: the next hop reads it back
           mbar_expect_tx(&bars[st], len);
-          if (p.sync_mode & 64)   // L2 priority hints (experiment)
-            bulk_load_hint(stages + (size_t)st * CH, p.base[u.src_loc] + u.src_off + off, len, &bars[st],
-                           pol_first);
-          else
-            bulk_load(stages + (size_t)st * CH, p.base[u.src_loc] + u.src_off + off, len, &bars[st]);
+          bulk_load(stages + (size_t)st * CH, p.base[u.src_loc] + u.src_off + off, len, &bars[st]);
           ++nl;
           return true;
         };
@@ -1383,11 +1350,7 @@ __device__ __forceinline__ void chain_body(const KParams& p, const uint32_t epoc
         while (ns < nl) {
           const uint32_t st = (g0 + ns) % S;
           mbar_wait(&bars[st], ((g0 + ns) / S) & 1);
-          if (p.sync_mode & 64)
-            bulk_store_hint(ring_dst[st], stages + (size_t)st * CH, ring_n[st],
-                            ring_keep[st] ? pol_last : pol_first);
-          else
-            bulk_store(ring_dst[st], stages + (size_t)st * CH, ring_n[st]);
+          bulk_store(ring_dst[st], stages + (size_t)st * CH, ring_n[st]);
           ++ns;
           if (more) {
             if (S == 1) {
