@@ -525,6 +525,19 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// Race hunting on the device (tests only).  sync_mode bit 6: before every step /
+// unit / chain task the CTA naps a pseudo-random 0-16 us (keyed by epoch, CTA and
+// wait range), so producers and consumers finish in orders the default timing
+// never produces.  Bit 7 (mutation self-test): the dependency waits are skipped, so
+// a perturbed run must then deliver a wrong transpose -- proof that the check
+// bites.  Entry/exit barriers are unaffected.
+constexpr int kSyncPerturb = 64, kSyncNoWaits = 128;
+__device__ __forceinline__ void perturb_nap(uint32_t epoch, uint32_t key) {
+  uint32_t h = epoch * 0x9E3779B1u ^ blockIdx.x * 0x85EBCA77u ^ key * 0xC2B2AE3Du;
+  h ^= h >> 15; h *= 0x2C1B3C6Du; h ^= h >> 12; h *= 0x297A2D39u; h ^= h >> 15;
+  if (h & 1) __nanosleep((h >> 8) & 16383);
+}
+
 // Warp 0 waits until every listed flag reached `epoch`: each lane polls its
 // flags with relaxed loads (optionally backing off), then every lane executes
 // fence.acq_rel (the PTX acquire pattern: morally-strong read + fence).
@@ -535,6 +548,8 @@ __device__ bool warp_wait_flags(const uint32_t* flags, const int32_t* idx, int32
   const int lane = threadIdx.x & 31;
   bool ok = true;
   uint64_t t0 = 0;
+  if (mode & kSyncPerturb) perturb_nap(epoch, (uint32_t)lo * 7919u + (uint32_t)hi);
+  if (mode & kSyncNoWaits) hi = lo;
   for (int32_t i = lo + lane; i < hi; i += 32) {
     const uint32_t* f = flags + idx[i];
     uint32_t spins = 0;
@@ -707,7 +722,7 @@ __device__ __forceinline__ void exec_body(const KParams& p, const uint32_t epoch
       continue;
     }
     if (tid == 0 && cs.we <= cs.wb) tl[3 + p.T + t] = 0;
-    bool waited = cs.we <= cs.wb;
+    bool waited = cs.we <= cs.wb && !(p.sync_mode & kSyncPerturb);
     for (int32_t base = cs.pb; base < cs.pe; base += p.batch) {
       const int n = min(p.batch, cs.pe - base);
       DevPiece* pcs = s_pc;
@@ -1034,7 +1049,7 @@ __device__ __forceinline__ void dyn_body(const KParams& p, const uint32_t epoch)
       return __shfl_sync(0xffffffffu, ok, 0);
     }
     const DevUnit& u = s_u[sl];
-    if (s_idx[sl] < 0 || u.we <= u.wb) return true;
+    if (s_idx[sl] < 0 || (u.we <= u.wb && !(p.sync_mode & kSyncPerturb))) return true;
     const uint64_t w0 = globaltimer();
     bool ok = warp_wait_flags(my_flags, p.unit_wait, u.wb, u.we, epoch, p.timeout_ns, p.err,
                               sys, p.sync_mode);
@@ -1311,7 +1326,7 @@ __device__ __forceinline__ void chain_body(const KParams& p, const uint32_t epoc
     if (task < 0) break;
     const int32_t ub = p.chain_begin[task], ue = p.chain_begin[task + 1];
     const DevUnit head = p.units[ub];
-    if (warp == 0 && head.we > head.wb) {
+    if (warp == 0 && (head.we > head.wb || (p.sync_mode & kSyncPerturb))) {
       const uint64_t w0 = globaltimer();
       if (!warp_wait_flags(my_flags, p.unit_wait, head.wb, head.we, epoch, p.timeout_ns, p.err, sys,
                            p.sync_mode) && tid == 0)
@@ -1824,7 +1839,7 @@ int a2a_plan_set_recv_buffers(a2a_plan* plan, int32_t count) {
 
 int a2a_plan_set_sync_mode(a2a_plan* plan, int32_t mode) {
   return guard([&]() -> int {
-    if (!plan || mode < 0 || mode > 63) return fail(A2A_ERR_INVALID, "bad sync mode");
+    if (!plan || mode < 0 || mode > 255) return fail(A2A_ERR_INVALID, "bad sync mode");
     plan->p.sync_mode = mode;
     return A2A_OK;
   });

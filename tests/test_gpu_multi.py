@@ -46,7 +46,7 @@ def _port():
 
 
 def _rank_main(rank, world, port, name, m, reps, q, engine="lsu", sched="static", reuse=False,
-               proto="simple", graph=False, lowering="hop"):
+               proto="simple", graph=False, lowering="hop", sync_mode=None):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     try:
@@ -72,6 +72,8 @@ def _rank_main(rank, world, port, name, m, reps, q, engine="lsu", sched="static"
         plan.set_schedule_spec(sched)      # "<mode>[:<unit bytes>[:<pinned NVLink CTAs>]]"
         plan.bind(rank, device=rank)
         plan.set_timeout(20.0)
+        if sync_mode is not None:
+            plan.set_sync_mode(sync_mode)
         connect(plan)
         nodes = local_nodes(plan, rank)
         # LL: only local CTAs write recv, so any device buffer works
@@ -512,3 +514,61 @@ def test_multiprocess_chain(world, name, m, lowering):
         assert len(r) == 3, r
         assert r[1], f"rank {r[0]}: recv mismatch"
         assert r[2], f"rank {r[0]}: link counters differ from schedule"
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("name,m,engine,proto,sched", [
+    ("gk8_2", 1 << 20, "tma", "simple", "static"),
+    ("gk8_2", 65536 + 64, "lsu", "simple", "static"),
+    ("gk8_2", 1 << 20, "tma", "simple", "cp:262144"),
+    ("hypercube3", 1 << 20, "tma", "simple", "spread:262144"),
+    ("torus4x4x4", 65536, "tma", "simple", "mix:65536"),
+    ("gk8_2", 1 << 20, "tma", "simple", "chain:262144"),
+    ("hypercube3", 65536 + 40, "lsu", "ll128", "static"),
+    ("torus2x4_h2", 4096 + 7, "lsu", "ll", "static")])
+def test_multiprocess_perturbed(world, name, m, engine, proto, sched):
+    """Race hunting across GPUs (tests/test_gpu_race.py): every CTA naps a
+    pseudo-random 0-16 us before each step / unit / task (sync_mode bit 6), so
+    producers and consumers on different GPUs finish in new orders every
+    repeat; every repeat is bit-exact."""
+    if _ngpu() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_rank_main,
+                      args=(r, world, port, name, m, 4, q, engine, sched, False, proto,
+                            False, "hop", 2 | 64))
+          for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=300) for _ in ps]
+    _reap(ps)
+    for r in sorted(res, key=lambda x: x[0]):
+        assert len(r) == 3, r
+        assert r[1], f"rank {r[0]}: recv mismatch"
+        assert r[2], f"rank {r[0]}: link counters differ from schedule"
+
+
+@pytest.mark.parametrize("sched", ["static", "cp:262144"])
+def test_multiprocess_mutation_without_waits_is_caught(sched):
+    """The same perturbation with the dependency waits skipped (bit 7) must
+    give a wrong transpose on some rank."""
+    world = 2
+    if _ngpu() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_rank_main,
+                      args=(r, world, port, "gk8_2", 1 << 20, 4, q, "tma", sched, False, "simple",
+                            False, "hop", 2 | 64 | 128))
+          for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=300) for _ in ps]
+    _reap(ps)
+    assert all(len(r) == 3 for r in res), res
+    assert not all(r[1] for r in res), "dropped dependencies went unnoticed"
