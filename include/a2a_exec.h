@@ -283,8 +283,9 @@ int a2a_plan_read_timeline(a2a_plan* plan, uint64_t* out, int32_t* out_cols);
  * bit3 = __nanosleep backoff while polling, bit4 = ld.acquire polling instead
  * of ld.relaxed + fence.acq_rel, bit5 = one fence.acq_rel then relaxed flag
  * stores (peers first).  Default 2.  Race hunting (tests): bit6 = every CTA naps
- * a pseudo-random 0-16 us before each step / unit / chain task; bit7 = skip the
- * dependency waits (mutation self-test: a perturbed run must then fail). */
+ * a pseudo-random 0-16 us (1 in 16: up to 260 us) before each step / unit /
+ * chain task; bit7 = skip the dependency waits (mutation self-test: a
+ * perturbed run must then fail). */
 int a2a_plan_set_sync_mode(a2a_plan* plan, int32_t mode);
 /* device-side flag-wait timeout (ns, default 10 s) */
 int a2a_plan_set_timeout(a2a_plan* plan, int64_t timeout_ns);

@@ -526,16 +526,19 @@ __device__ __forceinline__ void fence_proxy_async() {
 }
 
 // Race hunting on the device (tests only).  sync_mode bit 6: before every step /
-// unit / chain task the CTA naps a pseudo-random 0-16 us (keyed by epoch, CTA and
-// wait range), so producers and consumers finish in orders the default timing
-// never produces.  Bit 7 (mutation self-test): the dependency waits are skipped, so
-// a perturbed run must then deliver a wrong transpose -- proof that the check
-// bites.  Entry/exit barriers are unaffected.
+// unit / chain task the CTA naps a pseudo-random 0-16 us, one time in 16 up to
+// 260 us (keyed by epoch, CTA and wait range), so producers and consumers finish
+// in orders the default timing never produces.  Bit 7 (mutation self-test): the
+// dependency waits are skipped, so a perturbed run must then deliver a wrong
+// transpose -- proof that the check bites.  Entry/exit barriers are unaffected.
 constexpr int kSyncPerturb = 64, kSyncNoWaits = 128;
 __device__ __forceinline__ void perturb_nap(uint32_t epoch, uint32_t key) {
   uint32_t h = epoch * 0x9E3779B1u ^ blockIdx.x * 0x85EBCA77u ^ key * 0xC2B2AE3Du;
   h ^= h >> 15; h *= 0x2C1B3C6Du; h ^= h >> 12; h *= 0x297A2D39u; h ^= h >> 15;
-  if (h & 1) __nanosleep((h >> 8) & 16383);
+  if (h & 1) return;
+  // mostly short naps; one in 16 long enough that a producer which grabbed its
+  // unit early finishes after consumers queued hundreds of units later
+  __nanosleep(((h >> 1) & 7) == 0 ? (h >> 8) & 262143 : (h >> 8) & 16383);
 }
 
 // Warp 0 waits until every listed flag reached `epoch`: each lane polls its

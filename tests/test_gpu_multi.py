@@ -528,9 +528,9 @@ def test_multiprocess_chain(world, name, m, lowering):
     ("torus2x4_h2", 4096 + 7, "lsu", "ll", "static")])
 def test_multiprocess_perturbed(world, name, m, engine, proto, sched):
     """Race hunting across GPUs (tests/test_gpu_race.py): every CTA naps a
-    pseudo-random 0-16 us before each step / unit / task (sync_mode bit 6), so
-    producers and consumers on different GPUs finish in new orders every
-    repeat; every repeat is bit-exact."""
+    pseudo-random 0-16 us (1 in 16: up to 260 us) before each step / unit /
+    task (sync_mode bit 6), so producers and consumers on different GPUs
+    finish in new orders every repeat; every repeat is bit-exact."""
     if _ngpu() < world:
         pytest.skip(f"needs {world} GPUs")
     import torch.multiprocessing as mp

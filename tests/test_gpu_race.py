@@ -3,8 +3,9 @@
 compute-sanitizer is closed on this pool, and the host emulator
 (tests/test_emulation.py) is a model of the device, not the device.  This is
 the on-hardware counterpart.  With sync_mode bit 6 every CTA naps a
-pseudo-random 0-16 us before each step, unit or chain task; the nap is keyed by
-the execute's epoch, so every repeat runs a different interleaving.  Each
+pseudo-random 0-16 us (one time in 16 up to 260 us) before each step, unit or
+chain task; the nap is keyed by the execute's epoch, so every repeat runs a
+different interleaving.  Each
 repeat uses a fresh send buffer, so a stale read of the previous repeat's
 scratch or recv cannot pass by accident.  The check is the reference's
 delivery postcondition, recv[d][s] == send[s][d] (evaluate.py:114-126).
