@@ -34,7 +34,7 @@ def _cuda():
     torch.cuda.synchronize()
 
 
-def _runs(a, m, sched, mode, reps, proto="simple", engine="tma", seed=0):
+def _runs(a, m, sched, mode, reps, proto="simple", engine="tma", seed=0, ctas=0):
     """Execute `reps` all-to-alls with fresh random send buffers; return how
     many delivered the exact transpose."""
     from paper_2309_13541_b200.executor import Plan
@@ -45,7 +45,7 @@ def _runs(a, m, sched, mode, reps, proto="simple", engine="tma", seed=0):
         p.set_engine(engine)
         if proto == "simple":
             p.set_schedule_spec(sched)
-        p.bind(0)
+        p.bind(0, num_ctas=ctas)
         p.set_sync_mode(mode)
         p.set_timeout(20.0)
         r = torch.empty((n, n, m), dtype=torch.uint8, device="cuda")
@@ -58,7 +58,9 @@ def _runs(a, m, sched, mode, reps, proto="simple", engine="tma", seed=0):
 
 
 CASES = [("gk8_2", 65536 + 40), ("gk8_2", 1 << 20), ("torus2x4_h2", 262144 + 16),
-         ("hypercube3", 1 << 20), ("ts_torus3x3", 65536), ("torus4x4x4", 16384)]
+         ("hypercube3", 1 << 20), ("ts_torus3x3", 65536), ("torus4x4x4", 16384),
+         ("gk8_2_h1", 4096 + 7), ("torus2x4", 300000), ("ts_gk8_2", 65536 + 16),
+         ("ts_hypercube3", 1000), ("gk64_4", 8192)]
 
 
 @pytest.mark.parametrize("name,m", CASES)
@@ -76,8 +78,8 @@ def test_perturbed_interleavings_deliver_transpose(name, m, sched, engine, artif
 
 
 @pytest.mark.parametrize("name,m", [("gk8_2", 1 << 20), ("hypercube3", 1 << 20),
-                                    ("torus2x4_h2", 262144 + 16)])
-@pytest.mark.parametrize("sched", ["static", "cp:65536", "mix:65536"])
+                                    ("torus2x4_h2", 262144 + 16), ("torus4x4x4", 16384)])
+@pytest.mark.parametrize("sched", ["static", "cp:65536", "mix:65536", "spread:65536"])
 def test_mutation_without_waits_is_caught(name, m, sched, artifacts):
     """Same perturbation with the dependency waits skipped: the transpose
     check must catch the missing dependencies in at least one repeat."""
@@ -85,3 +87,13 @@ def test_mutation_without_waits_is_caught(name, m, sched, artifacts):
     reps = 6
     good = _runs(a, m, sched, DEFAULT_SYNC | PERTURB | NO_WAITS, reps, seed=7)
     assert good < reps
+
+
+@pytest.mark.parametrize("name,m", [("gk8_2", 1 << 20), ("torus4x4x4", 65536)])
+@pytest.mark.parametrize("sched", ["static", "cp:65536", "spread:65536", "chain:262144"])
+@pytest.mark.parametrize("ctas", [1, 3, 37])
+def test_perturbed_few_ctas(name, m, sched, ctas, artifacts):
+    """Few CTAs: each runs many steps / units in a row, so the naps reorder
+    long per-CTA sequences rather than one item per SM."""
+    a = artifacts(name)
+    assert _runs(a, m, sched, DEFAULT_SYNC | PERTURB, 3, seed=ctas, ctas=ctas) == 3
