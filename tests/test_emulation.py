@@ -341,7 +341,7 @@ def test_chain_interleavings_deliver_transpose(name, G, m, unit, mode, artifacts
         pytest.skip("more GPUs than nodes")
     send = make_send(a.g.n, m, seed=G)
     with Plan(a.g, a.sched, m=m, n_gpus=G) as p:
-        p.set_schedule("chain", unit)
+        p.set_schedule(mode, unit)
         nodes = [local_nodes(p, g) for g in range(G)]
         for nc in (1, 7, 148):
             recvs = p.emulate([send[ns] for ns in nodes], num_ctas=nc, seed=nc)

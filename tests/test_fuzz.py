@@ -4,7 +4,9 @@ Random digraphs, Q, shard sizes, routes with random step gaps and mid-route
 re-splits, random placements on 1..8 GPUs.  CPU: the native validation accepts
 them with the oracle's modelled T, and the device protocol emulated in random
 interleavings (static programs, dynamic unit queues, LL lines) delivers the
-transpose.  GPU: bit-exact against the oracle for every protocol and engine.
+transpose (chain mode with a 32-byte TMA ring, so the random routes' local hops
+link into chains).  GPU: bit-exact against the oracle for every protocol and
+engine.
 """
 from __future__ import annotations
 
@@ -30,9 +32,12 @@ def test_random_schedule_emulation(seed):
                                ("simple", "cp", False), ("simple", "mix", True),
                                ("simple", "ready", False), ("simple", "ready", True),
                                ("simple", "spread", False),
+                               ("simple", "chain", False), ("simple", "chaind", False),
                                ("ll", "static", False), ("ll128", "static", False)):
         with Plan(g, sched, m=m, n_gpus=G, placement=placement, protocol=proto,
                   reuse_scratch=reuse) as p:
+            if mode.startswith("chain"):
+                p.set_engine("tma", 16, 2)    # a 32-byte ring: hops of >= 32 B link
             if mode != "static":
                 p.set_schedule(mode, 256)
             assert p.model_time(m) == pytest.approx(T, rel=0, abs=0)
@@ -42,6 +47,23 @@ def test_random_schedule_emulation(seed):
                 for r in range(G):
                     assert np.array_equal(recvs[r], want[nodes[r]]), (proto, mode, reuse, nc, r)
                 p.check_bounds(nc)
+
+
+def test_random_schedules_form_chains():
+    """Sanity of the chain fuzzing above: with the 32-byte ring, many random
+    schedules do link hops into chains (a linked hop drops its wait entries)."""
+    linked = 0
+    for seed in SEEDS[:60]:
+        g, sched, m, _, _ = random_case(seed)
+        waits = {}
+        for mode in ("cp", "chain"):
+            with Plan(g, sched, m=m) as p:
+                p.set_engine("tma", 16, 2)
+                p.set_schedule(mode, 256)
+                waits[mode] = p.dyn_stats(0, 7)["wait_entries"]
+        assert waits["chain"] <= waits["cp"]
+        linked += waits["chain"] < waits["cp"]
+    assert linked >= 15
 
 
 @pytest.mark.gpu
@@ -59,9 +81,13 @@ def test_random_schedule_gpu(seed):
                                     ("simple", "list", "tma", 2), ("simple", "ready", "tma", 0),
                                     ("simple", "ready", "lsu", 3), ("ll", "static", "lsu", 0),
                                     ("ll", "static", "tma", 3), ("ll128", "static", "lsu", 0),
-                                    ("ll128", "static", "tma", 2)):
+                                    ("ll128", "static", "tma", 2), ("simple", "chain", "tma16", 0),
+                                    ("simple", "chaind", "tma16", 3), ("simple", "chain", "lsu", 2)):
         with Plan(g, sched, m=m, protocol=proto) as p:
-            p.set_engine(engine)
+            if engine == "tma16":
+                p.set_engine("tma", 16, 2)
+            else:
+                p.set_engine(engine)
             if mode != "static":
                 p.set_schedule(mode, 256)
             p.bind(0, num_ctas=nc)
