@@ -1,7 +1,7 @@
 """Host bounds audit of every device copy range (compute-sanitizer is closed on
 this GPU pool; this is its address-math half): all artifacts, 1/2/4/8 GPUs,
-static and dynamic schedules, scratch reuse on/off, the LL protocol, odd shard
-sizes."""
+static and dynamic schedules, chains, scratch reuse on/off, the LL protocols,
+odd shard sizes."""
 from __future__ import annotations
 
 import pytest
@@ -14,7 +14,7 @@ NAMES = [n for n in list_artifacts() if not n.startswith("gk256")]
 
 @pytest.mark.parametrize("name", NAMES)
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
-@pytest.mark.parametrize("sched", ["static", "cp", "mix"])
+@pytest.mark.parametrize("sched", ["static", "cp", "mix", "spread", "chain", "chaind"])
 @pytest.mark.parametrize("reuse", [False, True])
 def test_every_copy_range_in_bounds(name, G, sched, reuse, artifacts):
     a = artifacts(name)
