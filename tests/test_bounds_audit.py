@@ -47,3 +47,16 @@ def test_gk256_in_bounds(artifacts):
     a = load_artifact("gk256_4", native=True, verify=False)
     with Plan(a.g, a.sched, m=4096 + 64, n_gpus=8, reuse_scratch=True) as p:
         assert p.check_bounds(148)
+
+
+@pytest.mark.parametrize("name", ["gk8_2", "hypercube3", "torus4x4x4", "ts_torus3x3"])
+@pytest.mark.parametrize("G", [1, 2, 4])
+@pytest.mark.parametrize("mode", ["chain", "chaind"])
+def test_linked_chains_in_bounds(name, G, mode, artifacts):
+    """Chains at sizes where hops link (>= one TMA ring per unit), incl. a
+    shard size that is not 16-byte clean."""
+    a = artifacts(name)
+    for m in (1 << 20, (1 << 20) + 48, 262144 + 4):
+        with Plan(a.g, a.sched, m=m, n_gpus=G, placement="optimized") as p:
+            p.set_schedule(mode, 262144)
+            assert p.check_bounds(148)
