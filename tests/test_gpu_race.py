@@ -34,9 +34,11 @@ def _cuda():
     torch.cuda.synchronize()
 
 
-def _runs(a, m, sched, mode, reps, proto="simple", engine="tma", seed=0, ctas=0):
+def _runs(a, m, sched, mode, reps, proto="simple", engine="tma", seed=0, ctas=0,
+          stop_on_bad=False):
     """Execute `reps` all-to-alls with fresh random send buffers; return how
-    many delivered the exact transpose."""
+    many delivered the exact transpose (with `stop_on_bad`, stop at the first
+    wrong one and return -1)."""
     from paper_2309_13541_b200.executor import Plan
     n = a.g.n
     g = torch.Generator(device="cuda").manual_seed(seed)
@@ -53,7 +55,10 @@ def _runs(a, m, sched, mode, reps, proto="simple", engine="tma", seed=0, ctas=0)
             s = torch.randint(0, 256, (n, n, m), dtype=torch.uint8, device="cuda", generator=g)
             p.execute(s, r)
             p.sync()
-            good += bool(torch.equal(r, s.transpose(0, 1).contiguous()))
+            ok = bool(torch.equal(r, s.transpose(0, 1).contiguous()))
+            if stop_on_bad and not ok:
+                return -1
+            good += ok
     return good
 
 
@@ -84,9 +89,9 @@ def test_mutation_without_waits_is_caught(name, m, sched, artifacts):
     """Same perturbation with the dependency waits skipped: the transpose
     check must catch the missing dependencies in at least one repeat."""
     a = artifacts(name)
-    reps = 6
-    good = _runs(a, m, sched, DEFAULT_SYNC | PERTURB | NO_WAITS, reps, seed=7)
-    assert good < reps
+    reps = 24          # the first wrong transpose ends the test (usually the first repeat)
+    good = _runs(a, m, sched, DEFAULT_SYNC | PERTURB | NO_WAITS, reps, seed=7, stop_on_bad=True)
+    assert good < 0, f"{reps} perturbed runs without dependency waits all delivered"
 
 
 @pytest.mark.parametrize("name,m", [("gk8_2", 1 << 20), ("torus4x4x4", 65536)])
