@@ -563,7 +563,7 @@ def test_multiprocess_mutation_without_waits_is_caught(sched):
     q = ctx.Queue()
     port = _port()
     ps = [ctx.Process(target=_rank_main,
-                      args=(r, world, port, "gk8_2", 1 << 20, 4, q, "tma", sched, False, "simple",
+                      args=(r, world, port, "gk8_2", 1 << 20, 8, q, "tma", sched, False, "simple",
                             False, "hop", 2 | 64 | 128))
           for r in range(world)]
     for p in ps:
