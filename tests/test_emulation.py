@@ -328,7 +328,7 @@ def test_without_self_copy(name, G, sched, artifacts):
 
 @pytest.mark.parametrize("name", ["gk8_2", "torus2x4", "hypercube3", "torus2x4_h2", "ts_gk8_2",
                                   "ts_torus3x3"])
-@pytest.mark.parametrize("G", [1, 2, 4])
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
 @pytest.mark.parametrize("m,unit", [(1 << 20, 262144), (262144 + 48, 196608), (1000, 0)])
 @pytest.mark.parametrize("mode", ["chain", "chaind"])
 def test_chain_interleavings_deliver_transpose(name, G, m, unit, mode, artifacts):
