@@ -88,7 +88,7 @@ def test_offsets_rejects(artifacts):
 @pytest.mark.parametrize("name", ["gk8_2", "hypercube3", "torus2x4_h2"])
 @pytest.mark.parametrize("G", [2, 4, 8])
 @pytest.mark.parametrize("sched", ["static", "mix:1024", "cp:1024", "ready:1024", "cp:1024:64",
-                                   "spread:1024", "ll"])
+                                   "spread:1024", "ll", "ll128", "chain:1024", "chaind:1024"])
 def test_every_autotune_order_delivers(name, G, sched, artifacts):
     """bench.balanced_artifact + every execution schedule bench.py's autotune
     tries, emulated at 13 and 148 CTAs per GPU."""
@@ -149,3 +149,26 @@ def test_split_path_schedule(name, parts, artifacts):
     m = 4096 + 7
     with Plan(a.g, s, m=m, copy_self=False) as p, Plan(a.g, a.sched, m=m, copy_self=False) as q:
         assert np.array_equal(p.link_bytes().sum(axis=0), q.link_bytes().sum(axis=0))
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+@pytest.mark.parametrize("sched", ["chain:262144", "chaind:262144"])
+def test_balanced_lowering_linked_chains_deliver(G, sched, artifacts):
+    """Chains at a size where hops link, on the balanced lowering with route
+    pieces and extra steps (at 2 and 4 GPUs the hypercube keeps local hops)."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    a = artifacts("hypercube3")
+    m = 1 << 20
+    art, pl = bench.balanced_artifact(a, 16 << 20, G, "optimized")
+    send = make_send(a.g.n, m, seed=G)
+    want = np.swapaxes(send, 0, 1)
+    with bench.make_plan(art, m, G, pl, sched, copy_self=False) as p:
+        nodes = [local_nodes(p, r) for r in range(G)]
+        recvs = p.emulate([send[ns] for ns in nodes], num_ctas=37, seed=G)
+        for r in range(G):
+            for i, v in enumerate(nodes[r]):
+                off = [s for s in range(a.g.n) if s != v]
+                assert np.array_equal(recvs[r][i, off], want[v, off]), (r, v)
