@@ -60,8 +60,8 @@ struct KParams {
   int32_t ll;                              // A2A_PROTO_LL: cross-GPU bytes as LL lines
   int32_t ll128, smem_ll;                  // A2A_PROTO_LL128 lines; its per-warp gather smem
   int32_t tma_chunk, tma_stages;           // TMA engine: bytes per bulk copy, ring depth
-  int32_t sync_mode;                       // bit0: acq_rel (not sc) publish fence; bit1: no
-                                           // explicit publish fence; bit2: force .sys at G=1
+  int32_t sync_mode;                       // a2a_plan_set_sync_mode bits (include/a2a_exec.h):
+                                           // 0-5 publish/poll variants, 6 perturb, 7 no waits
   int32_t smem_prog, smem_batch, batch;    // dynamic smem offsets, pieces per staged batch
   unsigned long long* timeline;            // [nC][2T'+3] %globaltimer stamps (see read_timeline)
   // dynamic mode (a2a_dyn_kernel)
