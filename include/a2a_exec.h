@@ -285,7 +285,7 @@ int a2a_plan_read_timeline(a2a_plan* plan, uint64_t* out, int32_t* out_cols);
  * stores (peers first).  Default 2.  Race hunting (tests): bit6 = every CTA naps
  * a pseudo-random 0-16 us (1 in 16: up to 260 us) before each step / unit /
  * chain task; bit7 = skip the dependency waits (mutation self-test: a
- * perturbed run must then fail). */
+ * perturbed run must then fail; refused unless A2A_ALLOW_MUTATION=1). */
 int a2a_plan_set_sync_mode(a2a_plan* plan, int32_t mode);
 /* device-side flag-wait timeout (ns, default 10 s) */
 int a2a_plan_set_timeout(a2a_plan* plan, int64_t timeout_ns);

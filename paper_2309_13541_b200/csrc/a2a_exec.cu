@@ -1843,6 +1843,10 @@ int a2a_plan_set_recv_buffers(a2a_plan* plan, int32_t count) {
 int a2a_plan_set_sync_mode(a2a_plan* plan, int32_t mode) {
   return guard([&]() -> int {
     if (!plan || mode < 0 || mode > 255) return fail(A2A_ERR_INVALID, "bad sync mode");
+    // bit 7 breaks the all-to-all on purpose (mutation self-test): tests only
+    const char* mut = getenv("A2A_ALLOW_MUTATION");
+    if ((mode & kSyncNoWaits) && !(mut && mut[0] == '1'))
+      return fail(A2A_ERR_INVALID, "bad sync mode: bit 7 (skipped waits) needs A2A_ALLOW_MUTATION=1");
     plan->p.sync_mode = mode;
     return A2A_OK;
   });

@@ -552,13 +552,14 @@ def test_multiprocess_perturbed(world, name, m, engine, proto, sched):
 
 
 @pytest.mark.parametrize("sched", ["static", "cp:262144"])
-def test_multiprocess_mutation_without_waits_is_caught(sched):
+def test_multiprocess_mutation_without_waits_is_caught(sched, monkeypatch):
     """The same perturbation with the dependency waits skipped (bit 7) must
     give a wrong transpose on some rank."""
     world = 2
     if _ngpu() < world:
         pytest.skip(f"needs {world} GPUs")
     import torch.multiprocessing as mp
+    monkeypatch.setenv("A2A_ALLOW_MUTATION", "1")     # inherited by the spawned ranks
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()

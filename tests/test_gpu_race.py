@@ -85,10 +85,11 @@ def test_perturbed_interleavings_deliver_transpose(name, m, sched, engine, artif
 @pytest.mark.parametrize("name,m", [("gk8_2", 1 << 20), ("hypercube3", 1 << 20),
                                     ("torus2x4_h2", 262144 + 16), ("torus4x4x4", 16384)])
 @pytest.mark.parametrize("sched", ["static", "cp:65536", "mix:65536", "spread:65536"])
-def test_mutation_without_waits_is_caught(name, m, sched, artifacts):
+def test_mutation_without_waits_is_caught(name, m, sched, artifacts, monkeypatch):
     """Same perturbation with the dependency waits skipped: the transpose
     check must catch the missing dependencies in at least one repeat."""
     a = artifacts(name)
+    monkeypatch.setenv("A2A_ALLOW_MUTATION", "1")
     reps = 24          # the first wrong transpose ends the test (usually the first repeat)
     good = _runs(a, m, sched, DEFAULT_SYNC | PERTURB | NO_WAITS, reps, seed=7, stop_on_bad=True)
     assert good < 0, f"{reps} perturbed runs without dependency waits all delivered"

@@ -163,13 +163,16 @@ def test_plan_rejects_bad_args(artifacts):
         Plan(a.g, a.sched, m=16, placement=[0] * 7)
 
 
-def test_sync_mode_range(artifacts):
+def test_sync_mode_range(artifacts, monkeypatch):
     """Sync-mode bits 0-7 (bit 6 = perturbation, bit 7 = skipped waits for the
     mutation self-test); anything wider is rejected before it reaches a kernel."""
     a = artifacts("torus2x4")
     with Plan(a.g, a.sched, m=16) as p:
-        for mode in (0, 2, 2 | 64, 2 | 64 | 128, 255):
+        for mode in (0, 2, 2 | 64, 63 | 64):
             p.set_sync_mode(mode)
-        for bad in (-1, 256):
+        for bad in (-1, 256, 2 | 128, 255):     # bit 7 only with A2A_ALLOW_MUTATION=1
             with pytest.raises(ValueError, match="bad sync mode"):
                 p.set_sync_mode(bad)
+        monkeypatch.setenv("A2A_ALLOW_MUTATION", "1")
+        p.set_sync_mode(2 | 64 | 128)
+        p.set_sync_mode(255)
